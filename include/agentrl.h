@@ -1,0 +1,202 @@
+/*
+ * agentrl.h -- C ABI of the B200-native (sm_100a) AgentRL hot-path library
+ * (libagentrl.so).  Paper: arxiv 2510.04206 "AgentRL" (PAPER.md in the task's
+ * reference; citations P:<line> below).
+ *
+ * Two operations and their composition:
+ *   agentrl_task_adv_norm        GRPO group advantage followed by the
+ *                                paper's task advantage normalization, sec 3.2
+ *                                Eq.1, over the loss-masked
+ *                                assistant tokens of each task in the GLOBAL
+ *                                batch (all ranks).
+ *   agentrl_policy_loss_fwd_bwd  token-level PPO-clip loss with
+ *                                the DAPO token-level mean through
+ *                                the LM head (token factorisation P:1182-1190),
+ *                                and its exact gradients grad_hidden, grad_W.
+ *   agentrl_grpo_step            the two above, back to back on one stream.
+ *
+ * Conventions (all entry points)
+ *   - Every pointer is DEVICE memory unless its name starts with host_.
+ *   - The caller owns all memory.  The library never allocates persistent
+ *     device memory; scratch comes from a caller workspace whose size the
+ *     matching agentrl_*_workspace_size() returns.  The workspace base must
+ *     be 1024-byte aligned.
+ *   - Entry points are stream-ordered and asynchronous: they enqueue work on
+ *     `stream` and return; no host synchronisation happens inside (the only
+ *     host<->device traffic is kernel arguments).  Distinct workspaces make
+ *     concurrent calls safe.  Every launch configuration is independent of the
+ *     data, so calls can be captured in a CUDA graph.
+ *   - Return value: synchronous status for host-checkable problems (AGENTRL_*
+ *     codes below).  Data-dependent problems are OR-ed into the device word
+ *     *d_status (int32, caller zeroes it) as AGENTRL_ST_* bits; the call still
+ *     completes and writes defined (possibly zero) outputs.
+ *   - comm == NULL means single GPU.  With a communicator, the per-task
+ *     statistics, the masked-token count and the loss are all-reduced (sum,
+ *     fp64) and grad_W is all-reduced (sum, fp32) over NCCL; each rank must
+ *     hold WHOLE groups (a group never spans ranks).
+ */
+#ifndef AGENTRL_H_
+#define AGENTRL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- synchronous return codes ------------------------------------------ */
+#define AGENTRL_OK 0
+#define AGENTRL_ERR_INVALID_ARG (-1) /* null pointer, eps outside range, n_tasks<=0 ... */
+#define AGENTRL_ERR_SHAPE (-2)       /* d % 64 != 0, V % 8 != 0, T < 0, misaligned pointer */
+#define AGENTRL_ERR_WORKSPACE (-3)   /* workspace too small or misaligned */
+#define AGENTRL_ERR_CUDA (-4)        /* a CUDA runtime / driver call failed */
+#define AGENTRL_ERR_NCCL (-5)        /* an NCCL call failed (or NCCL unavailable) */
+#define AGENTRL_ERR_UNSUPPORTED (-6) /* device is not sm_100 */
+
+/* ---- device status bits (OR-ed into *d_status) -------------------------- */
+#define AGENTRL_ST_BAD_TARGET 1          /* a masked token's target not in [0,V) */
+#define AGENTRL_ST_NONFINITE 2           /* non-finite loss / logp ("abort") */
+#define AGENTRL_ST_BAD_OFFSETS 4         /* traj_offsets not 0..T nondecreasing */
+#define AGENTRL_ST_GROUP_SPANS_TASKS 8   /* a group's members have different task_id */
+#define AGENTRL_ST_GROUP_TOO_SMALL 16    /* a group has one trajectory */
+#define AGENTRL_ST_NO_TOKENS 32          /* global masked-token count N == 0 */
+
+typedef struct agentrl_comm_s* agentrl_comm;
+typedef struct CUstream_st* agentrl_stream; /* == cudaStream_t */
+
+/*
+ * Batch descriptor: a packed local token stream of T tokens holding n_traj
+ * trajectories, each a CSR segment of the stream.
+ *   traj_offsets [n_traj+1] int64: segment g = [off[g], off[g+1]); off[0]=0,
+ *                off[n_traj]=T, nondecreasing (else AGENTRL_ST_BAD_OFFSETS).
+ *   task_id      [n_traj] int32 in [0, n_tasks) -- the task T_i;
+ *                task ids are GLOBAL across ranks.
+ *   group_id     [n_traj] int32 in [0, n_groups) -- the group G_{i,j} of
+ *                K_{i,j} trajectories of one sample; rank-local
+ *                dense ids.  All members of a group share one task_id.
+ *   rewards      [n_traj] float -- trajectory reward R.
+ *   loss_mask    [T] uint8 -- nonzero marks the tokens y_{t,k} of actions
+ *                (assistant turns), i.e. the index set of A_i^tok.
+ */
+typedef struct {
+    int64_t T;
+    int32_t n_traj, n_groups, n_tasks;
+    const int64_t* traj_offsets;
+    const int32_t* task_id;
+    const int32_t* group_id;
+    const float* rewards;
+    const uint8_t* loss_mask;
+} agentrl_batch;
+
+/*
+ * Part 1 -- task advantage normalization (Eq.1 after GRPO P:1263).
+ *   A_hat_g  = (R_g - mean_j) / max(std_j, eps_std), population std over the
+ *              group; exactly 0 when every reward of the group is equal.
+ *   mu_i, sigma_i = mean / population std of A_hat over every masked token of
+ *              task i in the global batch (each token counts once).
+ *   adv_tok[t] = mask_t ? (A_hat_g(t) - mu_i) / max(sigma_i, eps_std) : 0.
+ * Outputs:
+ *   adv_tok      [T] float (required)
+ *   task_stats   [n_tasks*3] double: (N_i, mu_i, sigma_i), global; or NULL
+ *   n_mask_global [1] int64: N = sum_i N_i (global); or NULL
+ * eps_std > 0 (default 1e-6); n_tasks > 0.
+ */
+size_t agentrl_task_adv_norm_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
+                                            int32_t n_tasks);
+int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok,
+                          double* task_stats, int64_t* n_mask_global, void* ws,
+                          size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
+                          agentrl_stream stream);
+
+/*
+ * Part 2 -- PPO-clip loss, forward and backward, through the LM head.
+ * Inputs (device):
+ *   hidden   [T,d] bf16 row-major: final normed hidden state of each token
+ *   W_head   [V,d] bf16 row-major (nn.Linear layout, no bias): logits
+ *            z_{t,v} = logit_scale * <hidden_t, W_v>
+ *   target   [T] int32: the sampled token y_t aligned with hidden_t (the
+ *            caller shifts labels)
+ *   adv_tok  [T] float: token advantages (from part 1)
+ *   old_logp [T] float: behaviour log-probs log pi_old(y_t)
+ *   loss_mask[T] uint8
+ *   n_mask_global [1] int64 (device): N in the 1/N token-level mean
+ * Per masked token t:
+ *   logp_t = z_{t,y_t} - logsumexp_v z_{t,v};  rho_t = exp(logp_t - old_t)
+ *   term_t = min(rho_t A_t, clip(rho_t, 1-eps_low, 1+eps_high) A_t)
+ *   loss   = -(1/N) sum_t term_t        (the paper maximises J; loss = -J)
+ * Gradients (exact; the clip branch has zero gradient only where it is
+ * strictly active: A>0 & rho>1+eps_high or A<0 & rho<1-eps_low):
+ *   G_{t,v} = c_t (softmax_v - [v=y_t]),  c_t = unclipped ? rho_t A_t / N : 0
+ *   grad_hidden = logit_scale * G W        (rows of unmasked tokens are 0)
+ *   grad_W      = logit_scale * G^T hidden (summed over ranks if grad_W_mode=1)
+ * Shapes: d % 64 == 0, V % 8 == 0, 1 <= V.  Arithmetic: bf16 operands on
+ * tcgen05 tensor cores with fp32 accumulation; softmax statistics fp32; loss
+ * and statistics reductions fp64.
+ */
+typedef struct {
+    int64_t T;
+    int32_t d, V;
+    const void* hidden;   /* __nv_bfloat16 [T,d] */
+    const void* W_head;   /* __nv_bfloat16 [V,d] */
+    const int32_t* target;
+    const float* adv_tok;
+    const float* old_logp;
+    const uint8_t* loss_mask;
+    float clip_eps_low, clip_eps_high; /* [0,1) and >= 0; default 0.2, 0.2 */
+    float logit_scale;                 /* > 0; default 1.0 */
+    const int64_t* n_mask_global;      /* device [1] */
+    int32_t grad_W_mode;               /* 0 = local sum only, 1 = all-reduce over comm */
+    int32_t reserved;
+} agentrl_loss_args;
+
+/* Outputs.  loss and grad_hidden / grad_W are required; the others may be NULL.
+ *   loss        [1] double: this rank's share -(1/N) sum_{local t} term_t; with a
+ *               communicator it is all-reduced, i.e. the global loss
+ *   logp        [T] float: logp_t on masked tokens, 0 elsewhere
+ *   grad_hidden [T,d] bf16 (overwritten)
+ *   grad_W      [V,d] float (overwritten)
+ *   loss_stats  [4] double: clip fraction, mean rho, mean logp, masked tokens
+ *               (local) */
+typedef struct {
+    double* loss;
+    float* logp;
+    void* grad_hidden;
+    float* grad_W;
+    double* loss_stats;
+} agentrl_loss_out;
+
+size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V);
+int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
+                                size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
+                                agentrl_stream stream);
+
+/* Fused: part 1 then part 2 (a->adv_tok and a->n_mask_global are ignored; the
+ * step uses its own).  adv_tok_out [T] float required; task_stats optional. */
+size_t agentrl_grpo_step_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
+                                        int32_t n_tasks, int32_t d, int32_t V);
+int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss_args* a,
+                      const agentrl_loss_out* o, float* adv_tok_out, double* task_stats,
+                      void* ws, size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
+                      agentrl_stream stream);
+
+/* ---- communicator (NCCL over NVLink; loaded lazily with dlopen) ----------
+ * Rank 0 calls agentrl_comm_unique_id, the caller broadcasts the 128 bytes
+ * (e.g. over a torch.distributed process group), then every rank calls
+ * agentrl_comm_init on its own device.  Returns AGENTRL_ERR_NCCL if
+ * libnccl.so.2 cannot be loaded. */
+int agentrl_comm_unique_id(unsigned char host_id[128]);
+int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned char host_id[128]);
+int agentrl_comm_destroy(agentrl_comm comm);
+
+/* ---- misc -------------------------------------------------------------- */
+const char* agentrl_status_string(int code); /* text for a return code or status bit */
+int agentrl_version(void);                    /* major*10000 + minor*100 + patch */
+/* Number of kernel launches the last call on this thread enqueued (for the
+ * bench's gpu_launches claim). */
+int agentrl_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGENTRL_H_ */

@@ -1,0 +1,250 @@
+"""paper_2510_04206_b200 -- B200-native (sm_100a) AgentRL hot path.
+
+Thin ctypes binding over ``libagentrl.so`` (C ABI: ``include/agentrl.h``).  This
+module only marshals arguments: every step of the path runs in the library's CUDA
+kernels.  PyTorch is used for device memory, streams and process groups.  There is
+no CPU fallback: importing this package without the built library raises.
+
+Entry points (same names as the C ABI):
+    agentrl_task_adv_norm        PAPER.md P:543-579 (sec 3.2 Eq.1) after P:1263 (GRPO)
+    agentrl_policy_loss_fwd_bwd
+    agentrl_grpo_step            both, back to back
+plus ``Step`` (owns workspace/outputs for repeated calls) and ``Comm`` (NCCL).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libagentrl.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not built: run `python -m paper_2510_04206_b200.build` "
+        "(there is no CPU fallback for this package)")
+
+_lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+# ---- status codes / bits (include/agentrl.h)
+OK = 0
+ERR_INVALID_ARG, ERR_SHAPE, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = -1, -2, -3, -4, -5, -6
+ST_BAD_TARGET, ST_NONFINITE, ST_BAD_OFFSETS = 1, 2, 4
+ST_GROUP_SPANS_TASKS, ST_GROUP_TOO_SMALL, ST_NO_TOKENS = 8, 16, 32
+
+EXPORTED = (
+    "agentrl_task_adv_norm_workspace_size", "agentrl_task_adv_norm",
+    "agentrl_policy_loss_workspace_size", "agentrl_policy_loss_fwd_bwd",
+    "agentrl_grpo_step_workspace_size", "agentrl_grpo_step",
+    "agentrl_comm_unique_id", "agentrl_comm_init", "agentrl_comm_destroy",
+    "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
+)
+
+
+class Batch(C.Structure):
+    _fields_ = [("T", C.c_int64), ("n_traj", C.c_int32), ("n_groups", C.c_int32),
+                ("n_tasks", C.c_int32), ("traj_offsets", C.c_void_p), ("task_id", C.c_void_p),
+                ("group_id", C.c_void_p), ("rewards", C.c_void_p), ("loss_mask", C.c_void_p)]
+
+
+class LossArgs(C.Structure):
+    _fields_ = [("T", C.c_int64), ("d", C.c_int32), ("V", C.c_int32), ("hidden", C.c_void_p),
+                ("W_head", C.c_void_p), ("target", C.c_void_p), ("adv_tok", C.c_void_p),
+                ("old_logp", C.c_void_p), ("loss_mask", C.c_void_p),
+                ("clip_eps_low", C.c_float), ("clip_eps_high", C.c_float),
+                ("logit_scale", C.c_float), ("n_mask_global", C.c_void_p),
+                ("grad_W_mode", C.c_int32), ("reserved", C.c_int32)]
+
+
+class LossOut(C.Structure):
+    _fields_ = [("loss", C.c_void_p), ("logp", C.c_void_p), ("grad_hidden", C.c_void_p),
+                ("grad_W", C.c_void_p), ("loss_stats", C.c_void_p)]
+
+
+_P, _i64, _i32, _f64, _sz = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_size_t
+_lib.agentrl_task_adv_norm_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
+_lib.agentrl_task_adv_norm_workspace_size.restype = _sz
+_lib.agentrl_task_adv_norm.argtypes = [C.POINTER(Batch), _f64, _P, _P, _P, _P, _sz, _P, _P, _P]
+_lib.agentrl_policy_loss_workspace_size.argtypes = [_i64, _i32, _i32]
+_lib.agentrl_policy_loss_workspace_size.restype = _sz
+_lib.agentrl_policy_loss_fwd_bwd.argtypes = [C.POINTER(LossArgs), C.POINTER(LossOut), _P, _sz,
+                                             _P, _P, _P]
+_lib.agentrl_grpo_step_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i32, _i32]
+_lib.agentrl_grpo_step_workspace_size.restype = _sz
+_lib.agentrl_grpo_step.argtypes = [C.POINTER(Batch), _f64, C.POINTER(LossArgs),
+                                   C.POINTER(LossOut), _P, _P, _P, _sz, _P, _P, _P]
+_lib.agentrl_comm_unique_id.argtypes = [C.c_char_p]
+_lib.agentrl_comm_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_char_p]
+_lib.agentrl_comm_destroy.argtypes = [_P]
+_lib.agentrl_status_string.argtypes = [C.c_int]
+_lib.agentrl_status_string.restype = C.c_char_p
+_lib.agentrl_version.restype = C.c_int
+_lib.agentrl_last_launch_count.restype = C.c_int
+
+
+def lib():
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return _lib.agentrl_status_string(int(code)).decode()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != OK:
+        raise RuntimeError(f"{what} failed: {rc} ({status_string(rc)})")
+
+
+# --------------------------------------------------------------------------- C ABI mirrors
+def make_batch(b) -> Batch:
+    """``b``: dict of device tensors traj_offsets (int64), task_id, group_id (int32),
+    rewards (float32), loss_mask (uint8), plus ints T, n_groups, n_tasks."""
+    return Batch(int(b["T"]), int(b["task_id"].numel()), int(b["n_groups"]), int(b["n_tasks"]),
+                 _ptr(b["traj_offsets"]), _ptr(b["task_id"]), _ptr(b["group_id"]),
+                 _ptr(b["rewards"]), _ptr(b["loss_mask"]))
+
+
+def make_loss_args(T, hidden, W_head, target, old_logp, loss_mask, adv_tok=None,
+                   n_mask_global=None, eps_low=0.2, eps_high=0.2, logit_scale=1.0,
+                   grad_W_mode=0) -> LossArgs:
+    d = int(hidden.shape[1])
+    V = int(W_head.shape[0])
+    return LossArgs(int(T), d, V, _ptr(hidden), _ptr(W_head), _ptr(target), _ptr(adv_tok),
+                    _ptr(old_logp), _ptr(loss_mask), float(eps_low), float(eps_high),
+                    float(logit_scale), _ptr(n_mask_global), int(grad_W_mode), 0)
+
+
+def make_loss_out(loss, grad_hidden, grad_W, logp=None, loss_stats=None) -> LossOut:
+    return LossOut(_ptr(loss), _ptr(logp), _ptr(grad_hidden), _ptr(grad_W), _ptr(loss_stats))
+
+
+def agentrl_task_adv_norm_workspace_size(T, n_traj, n_groups, n_tasks) -> int:
+    return int(_lib.agentrl_task_adv_norm_workspace_size(T, n_traj, n_groups, n_tasks))
+
+
+def agentrl_policy_loss_workspace_size(T, d, V) -> int:
+    return int(_lib.agentrl_policy_loss_workspace_size(T, d, V))
+
+
+def agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V) -> int:
+    return int(_lib.agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V))
+
+
+def agentrl_task_adv_norm(batch: Batch, eps_std, adv_tok, task_stats, n_mask_global, ws,
+                          comm=None, d_status=None, stream=None) -> int:
+    return _lib.agentrl_task_adv_norm(C.byref(batch), float(eps_std), _ptr(adv_tok),
+                                      _ptr(task_stats), _ptr(n_mask_global), _ptr(ws),
+                                      ws.numel() * ws.element_size(), comm, _ptr(d_status),
+                                      _stream(stream))
+
+
+def agentrl_policy_loss_fwd_bwd(args: LossArgs, out: LossOut, ws, comm=None, d_status=None,
+                                stream=None) -> int:
+    return _lib.agentrl_policy_loss_fwd_bwd(C.byref(args), C.byref(out), _ptr(ws),
+                                            ws.numel() * ws.element_size(), comm,
+                                            _ptr(d_status), _stream(stream))
+
+
+def agentrl_grpo_step(batch: Batch, eps_std, args: LossArgs, out: LossOut, adv_tok_out,
+                      task_stats, ws, comm=None, d_status=None, stream=None) -> int:
+    return _lib.agentrl_grpo_step(C.byref(batch), float(eps_std), C.byref(args), C.byref(out),
+                                  _ptr(adv_tok_out), _ptr(task_stats), _ptr(ws),
+                                  ws.numel() * ws.element_size(), comm, _ptr(d_status),
+                                  _stream(stream))
+
+
+def last_launch_count() -> int:
+    return int(_lib.agentrl_last_launch_count())
+
+
+def alloc_workspace(nbytes: int, device="cuda"):
+    """uint8 device buffer with a 1024-byte aligned base (torch allocations are >= 512 B
+    aligned; over-allocate and slice to be safe)."""
+    import torch
+    raw = torch.empty(int(nbytes) + 1024, dtype=torch.uint8, device=device)
+    off = (-raw.data_ptr()) % 1024
+    return raw[off:off + int(nbytes)]
+
+
+class Comm:
+    """NCCL communicator owned by the library (bootstrap id broadcast by the caller)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        h = C.c_void_p()
+        _check(_lib.agentrl_comm_init(C.byref(h), int(world), int(rank), uid), "agentrl_comm_init")
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.agentrl_comm_unique_id(buf), "agentrl_comm_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None):
+        """Bootstrap over an initialised torch.distributed group (plumbing only)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = cls.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8,
+                         device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.broadcast(t, src=0, group=group)
+        return cls(world, rank, bytes(t.cpu().tolist()))
+
+    def destroy(self):
+        if self.handle:
+            _lib.agentrl_comm_destroy(self.handle)
+            self.handle = None
+
+
+class Step:
+    """Owns the workspace and outputs of repeated ``agentrl_grpo_step`` calls on fixed shapes.
+
+    ``batch``: device tensors (see make_batch); ``W_head`` bf16 [V,d]; per call pass hidden
+    (bf16 [T,d]), target (int32), old_logp (float32).  Outputs are attributes.
+    """
+
+    def __init__(self, T, n_traj, n_groups, n_tasks, d, V, device="cuda", eps_std=1e-6,
+                 eps_low=0.2, eps_high=0.2, logit_scale=1.0, comm: Comm | None = None,
+                 grad_W_mode=None):
+        import torch
+        self.T, self.d, self.V = int(T), int(d), int(V)
+        self.eps_std, self.eps_low, self.eps_high, self.scale = eps_std, eps_low, eps_high, logit_scale
+        self.comm = comm
+        self.grad_W_mode = (1 if comm is not None else 0) if grad_W_mode is None else grad_W_mode
+        self.ws = alloc_workspace(agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks,
+                                                                   d, V), device)
+        self.n_tasks = n_tasks
+        self.adv_tok = torch.empty(T, dtype=torch.float32, device=device)
+        self.task_stats = torch.empty(n_tasks, 3, dtype=torch.float64, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.logp = torch.empty(T, dtype=torch.float32, device=device)
+        self.grad_hidden = torch.empty(T, d, dtype=torch.bfloat16, device=device)
+        self.grad_W = torch.empty(V, d, dtype=torch.float32, device=device)
+        self.loss_stats = torch.zeros(4, dtype=torch.float64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def __call__(self, batch, hidden, W_head, target, old_logp, stream=None, zero_status=True):
+        if zero_status:
+            self.status.zero_()
+        b = make_batch(batch)
+        a = make_loss_args(self.T, hidden, W_head, target, old_logp, batch["loss_mask"],
+                           eps_low=self.eps_low, eps_high=self.eps_high,
+                           logit_scale=self.scale, grad_W_mode=self.grad_W_mode)
+        o = make_loss_out(self.loss, self.grad_hidden, self.grad_W, self.logp, self.loss_stats)
+        rc = agentrl_grpo_step(b, self.eps_std, a, o, self.adv_tok, self.task_stats, self.ws,
+                               self.comm.handle if self.comm else None, self.status, stream)
+        _check(rc, "agentrl_grpo_step")
+        return self

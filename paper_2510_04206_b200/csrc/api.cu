@@ -1,0 +1,268 @@
+// api.cu -- the C ABI declared in include/agentrl.h: argument validation, workspace planning,
+// device checks, the NCCL communicator (loaded lazily with dlopen) and status strings.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "internal.h"
+
+namespace agentrl {
+
+static thread_local int g_launches = 0;
+void count_launch(int n) { g_launches += n; }
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+    }
+    return n;
+}
+
+int check_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AGENTRL_ERR_CUDA;
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+        return AGENTRL_ERR_CUDA;
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) return AGENTRL_ERR_UNSUPPORTED;  // built for sm_100a only
+    return AGENTRL_OK;
+}
+
+// ---------------------------------------------------------------------------- NCCL (dlopen)
+typedef struct {
+    char internal[128];
+} nccl_uid_t;
+typedef void* nccl_comm_t;
+typedef int (*fn_getUniqueId)(nccl_uid_t*);
+typedef int (*fn_commInitRank)(nccl_comm_t*, int, nccl_uid_t, int);
+typedef int (*fn_commDestroy)(nccl_comm_t);
+typedef int (*fn_allReduce)(const void*, void*, size_t, int /*dtype*/, int /*op*/, nccl_comm_t,
+                            cudaStream_t);
+enum { NCCL_INT64 = 4, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+
+struct NcclApi {
+    void* h = nullptr;
+    fn_getUniqueId getUniqueId = nullptr;
+    fn_commInitRank commInitRank = nullptr;
+    fn_commDestroy commDestroy = nullptr;
+    fn_allReduce allReduce = nullptr;
+};
+static NcclApi* nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        // prefer a libnccl already loaded into the process (e.g. torch's), else the system one
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.h = h;
+        api.getUniqueId = (fn_getUniqueId)dlsym(h, "ncclGetUniqueId");
+        api.commInitRank = (fn_commInitRank)dlsym(h, "ncclCommInitRank");
+        api.commDestroy = (fn_commDestroy)dlsym(h, "ncclCommDestroy");
+        api.allReduce = (fn_allReduce)dlsym(h, "ncclAllReduce");
+    });
+    if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.allReduce)
+        return nullptr;
+    return &api;
+}
+
+}  // namespace agentrl
+
+struct agentrl_comm_s {
+    agentrl::nccl_comm_t comm;
+    int world, rank;
+};
+
+namespace agentrl {
+static int allreduce(agentrl_comm c, void* buf, size_t n, int dtype, cudaStream_t s) {
+    NcclApi* api = nccl();
+    if (!api || !c) return AGENTRL_ERR_NCCL;
+    if (n == 0) return AGENTRL_OK;
+    return api->allReduce(buf, buf, n, dtype, NCCL_SUM, c->comm, s) == 0 ? AGENTRL_OK
+                                                                         : AGENTRL_ERR_NCCL;
+}
+int comm_allreduce_f64(agentrl_comm c, double* b, size_t n, cudaStream_t s) {
+    return allreduce(c, b, n, NCCL_FLOAT64, s);
+}
+int comm_allreduce_f32(agentrl_comm c, float* b, size_t n, cudaStream_t s) {
+    return allreduce(c, b, n, NCCL_FLOAT32, s);
+}
+int comm_allreduce_i64(agentrl_comm c, int64_t* b, size_t n, cudaStream_t s) {
+    return allreduce(c, b, n, NCCL_INT64, s);
+}
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static int check_batch(const agentrl_batch* b, double eps_std) {
+    if (!b || !(eps_std > 0.0) || b->n_tasks <= 0 || b->n_traj < 0 || b->n_groups < 0)
+        return AGENTRL_ERR_INVALID_ARG;
+    if (b->T < 0 || b->T >= (int64_t)1 << 31) return AGENTRL_ERR_SHAPE;
+    if (!b->traj_offsets || (b->n_traj > 0 && (!b->task_id || !b->group_id || !b->rewards)) ||
+        (b->T > 0 && !b->loss_mask))
+        return AGENTRL_ERR_INVALID_ARG;
+    return AGENTRL_OK;
+}
+
+static int check_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, bool fused) {
+    if (!a || !o || !o->loss || !o->grad_hidden || !o->grad_W) return AGENTRL_ERR_INVALID_ARG;
+    if (!(a->clip_eps_low >= 0.f && a->clip_eps_low < 1.f) || !(a->clip_eps_high >= 0.f) ||
+        !(a->logit_scale > 0.f))
+        return AGENTRL_ERR_INVALID_ARG;
+    if (a->T < 0 || a->T >= (int64_t)1 << 31 || a->d <= 0 || a->d % 64 != 0 || a->V < 8 ||
+        a->V % 8 != 0)
+        return AGENTRL_ERR_SHAPE;
+    if (!a->hidden || !a->W_head || !a->target || !a->old_logp || !a->loss_mask)
+        return AGENTRL_ERR_INVALID_ARG;
+    if (!fused && (!a->adv_tok || !a->n_mask_global)) return AGENTRL_ERR_INVALID_ARG;
+    if (!aligned(a->hidden, 16) || !aligned(a->W_head, 16) || !aligned(o->grad_hidden, 16) ||
+        !aligned(o->grad_W, 16))
+        return AGENTRL_ERR_SHAPE;
+    if (a->grad_W_mode < 0 || a->grad_W_mode > 1) return AGENTRL_ERR_INVALID_ARG;
+    return AGENTRL_OK;
+}
+
+}  // namespace agentrl
+
+using namespace agentrl;
+
+extern "C" {
+
+size_t agentrl_task_adv_norm_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
+                                            int32_t n_tasks) {
+    return plan_adv(T, n_traj, n_groups, n_tasks).total;
+}
+
+int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok,
+                          double* task_stats, int64_t* n_mask_global, void* ws, size_t ws_bytes,
+                          agentrl_comm comm, int32_t* d_status, agentrl_stream stream) {
+    g_launches = 0;
+    int rc = check_batch(b, eps_std);
+    if (rc) return rc;
+    if ((b->T > 0 && !adv_tok) || !d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
+    if ((rc = check_device())) return rc;
+    AdvWs w = plan_adv(b->T, b->n_traj, b->n_groups, b->n_tasks);
+    if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
+    return launch_adv_norm(b, eps_std, adv_tok, task_stats, n_mask_global,
+                           static_cast<uint8_t*>(ws), w, comm, d_status,
+                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V) {
+    return plan_loss(T, d, V).total;
+}
+
+int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
+                                size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
+                                agentrl_stream stream) {
+    g_launches = 0;
+    int rc = check_loss(a, o, false);
+    if (rc) return rc;
+    if (!d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
+    if ((rc = check_device())) return rc;
+    LossWs w = plan_loss(a->T, a->d, a->V);
+    if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
+    return launch_policy_loss(a, o, static_cast<uint8_t*>(ws), w, nullptr, nullptr, nullptr,
+                              nullptr, comm, d_status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t agentrl_grpo_step_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
+                                        int32_t n_tasks, int32_t d, int32_t V) {
+    AdvWs wa = plan_adv(T, n_traj, n_groups, n_tasks);
+    return plan_loss(T, d, V, align_up(wa.total, 1024)).total;
+}
+
+int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss_args* a,
+                      const agentrl_loss_out* o, float* adv_tok_out, double* task_stats, void* ws,
+                      size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
+                      agentrl_stream stream) {
+    g_launches = 0;
+    int rc = check_batch(b, eps_std);
+    if (rc) return rc;
+    if ((rc = check_loss(a, o, true))) return rc;
+    if (a->T != b->T || a->loss_mask != b->loss_mask) return AGENTRL_ERR_INVALID_ARG;
+    if ((b->T > 0 && !adv_tok_out) || !d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
+    if ((rc = check_device())) return rc;
+    AdvWs wa = plan_adv(b->T, b->n_traj, b->n_groups, b->n_tasks);
+    LossWs wl = plan_loss(a->T, a->d, a->V, align_up(wa.total, 1024));
+    if (ws_bytes < wl.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int64_t* meta = reinterpret_cast<int64_t*>(w8 + wa.meta);
+    if ((rc = launch_adv_norm(b, eps_std, adv_tok_out, task_stats, nullptr, w8, wa, comm,
+                              d_status, s)))
+        return rc;
+    const int before = g_launches;
+    rc = launch_policy_loss(a, o, w8, wl, reinterpret_cast<const int32_t*>(w8 + wa.idx),
+                            meta /* [0] local rows */,
+                            reinterpret_cast<const float*>(w8 + wa.adv_c),
+                            meta + 1 /* global N */, comm, d_status, s);
+    (void)before;
+    return rc;
+}
+
+int agentrl_comm_unique_id(unsigned char host_id[128]) {
+    NcclApi* api = nccl();
+    if (!api || !host_id) return AGENTRL_ERR_NCCL;
+    nccl_uid_t id;
+    if (api->getUniqueId(&id) != 0) return AGENTRL_ERR_NCCL;
+    memcpy(host_id, id.internal, 128);
+    return AGENTRL_OK;
+}
+
+int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned char host_id[128]) {
+    NcclApi* api = nccl();
+    if (!out || world <= 0 || rank < 0 || rank >= world || !host_id)
+        return AGENTRL_ERR_INVALID_ARG;
+    if (!api) return AGENTRL_ERR_NCCL;
+    nccl_uid_t id;
+    memcpy(id.internal, host_id, 128);
+    agentrl_comm c = new agentrl_comm_s{nullptr, world, rank};
+    if (api->commInitRank(&c->comm, world, id, rank) != 0) {
+        delete c;
+        return AGENTRL_ERR_NCCL;
+    }
+    *out = c;
+    return AGENTRL_OK;
+}
+
+int agentrl_comm_destroy(agentrl_comm comm) {
+    if (!comm) return AGENTRL_OK;
+    NcclApi* api = nccl();
+    int rc = AGENTRL_OK;
+    if (api && comm->comm && api->commDestroy(comm->comm) != 0) rc = AGENTRL_ERR_NCCL;
+    delete comm;
+    return rc;
+}
+
+const char* agentrl_status_string(int code) {
+    switch (code) {
+        case AGENTRL_OK: return "ok";
+        case AGENTRL_ERR_INVALID_ARG: return "invalid argument";
+        case AGENTRL_ERR_SHAPE: return "unsupported shape or misaligned pointer";
+        case AGENTRL_ERR_WORKSPACE: return "workspace too small or misaligned";
+        case AGENTRL_ERR_CUDA: return "CUDA error";
+        case AGENTRL_ERR_NCCL: return "NCCL error or NCCL unavailable";
+        case AGENTRL_ERR_UNSUPPORTED: return "device is not sm_100 (B200)";
+        case AGENTRL_ST_BAD_TARGET: return "target token id outside [0, V)";
+        case AGENTRL_ST_NONFINITE: return "non-finite loss or log-prob";
+        case AGENTRL_ST_BAD_OFFSETS: return "trajectory offsets inconsistent with T";
+        case AGENTRL_ST_GROUP_SPANS_TASKS: return "a group spans tasks (or ids out of range)";
+        case AGENTRL_ST_GROUP_TOO_SMALL: return "a group has fewer than 2 trajectories";
+        case AGENTRL_ST_NO_TOKENS: return "no loss-masked tokens in the batch";
+        default: return "unknown";
+    }
+}
+
+int agentrl_version(void) { return 100; }
+int agentrl_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// gemm_sm100.cuh -- persistent, warp-specialised tcgen05 GEMM for sm_100a with the three
+// fused epilogues of the LM-head loss path.
+//
+//   D[BM x BN] (fp32, TMEM) = sum_k A[BM x BK] * B[BN x BK]^T, bf16 operands staged by TMA
+//   (SWIZZLE_128B) through a STAGES-deep shared-memory ring; one elected thread issues
+//   tcgen05.mma (M=128, N=256, K=16); two TMEM accumulators (2 x 256 columns) let the
+//   epilogue of tile i overlap the MMAs of tile i+1.
+//
+//   warp 0      : TMA producer (one lane)
+//   warp 1      : TMEM allocator + MMA issuer (one lane)
+//   warps 2..5  : epilogue; warp w reads TMEM lanes 32*(w%4) .. +31 (row = lane)
+//
+// Operand majors: A/B either K-major (K contiguous; one TMA box {64, rows}) or MN-major (MN
+// contiguous; boxes {64 (MN), 64 (K)} stacked along MN, LBO = 8 KB between 64-wide atoms).
+//
+// Epilogues (row r = output row, 256 columns per tile):
+//   EPI_FWD   logits z = s*acc: per (row, tile) max m and l = sum exp(z-m) over valid columns,
+//             P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls in the
+//             tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
+//   EPI_GRADH grad_hidden[idx[r], :] = bf16(s * acc)   (scatter to the original token row)
+//   EPI_GRADW grad_W[r, :] = s * acc (fp32); zeros if the (dynamic) K extent is 0.
+#pragma once
+#include "ptx.cuh"
+
+namespace agentrl {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_A_STAGE = GEMM_BM * GEMM_BK * 2;  // 16 KB
+constexpr int GEMM_B_STAGE = GEMM_BN * GEMM_BK * 2;  // 32 KB
+constexpr int GEMM_SMEM_BYTES =
+    GEMM_STAGES * (GEMM_A_STAGE + GEMM_B_STAGE) + 1024 /*barriers*/ + 1024 /*align slack*/;
+
+enum { EPI_FWD = 0, EPI_GRADH = 1, EPI_GRADW = 2 };
+
+struct GemmArgs {
+    // problem: rows M (dynamic if m_dev), cols N, reduction K (dynamic if k_dev)
+    int64_t M_static;
+    const int64_t* m_dev;
+    int32_t N;
+    int64_t K_static;
+    const int64_t* k_dev;
+    int32_t group_m;  // raster: tiles grouped by group_m row-blocks, columns fastest inside
+    float scale;      // logit_scale s
+    // EPI_FWD
+    const int32_t* tgt;  // [rows] target token of each compacted row
+    __half* P;           // [rows, ldP] exp(z - m_tile), fp16
+    int64_t ldP;
+    float2* part;  // [rows, n_tiles] (m, l)
+    int32_t n_tiles;
+    float* zy;  // [rows]
+    // EPI_GRADH
+    const int32_t* idx;  // [rows] original token index
+    __nv_bfloat16* gh;   // [T, ldo]
+    // EPI_GRADW
+    float* gw;  // [V, ldo]
+    int64_t ldo;
+};
+
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t num_n,
+                                            int32_t group_m, int64_t& m_blk, int64_t& n_blk) {
+    const int64_t per_group = (int64_t)group_m * num_n;
+    const int64_t g = tile / per_group;
+    const int64_t first_m = g * group_m;
+    const int64_t gm = min((int64_t)group_m, num_m - first_m);
+    const int64_t local = tile - first_m * num_n;
+    m_blk = first_m + local % gm;
+    n_blk = local / gm;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + GEMM_STAGES * GEMM_A_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + GEMM_STAGES * GEMM_B_STAGE);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + GEMM_STAGES;
+    uint64_t* tfull = bars + 2 * GEMM_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    const int64_t M = p.m_dev ? *p.m_dev : p.M_static;
+    const int64_t K = p.k_dev ? *p.k_dev : p.K_static;
+    const int64_t num_m = (M + GEMM_BM - 1) / GEMM_BM;
+    const int64_t num_n = (p.N + GEMM_BN - 1) / GEMM_BN;
+    const int64_t num_tiles = num_m * num_n;
+    const int64_t num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < GEMM_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_mbar_init();
+        fence_proxy_async_smem();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t pol_a = policy_evict_normal();
+            const uint64_t pol_b = policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int64_t m_blk, n_blk;
+                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                const int32_t m0 = (int32_t)(m_blk * GEMM_BM);
+                const int32_t n0 = (int32_t)(n_blk * GEMM_BN);
+                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], GEMM_A_STAGE + GEMM_B_STAGE);
+                    const int32_t k0 = (int32_t)(kb * GEMM_BK);
+                    uint8_t* a_dst = sA + stage * GEMM_A_STAGE;
+                    uint8_t* b_dst = sB + stage * GEMM_B_STAGE;
+                    if (!A_MN) {
+                        tma_load_2d(&tmA, &full[stage], a_dst, k0, m0, pol_a);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < GEMM_BM / 64; ++i)
+                            tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + i * 64, k0,
+                                        pol_a);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(&tmB, &full[stage], b_dst, k0, n0, pol_b);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < GEMM_BN / 64; ++i)
+                            tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + i * 64, k0,
+                                        pol_b);
+                    }
+                    if (++stage == GEMM_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(GEMM_BM, GEMM_BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_BN);
+                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + stage * GEMM_A_STAGE);
+                    const uint32_t b_base = smem_u32(sB + stage * GEMM_B_STAGE);
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k) {
+                        const uint64_t adesc =
+                            A_MN ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
+                        const uint64_t bdesc =
+                            B_MN ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
+                        tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+                    tc_commit(&empty[stage]);
+                    if (++stage == GEMM_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int64_t m_blk, n_blk;
+            tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+            const int64_t row = m_blk * GEMM_BM + q * 32 + lane;
+            const bool row_ok = row < M;
+            const int32_t col0 = (int32_t)(n_blk * GEMM_BN);
+            const int32_t ncol = min(GEMM_BN, p.N - col0);  // valid columns in this tile
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + lane_base + (uint32_t)(acc * GEMM_BN);
+            uint32_t r[32];
+
+            if constexpr (EPI == EPI_FWD) {
+                const float s = p.scale;
+                const float LOG2E = 1.4426950408889634f;
+                // pass 1: tile max over valid columns
+                float m = -INFINITY;
+#pragma unroll 1
+                for (int c = 0; c < GEMM_BN / 32; ++c) {
+                    tmem_ld_32x32b_x32(taddr + c * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (c * 32 + j < ncol) m = fmaxf(m, s * __uint_as_float(r[j]));
+                }
+                // pass 2: P~ = exp(z - m), l = sum P~, z_y
+                const int32_t y = row_ok ? p.tgt[row] : -1;
+                const int32_t yl = y - col0;
+                float l = 0.f;
+                const float mb = m * LOG2E;
+                __half* prow = p.P + (row_ok ? row : 0) * p.ldP + col0;
+#pragma unroll 1
+                for (int c = 0; c < GEMM_BN / 32; ++c) {
+                    tmem_ld_32x32b_x32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    float e[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float z = s * __uint_as_float(r[j]);
+                        const bool ok = c * 32 + j < ncol;
+                        e[j] = ok ? ex2_approx(fmaf(z, LOG2E, -mb)) : 0.f;
+                        l += e[j];
+                        if (c * 32 + j == yl && row_ok) p.zy[row] = z;
+                    }
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            if (c * 32 + j < ncol) {
+                                uint4 v;
+                                v.x = pack_half2(e[j + 0], e[j + 1]);
+                                v.y = pack_half2(e[j + 2], e[j + 3]);
+                                v.z = pack_half2(e[j + 4], e[j + 5]);
+                                v.w = pack_half2(e[j + 6], e[j + 7]);
+                                *reinterpret_cast<uint4*>(prow + c * 32 + j) = v;
+                            }
+                        }
+                    }
+                }
+                if (row_ok) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
+            } else if constexpr (EPI == EPI_GRADH) {
+                const float s = p.scale;
+                __nv_bfloat16* orow =
+                    p.gh + (row_ok ? (int64_t)p.idx[row] : 0) * p.ldo + col0;
+#pragma unroll 1
+                for (int c = 0; c < GEMM_BN / 32; ++c) {
+                    tmem_ld_32x32b_x32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            if (c * 32 + j < ncol) {
+                                uint4 v;
+                                v.x = pack_bf162(s * __uint_as_float(r[j + 0]),
+                                                 s * __uint_as_float(r[j + 1]));
+                                v.y = pack_bf162(s * __uint_as_float(r[j + 2]),
+                                                 s * __uint_as_float(r[j + 3]));
+                                v.z = pack_bf162(s * __uint_as_float(r[j + 4]),
+                                                 s * __uint_as_float(r[j + 5]));
+                                v.w = pack_bf162(s * __uint_as_float(r[j + 6]),
+                                                 s * __uint_as_float(r[j + 7]));
+                                *reinterpret_cast<uint4*>(orow + c * 32 + j) = v;
+                            }
+                        }
+                    }
+                }
+            } else {  // EPI_GRADW
+                const float s = num_kb > 0 ? p.scale : 0.f;
+                float* orow = p.gw + (row_ok ? row : 0) * p.ldo + col0;
+#pragma unroll 1
+                for (int c = 0; c < GEMM_BN / 32; ++c) {
+                    if (num_kb > 0) {
+                        tmem_ld_32x32b_x32(taddr + c * 32, r);
+                        tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = 0u;
+                    }
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            if (c * 32 + j < ncol) {
+                                float4 v = make_float4(s * __uint_as_float(r[j + 0]),
+                                                       s * __uint_as_float(r[j + 1]),
+                                                       s * __uint_as_float(r[j + 2]),
+                                                       s * __uint_as_float(r[j + 3]));
+                                *reinterpret_cast<float4*>(orow + c * 32 + j) = v;
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace agentrl

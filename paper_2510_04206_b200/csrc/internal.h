@@ -1,0 +1,87 @@
+// internal.h -- host-side declarations shared by the CUDA translation units of libagentrl.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/agentrl.h"
+
+namespace agentrl {
+
+constexpr int CHUNK_TOKENS = 4096;  // tokens per block in the token-parallel kernels
+constexpr int CHUNK_THREADS = 256;  // 16 tokens per thread
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over the caller's workspace (offsets only; the plan is computed identically
+// by the *_workspace_size() query and by the entry point).
+struct WsPlan {
+    size_t off = 0;
+    size_t take(size_t bytes, size_t align = 256) {
+        off = align_up(off, align);
+        size_t o = off;
+        off += bytes;
+        return o;
+    }
+};
+
+// ---- part 1 workspace (see adv_norm.cu) ----
+struct AdvWs {
+    size_t n_g, chunk_cnt, chunk_base, grp_cnt, grp_start, grp_fill, members;  // int32
+    size_t adv_hat;                                                               // double
+    size_t stats;     // double [3*n_tasks]: N_i, S_i, Q_i (local, then global)
+    size_t meta;      // int64 [4]: n_mask_local, n_mask_global, pad
+    size_t idx;       // int32 [T] compacted token positions
+    size_t adv_c;     // float [T] compacted advantages
+    size_t total;
+};
+AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, size_t base = 0);
+
+// Enqueue part 1.  Returns AGENTRL_* code.  comm may be null.
+int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
+                    int64_t* n_mask_global, uint8_t* ws, const AdvWs& w, agentrl_comm comm,
+                    int32_t* d_status, cudaStream_t stream);
+
+// ---- part 2 workspace (see lmhead.cu) ----
+struct LossWs {
+    size_t idx, meta;                       // int32 [T] (standalone path), int64 [4]
+    size_t chunk_cnt, chunk_base;           // int32 compaction scratch (standalone path)
+    size_t tgt_c, old_c, adv_c;             // compacted per-row inputs
+    size_t H;                               // bf16 [T_pad, d] gathered hidden rows
+    size_t P;                               // fp16/bf16 [T_pad, V]: P~ then G (in place)
+    size_t part;                            // float2 [T_pad, n_tiles]
+    size_t zy;                              // float [T_pad]
+    size_t row_term, row_rho, row_logp;     // double/float per row
+    size_t row_clip;                        // int32 per row
+    size_t red;                             // double [8] loss reduction output
+    size_t total;
+    int32_t n_tiles;
+};
+LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0);
+
+// Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:
+//   idx_dev  int32 [T] compacted token positions, rows_dev -> int64 number of rows (local T_eff),
+//   adv_c    float [T] compacted advantages, nglob -> int64 global masked count.
+int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
+                       const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
+                       const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
+                       int32_t* d_status, cudaStream_t stream);
+
+// ---- comm (comm.cpp) ----
+int comm_allreduce_f64(agentrl_comm c, double* buf, size_t n, cudaStream_t s);
+int comm_allreduce_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
+int comm_allreduce_i64(agentrl_comm c, int64_t* buf, size_t n, cudaStream_t s);
+
+// launch counter for the bench's gpu_launches claim
+void count_launch(int n = 1);
+int num_sms();
+int check_device();  // AGENTRL_OK or AGENTRL_ERR_UNSUPPORTED / _CUDA
+
+}  // namespace agentrl
+
+#define AG_CUDA(x)                                     \
+    do {                                               \
+        cudaError_t e_ = (x);                          \
+        if (e_ != cudaSuccess) return AGENTRL_ERR_CUDA; \
+    } while (0)

@@ -1,0 +1,537 @@
+// lmhead.cu -- part 2 of the hot path: token-level PPO-clip loss through the LM head and its
+// exact backward (PAPER.md P:1182-1190 token factorisation, P:1230-1241 PPO-clip,
+// P:1132-1141 token-level mean / decoupled eps).
+//
+//   K4 k_gather       compacted rows: H[p] = hidden[idx[p]], target/old/adv per row; rows
+//                     [T_eff, pad64) zeroed (they are inside GEMM3's K range)
+//   K5 gemm<FWD>      z = s * H W^T on tcgen05; epilogue: per (row, 256-col tile) max m and
+//                     l = sum exp(z - m), P~ = exp(z - m) -> fp16 [rows, V], z_y gathered
+//   K6 k_merge_g      per row: lse = logsumexp over tiles, logp, rho, PPO-clip term,
+//                     c = unclipped ? rho*A/N : 0; rewrites the row in place as
+//                     G = bf16(c * (P~ * exp(m_tile - lse) - [v == y]))
+//   K7 k_loss_reduce  fixed-order fp64 reduction of the per-row terms -> loss, stats
+//   K9 gemm<GRADW>    grad_W = s * G^T H      (A = G MN-major, B = H MN-major, K = T_eff)
+//   C3                NCCL all-reduce of grad_W on a side stream, overlapped with K8
+//   K8 gemm<GRADH>    grad_hidden[idx] = s * G W  (A = G K-major, B = W MN-major, K = V)
+//
+// Executed tensor work is 6 * T_eff * V * d FLOP (three GEMMs; no recompute: the fp16 P~
+// written by the forward epilogue replaces the second logits GEMM).  See DESIGN.md.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "gemm_sm100.cuh"
+#include "internal.h"
+
+namespace agentrl {
+
+// ---------------------------------------------------------------------------- tensor maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+// bf16 2-D tensor [outer, inner] (row stride = ld elements), box {box_inner, box_outer},
+// SWIZZLE_128B (box_inner * 2 B must be 128), out-of-bounds reads return zeros.
+static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return AGENTRL_ERR_CUDA;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? AGENTRL_OK : AGENTRL_ERR_CUDA;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
+                       int64_t max_tiles, cudaStream_t stream) {
+    auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     GEMM_SMEM_BYTES));
+        attr_done = true;
+    }
+    int grid = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(max_tiles, 1));
+    kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(a, b, g);
+    count_launch();
+    AG_CUDA(cudaGetLastError());
+    return AGENTRL_OK;
+}
+
+// ---------------------------------------------------------------------------- compaction
+// (standalone policy-loss entry: idx from loss_mask alone)
+__global__ void __launch_bounds__(CHUNK_THREADS)
+    k_mask_count(int64_t T, const uint8_t* __restrict__ mask, int32_t* __restrict__ chunk_cnt) {
+    const int64_t t0 = (int64_t)blockIdx.x * CHUNK_TOKENS + threadIdx.x * 16;
+    int32_t c = 0;
+    for (int i = 0; i < 16; ++i)
+        if (t0 + i < T) c += mask[t0 + i] != 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    __shared__ int32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s[w];
+        chunk_cnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_chunk_scan(int64_t n_chunks, int32_t* chunk, int64_t* meta) {
+    // one thread: n_chunks is T/4096 (<= 32768 at T = 2^27)
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int64_t i = 0; i < n_chunks; ++i) {
+            int32_t x = chunk[i];
+            chunk[i] = (int32_t)run;
+            run += x;
+        }
+        meta[0] = run;
+    }
+}
+
+__global__ void __launch_bounds__(CHUNK_THREADS)
+    k_compact(int64_t T, const uint8_t* __restrict__ mask, const float* __restrict__ adv_tok,
+              const int32_t* __restrict__ chunk_base, int32_t* __restrict__ idx,
+              float* __restrict__ adv_c) {
+    const int64_t t0 = (int64_t)blockIdx.x * CHUNK_TOKENS + threadIdx.x * 16;
+    int32_t c = 0;
+    for (int i = 0; i < 16; ++i)
+        if (t0 + i < T) c += mask[t0 + i] != 0;
+    // block exclusive scan
+    __shared__ int32_t s[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s[wid] = x;
+    __syncthreads();
+    int32_t woff = 0;
+    for (int w = 0; w < wid; ++w) woff += s[w];
+    int32_t pos = chunk_base[blockIdx.x] + woff + x - c;
+    for (int i = 0; i < 16; ++i) {
+        const int64_t t = t0 + i;
+        if (t < T && mask[t]) {
+            idx[pos] = (int32_t)t;
+            adv_c[pos] = adv_tok[t];
+            ++pos;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- K4 gather
+__global__ void __launch_bounds__(256)
+    k_gather(const int64_t* __restrict__ rows_dev, int64_t T, int32_t d, int32_t V,
+             const __nv_bfloat16* __restrict__ hidden, const int32_t* __restrict__ target,
+             const float* __restrict__ old_logp, const int32_t* __restrict__ idx,
+             __nv_bfloat16* __restrict__ H, int32_t* __restrict__ tgt_c,
+             float* __restrict__ old_c, int32_t* d_status) {
+    const int64_t rows = *rows_dev;
+    const int64_t rows_pad = (rows + 63) / 64 * 64;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    const int chunks = d / 8;  // 16-byte chunks per row
+    for (int64_t p = (int64_t)blockIdx.x * 8 + warp; p < rows_pad; p += nwarps) {
+        uint4* dst = reinterpret_cast<uint4*>(H + p * d);
+        if (p < rows) {
+            const int64_t t = idx[p];
+            const uint4* src = reinterpret_cast<const uint4*>(hidden + t * d);
+            for (int c = lane; c < chunks; c += 32) dst[c] = __ldg(src + c);
+            if (lane == 0) {
+                int32_t y = target[t];
+                if (y < 0 || y >= V) {
+                    atomicOr(d_status, AGENTRL_ST_BAD_TARGET);
+                    y = 0;
+                }
+                tgt_c[p] = y;
+                old_c[p] = old_logp[t];
+            }
+        } else {
+            for (int c = lane; c < chunks; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
+            if (lane == 0) {
+                tgt_c[p] = 0;
+                old_c[p] = 0.f;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- K6 merge + G
+constexpr int MERGE_THREADS = 256;
+
+__global__ void __launch_bounds__(MERGE_THREADS)
+    k_merge_g(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
+              int32_t V, int32_t n_tiles, const float2* __restrict__ part,
+              const float* __restrict__ zy, const int32_t* __restrict__ tgt_c,
+              const float* __restrict__ old_c, const float* __restrict__ adv_c,
+              const int32_t* __restrict__ idx, float eps_lo, float eps_hi,
+              uint16_t* __restrict__ PG /* fp16 P~ in, bf16 G out, [rows, V] */,
+              double* __restrict__ row_term, float* __restrict__ row_rho,
+              float* __restrict__ row_logp, int32_t* __restrict__ row_clip,
+              float* __restrict__ logp_out) {
+    extern __shared__ float s_f[];  // [n_tiles] scale per tile
+    __shared__ float s_red[MERGE_THREADS / 32];
+    __shared__ float s_bc[2];
+    const int64_t rows = *rows_dev;
+    const int64_t rows_pad = (rows + 63) / 64 * 64;
+    const double Nd = (double)*nglob_dev;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const float LOG2E = 1.4426950408889634f;
+
+    for (int64_t p = blockIdx.x; p < rows_pad; p += gridDim.x) {
+        uint4* row4 = reinterpret_cast<uint4*>(PG + p * (int64_t)V);
+        const int nvec = V / 8;
+        if (p >= rows) {  // padding rows inside GEMM3's K range: zero
+            for (int c = threadIdx.x; c < nvec; c += MERGE_THREADS) row4[c] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const float2* pr = part + p * (int64_t)n_tiles;
+        // lse over tiles: M = max m_j, L = sum l_j exp(m_j - M)   (fixed order per thread +
+        // fixed tree -> deterministic)
+        float mloc = -INFINITY;
+        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS) mloc = fmaxf(mloc, pr[j].x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+        if (lane == 0) s_red[wid] = mloc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float m = s_red[0];
+            for (int w = 1; w < MERGE_THREADS / 32; ++w) m = fmaxf(m, s_red[w]);
+            s_bc[0] = m;
+        }
+        __syncthreads();
+        const float M = s_bc[0];
+        float lloc = 0.f;
+        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS) {
+            const float2 ml = pr[j];
+            lloc += ml.y * ex2_approx((ml.x - M) * LOG2E);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lloc += __shfl_xor_sync(0xffffffffu, lloc, o);
+        __syncthreads();
+        if (lane == 0) s_red[wid] = lloc;
+        __syncthreads();
+        float c_t = 0.f;
+        if (threadIdx.x == 0) {
+            float L = 0.f;
+            for (int w = 0; w < MERGE_THREADS / 32; ++w) L += s_red[w];
+            const float lse = M + logf(L);
+            const float logp = zy[p] - lse;
+            const float A = adv_c[p];
+            const float rho = expf(logp - old_c[p]);
+            const float lo = 1.f - eps_lo, hi = 1.f + eps_hi;
+            const float rc = fminf(fmaxf(rho, lo), hi);
+            const double u = (double)rho * (double)A, cl = (double)rc * (double)A;
+            const double term = u < cl ? u : cl;
+            const bool clipped = (A > 0.f && rho > hi) || (A < 0.f && rho < lo);
+            c_t = clipped ? 0.f : (float)((double)rho * (double)A / Nd);
+            row_term[p] = term;
+            row_rho[p] = rho;
+            row_logp[p] = logp;
+            row_clip[p] = clipped ? 1 : 0;
+            if (logp_out) logp_out[idx[p]] = logp;
+            s_bc[0] = lse;
+            s_bc[1] = c_t;
+        }
+        __syncthreads();
+        const float lse = s_bc[0];
+        c_t = s_bc[1];
+        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
+            s_f[j] = c_t * ex2_approx((pr[j].x - lse) * LOG2E);
+        __syncthreads();
+        const int32_t y = tgt_c[p];
+        for (int c = threadIdx.x; c < nvec; c += MERGE_THREADS) {
+            const int v0 = c * 8;
+            const float f = s_f[v0 >> 8];  // 256-column tiles
+            uint4 in = row4[c];
+            const __half2* h2 = reinterpret_cast<const __half2*>(&in);
+            float g[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float2 x = __half22float2(h2[k]);
+                g[2 * k] = f * x.x;
+                g[2 * k + 1] = f * x.y;
+            }
+            if (y >= v0 && y < v0 + 8) g[y - v0] -= c_t;
+            uint4 out;
+            out.x = pack_bf162(g[0], g[1]);
+            out.y = pack_bf162(g[2], g[3]);
+            out.z = pack_bf162(g[4], g[5]);
+            out.w = pack_bf162(g[6], g[7]);
+            row4[c] = out;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------- K7 reduce
+__global__ void __launch_bounds__(1024)
+    k_loss_reduce(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
+                  const double* __restrict__ row_term, const float* __restrict__ row_rho,
+                  const float* __restrict__ row_logp, const int32_t* __restrict__ row_clip,
+                  double* __restrict__ loss_out, double* __restrict__ stats_out,
+                  int32_t* d_status) {
+    __shared__ double s[4][32];
+    const int64_t rows = *rows_dev;
+    const double N = (double)*nglob_dev;
+    double a = 0.0, b = 0.0, c = 0.0, e = 0.0;
+    // contiguous per-thread segments, fixed order
+    const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = min(rows, (int64_t)threadIdx.x * per), hi = min(rows, lo + per);
+    for (int64_t p = lo; p < hi; ++p) {
+        a += row_term[p];
+        b += (double)row_rho[p];
+        c += (double)row_logp[p];
+        e += (double)row_clip[p];
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+        e += __shfl_down_sync(0xffffffffu, e, o);
+    }
+    if (lane == 0) {
+        s[0][wid] = a;
+        s[1][wid] = b;
+        s[2][wid] = c;
+        s[3][wid] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double A = 0, B = 0, Cc = 0, E = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            A += s[0][w];
+            B += s[1][w];
+            Cc += s[2][w];
+            E += s[3][w];
+        }
+        const double loss = N > 0.0 ? -A / N : 0.0;
+        *loss_out = loss;
+        if (!isfinite(loss) || !isfinite(Cc)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
+        if (stats_out) {
+            const double r = rows > 0 ? (double)rows : 1.0;
+            stats_out[0] = E / r;
+            stats_out[1] = B / r;
+            stats_out[2] = Cc / r;
+            stats_out[3] = (double)rows;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- host
+LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
+    WsPlan p;
+    p.off = base;
+    LossWs w;
+    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    w.n_tiles = (int32_t)ceil_div(V, GEMM_BN);
+    w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
+    w.meta = p.take(sizeof(int64_t) * 4);
+    w.chunk_cnt = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
+    w.chunk_base = w.chunk_cnt;
+    w.tgt_c = p.take(sizeof(int32_t) * (size_t)rows_cap);
+    w.old_c = p.take(sizeof(float) * (size_t)rows_cap);
+    w.adv_c = p.take(sizeof(float) * (size_t)rows_cap);
+    w.H = p.take((size_t)rows_cap * d * 2, 1024);
+    w.P = p.take((size_t)rows_cap * V * 2, 1024);
+    w.part = p.take(sizeof(float2) * (size_t)rows_cap * w.n_tiles);
+    w.zy = p.take(sizeof(float) * (size_t)rows_cap);
+    w.row_term = p.take(sizeof(double) * (size_t)rows_cap);
+    w.row_rho = p.take(sizeof(float) * (size_t)rows_cap);
+    w.row_logp = p.take(sizeof(float) * (size_t)rows_cap);
+    w.row_clip = p.take(sizeof(int32_t) * (size_t)rows_cap);
+    w.red = p.take(sizeof(double) * 8);
+    w.total = p.off;
+    return w;
+}
+
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+static SideStream& side_stream() {
+    static thread_local SideStream ss;
+    if (!ss.s) {
+        cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ss.e0, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss.e1, cudaEventDisableTiming);
+    }
+    return ss;
+}
+
+int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
+                       const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
+                       const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
+                       int32_t* d_status, cudaStream_t stream) {
+    const int64_t T = a->T;
+    const int32_t d = a->d, V = a->V;
+    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    int64_t* meta = reinterpret_cast<int64_t*>(ws + w.meta);
+    int32_t* idx = reinterpret_cast<int32_t*>(ws + w.idx);
+    float* adv_c = reinterpret_cast<float*>(ws + w.adv_c);
+    int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + w.tgt_c);
+    float* old_c = reinterpret_cast<float*>(ws + w.old_c);
+    __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(ws + w.H);
+    uint16_t* PG = reinterpret_cast<uint16_t*>(ws + w.P);
+    float2* part = reinterpret_cast<float2*>(ws + w.part);
+    float* zy = reinterpret_cast<float*>(ws + w.zy);
+    double* row_term = reinterpret_cast<double*>(ws + w.row_term);
+    float* row_rho = reinterpret_cast<float*>(ws + w.row_rho);
+    float* row_logp = reinterpret_cast<float*>(ws + w.row_logp);
+    int32_t* row_clip = reinterpret_cast<int32_t*>(ws + w.row_clip);
+
+    // ---- compaction (standalone) or reuse of part 1's
+    if (!idx_dev) {
+        const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+        int32_t* chunk = reinterpret_cast<int32_t*>(ws + w.chunk_cnt);
+        AG_CUDA(cudaMemsetAsync(meta, 0, 4 * sizeof(int64_t), stream));
+        if (n_chunks > 0) {
+            k_mask_count<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, chunk);
+            k_chunk_scan<<<1, 32, 0, stream>>>(n_chunks, chunk, meta);
+            k_compact<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, a->adv_tok,
+                                                                         chunk, idx, adv_c);
+            count_launch(3);
+        }
+        idx_dev = idx;
+        rows_dev = meta;
+        adv_c_dev = adv_c;
+        nglob_dev = a->n_mask_global;
+    }
+
+    // ---- outputs that are defined everywhere
+    AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, stream));
+    if (o->logp) AG_CUDA(cudaMemsetAsync(o->logp, 0, (size_t)T * sizeof(float), stream));
+
+    // ---- K4 gather
+    {
+        int grid = num_sms() * 4;
+        k_gather<<<grid, 256, 0, stream>>>(rows_dev, T, d, V,
+                                           reinterpret_cast<const __nv_bfloat16*>(a->hidden),
+                                           a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
+                                           d_status);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
+    }
+
+    // ---- tensor maps
+    CUtensorMap mH_K, mH_MN, mW_K, mW_MN, mG_K, mG_MN;
+    int rc;
+    if ((rc = make_map(&mH_K, H, d, rows_cap, d, 64, 128))) return rc;
+    if ((rc = make_map(&mH_MN, H, d, rows_cap, d, 64, 64))) return rc;
+    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, 256))) return rc;
+    if ((rc = make_map(&mW_MN, a->W_head, d, V, d, 64, 64))) return rc;
+    if ((rc = make_map(&mG_K, PG, V, rows_cap, V, 64, 128))) return rc;
+    if ((rc = make_map(&mG_MN, PG, V, rows_cap, V, 64, 64))) return rc;
+
+    const int64_t max_m_tiles = rows_cap / GEMM_BM;
+    // ---- K5 forward GEMM + softmax-statistics epilogue
+    {
+        GemmArgs g{};
+        g.m_dev = rows_dev;
+        g.N = V;
+        g.K_static = d;
+        g.group_m = 16;
+        g.scale = a->logit_scale;
+        g.tgt = tgt_c;
+        g.P = reinterpret_cast<__half*>(PG);
+        g.ldP = V;
+        g.part = part;
+        g.n_tiles = w.n_tiles;
+        g.zy = zy;
+        if ((rc = launch_gemm<EPI_FWD, false, false>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
+                                                      stream)))
+            return rc;
+    }
+    // ---- K6 merge + loss terms + G (in place)
+    {
+        size_t smem = sizeof(float) * (size_t)w.n_tiles;
+        int grid = num_sms() * 8;
+        k_merge_g<<<grid, MERGE_THREADS, smem, stream>>>(
+            rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
+            a->clip_eps_low, a->clip_eps_high, PG, row_term, row_rho, row_logp, row_clip,
+            o->logp);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
+    }
+    // ---- K7 loss reduction (+ C2)
+    k_loss_reduce<<<1, 1024, 0, stream>>>(rows_dev, nglob_dev, row_term, row_rho, row_logp,
+                                          row_clip, o->loss, o->loss_stats, d_status);
+    count_launch();
+    AG_CUDA(cudaGetLastError());
+    if (comm) {
+        if ((rc = comm_allreduce_f64(comm, o->loss, 1, stream))) return rc;
+    }
+    // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff)
+    {
+        GemmArgs g{};
+        g.M_static = V;
+        g.N = d;
+        g.k_dev = rows_dev;
+        g.group_m = 1;
+        g.scale = a->logit_scale;
+        g.gw = o->grad_W;
+        g.ldo = d;
+        if ((rc = launch_gemm<EPI_GRADW, true, true>(mG_MN, mH_MN, g,
+                                                      ceil_div(V, GEMM_BM) * ceil_div(d, GEMM_BN),
+                                                      stream)))
+            return rc;
+    }
+    // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
+    SideStream* ss = nullptr;
+    if (comm && a->grad_W_mode == 1) {
+        ss = &side_stream();
+        AG_CUDA(cudaEventRecord(ss->e0, stream));
+        AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
+        if ((rc = comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s))) return rc;
+        AG_CUDA(cudaEventRecord(ss->e1, ss->s));
+    }
+    // ---- K8 grad_hidden = s G W   (M = T_eff, N = d, K = V), scattered to idx rows
+    {
+        GemmArgs g{};
+        g.m_dev = rows_dev;
+        g.N = d;
+        g.K_static = V;
+        g.group_m = 1;
+        g.scale = a->logit_scale;
+        g.idx = idx_dev;
+        g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
+        g.ldo = d;
+        if ((rc = launch_gemm<EPI_GRADH, false, true>(mG_K, mW_MN, g,
+                                                       max_m_tiles * ceil_div(d, GEMM_BN),
+                                                       stream)))
+            return rc;
+    }
+    if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
+    return AGENTRL_OK;
+}
+
+}  // namespace agentrl

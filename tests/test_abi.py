@@ -1,0 +1,92 @@
+"""Host-side checks (no GPU): the C-ABI library loads and exports every symbol that
+include/agentrl.h declares; the oracle and the CUDA path share no code; workspace
+planning is sane; the binding refuses to run without the library (no fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "agentrl.h")
+PKG = os.path.join(ROOT, "paper_2510_04206_b200")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(agentrl_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2510_04206_b200 import build
+    return build.build()
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    names = _declared()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+    import paper_2510_04206_b200 as ag
+    assert set(ag.EXPORTED) == set(names)
+
+
+def test_sm100a_code_in_library(libpath):
+    out = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out or "arch = sm_100a" in out
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert mnem in out, mnem  # tcgen05.mma, TMA loads, tcgen05.ld
+
+
+def test_host_calls_without_gpu(libpath):
+    import paper_2510_04206_b200 as ag
+    assert ag.lib().agentrl_version() == 100
+    assert ag.status_string(ag.ERR_WORKSPACE).startswith("workspace")
+    assert ag.status_string(ag.ST_NO_TOKENS).startswith("no loss-masked")
+    ws = ag.agentrl_grpo_step_workspace_size(131072, 640, 80, 5, 4096, 151552)
+    # P~/G buffer dominates: rows_cap * V * 2 bytes
+    assert ws >= 131072 * 151552 * 2
+    assert ws < 131072 * 151552 * 2 * 1.1
+    assert ag.agentrl_task_adv_norm_workspace_size(0, 0, 0, 1) > 0
+
+
+def test_oracle_and_product_share_no_code():
+    prod = []
+    for dp, _, fs in os.walk(PKG):
+        prod += [os.path.join(dp, f) for f in fs if f.endswith((".py", ".cu", ".cuh", ".h"))]
+    for p in prod:
+        s = open(p).read()
+        assert not re.search(r"^\s*(import|from)\s+oracle\b", s, re.M), p
+        assert "agentrl_oracle" not in s, p
+    for dp, _, fs in os.walk(os.path.join(ROOT, "oracle")):
+        for f in fs:
+            if f.endswith((".py", ".c", ".h")):
+                s = open(os.path.join(dp, f)).read()
+                code_lines = [ln for ln in s.splitlines()
+                              if re.match(r"\s*(#\s*include|import|from)\b", ln)]
+                for ln in code_lines:
+                    assert "paper_2510_04206_b200" not in ln and "agentrl.h" not in ln, (f, ln)
+                    assert "csrc" not in ln and "synth" not in ln, (f, ln)
+    s = open(os.path.join(ROOT, "synth", "__init__.py")).read()
+    assert "import oracle" not in s and "paper_2510_04206_b200" not in s
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    code = ("import sys, os, shutil; sys.path.insert(0, %r);"
+            "import importlib.util as u;"
+            "spec = u.spec_from_file_location('x', %r);"
+            "m = u.module_from_spec(spec);"
+            "m.__file__ = os.path.join(%r, '__init__.py');"
+            "spec.loader.exec_module(m)") % (ROOT, os.path.join(PKG, "__init__.py"), str(tmp_path))
+    # exec the binding with its __file__ pointing at an empty dir -> must raise ImportError
+    src = open(os.path.join(PKG, "__init__.py")).read()
+    fake = tmp_path / "__init__.py"
+    fake.write_text(src)
+    r = subprocess.run(["python", "-c", f"import runpy; runpy.run_path({str(fake)!r})"],
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr
+    del code
