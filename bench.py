@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: fused task-normalized GRPO LM-head loss fwd+bwd (agentrl_grpo_step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config glm9b] [--impl reference]
+
+One "step" = one agentrl_grpo_step over one synthetic batch (all section-8(a) rows:
+task advantage normalization, LM-head forward with the softmax epilogue, loss, grad_W,
+grad_hidden).  Rank 0 prints ONE JSON line.  For N > 1 launch with torchrun; each rank
+holds whole groups (LPT-balanced on masked tokens) of the same global batch (strong
+scaling) and the library all-reduces task statistics, the loss and grad_W over NCCL.
+
+value   = global packed tokens T / step time (max over ranks), inputs resident in HBM
+e2e     = same metric through the C ABI with the step's inputs copied from pinned host
+          memory each step and the loss/stats read back (copies inside the timed region)
+roofline: the dominant kernel's algorithmic FLOPs per launch / its CUDA-event duration
+          (recorded by the library on the launching stream during the timed region)
+cpu_baseline: the fp64 CPU oracle (test infrastructure) timed on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "fused GRPO loss fwd+bwd tokens/s"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="glm9b", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm=j.get("hbm_gbs", 6650.0), bf16=j.get("bf16_tflops", 1590.0),
+                    bf16_sus=j.get("bf16_tflops_sustained", 1400.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for k, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- inputs
+def build_inputs(cfg, rank, world):
+    """Global batch structure; this rank's shard (whole groups, LPT on masked tokens)."""
+    b = synth.make_structure(cfg)
+    if world > 1:
+        ng = np.zeros(len(b["task_id"]), np.int64)
+        off = b["traj_offsets"]
+        cs = np.concatenate([[0], np.cumsum(b["loss_mask"].astype(np.int64))])
+        ng = cs[off[1:]] - cs[off[:-1]]  # masked tokens per trajectory (input bookkeeping)
+        gtok = np.bincount(b["group_id"], weights=ng, minlength=b["n_groups"])
+        rog = synth.shard_groups_lpt(gtok, world)
+        lb = synth.shard_batch(b, rog, rank)
+    else:
+        lb = dict(b)
+    return b, lb
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+    return run_native(args, cfg, world, rank, local_rank)
+
+
+def run_native(args, cfg, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_04206_b200 as ag
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = ag.Comm.from_process_group() if world > 1 else None
+
+    gb, lb = build_inputs(cfg, rank, world)
+    T = int(lb["T"])
+    d, V = cfg.d, cfg.V
+    n_traj = len(lb["task_id"])
+    # ---- device-resident weights (generated on device, seeded: not a step input)
+    g = torch.Generator(device=dev)
+    g.manual_seed(synth.SEED_BASE + 77)
+    W = (torch.randn(V, d, generator=g, device=dev) * (3.0 / math.sqrt(d))).to(torch.bfloat16)
+    # ---- this rank's step inputs on host (pinned), seeded per rank
+    rng = np.random.default_rng(synth.SEED_BASE + 1000 * (rank + 1) + cfg.index)
+    hid = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+    gh = torch.Generator(device=dev)
+    gh.manual_seed(synth.SEED_BASE + 4242 + rank)
+    hid.copy_(torch.randn(T, d, generator=gh, device=dev).to(torch.bfloat16))
+    target = torch.from_numpy(rng.integers(0, V, size=T).astype(np.int32)).to(dev)
+    # planted 5% of masked rows: h = a W_y / |W_y|^2 + 0.5 noise (input generation)
+    mrows = np.nonzero(lb["loss_mask"])[0]
+    pr = torch.from_numpy(rng.choice(mrows, size=int(0.05 * len(mrows)), replace=False)).to(dev)
+    wy = W[target[pr].long()].float()
+    hid[pr] = (24.0 * wy / (wy * wy).sum(1, keepdim=True) + 0.5 * hid[pr].float()).to(torch.bfloat16)
+    bd = {k: (torch.from_numpy(np.ascontiguousarray(v)).to(dev) if isinstance(v, np.ndarray) else v)
+          for k, v in lb.items() if k != "token_index"}
+    bd["traj_offsets"] = bd["traj_offsets"].to(torch.int64)
+    for k in ("task_id", "group_id"):
+        bd[k] = bd[k].to(torch.int32)
+    bd["rewards"] = bd["rewards"].to(torch.float32)
+    bd["loss_mask"] = bd["loss_mask"].to(torch.uint8)
+    step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm)
+    # behaviour log-probs: one untimed forward (old = 0), then old = logp + delta
+    old = torch.zeros(T, dtype=torch.float32, device=dev)
+    step(bd, hid, W, target, old)
+    torch.cuda.synchronize()
+    delta = torch.from_numpy(synth.make_deltas(T, synth.SEED_BASE + 9 + rank).astype(np.float32))
+    old = (step.logp + delta.to(dev)) * bd["loss_mask"].float()
+    T_eff_local = int(lb["loss_mask"].astype(bool).sum())
+    T_eff_global = int(gb["loss_mask"].astype(bool).sum())
+    T_global = int(gb["T"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def one_step():
+        step(bd, hid, W, target, old)
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        one_step()
+    torch.cuda.synchronize()
+    launches_per_step = ag.last_launch_count()
+
+    # ---- timed region (device time, CUDA events, max over ranks)
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    ag.profile_start(64 * max(args.steps, 1))
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        one_step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    prof = ag.profile_stop()
+    clocks = clk.stop()
+    status = int(step.status.item())
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = T_global / (ms / 1e3)
+
+    # ---- e2e: host buffers through the C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hid_h = hid.cpu().pin_memory()
+        tgt_h = target.cpu().pin_memory()
+        old_h = old.cpu().pin_memory()
+        meta_h = {k: bd[k].cpu().pin_memory() for k in
+                  ("traj_offsets", "task_id", "group_id", "rewards", "loss_mask")}
+        loss_h = torch.empty(5, dtype=torch.float64).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in [hid_h, tgt_h, old_h, *meta_h.values()])
+        d2h = loss_h.numel() * loss_h.element_size()
+        stats_dev = torch.empty(5, dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            hid.copy_(hid_h, non_blocking=True)
+            target.copy_(tgt_h, non_blocking=True)
+            old.copy_(old_h, non_blocking=True)
+            for k, v in meta_h.items():
+                bd[k].copy_(v, non_blocking=True)
+            one_step()
+            stats_dev[0:1].copy_(step.loss)
+            stats_dev[1:5].copy_(step.loss_stats)
+            loss_h.copy_(stats_dev, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            tt = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_e2e = float(tt.item())
+        e2e = {"value": T_global / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e}
+
+    # ---- roofline of the dominant kernel (events recorded by the library, same stream)
+    pk = peaks()
+    gemm_names = {"gemm_fwd", "gemm_grad_W", "gemm_grad_hidden"}
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    kernel_ms = {k: (v[0] / max(v[1], 1), v[1]) for k, v in prof.items() if v[1] > 0}
+    if dom_name in gemm_names and dom_n > 0:
+        flop = 2.0 * T_eff_local * V * d
+        achieved = flop / (dom_ms / dom_n / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved,
+                "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
+                "peak_kind": f"{pk['src']} sustained bf16 (kernel timed inside a long step)",
+                "frac_of_burst": achieved / pk["bf16"],
+                "flop_per_launch": flop, "traffic": traffic_from_profiles(args.config, dom_name)}
+    else:
+        roof = {"bound": "hbm", "kernel": dom_name, "achieved": None, "peak": pk["hbm"],
+                "unit": "GB/s", "frac": None, "traffic": None}
+    step_flop = 6.0 * T_eff_global * V * d
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name, "T": T_global, "T_eff": T_eff_global, "d": d, "V": V,
+                   "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
+                   "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
+                       T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
+        "masked_tokens_per_s": T_eff_global / (ms / 1e3),
+        "step_tflops_algorithmic": step_flop / (ms / 1e3) / 1e12,
+        "clocks": clocks, "e2e": e2e,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "roofline": roof, "kernel_ms": kernel_ms, "status": status,
+        "loss": float(step.loss.item()), "clip_frac": float(step.loss_stats[0].item()),
+    }
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        if not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline(cfg, gb, args.cpu_seconds)
+        print(json.dumps(result), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(config, kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    return j.get(config, {}).get(kernel)
+
+
+# --------------------------------------------------------------------------- oracle timing
+def cpu_baseline(cfg, gb, seconds=15.0, rows=None):
+    """fp64 CPU oracle (as it stands) on a bounded sample: full adv-norm of the batch +
+    the loss fwd+bwd of the first `rows` masked tokens at full V, d; extrapolated."""
+    import oracle
+    cores = oracle.num_threads()
+    t0 = time.perf_counter()
+    an = oracle.task_adv_norm(gb)
+    t_adv = time.perf_counter() - t0
+    d, V = cfg.d, cfg.V
+    # per-token oracle cost ~ 3*V*d fp64 MACs; pick rows to fit `seconds`
+    if rows is None:
+        rows = 1
+        rng = np.random.default_rng(1)
+        W = rng.standard_normal((V, d)) * (3.0 / math.sqrt(d))
+        h = rng.standard_normal((rows, d))
+        t1 = time.perf_counter()
+        oracle.policy_loss_fwd_bwd(h, W, np.zeros(rows, np.int32), np.ones(rows), np.zeros(rows),
+                                   np.ones(rows, np.uint8), rows)
+        per = time.perf_counter() - t1
+        rows = int(max(1, min(256, (seconds - per) / max(per, 1e-3))))
+    else:
+        rng = np.random.default_rng(1)
+        W = rng.standard_normal((V, d)) * (3.0 / math.sqrt(d))
+    h = rng.standard_normal((rows, d))
+    t1 = time.perf_counter()
+    oracle.policy_loss_fwd_bwd(h, W, rng.integers(0, V, size=rows).astype(np.int32),
+                               rng.standard_normal(rows), np.full(rows, -12.0),
+                               np.ones(rows, np.uint8), rows)
+    t_loss = time.perf_counter() - t1
+    n_eff = int(an["n_mask"])
+    t_step = t_adv + t_loss / rows * n_eff
+    return {"value": int(gb["T"]) / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"adv-norm on the full batch ({t_adv:.3f} s) + loss fwd+bwd of {rows} "
+                      f"masked tokens at full V={V}, d={d} ({t_loss:.2f} s), extrapolated to "
+                      f"{n_eff} masked tokens"}
+
+
+def run_reference(args, cfg, world, rank):
+    """Reference arm = the fp64 CPU oracle as it stands, on this box's host cores."""
+    if rank != 0:
+        return 0
+    gb = synth.make_structure(cfg)
+    samples = []
+    for i in range(max(args.warmup, 0) + args.steps):
+        cb = cpu_baseline(cfg, gb, seconds=min(args.cpu_seconds, 10.0), rows=2 if i else None)
+        if i >= args.warmup:
+            samples.append(cb)
+    v = statistics.median([s["value"] for s in samples])
+    ms = int(gb["T"]) / v * 1e3
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference", "config": {"workload": cfg.name, "T": int(gb["T"]), "d": cfg.d,
+                                           "V": cfg.V, "parallelism": "host cores"},
+           "cpu_baseline": dict(samples[-1], value=v),
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

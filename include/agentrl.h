@@ -196,6 +196,18 @@ int agentrl_version(void);                    /* major*10000 + minor*100 + patch
  * bench's gpu_launches claim). */
 int agentrl_last_launch_count(void);
 
+/* ---- per-kernel timing (CUDA events on the launching stream) -------------
+ * agentrl_profile_start(n) pre-creates 2n events and makes every following call
+ * record an event pair around each of its kernels (on the stream it launches
+ * on), up to n pairs.  agentrl_profile_stop synchronises those events and
+ * writes, per kernel id, the summed milliseconds and the launch count.  Kernel
+ * ids: 0 count, 1 stats, 2 apply, 3 compact, 4 gather, 5 fwd GEMM, 6 merge+G,
+ * 7 loss reduce, 8 grad_W GEMM, 9 grad_hidden GEMM. */
+#define AGENTRL_NUM_KERNEL_IDS 10
+int agentrl_profile_start(int max_pairs);
+int agentrl_profile_stop(double* host_ms_sum, int* host_counts, int n_ids);
+const char* agentrl_kernel_name(int id);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,7 +38,9 @@ EXPORTED = (
     "agentrl_grpo_step_workspace_size", "agentrl_grpo_step",
     "agentrl_comm_unique_id", "agentrl_comm_init", "agentrl_comm_destroy",
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
+    "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
 )
+NUM_KERNEL_IDS = 10
 
 
 class Batch(C.Structure):
@@ -80,6 +82,10 @@ _lib.agentrl_status_string.argtypes = [C.c_int]
 _lib.agentrl_status_string.restype = C.c_char_p
 _lib.agentrl_version.restype = C.c_int
 _lib.agentrl_last_launch_count.restype = C.c_int
+_lib.agentrl_profile_start.argtypes = [C.c_int]
+_lib.agentrl_profile_stop.argtypes = [_P, _P, C.c_int]
+_lib.agentrl_kernel_name.argtypes = [C.c_int]
+_lib.agentrl_kernel_name.restype = C.c_char_p
 
 
 def lib():
@@ -166,6 +172,22 @@ def agentrl_grpo_step(batch: Batch, eps_std, args: LossArgs, out: LossOut, adv_t
 
 def last_launch_count() -> int:
     return int(_lib.agentrl_last_launch_count())
+
+
+def profile_start(max_pairs: int = 4096) -> None:
+    """Record a CUDA-event pair around every kernel the library launches (on the stream
+    it launches on) until profile_stop()."""
+    _check(_lib.agentrl_profile_start(int(max_pairs)), "agentrl_profile_start")
+
+
+def profile_stop() -> dict:
+    """{kernel name: (summed ms, launches)} since profile_start()."""
+    ms = (C.c_double * NUM_KERNEL_IDS)()
+    cnt = (C.c_int * NUM_KERNEL_IDS)()
+    _check(_lib.agentrl_profile_stop(C.cast(ms, C.c_void_p), C.cast(cnt, C.c_void_p),
+                                     NUM_KERNEL_IDS), "agentrl_profile_stop")
+    return {_lib.agentrl_kernel_name(i).decode(): (float(ms[i]), int(cnt[i]))
+            for i in range(NUM_KERNEL_IDS)}
 
 
 def alloc_workspace(nbytes: int, device="cuda"):

@@ -427,21 +427,26 @@ int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, doub
     AG_CUDA(cudaMemsetAsync(ws + w.n_g, 0, w.chunk_cnt - w.n_g, stream));
     AG_CUDA(cudaMemsetAsync(ws + w.stats, 0, (w.meta + 4 * sizeof(int64_t)) - w.stats, stream));
     if (n_chunks > 0) {
+        ProfScope ps(KID_COUNT, stream);
         k_count<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(
             T, b->n_traj, b->n_groups, b->traj_offsets, b->group_id, b->loss_mask, n_g, chunk,
             grp_cnt);
         count_launch();
     }
+    {
+    ProfScope ps(KID_STATS, stream);
     k_stats<<<1, STATS_THREADS, 0, stream>>>(T, b->n_traj, b->n_groups, b->n_tasks, n_chunks,
                                              b->traj_offsets, b->task_id, b->group_id, b->rewards,
                                              eps_std, n_g, chunk, grp_cnt, grp_start, grp_fill,
                                              members, adv_hat, stats, meta, d_status);
+    }
     count_launch();
     AG_CUDA(cudaGetLastError());
     if (comm) {
         int rc = comm_allreduce_f64(comm, stats, (size_t)3 * b->n_tasks, stream);
         if (rc != AGENTRL_OK) return rc;
     }
+    ProfScope ps_apply(KID_APPLY, stream);
     if (n_chunks > 0) {
         k_apply<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(
             T, b->n_traj, b->n_tasks, b->traj_offsets, b->task_id, b->loss_mask, adv_hat, stats,

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -13,6 +14,39 @@ namespace agentrl {
 
 static thread_local int g_launches = 0;
 void count_launch(int n) { g_launches += n; }
+
+// ---------------------------------------------------------------------------- profiling
+struct ProfRec {
+    int kid;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<cudaEvent_t> g_prof_pool;
+static std::vector<ProfRec> g_prof_recs;
+static size_t g_prof_next = 0;
+static int g_prof_open[KID_N];
+
+void prof_mark(int kid, bool begin, cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (begin) {
+        if (g_prof_next + 2 > g_prof_pool.size()) {
+            g_prof_open[kid] = -1;
+            return;
+        }
+        ProfRec r{kid, g_prof_pool[g_prof_next], g_prof_pool[g_prof_next + 1]};
+        g_prof_next += 2;
+        cudaEventRecord(r.a, s);
+        g_prof_open[kid] = (int)g_prof_recs.size();
+        g_prof_recs.push_back(r);
+    } else {
+        const int i = g_prof_open[kid];
+        if (i < 0) return;
+        cudaEventRecord(g_prof_recs[i].b, s);
+        g_prof_open[kid] = -1;
+    }
+}
 
 int num_sms() {
     static int n = 0;
@@ -263,6 +297,55 @@ const char* agentrl_status_string(int code) {
 }
 
 int agentrl_version(void) { return 100; }
+
+int agentrl_profile_start(int max_pairs) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (max_pairs <= 0) return AGENTRL_ERR_INVALID_ARG;
+    for (auto e : g_prof_pool) cudaEventDestroy(e);
+    g_prof_pool.assign(2 * (size_t)max_pairs, nullptr);
+    for (auto& e : g_prof_pool)
+        if (cudaEventCreate(&e) != cudaSuccess) return AGENTRL_ERR_CUDA;
+    g_prof_recs.clear();
+    g_prof_next = 0;
+    for (int k = 0; k < KID_N; ++k) g_prof_open[k] = -1;
+    g_prof_on = true;
+    return AGENTRL_OK;
+}
+
+int agentrl_profile_stop(double* ms_sum, int* counts, int n_ids) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = false;
+    for (int k = 0; k < n_ids; ++k) {
+        if (ms_sum) ms_sum[k] = 0.0;
+        if (counts) counts[k] = 0;
+    }
+    int rc = AGENTRL_OK;
+    for (auto& r : g_prof_recs) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) {
+            rc = AGENTRL_ERR_CUDA;
+            continue;
+        }
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
+            rc = AGENTRL_ERR_CUDA;
+            continue;
+        }
+        if (r.kid < n_ids) {
+            if (ms_sum) ms_sum[r.kid] += ms;
+            if (counts) counts[r.kid] += 1;
+        }
+    }
+    g_prof_recs.clear();
+    g_prof_next = 0;
+    return rc;
+}
+
+const char* agentrl_kernel_name(int id) {
+    static const char* names[KID_N] = {"k_count", "k_stats", "k_apply", "k_compact",
+                                       "k_gather", "gemm_fwd", "k_merge_g", "k_loss_reduce",
+                                       "gemm_grad_W", "gemm_grad_hidden"};
+    return (id >= 0 && id < KID_N) ? names[id] : "unknown";
+}
 int agentrl_last_launch_count(void) { return g_launches; }
 
 }  // extern "C"

@@ -75,6 +75,19 @@ int comm_allreduce_i64(agentrl_comm c, int64_t* buf, size_t n, cudaStream_t s);
 
 // launch counter for the bench's gpu_launches claim
 void count_launch(int n = 1);
+
+// per-kernel event timing (agentrl_profile_start/stop)
+enum KernelId {
+    KID_COUNT = 0, KID_STATS, KID_APPLY, KID_COMPACT, KID_GATHER, KID_FWD, KID_MERGE,
+    KID_REDUCE, KID_GRADW, KID_GRADH, KID_N
+};
+void prof_mark(int kid, bool begin, cudaStream_t s);
+struct ProfScope {
+    int kid;
+    cudaStream_t s;
+    ProfScope(int k, cudaStream_t st) : kid(k), s(st) { prof_mark(kid, true, s); }
+    ~ProfScope() { prof_mark(kid, false, s); }
+};
 int num_sms();
 int check_device();  // AGENTRL_OK or AGENTRL_ERR_UNSUPPORTED / _CUDA
 

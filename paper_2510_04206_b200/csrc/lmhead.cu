@@ -66,6 +66,7 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 template <int EPI, bool A_MN, bool B_MN>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream) {
+    ProfScope ps(EPI == EPI_FWD ? KID_FWD : (EPI == EPI_GRADW ? KID_GRADW : KID_GRADH), stream);
     auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -415,6 +416,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         int32_t* chunk = reinterpret_cast<int32_t*>(ws + w.chunk_cnt);
         AG_CUDA(cudaMemsetAsync(meta, 0, 4 * sizeof(int64_t), stream));
         if (n_chunks > 0) {
+            ProfScope ps(KID_COMPACT, stream);
             k_mask_count<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, chunk);
             k_chunk_scan<<<1, 32, 0, stream>>>(n_chunks, chunk, meta);
             k_compact<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, a->adv_tok,
@@ -434,6 +436,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     // ---- K4 gather
     {
         int grid = num_sms() * 4;
+        ProfScope ps(KID_GATHER, stream);
         k_gather<<<grid, 256, 0, stream>>>(rows_dev, T, d, V,
                                            reinterpret_cast<const __nv_bfloat16*>(a->hidden),
                                            a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
@@ -475,6 +478,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     {
         size_t smem = sizeof(float) * (size_t)w.n_tiles;
         int grid = num_sms() * 8;
+        ProfScope ps(KID_MERGE, stream);
         k_merge_g<<<grid, MERGE_THREADS, smem, stream>>>(
             rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
             a->clip_eps_low, a->clip_eps_high, PG, row_term, row_rho, row_logp, row_clip,
@@ -483,8 +487,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         AG_CUDA(cudaGetLastError());
     }
     // ---- K7 loss reduction (+ C2)
-    k_loss_reduce<<<1, 1024, 0, stream>>>(rows_dev, nglob_dev, row_term, row_rho, row_logp,
-                                          row_clip, o->loss, o->loss_stats, d_status);
+    {
+        ProfScope ps(KID_REDUCE, stream);
+        k_loss_reduce<<<1, 1024, 0, stream>>>(rows_dev, nglob_dev, row_term, row_rho, row_logp,
+                                              row_clip, o->loss, o->loss_stats, d_status);
+    }
     count_launch();
     AG_CUDA(cudaGetLastError());
     if (comm) {
