@@ -14,7 +14,8 @@
 // contiguous; boxes {64 (MN), 64 (K)} stacked along MN, LBO = 8 KB between 64-wide atoms).
 //
 // Epilogues (row r = output row, 256 columns per tile):
-//   EPI_FWD   logits z = s*acc: per (row, tile) max m and l = sum exp(z-m) over valid columns,
+//   EPI_FWD   logits z = s*acc: per (row, tile) max m and l' = sum exp(z-m) - 1 over valid
+//             columns (the first max element is left out of the sum: no cancellation later),
 //             P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls in the
 //             tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
 //   EPI_GRADH grad_hidden[idx[r], :] = bf16(s * acc)   (scatter to the original token row)
@@ -231,10 +232,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     for (int j = 0; j < 32; ++j)
                         if (c * 32 + j < ncol) m = fmaxf(m, s * __uint_as_float(r[j]));
                 }
-                // pass 2: P~ = exp(z - m), l = sum P~, z_y
+                // pass 2: P~ = exp(z - m), l' = sum P~ - 1 (the first max element is left out
+                // of the sum instead of subtracting 1 afterwards, so l' keeps full relative
+                // precision when the tile max dominates -- p_y close to 1), z_y
                 const int32_t y = row_ok ? p.tgt[row] : -1;
                 const int32_t yl = y - col0;
                 float l = 0.f;
+                bool max_seen = false;
                 const float mb = m * LOG2E;
                 __half* prow = p.P + (row_ok ? row : 0) * p.ldP + col0;
 #pragma unroll 1
@@ -247,7 +251,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         const float z = s * __uint_as_float(r[j]);
                         const bool ok = c * 32 + j < ncol;
                         e[j] = ok ? ex2_approx(fmaf(z, LOG2E, -mb)) : 0.f;
-                        l += e[j];
+                        const bool is_max = ok && !max_seen && z == m;
+                        max_seen |= is_max;
+                        if (is_max) e[j] = 1.f;
+                        l += is_max ? 0.f : e[j];
                         if (c * 32 + j == yl && row_ok) p.zy[row] = z;
                     }
                     if (row_ok) {

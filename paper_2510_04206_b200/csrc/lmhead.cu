@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(MERGE_THREADS)
               float* __restrict__ logp_out) {
     extern __shared__ float s_f[];  // [n_tiles] scale per tile
     __shared__ float s_red[MERGE_THREADS / 32];
-    __shared__ float s_bc[2];
+    __shared__ int s_jm[MERGE_THREADS / 32];
+    __shared__ float s_bc[3];
     const int64_t rows = *rows_dev;
     const int64_t rows_pad = (rows + 63) / 64 * 64;
     const double Nd = (double)*nglob_dev;
@@ -228,21 +229,32 @@ __global__ void __launch_bounds__(MERGE_THREADS)
         }
         __syncthreads();
         const float M = s_bc[0];
+        // first tile holding the row max (its l' enters without the leading 1)
+        int jloc = 0x7fffffff;
+        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
+            if (pr[j].x == M) jloc = min(jloc, j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) jloc = min(jloc, __shfl_xor_sync(0xffffffffu, jloc, o));
+        __syncthreads();
+        if (lane == 0) s_jm[wid] = jloc;
+        __syncthreads();
+        int jM = s_jm[0];
+        for (int w = 1; w < MERGE_THREADS / 32; ++w) jM = min(jM, s_jm[w]);
+        // L' = sum_v exp(z_v - M) - 1 = l'_{jM} + sum_{j != jM} (1 + l'_j) exp(m_j - M)
         float lloc = 0.f;
         for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS) {
             const float2 ml = pr[j];
-            lloc += ml.y * ex2_approx((ml.x - M) * LOG2E);
+            lloc += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lloc += __shfl_xor_sync(0xffffffffu, lloc, o);
-        __syncthreads();
         if (lane == 0) s_red[wid] = lloc;
         __syncthreads();
         float c_t = 0.f;
         if (threadIdx.x == 0) {
-            float L = 0.f;
-            for (int w = 0; w < MERGE_THREADS / 32; ++w) L += s_red[w];
-            const float lse = M + logf(L);
+            float Lm1 = 0.f;
+            for (int w = 0; w < MERGE_THREADS / 32; ++w) Lm1 += s_red[w];
+            const float lse = M + log1pf(Lm1);
             const float logp = zy[p] - lse;
             const float A = adv_c[p];
             const float rho = expf(logp - old_c[p]);
@@ -259,10 +271,13 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             if (logp_out) logp_out[idx[p]] = logp;
             s_bc[0] = lse;
             s_bc[1] = c_t;
+            // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
+            s_bc[2] = c_t * expm1f(logp);
         }
         __syncthreads();
         const float lse = s_bc[0];
         c_t = s_bc[1];
+        const float g_y = s_bc[2];
         for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
             s_f[j] = c_t * ex2_approx((pr[j].x - lse) * LOG2E);
         __syncthreads();
@@ -279,7 +294,9 @@ __global__ void __launch_bounds__(MERGE_THREADS)
                 g[2 * k] = f * x.x;
                 g[2 * k + 1] = f * x.y;
             }
-            if (y >= v0 && y < v0 + 8) g[y - v0] -= c_t;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (v0 + k == y) g[k] = g_y;
             uint4 out;
             out.x = pack_bf162(g[0], g[1]);
             out.y = pack_bf162(g[2], g[3]);

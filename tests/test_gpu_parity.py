@@ -228,7 +228,12 @@ def _full_size_case(ag, cfg_name, n_spot=24):
     logp = step.logp.cpu().numpy()
     gh = step.grad_hidden.float().cpu().numpy()
     rng = np.random.default_rng(5)
-    rows = np.sort(rng.choice(an["idx"], size=n_spot, replace=False))
+    rows = rng.choice(an["idx"], size=n_spot, replace=False)
+    # always include rows where p_y is close to 1 (planted: |h| far above the bulk), the
+    # onehot-cancellation case
+    hn = np.abs(f64(hb[an["idx"]])).max(1)
+    planted = an["idx"][np.argsort(-hn)[:4]]
+    rows = np.unique(np.concatenate([rows, planted]))
     Wf = f64(Wb)
     h_rows = f64(hb[rows])
     r = oracle.policy_loss_rows(h_rows, Wf, y[rows], an["adv_tok"][rows].astype(np.float32)
