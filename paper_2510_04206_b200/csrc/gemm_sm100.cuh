@@ -1,19 +1,26 @@
 // gemm_sm100.cuh -- persistent, warp-specialised tcgen05 GEMM for sm_100a with the three
 // fused epilogues of the LM-head loss path.
 //
-//   D[BM x BN] (fp32, TMEM) = sum_k A[BM x BK] * B[BN x BK]^T, bf16 operands staged by TMA
-//   (SWIZZLE_128B) through a STAGES-deep shared-memory ring; one elected thread issues
-//   tcgen05.mma (M=128, N=256, K=16); two TMEM accumulators (2 x 256 columns) let the
-//   epilogue of tile i overlap the MMAs of tile i+1.
+//   D (fp32, TMEM) = sum_k A * B^T, bf16 operands staged by TMA (SWIZZLE_128B) through a
+//   STAGES-deep shared-memory ring; one elected thread issues tcgen05.mma (K=16); two TMEM
+//   accumulators (2 x 256 fp32 columns) let the epilogue of tile i overlap the MMAs of tile
+//   i+1.
+//
+//   PAIR = true  (default): a CTA pair (cluster of 2, cta_group::2) computes a 256 x 256 tile.
+//                Each CTA stages 128 rows of A and 128 rows (half) of B per k-block; the
+//                leader CTA issues tcgen05.mma.cta_group::2 (M=256, N=256) and commits to
+//                both CTAs' barriers; TMA bytes of both CTAs complete on the leader's full
+//                barrier.  Per SM this halves B's shared-memory and L2->SM traffic.
+//   PAIR = false: one CTA computes a 128 x 256 tile with cta_group::1 (kept for A/B tests).
 //
 //   warp 0      : TMA producer (one lane)
-//   warp 1      : TMEM allocator + MMA issuer (one lane)
+//   warp 1      : TMEM allocator + MMA issuer (one lane, leader CTA)
 //   warps 2..5  : epilogue; warp w reads TMEM lanes 32*(w%4) .. +31 (row = lane)
 //
 // Operand majors: A/B either K-major (K contiguous; one TMA box {64, rows}) or MN-major (MN
 // contiguous; boxes {64 (MN), 64 (K)} stacked along MN, LBO = 8 KB between 64-wide atoms).
 //
-// Epilogues (row r = output row, 256 columns per tile):
+// Epilogues (row r = output row; each CTA owns 128 rows x 256 columns of the tile):
 //   EPI_FWD   logits z = s*acc: per (row, tile) max m and l' = sum exp(z-m) - 1 over valid
 //             columns (the first max element is left out of the sum: no cancellation later),
 //             P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls in the
@@ -25,15 +32,21 @@
 
 namespace agentrl {
 
-constexpr int GEMM_BM = 128;
-constexpr int GEMM_BN = 256;
+constexpr int GEMM_BM = 128;  // rows per CTA
+constexpr int GEMM_BN = 256;  // columns per tile
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_STAGES = 4;
 constexpr int GEMM_THREADS = 192;
 constexpr int GEMM_A_STAGE = GEMM_BM * GEMM_BK * 2;  // 16 KB
-constexpr int GEMM_B_STAGE = GEMM_BN * GEMM_BK * 2;  // 32 KB
-constexpr int GEMM_SMEM_BYTES =
-    GEMM_STAGES * (GEMM_A_STAGE + GEMM_B_STAGE) + 1024 /*barriers*/ + 1024 /*align slack*/;
+
+template <bool PAIR>
+struct GemmCfg {
+    static constexpr int B_ROWS = PAIR ? GEMM_BN / 2 : GEMM_BN;   // B rows staged per CTA
+    static constexpr int B_STAGE = B_ROWS * GEMM_BK * 2;          // 16 KB / 32 KB
+    static constexpr int STAGES = PAIR ? 6 : 4;
+    static constexpr int TILE_M = PAIR ? 2 * GEMM_BM : GEMM_BM;   // rows per tile
+    static constexpr int SMEM = STAGES * (GEMM_A_STAGE + B_STAGE) + 1024 + 1024;
+    static constexpr int TX_BYTES = (GEMM_A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
+};
 
 enum { EPI_FWD = 0, EPI_GRADH = 1, EPI_GRADW = 2 };
 
@@ -45,12 +58,13 @@ struct GemmArgs {
     int64_t K_static;
     const int64_t* k_dev;
     int32_t group_m;  // raster: tiles grouped by group_m row-blocks, columns fastest inside
+    int32_t pol_a, pol_b;  // L2 policy per operand: 0 normal, 1 evict_first, 2 evict_last
     float scale;      // logit_scale s
     // EPI_FWD
     const int32_t* tgt;  // [rows] target token of each compacted row
-    __half* P;           // [rows, ldP] exp(z - m_tile), fp16
+    __half* P;           // [rows, ldP] exp(z - m), fp16
     int64_t ldP;
-    float2* part;  // [rows, n_tiles] (m, l)
+    float2* part;  // [rows, n_tiles] (m, l')
     int32_t n_tiles;
     float* zy;  // [rows]
     // EPI_GRADH
@@ -72,40 +86,49 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t
     n_blk = local / gm;
 }
 
-template <int EPI, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+__device__ __forceinline__ uint64_t make_policy(int which) {
+    return which == 1 ? policy_evict_first() : (which == 2 ? policy_evict_last() : policy_evict_normal());
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool PAIR>
+__device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                          const GemmArgs& p) {
+    using Cfg = GemmCfg<PAIR>;
+    constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + GEMM_STAGES * GEMM_A_STAGE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + GEMM_STAGES * GEMM_B_STAGE);
+    uint8_t* sB = smem + STAGES * GEMM_A_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_STAGE);
     uint64_t* full = bars;
-    uint64_t* empty = bars + GEMM_STAGES;
-    uint64_t* tfull = bars + 2 * GEMM_STAGES;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int64_t unit = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t n_units = PAIR ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
     const int64_t M = p.m_dev ? *p.m_dev : p.M_static;
     const int64_t K = p.k_dev ? *p.k_dev : p.K_static;
-    const int64_t num_m = (M + GEMM_BM - 1) / GEMM_BM;
+    const int64_t num_m = (M + Cfg::TILE_M - 1) / Cfg::TILE_M;
     const int64_t num_n = (p.N + GEMM_BN - 1) / GEMM_BN;
     const int64_t num_tiles = num_m * num_n;
     const int64_t num_kb = (K + GEMM_BK - 1) / GEMM_BK;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < GEMM_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], PAIR ? 8 : 4);  // one arrive per epilogue warp (x2 CTAs)
         }
         fence_mbar_init();
         fence_proxy_async_smem();
@@ -114,47 +137,70 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            const uint64_t pol_a = policy_evict_normal();
-            const uint64_t pol_b = policy_evict_normal();
+            const uint64_t pol_a = make_policy(p.pol_a);
+            const uint64_t pol_b = make_policy(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
-                const int32_t m0 = (int32_t)(m_blk * GEMM_BM);
-                const int32_t n0 = (int32_t)(n_blk * GEMM_BN);
+                const int32_t m0 = (int32_t)(m_blk * Cfg::TILE_M + rank * GEMM_BM);
+                const int32_t n0 = (int32_t)(n_blk * GEMM_BN + rank * Cfg::B_ROWS);
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], GEMM_A_STAGE + GEMM_B_STAGE);
                     const int32_t k0 = (int32_t)(kb * GEMM_BK);
                     uint8_t* a_dst = sA + stage * GEMM_A_STAGE;
-                    uint8_t* b_dst = sB + stage * GEMM_B_STAGE;
-                    if (!A_MN) {
-                        tma_load_2d(&tmA, &full[stage], a_dst, k0, m0, pol_a);
-                    } else {
+                    uint8_t* b_dst = sB + stage * Cfg::B_STAGE;
+                    if constexpr (PAIR) {
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (leader) mbar_arrive_expect_tx_cluster(fb, Cfg::TX_BYTES);
+                        if (!A_MN) {
+                            tma_load_2d_pair(&tmA, fb, a_dst, k0, m0, pol_a);
+                        } else {
 #pragma unroll
-                        for (int i = 0; i < GEMM_BM / 64; ++i)
-                            tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + i * 64, k0,
-                                        pol_a);
-                    }
-                    if (!B_MN) {
-                        tma_load_2d(&tmB, &full[stage], b_dst, k0, n0, pol_b);
-                    } else {
+                            for (int i = 0; i < GEMM_BM / 64; ++i)
+                                tma_load_2d_pair(&tmA, fb, a_dst + i * 8192, m0 + i * 64, k0, pol_a);
+                        }
+                        if (!B_MN) {
+                            tma_load_2d_pair(&tmB, fb, b_dst, k0, n0, pol_b);
+                        } else {
 #pragma unroll
-                        for (int i = 0; i < GEMM_BN / 64; ++i)
-                            tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + i * 64, k0,
-                                        pol_b);
+                            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
+                                tma_load_2d_pair(&tmB, fb, b_dst + i * 8192, n0 + i * 64, k0, pol_b);
+                        }
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
+                        if (!A_MN) {
+                            tma_load_2d(&tmA, &full[stage], a_dst, k0, m0, pol_a);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < GEMM_BM / 64; ++i)
+                                tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + i * 64, k0,
+                                            pol_a);
+                        }
+                        if (!B_MN) {
+                            tma_load_2d(&tmB, &full[stage], b_dst, k0, n0, pol_b);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
+                                tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + i * 64, k0,
+                                            pol_b);
+                        }
                     }
-                    if (++stage == GEMM_STAGES) {
+                    if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -164,13 +210,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(GEMM_BM, GEMM_BN, A_MN, B_MN);
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, GEMM_BN, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_BN);
@@ -178,7 +224,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sA + stage * GEMM_A_STAGE);
-                    const uint32_t b_base = smem_u32(sB + stage * GEMM_B_STAGE);
+                    const uint32_t b_base = smem_u32(sB + stage * Cfg::B_STAGE);
 #pragma unroll
                     for (int k = 0; k < GEMM_BK / 16; ++k) {
                         const uint64_t adesc =
@@ -187,15 +233,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         const uint64_t bdesc =
                             B_MN ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
                                  : umma_desc_sw128(b_base + k * 32, 16, 1024);
-                        tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                        const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                        if constexpr (PAIR) tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, accum);
+                        else tc_mma_f16(d_tmem, adesc, bdesc, idesc, accum);
                     }
-                    tc_commit(&empty[stage]);
-                    if (++stage == GEMM_STAGES) {
+                    if constexpr (PAIR) tc_commit_pair_mc(&empty[stage], 0x3);
+                    else tc_commit(&empty[stage]);
+                    if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit(&tfull[acc]);
+                if constexpr (PAIR) tc_commit_pair_mc(&tfull[acc], 0x3);
+                else tc_commit(&tfull[acc]);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -205,12 +255,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint32_t tempty_leader0 = 0u, tempty_leader1 = 0u;
+        if constexpr (PAIR) {
+            tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+            tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+        }
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
             int64_t m_blk, n_blk;
             tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
-            const int64_t row = m_blk * GEMM_BM + q * 32 + lane;
+            const int64_t row = m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
             const bool row_ok = row < M;
             const int32_t col0 = (int32_t)(n_blk * GEMM_BN);
             const int32_t ncol = min(GEMM_BN, p.N - col0);  // valid columns in this tile
@@ -325,7 +380,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                else mbar_arrive(&tempty[acc]);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -333,8 +392,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // peer done with TMEM / remote barriers before teardown
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem_base, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_dealloc_pair(tmem_base, 512);
+        else tmem_dealloc(tmem_base, 512);
+    }
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+    gemm_body<EPI, A_MN, B_MN, true>(tmA, tmB, p);
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+    gemm_body<EPI, A_MN, B_MN, false>(tmA, tmB, p);
 }
 
 }  // namespace agentrl

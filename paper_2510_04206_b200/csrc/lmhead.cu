@@ -63,19 +63,43 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS ? AGENTRL_OK : AGENTRL_ERR_CUDA;
 }
 
+// CTA-pair (cta_group::2) GEMMs unless AGENTRL_GEMM_PAIR=0 (1-CTA variant, for A/B runs)
+static bool gemm_use_pair() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("AGENTRL_GEMM_PAIR");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int EPI, bool A_MN, bool B_MN>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream) {
     ProfScope ps(EPI == EPI_FWD ? KID_FWD : (EPI == EPI_GRADW ? KID_GRADW : KID_GRADH), stream);
-    auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     GEMM_SMEM_BYTES));
-        attr_done = true;
+    // max_tiles is counted in 128-row tiles; a CTA pair covers 256 rows.
+    if (gemm_use_pair()) {
+        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN>;
+        constexpr int smem = GemmCfg<true>::SMEM;
+        static bool attr_done = false;  // per instantiation
+        if (!attr_done) {
+            AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_done = true;
+        }
+        int64_t grid = std::min<int64_t>(num_sms() & ~1, std::max<int64_t>(max_tiles, 2));
+        grid &= ~int64_t(1);
+        kern<<<(unsigned)grid, GEMM_THREADS, smem, stream>>>(a, b, g);
+    } else {
+        auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
+        constexpr int smem = GemmCfg<false>::SMEM;
+        static bool attr_done = false;
+        if (!attr_done) {
+            AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_done = true;
+        }
+        int grid = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(max_tiles, 1));
+        kern<<<grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     }
-    int grid = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(max_tiles, 1));
-    kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(a, b, g);
     count_launch();
     AG_CUDA(cudaGetLastError());
     return AGENTRL_OK;
@@ -467,7 +491,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     int rc;
     if ((rc = make_map(&mH_K, H, d, rows_cap, d, 64, 128))) return rc;
     if ((rc = make_map(&mH_MN, H, d, rows_cap, d, 64, 64))) return rc;
-    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, 256))) return rc;
+    // K-major B box = the B rows one CTA stages (128 in a CTA pair, 256 alone)
+    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, gemm_use_pair() ? 128 : 256))) return rc;
     if ((rc = make_map(&mW_MN, a->W_head, d, V, d, 64, 64))) return rc;
     if ((rc = make_map(&mG_K, PG, V, rows_cap, V, 64, 128))) return rc;
     if ((rc = make_map(&mG_MN, PG, V, rows_cap, V, 64, 64))) return rc;
