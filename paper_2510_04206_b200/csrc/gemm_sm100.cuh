@@ -166,7 +166,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     uint8_t* b_dst = sB + stage * Cfg::B_STAGE;
                     if constexpr (PAIR) {
                         const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (leader) mbar_arrive_expect_tx_cluster(fb, Cfg::TX_BYTES);
+                        // leader: arm its own full barrier for both CTAs' bytes (CTA scope; the
+                        // peer's TMA completes its bytes on it directly)
+                        if (leader) mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
                         if (!A_MN) {
                             tma_load_2d_pair(&tmA, fb, a_dst, k0, m0, pol_a);
                         } else {

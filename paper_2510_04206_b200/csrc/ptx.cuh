@@ -172,8 +172,9 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
     return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    // CUTLASS ClusterBarrier::arrive(cta_id) form (default .release at .cta scope: no GPU-scope
+    // fence is emitted; TMEM reads are ordered by tcgen05.fence::before_thread_sync)
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA load: data lands in this CTA's smem, transaction bytes complete on the barrier at
 // `bar_cluster` (the leader CTA's full barrier).
