@@ -2,16 +2,20 @@
 // fused epilogues of the LM-head loss path.
 //
 //   D (fp32, TMEM) = sum_k A * B^T, bf16 operands staged by TMA (SWIZZLE_128B) through a
-//   STAGES-deep shared-memory ring; one elected thread issues tcgen05.mma (K=16); two TMEM
-//   accumulators (2 x 256 fp32 columns) let the epilogue of tile i overlap the MMAs of tile
-//   i+1.
+//   STAGES-deep shared-memory ring; one elected thread issues tcgen05.mma (K=16).
 //
-//   PAIR = true  (default): a CTA pair (cluster of 2, cta_group::2) computes a 256 x 256 tile.
-//                Each CTA stages 128 rows of A and 128 rows (half) of B per k-block; the
-//                leader CTA issues tcgen05.mma.cta_group::2 (M=256, N=256) and commits to
-//                both CTAs' barriers; TMA bytes of both CTAs complete on the leader's full
-//                barrier.  Per SM this halves B's shared-memory and L2->SM traffic.
-//   PAIR = false: one CTA computes a 128 x 256 tile with cta_group::1 (kept for A/B tests).
+//   PAIR = true  (default): a CTA pair (cluster of 2, cta_group::2) computes a 256-row tile.
+//                Each CTA stages 128 rows of A and half of B's rows per k-block; the leader
+//                CTA issues tcgen05.mma.cta_group::2 (M=256, N=256) and commits to both CTAs'
+//                barriers; TMA bytes of both CTAs complete on the leader's full barrier.
+//   PAIR = false: one CTA computes a 128-row tile with cta_group::1 (kept for A/B tests).
+//
+//   NSPLIT = 1: 256-column tiles, two TMEM accumulators (2 x 256 fp32 columns) so the
+//               epilogue of tile i overlaps the MMAs of tile i+1 (short-K GEMMs: forward).
+//   NSPLIT = 2: 512-column tiles (two N=256 MMAs per K step into one 512-column
+//               accumulator).  A third more MMA work per staged byte, half the re-reads of
+//               the shared operand; for the long-K backward GEMMs (K = V or T_eff) the
+//               un-overlapped epilogue is ~1% of a tile.
 //
 //   warp 0      : TMA producer (one lane)
 //   warp 1      : TMEM allocator + MMA issuer (one lane, leader CTA)
@@ -20,11 +24,11 @@
 // Operand majors: A/B either K-major (K contiguous; one TMA box {64, rows}) or MN-major (MN
 // contiguous; boxes {64 (MN), 64 (K)} stacked along MN, LBO = 8 KB between 64-wide atoms).
 //
-// Epilogues (row r = output row; each CTA owns 128 rows x 256 columns of the tile):
-//   EPI_FWD   logits z = s*acc: per (row, tile) max m and l' = sum exp(z-m) - 1 over valid
-//             columns (the first max element is left out of the sum: no cancellation later),
-//             P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls in the
-//             tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
+// Epilogues (row r = output row; each CTA owns 128 rows of the tile):
+//   EPI_FWD   logits z = s*acc: per (row, 256-col tile) max m and l' = sum exp(z-m) - 1 over
+//             valid columns (the first max element is left out of the sum: no cancellation
+//             later), P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls
+//             in the tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
 //   EPI_GRADH grad_hidden[idx[r], :] = bf16(s * acc)   (scatter to the original token row)
 //   EPI_GRADW grad_W[r, :] = s * acc (fp32); zeros if the (dynamic) K extent is 0.
 #pragma once
@@ -33,17 +37,21 @@
 namespace agentrl {
 
 constexpr int GEMM_BM = 128;  // rows per CTA
-constexpr int GEMM_BN = 256;  // columns per tile
+constexpr int GEMM_BN = 256;  // columns per MMA (and per FWD statistics tile)
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 192;
 constexpr int GEMM_A_STAGE = GEMM_BM * GEMM_BK * 2;  // 16 KB
 
-template <bool PAIR>
+template <bool PAIR, int NSPLIT>
 struct GemmCfg {
-    static constexpr int B_ROWS = PAIR ? GEMM_BN / 2 : GEMM_BN;   // B rows staged per CTA
-    static constexpr int B_STAGE = B_ROWS * GEMM_BK * 2;          // 16 KB / 32 KB
-    static constexpr int STAGES = PAIR ? 6 : 4;
-    static constexpr int TILE_M = PAIR ? 2 * GEMM_BM : GEMM_BM;   // rows per tile
+    static_assert(NSPLIT == 1 || (NSPLIT == 2 && PAIR), "512-column tiles need a CTA pair");
+    static constexpr int B_ROWS = PAIR ? GEMM_BN / 2 : GEMM_BN;  // B rows per CTA per MMA
+    static constexpr int B_HALF = B_ROWS * GEMM_BK * 2;          // bytes per MMA's B slice
+    static constexpr int B_STAGE = NSPLIT * B_HALF;
+    static constexpr int STAGES = PAIR ? (NSPLIT == 1 ? 6 : 4) : 4;
+    static constexpr int TILE_M = PAIR ? 2 * GEMM_BM : GEMM_BM;  // rows per tile
+    static constexpr int TILE_N = GEMM_BN * NSPLIT;              // columns per tile
+    static constexpr int ACC_BUFS = NSPLIT == 1 ? 2 : 1;
     static constexpr int SMEM = STAGES * (GEMM_A_STAGE + B_STAGE) + 1024 + 1024;
     static constexpr int TX_BYTES = (GEMM_A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
@@ -57,9 +65,9 @@ struct GemmArgs {
     int32_t N;
     int64_t K_static;
     const int64_t* k_dev;
-    int32_t group_m;  // raster: tiles grouped by group_m row-blocks, columns fastest inside
+    int32_t group_m;       // raster: tiles grouped by group_m row-blocks, columns fastest inside
     int32_t pol_a, pol_b;  // L2 policy per operand: 0 normal, 1 evict_first, 2 evict_last
-    float scale;      // logit_scale s
+    float scale;           // logit_scale s
     // EPI_FWD
     const int32_t* tgt;  // [rows] target token of each compacted row
     __half* P;           // [rows, ldP] exp(z - m), fp16
@@ -87,14 +95,58 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t
 }
 
 __device__ __forceinline__ uint64_t make_policy(int which) {
-    return which == 1 ? policy_evict_first() : (which == 2 ? policy_evict_last() : policy_evict_normal());
+    return which == 1 ? policy_evict_first()
+                      : (which == 2 ? policy_evict_last() : policy_evict_normal());
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool PAIR>
+template <int ACC_BUFS>
+__device__ __forceinline__ void advance_acc(int& acc, uint32_t& acc_phase) {
+    if constexpr (ACC_BUFS == 2) {
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+    } else {
+        acc_phase ^= 1;
+    }
+}
+
+// TMA loads of one k-block: A (128 rows of this CTA) and B (per MMA half: B_ROWS rows)
+template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT>
+__device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                           uint64_t* full_bar, uint32_t full_bar_leader,
+                                           uint8_t* a_dst, uint8_t* b_dst, int32_t m0,
+                                           int32_t n0, int32_t k0, uint64_t pol_a,
+                                           uint64_t pol_b) {
+    using Cfg = GemmCfg<PAIR, NSPLIT>;
+    auto ld = [&](const CUtensorMap& m, uint8_t* dst, int32_t x, int32_t y, uint64_t pol) {
+        if constexpr (PAIR) tma_load_2d_pair(&m, full_bar_leader, dst, x, y, pol);
+        else tma_load_2d(&m, full_bar, dst, x, y, pol);
+    };
+    if constexpr (!A_MN) {
+        ld(tmA, a_dst, k0, m0, pol_a);
+    } else {
+#pragma unroll
+        for (int i = 0; i < GEMM_BM / 64; ++i) ld(tmA, a_dst + i * 8192, m0 + i * 64, k0, pol_a);
+    }
+#pragma unroll
+    for (int h = 0; h < NSPLIT; ++h) {
+        const int32_t nh = n0 + h * GEMM_BN;
+        uint8_t* bd = b_dst + h * Cfg::B_HALF;
+        if constexpr (!B_MN) {
+            ld(tmB, bd, k0, nh, pol_b);
+        } else {
+#pragma unroll
+            for (int i = 0; i < Cfg::B_ROWS / 64; ++i) ld(tmB, bd + i * 8192, nh + i * 64, k0, pol_b);
+        }
+    }
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                           const GemmArgs& p) {
-    using Cfg = GemmCfg<PAIR>;
+    using Cfg = GemmCfg<PAIR, NSPLIT>;
+    static_assert(EPI != EPI_FWD || NSPLIT == 1, "forward statistics are per 256-column tile");
     constexpr int STAGES = Cfg::STAGES;
+    constexpr int ACC_BUFS = Cfg::ACC_BUFS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -117,7 +169,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     const int64_t M = p.m_dev ? *p.m_dev : p.M_static;
     const int64_t K = p.k_dev ? *p.k_dev : p.K_static;
     const int64_t num_m = (M + Cfg::TILE_M - 1) / Cfg::TILE_M;
-    const int64_t num_n = (p.N + GEMM_BN - 1) / GEMM_BN;
+    const int64_t num_n = (p.N + Cfg::TILE_N - 1) / Cfg::TILE_N;
     const int64_t num_tiles = num_m * num_n;
     const int64_t num_kb = (K + GEMM_BK - 1) / GEMM_BK;
 
@@ -158,50 +210,21 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int32_t m0 = (int32_t)(m_blk * Cfg::TILE_M + rank * GEMM_BM);
-                const int32_t n0 = (int32_t)(n_blk * GEMM_BN + rank * Cfg::B_ROWS);
+                const int32_t n0 = (int32_t)(n_blk * Cfg::TILE_N + rank * Cfg::B_ROWS);
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    const int32_t k0 = (int32_t)(kb * GEMM_BK);
-                    uint8_t* a_dst = sA + stage * GEMM_A_STAGE;
-                    uint8_t* b_dst = sB + stage * Cfg::B_STAGE;
+                    uint32_t fb = 0;
                     if constexpr (PAIR) {
-                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        fb = mapa_shared(smem_u32(&full[stage]), 0);
                         // leader: arm its own full barrier for both CTAs' bytes (CTA scope; the
                         // peer's TMA completes its bytes on it directly)
                         if (leader) mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
-                        if (!A_MN) {
-                            tma_load_2d_pair(&tmA, fb, a_dst, k0, m0, pol_a);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < GEMM_BM / 64; ++i)
-                                tma_load_2d_pair(&tmA, fb, a_dst + i * 8192, m0 + i * 64, k0, pol_a);
-                        }
-                        if (!B_MN) {
-                            tma_load_2d_pair(&tmB, fb, b_dst, k0, n0, pol_b);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
-                                tma_load_2d_pair(&tmB, fb, b_dst + i * 8192, n0 + i * 64, k0, pol_b);
-                        }
                     } else {
                         mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
-                        if (!A_MN) {
-                            tma_load_2d(&tmA, &full[stage], a_dst, k0, m0, pol_a);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < GEMM_BM / 64; ++i)
-                                tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + i * 64, k0,
-                                            pol_a);
-                        }
-                        if (!B_MN) {
-                            tma_load_2d(&tmB, &full[stage], b_dst, k0, n0, pol_b);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
-                                tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + i * 64, k0,
-                                            pol_b);
-                        }
                     }
+                    load_stage<A_MN, B_MN, PAIR, NSPLIT>(
+                        tmA, tmB, &full[stage], fb, sA + stage * GEMM_A_STAGE,
+                        sB + stage * Cfg::B_STAGE, m0, n0, (int32_t)(kb * GEMM_BK), pol_a, pol_b);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -232,12 +255,17 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const uint64_t adesc =
                             A_MN ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
                                  : umma_desc_sw128(a_base + k * 32, 16, 1024);
-                        const uint64_t bdesc =
-                            B_MN ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
                         const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-                        if constexpr (PAIR) tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, accum);
-                        else tc_mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+#pragma unroll
+                        for (int h = 0; h < NSPLIT; ++h) {
+                            const uint32_t bh = b_base + h * Cfg::B_HALF;
+                            const uint64_t bdesc =
+                                B_MN ? umma_desc_sw128(bh + k * 2048, 8192, 1024)
+                                     : umma_desc_sw128(bh + k * 32, 16, 1024);
+                            const uint32_t dh = d_tmem + (uint32_t)(h * GEMM_BN);
+                            if constexpr (PAIR) tc_mma_f16_pair(dh, adesc, bdesc, idesc, accum);
+                            else tc_mma_f16(dh, adesc, bdesc, idesc, accum);
+                        }
                     }
                     if constexpr (PAIR) tc_commit_pair_mc(&empty[stage], 0x3);
                     else tc_commit(&empty[stage]);
@@ -248,8 +276,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 }
                 if constexpr (PAIR) tc_commit_pair_mc(&tfull[acc], 0x3);
                 else tc_commit(&tfull[acc]);
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+                advance_acc<ACC_BUFS>(acc, acc_phase);
             }
         }
         __syncwarp();
@@ -269,113 +296,117 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
             const int64_t row = m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
             const bool row_ok = row < M;
-            const int32_t col0 = (int32_t)(n_blk * GEMM_BN);
-            const int32_t ncol = min(GEMM_BN, p.N - col0);  // valid columns in this tile
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + lane_base + (uint32_t)(acc * GEMM_BN);
             uint32_t r[32];
+#pragma unroll 1
+            for (int h = 0; h < NSPLIT; ++h) {
+                const int32_t col0 = (int32_t)(n_blk * Cfg::TILE_N + h * GEMM_BN);
+                const int32_t ncol = min(GEMM_BN, p.N - col0);  // valid columns (may be <= 0)
+                const uint32_t taddr =
+                    tmem_base + lane_base + (uint32_t)(acc * GEMM_BN + h * GEMM_BN);
 
-            if constexpr (EPI == EPI_FWD) {
-                const float s = p.scale;
-                const float LOG2E = 1.4426950408889634f;
-                // pass 1: tile max over valid columns
-                float m = -INFINITY;
+                if constexpr (EPI == EPI_FWD) {
+                    const float s = p.scale;
+                    const float LOG2E = 1.4426950408889634f;
+                    // pass 1: tile max over valid columns
+                    float m = -INFINITY;
 #pragma unroll 1
-                for (int c = 0; c < GEMM_BN / 32; ++c) {
-                    tmem_ld_32x32b_x32(taddr + c * 32, r);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c * 32 + j < ncol) m = fmaxf(m, s * __uint_as_float(r[j]));
-                }
-                // pass 2: P~ = exp(z - m), l' = sum P~ - 1 (the first max element is left out
-                // of the sum instead of subtracting 1 afterwards, so l' keeps full relative
-                // precision when the tile max dominates -- p_y close to 1), z_y
-                const int32_t y = row_ok ? p.tgt[row] : -1;
-                const int32_t yl = y - col0;
-                float l = 0.f;
-                bool max_seen = false;
-                const float mb = m * LOG2E;
-                __half* prow = p.P + (row_ok ? row : 0) * p.ldP + col0;
-#pragma unroll 1
-                for (int c = 0; c < GEMM_BN / 32; ++c) {
-                    tmem_ld_32x32b_x32(taddr + c * 32, r);
-                    tmem_ld_wait();
-                    float e[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float z = s * __uint_as_float(r[j]);
-                        const bool ok = c * 32 + j < ncol;
-                        e[j] = ok ? ex2_approx(fmaf(z, LOG2E, -mb)) : 0.f;
-                        const bool is_max = ok && !max_seen && z == m;
-                        max_seen |= is_max;
-                        if (is_max) e[j] = 1.f;
-                        l += is_max ? 0.f : e[j];
-                        if (c * 32 + j == yl && row_ok) p.zy[row] = z;
-                    }
-                    if (row_ok) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            if (c * 32 + j < ncol) {
-                                uint4 v;
-                                v.x = pack_half2(e[j + 0], e[j + 1]);
-                                v.y = pack_half2(e[j + 2], e[j + 3]);
-                                v.z = pack_half2(e[j + 4], e[j + 5]);
-                                v.w = pack_half2(e[j + 6], e[j + 7]);
-                                *reinterpret_cast<uint4*>(prow + c * 32 + j) = v;
-                            }
-                        }
-                    }
-                }
-                if (row_ok) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
-            } else if constexpr (EPI == EPI_GRADH) {
-                const float s = p.scale;
-                __nv_bfloat16* orow =
-                    p.gh + (row_ok ? (int64_t)p.idx[row] : 0) * p.ldo + col0;
-#pragma unroll 1
-                for (int c = 0; c < GEMM_BN / 32; ++c) {
-                    tmem_ld_32x32b_x32(taddr + c * 32, r);
-                    tmem_ld_wait();
-                    if (row_ok) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            if (c * 32 + j < ncol) {
-                                uint4 v;
-                                v.x = pack_bf162(s * __uint_as_float(r[j + 0]),
-                                                 s * __uint_as_float(r[j + 1]));
-                                v.y = pack_bf162(s * __uint_as_float(r[j + 2]),
-                                                 s * __uint_as_float(r[j + 3]));
-                                v.z = pack_bf162(s * __uint_as_float(r[j + 4]),
-                                                 s * __uint_as_float(r[j + 5]));
-                                v.w = pack_bf162(s * __uint_as_float(r[j + 6]),
-                                                 s * __uint_as_float(r[j + 7]));
-                                *reinterpret_cast<uint4*>(orow + c * 32 + j) = v;
-                            }
-                        }
-                    }
-                }
-            } else {  // EPI_GRADW
-                const float s = num_kb > 0 ? p.scale : 0.f;
-                float* orow = p.gw + (row_ok ? row : 0) * p.ldo + col0;
-#pragma unroll 1
-                for (int c = 0; c < GEMM_BN / 32; ++c) {
-                    if (num_kb > 0) {
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
                         tmem_ld_32x32b_x32(taddr + c * 32, r);
                         tmem_ld_wait();
-                    } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) r[j] = 0u;
+                        for (int j = 0; j < 32; ++j)
+                            if (c * 32 + j < ncol) m = fmaxf(m, s * __uint_as_float(r[j]));
                     }
-                    if (row_ok) {
+                    // pass 2: P~ = exp(z - m), l' = sum P~ - 1 (the first max element is left
+                    // out of the sum instead of subtracting 1 afterwards, so l' keeps full
+                    // relative precision when the tile max dominates -- p_y close to 1), z_y
+                    const int32_t y = row_ok ? p.tgt[row] : -1;
+                    const int32_t yl = y - col0;
+                    float l = 0.f;
+                    bool max_seen = false;
+                    const float mb = m * LOG2E;
+                    __half* prow = p.P + (row_ok ? row : 0) * p.ldP + col0;
+#pragma unroll 1
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
+                        tmem_ld_32x32b_x32(taddr + c * 32, r);
+                        tmem_ld_wait();
+                        float e[32];
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            if (c * 32 + j < ncol) {
-                                float4 v = make_float4(s * __uint_as_float(r[j + 0]),
-                                                       s * __uint_as_float(r[j + 1]),
-                                                       s * __uint_as_float(r[j + 2]),
-                                                       s * __uint_as_float(r[j + 3]));
-                                *reinterpret_cast<float4*>(orow + c * 32 + j) = v;
+                        for (int j = 0; j < 32; ++j) {
+                            const float z = s * __uint_as_float(r[j]);
+                            const bool ok = c * 32 + j < ncol;
+                            e[j] = ok ? ex2_approx(fmaf(z, LOG2E, -mb)) : 0.f;
+                            const bool is_max = ok && !max_seen && z == m;
+                            max_seen |= is_max;
+                            if (is_max) e[j] = 1.f;
+                            l += is_max ? 0.f : e[j];
+                            if (c * 32 + j == yl && row_ok) p.zy[row] = z;
+                        }
+                        if (row_ok) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                if (c * 32 + j < ncol) {
+                                    uint4 v;
+                                    v.x = pack_half2(e[j + 0], e[j + 1]);
+                                    v.y = pack_half2(e[j + 2], e[j + 3]);
+                                    v.z = pack_half2(e[j + 4], e[j + 5]);
+                                    v.w = pack_half2(e[j + 6], e[j + 7]);
+                                    *reinterpret_cast<uint4*>(prow + c * 32 + j) = v;
+                                }
+                            }
+                        }
+                    }
+                    if (row_ok) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
+                } else if constexpr (EPI == EPI_GRADH) {
+                    const float s = p.scale;
+                    __nv_bfloat16* orow =
+                        p.gh + (row_ok ? (int64_t)p.idx[row] : 0) * p.ldo + col0;
+#pragma unroll 1
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
+                        tmem_ld_32x32b_x32(taddr + c * 32, r);
+                        tmem_ld_wait();
+                        if (row_ok) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                if (c * 32 + j < ncol) {
+                                    uint4 v;
+                                    v.x = pack_bf162(s * __uint_as_float(r[j + 0]),
+                                                     s * __uint_as_float(r[j + 1]));
+                                    v.y = pack_bf162(s * __uint_as_float(r[j + 2]),
+                                                     s * __uint_as_float(r[j + 3]));
+                                    v.z = pack_bf162(s * __uint_as_float(r[j + 4]),
+                                                     s * __uint_as_float(r[j + 5]));
+                                    v.w = pack_bf162(s * __uint_as_float(r[j + 6]),
+                                                     s * __uint_as_float(r[j + 7]));
+                                    *reinterpret_cast<uint4*>(orow + c * 32 + j) = v;
+                                }
+                            }
+                        }
+                    }
+                } else {  // EPI_GRADW
+                    const float s = num_kb > 0 ? p.scale : 0.f;
+                    float* orow = p.gw + (row_ok ? row : 0) * p.ldo + col0;
+#pragma unroll 1
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
+                        if (num_kb > 0) {
+                            tmem_ld_32x32b_x32(taddr + c * 32, r);
+                            tmem_ld_wait();
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) r[j] = 0u;
+                        }
+                        if (row_ok) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                if (c * 32 + j < ncol) {
+                                    float4 v = make_float4(s * __uint_as_float(r[j + 0]),
+                                                           s * __uint_as_float(r[j + 1]),
+                                                           s * __uint_as_float(r[j + 2]),
+                                                           s * __uint_as_float(r[j + 3]));
+                                    *reinterpret_cast<float4*>(orow + c * 32 + j) = v;
+                                }
                             }
                         }
                     }
@@ -387,8 +418,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 if constexpr (PAIR) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
                 else mbar_arrive(&tempty[acc]);
             }
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            advance_acc<ACC_BUFS>(acc, acc_phase);
         }
     }
 
@@ -402,18 +432,18 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     }
 }
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, true>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, true, NSPLIT>(tmA, tmB, p);
 }
 
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, false>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, false, 1>(tmA, tmB, p);
 }
 
 }  // namespace agentrl

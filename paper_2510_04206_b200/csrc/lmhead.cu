@@ -73,14 +73,25 @@ static bool gemm_use_pair() {
     return v == 1;
 }
 
-template <int EPI, bool A_MN, bool B_MN>
+// 512-column tiles for the long-K backward GEMMs (CTA pairs only) unless
+// AGENTRL_GEMM_NSPLIT=1
+static bool gemm_wide_n() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("AGENTRL_GEMM_NSPLIT");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1 && gemm_use_pair();
+}
+
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream) {
     ProfScope ps(EPI == EPI_FWD ? KID_FWD : (EPI == EPI_GRADW ? KID_GRADW : KID_GRADH), stream);
-    // max_tiles is counted in 128-row tiles; a CTA pair covers 256 rows.
+    // max_tiles is counted in 128 x 256 tiles (an upper bound of the CTAs worth launching)
     if (gemm_use_pair()) {
-        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN>;
-        constexpr int smem = GemmCfg<true>::SMEM;
+        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT>;
+        constexpr int smem = GemmCfg<true, NSPLIT>::SMEM;
         static bool attr_done = false;  // per instantiation
         if (!attr_done) {
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -91,7 +102,7 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
         kern<<<(unsigned)grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     } else {
         auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
-        constexpr int smem = GemmCfg<false>::SMEM;
+        constexpr int smem = GemmCfg<false, 1>::SMEM;
         static bool attr_done = false;
         if (!attr_done) {
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -512,7 +523,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.part = part;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
-        if ((rc = launch_gemm<EPI_FWD, false, false>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
+        if ((rc = launch_gemm<EPI_FWD, false, false, 1>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
                                                       stream)))
             return rc;
     }
@@ -549,10 +560,10 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
         g.ldo = d;
-        if ((rc = launch_gemm<EPI_GRADW, true, true>(mG_MN, mH_MN, g,
-                                                      ceil_div(V, GEMM_BM) * ceil_div(d, GEMM_BN),
-                                                      stream)))
-            return rc;
+        const int64_t tiles = ceil_div(V, GEMM_BM) * ceil_div(d, GEMM_BN);
+        rc = gemm_wide_n() ? launch_gemm<EPI_GRADW, true, true, 2>(mG_MN, mH_MN, g, tiles, stream)
+                           : launch_gemm<EPI_GRADW, true, true, 1>(mG_MN, mH_MN, g, tiles, stream);
+        if (rc) return rc;
     }
     // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
     SideStream* ss = nullptr;
@@ -574,10 +585,10 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.idx = idx_dev;
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
         g.ldo = d;
-        if ((rc = launch_gemm<EPI_GRADH, false, true>(mG_K, mW_MN, g,
-                                                       max_m_tiles * ceil_div(d, GEMM_BN),
-                                                       stream)))
-            return rc;
+        const int64_t tiles = max_m_tiles * ceil_div(d, GEMM_BN);
+        rc = gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream)
+                           : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream);
+        if (rc) return rc;
     }
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
     return AGENTRL_OK;
