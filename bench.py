@@ -285,6 +285,7 @@ def run_native(args, cfg, world, rank, local_rank):
     else:
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": None, "peak": pk["hbm"],
                 "unit": "GB/s", "frac": None, "traffic": None}
+    adv = adv_norm_timing(ag, bd, lb, dev, pk["hbm"]) if rank == 0 else None
     step_flop = 6.0 * T_eff_global * V * d
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -299,7 +300,7 @@ def run_native(args, cfg, world, rank, local_rank):
         "step_tflops_algorithmic": step_flop / (ms / 1e3) / 1e12,
         "clocks": clocks, "e2e": e2e,
         "gpu_launches": int(launches_per_step * args.steps),
-        "roofline": roof, "kernel_ms": kernel_ms, "status": status,
+        "roofline": roof, "adv_norm": adv, "kernel_ms": kernel_ms, "status": status,
         "loss": float(step.loss.item()), "clip_frac": float(step.loss_stats[0].item()),
     }
     if world > 1:
@@ -312,6 +313,42 @@ def run_native(args, cfg, world, rank, local_rank):
         comm.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
+    """Part 1 alone (agentrl_task_adv_norm) at this rank's batch size, single GPU, cold L2
+    (a 2 x L2 buffer is written before every timed call).  Algorithmic bytes: mask T B +
+    adv_tok 4T B + 20 B per trajectory (offsets, ids, reward)."""
+    import torch
+    T = int(lb["T"])
+    n_traj = len(lb["task_id"])
+    ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, lb["n_groups"],
+                                                                    lb["n_tasks"]), dev)
+    adv = torch.empty(T, dtype=torch.float32, device=dev)
+    ts = torch.empty(lb["n_tasks"], 3, dtype=torch.float64, device=dev)
+    nm = torch.empty(1, dtype=torch.int64, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    batch = ag.make_batch(bd)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+    times = []
+    for i in range(iters + 3):
+        flush.fill_(float(i))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rc = ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st)
+        e1.record()
+        torch.cuda.synchronize()
+        if rc != 0:
+            return None
+        if i >= 3:
+            times.append(e0.elapsed_time(e1))
+    times.sort()
+    ms = times[len(times) // 2]
+    by = 5 * T + 20 * n_traj
+    return {"latency_us": ms * 1e3, "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
+            "frac_hbm": by / (ms / 1e3) / 1e9 / hbm_gbs, "cold_l2": True,
+            "note": "launch-latency bound at this size; see profiles/*adv_sweep* for the T sweep"}
 
 
 def traffic_from_profiles(config, kernel):

@@ -247,6 +247,31 @@ def make_old_logp_free(T: int, seed: int, mean=-9.0, sd=3.0):
     return np.minimum(rng.normal(mean, sd, size=T), -1e-3).astype(np.float32)
 
 
+def make_sweep_structure(T: int, tok_per_traj: int = 400, K: int = 8, n_tasks: int = 5,
+                         seed: int = SEED_BASE + 99):
+    """Vectorised batch structure for the adv-norm bandwidth sweep (~400
+    tokens/trajectory, 5 tasks, G=8): fixed-length trajectories of 5 turns, each turn an
+    observation span then an assistant span (~40% assistant), rewards {1, 0, -0.2}."""
+    rng = np.random.default_rng(seed)
+    n_traj = max(K, (T // tok_per_traj) // K * K)
+    lens = np.full(n_traj, T // n_traj, np.int64)
+    lens[: T - int(lens.sum())] += 1
+    off = np.zeros(n_traj + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    n_groups = n_traj // K
+    group_id = np.repeat(np.arange(n_groups), K).astype(np.int32)
+    task_id = (group_id % n_tasks).astype(np.int32)
+    pos = np.arange(T, dtype=np.int64)
+    traj = np.repeat(np.arange(n_traj), lens)
+    rel = (pos - off[traj]) * 5 // lens[traj]              # turn index 0..4
+    within = (pos - off[traj]) - rel * lens[traj] // 5      # position inside the turn
+    turn_len = lens[traj] // 5
+    mask = (within >= (turn_len * 6) // 10).astype(np.uint8)  # last 40% of each turn
+    rewards = rng.choice(np.asarray([1.0, 0.0, -0.2], np.float32), size=n_traj)
+    return dict(T=int(T), traj_offsets=off, task_id=task_id, group_id=group_id,
+                rewards=rewards, loss_mask=mask, n_groups=int(n_groups), n_tasks=n_tasks)
+
+
 def shard_groups_lpt(group_tokens: np.ndarray, world: int) -> np.ndarray:
     """Deterministic LPT bin-packing of whole groups onto ranks:
     largest masked-token count first (ties: lower group id) to the least-loaded
