@@ -19,6 +19,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include <mutex>
 
 #include "gemm_sm100.cuh"
@@ -71,6 +74,20 @@ static bool gemm_use_pair() {
         v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
+}
+
+// L2 eviction policy per GEMM operand (0 normal, 1 evict_first, 2 evict_last); the defaults
+// can be overridden for experiments with AGENTRL_L2POL="fa fb wa wb ha hb" (six digits).
+static int l2_policy(int which, int dflt) {
+    const char* e = getenv("AGENTRL_L2POL");
+    if (!e || (int)strlen(e) < 6) return dflt;
+    const int v = e[which] - '0';
+    return (v >= 0 && v <= 2) ? v : dflt;
+}
+static int gemm_group_m() {
+    const char* e = getenv("AGENTRL_GROUP_M");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 16;
 }
 
 // 512-column tiles for the long-K backward GEMMs (CTA pairs only) unless
@@ -515,7 +532,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.m_dev = rows_dev;
         g.N = V;
         g.K_static = d;
-        g.group_m = 16;
+        g.group_m = gemm_group_m();
+        g.pol_a = l2_policy(0, 2);  // H rows of the current row group: reused by every column
+        g.pol_b = l2_policy(1, 1);  // W: streamed, shared only by the concurrent row tiles
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
         g.P = reinterpret_cast<__half*>(PG);
@@ -557,6 +576,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.N = d;
         g.k_dev = rows_dev;
         g.group_m = 1;
+        g.pol_a = l2_policy(2, 1);  // G^T: each column block read by one wave only
+        g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
         g.ldo = d;
@@ -581,6 +602,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.N = d;
         g.K_static = V;
         g.group_m = 1;
+        g.pol_a = l2_policy(4, 1);  // G rows: read by one wave only
+        g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
         g.scale = a->logit_scale;
         g.idx = idx_dev;
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
