@@ -84,11 +84,15 @@ static int l2_policy(int which, int dflt) {
     const int v = e[which] - '0';
     return (v >= 0 && v <= 2) ? v : dflt;
 }
-static int gemm_group_m() {
-    const char* e = getenv("AGENTRL_GROUP_M");
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
     const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : 16;
+    return v > 0 ? v : dflt;
 }
+static int gemm_group_m() { return env_int("AGENTRL_GROUP_M", 16); }
+static int gemm_group_m_bwd() { return env_int("AGENTRL_GROUP_M_BWD", 1); }
+// persistent grid (one CTA per SM) unless AGENTRL_GEMM_FULLGRID=1 (one CTA per tile)
+static bool gemm_full_grid() { return env_int("AGENTRL_GEMM_FULLGRID", 0) == 1; }
 
 // 512-column tiles for the long-K backward GEMMs (CTA pairs only) unless
 // AGENTRL_GEMM_NSPLIT=1
@@ -114,7 +118,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             attr_done = true;
         }
-        int64_t grid = std::min<int64_t>(num_sms() & ~1, std::max<int64_t>(max_tiles, 2));
+        int64_t grid = gemm_full_grid() ? 2 * std::max<int64_t>(max_tiles, 1)
+                                        : std::min<int64_t>(num_sms() & ~1, std::max<int64_t>(max_tiles, 2));
         grid &= ~int64_t(1);
         kern<<<(unsigned)grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     } else {
@@ -575,7 +580,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.M_static = V;
         g.N = d;
         g.k_dev = rows_dev;
-        g.group_m = 1;
+        g.group_m = gemm_group_m_bwd();
         g.pol_a = l2_policy(2, 1);  // G^T: each column block read by one wave only
         g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
         g.scale = a->logit_scale;
@@ -601,7 +606,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.m_dev = rows_dev;
         g.N = d;
         g.K_static = V;
-        g.group_m = 1;
+        g.group_m = gemm_group_m_bwd();
         g.pol_a = l2_policy(4, 1);  // G rows: read by one wave only
         g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
         g.scale = a->logit_scale;
