@@ -81,7 +81,12 @@ struct GemmArgs {
     // EPI_GRADW
     float* gw;  // [V, ldo]
     int64_t ldo;
+    // dynamic tile scheduler: zeroed int counter (tiles claimed in global order), or null for
+    // the static persistent schedule (tile = unit + i * units)
+    int* tile_counter;
 };
+
+constexpr int QD = 4;  // tile-queue depth (dynamic scheduler)
 
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t num_n,
                                             int32_t group_m, int64_t& m_blk, int64_t& n_blk) {
@@ -157,7 +162,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tq_full = tempty + 2;   // tile queue (dynamic scheduler): QD slots
+    uint64_t* tq_empty = tq_full + QD;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + QD);
+    volatile int32_t* tile_q = reinterpret_cast<volatile int32_t*>(tmem_slot + 4);
+    const bool dyn = p.tile_counter != nullptr;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -181,6 +190,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], PAIR ? 8 : 4);  // one arrive per epilogue warp (x2 CTAs)
+        }
+        for (int q = 0; q < QD; ++q) {
+            mbar_init(&tq_full[q], 1);
+            // consumers of a queue slot: leader MMA + 4 epilogue warps (+ peer producer and its
+            // 4 epilogue warps); only the leader's tq_empty is used
+            mbar_init(&tq_empty[q], PAIR ? 10 : 5);
         }
         fence_mbar_init();
         fence_proxy_async_smem();
@@ -206,7 +221,31 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             const uint64_t pol_b = make_policy(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+            for (int64_t it = 0;; ++it) {
+                int64_t tile;
+                if (!dyn) {
+                    tile = unit + it * n_units;
+                } else {
+                    const int slot = (int)(it & (QD - 1));
+                    const uint32_t ph = (uint32_t)(it / QD) & 1u;
+                    if (leader) {  // claim the next tile in global order, publish to the pair
+                        mbar_wait(&tq_empty[slot], ph ^ 1);
+                        tile = atomicAdd(p.tile_counter, 1);
+                        tile_q[slot] = (int32_t)tile;
+                        mbar_arrive(&tq_full[slot]);
+                        if constexpr (PAIR) {
+                            const uint32_t pf = mapa_shared(smem_u32(&tq_full[slot]), 1);
+                            mbar_arrive_expect_tx_remote(pf, 4);
+                            st_async_remote_u32(mapa_shared(smem_u32((const void*)&tile_q[slot]), 1),
+                                                (uint32_t)tile, pf);
+                        }
+                    } else {
+                        mbar_wait(&tq_full[slot], ph);
+                        tile = tile_q[slot];
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
+                    }
+                }
+                if (tile >= num_tiles) break;
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int32_t m0 = (int32_t)(m_blk * Cfg::TILE_M + rank * GEMM_BM);
@@ -241,7 +280,17 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+            for (int64_t it = 0;; ++it) {
+                int64_t tile;
+                if (!dyn) {
+                    tile = unit + it * n_units;
+                } else {
+                    const int slot = (int)(it & (QD - 1));
+                    mbar_wait(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                    tile = tile_q[slot];
+                    mbar_arrive(&tq_empty[slot]);
+                }
+                if (tile >= num_tiles) break;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_BN);
@@ -291,7 +340,21 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         }
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+        for (int64_t it = 0;; ++it) {
+            int64_t tile;
+            if (!dyn) {
+                tile = unit + it * n_units;
+            } else {
+                const int slot = (int)(it & (QD - 1));
+                mbar_wait(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                tile = tile_q[slot];
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(&tq_empty[slot]);
+                    else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
+                }
+            }
+            if (tile >= num_tiles) break;
             int64_t m_blk, n_blk;
             tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
             const int64_t row = m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;

@@ -55,6 +55,7 @@ struct LossWs {
     size_t row_term, row_rho, row_logp;     // double/float per row
     size_t row_clip;                        // int32 per row
     size_t red;                             // double [8] loss reduction output
+    size_t sched;                           // int [16] GEMM tile counters (dynamic scheduler)
     size_t total;
     int32_t n_tiles;
 };

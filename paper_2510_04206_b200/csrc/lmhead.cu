@@ -91,6 +91,12 @@ static int env_int(const char* name, int dflt) {
 }
 static int gemm_group_m() { return env_int("AGENTRL_GROUP_M", 16); }
 static int gemm_group_m_bwd() { return env_int("AGENTRL_GROUP_M_BWD", 1); }
+// dynamic tile scheduler (atomic counter, tiles claimed in global order) unless
+// AGENTRL_GEMM_SCHED=static (tile = unit + i * units: pairs drift apart over long runs)
+static bool gemm_dynamic() {
+    const char* e = getenv("AGENTRL_GEMM_SCHED");
+    return !(e && strcmp(e, "static") == 0);
+}
 // persistent grid (one CTA per SM) unless AGENTRL_GEMM_FULLGRID=1 (one CTA per tile)
 static bool gemm_full_grid() { return env_int("AGENTRL_GEMM_FULLGRID", 0) == 1; }
 
@@ -445,6 +451,7 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.row_logp = p.take(sizeof(float) * (size_t)rows_cap);
     w.row_clip = p.take(sizeof(int32_t) * (size_t)rows_cap);
     w.red = p.take(sizeof(double) * 8);
+    w.sched = p.take(sizeof(int) * 16);
     w.total = p.off;
     return w;
 }
@@ -483,6 +490,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float* row_rho = reinterpret_cast<float*>(ws + w.row_rho);
     float* row_logp = reinterpret_cast<float*>(ws + w.row_logp);
     int32_t* row_clip = reinterpret_cast<int32_t*>(ws + w.row_clip);
+    int* sched = reinterpret_cast<int*>(ws + w.sched);
+    int* ctr_fwd = gemm_dynamic() ? sched + 0 : nullptr;
+    int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
+    int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
+    AG_CUDA(cudaMemsetAsync(sched, 0, 16 * sizeof(int), stream));
 
     // ---- compaction (standalone) or reuse of part 1's
     if (!idx_dev) {
@@ -540,6 +552,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.group_m = gemm_group_m();
         g.pol_a = l2_policy(0, 2);  // H rows of the current row group: reused by every column
         g.pol_b = l2_policy(1, 1);  // W: streamed, shared only by the concurrent row tiles
+        g.tile_counter = ctr_fwd;
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
         g.P = reinterpret_cast<__half*>(PG);
@@ -583,6 +596,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.group_m = gemm_group_m_bwd();
         g.pol_a = l2_policy(2, 1);  // G^T: each column block read by one wave only
         g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
+        g.tile_counter = ctr_gw;
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
         g.ldo = d;
@@ -609,6 +623,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.group_m = gemm_group_m_bwd();
         g.pol_a = l2_policy(4, 1);  // G rows: read by one wave only
         g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
+        g.tile_counter = ctr_gh;
         g.scale = a->logit_scale;
         g.idx = idx_dev;
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);

@@ -225,6 +225,22 @@ __device__ __forceinline__ void tc_commit_pair_mc(uint64_t* bar, uint16_t mask) 
         : "memory");
 }
 
+// remote arm: one arrival + expect `bytes` of transaction on a barrier in another CTA
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+                 "r"(bytes)
+                 : "memory");
+}
+// 4-byte store into another CTA's smem that completes as transaction bytes on its barrier
+__device__ __forceinline__ void st_async_remote_u32(uint32_t cluster_addr, uint32_t v,
+                                                    uint32_t cluster_bar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(
+            cluster_addr),
+        "r"(v), "r"(cluster_bar)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
