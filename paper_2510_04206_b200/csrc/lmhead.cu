@@ -90,7 +90,7 @@ static int env_int(const char* name, int dflt) {
     return v > 0 ? v : dflt;
 }
 static int gemm_group_m() { return env_int("AGENTRL_GROUP_M", 16); }
-static int gemm_group_m_bwd() { return env_int("AGENTRL_GROUP_M_BWD", 1); }
+static int gemm_group_m_bwd() { return env_int("AGENTRL_GROUP_M_BWD", 8); }
 // dynamic tile scheduler (atomic counter, tiles claimed in global order) unless
 // AGENTRL_GEMM_SCHED=static (tile = unit + i * units: pairs drift apart over long runs)
 static bool gemm_dynamic() {
