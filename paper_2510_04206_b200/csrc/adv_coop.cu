@@ -1,0 +1,490 @@
+// adv_coop.cu -- part 1 (GRPO group advantage P:1263, then task advantage normalization,
+// sec 3.2 Eq.1) as ONE cooperative persistent kernel with grid-wide barriers
+// between its phases (two launches around the NCCL all-reduce when a communicator is given).
+//
+//   phase 0  zero the integer scratch (n_g, K_j, fill counters)
+//   phase A  token-parallel (4096-token chunks, 16 B mask loads): n_g via integer atomics,
+//            per-chunk masked counts; trajectory-parallel: K_j, offsets validation
+//   phase B1 block 0: exclusive scans of chunk counts (-> compaction bases) and K_j
+//   phase B2 trajectory-parallel: group member lists (atomic slots)
+//   phase B3 group-parallel: sort members (-> deterministic order), exact-equal rule,
+//            population std, A_hat_g (fp64); per-group (N, S, Q) = (sum n, sum n A, sum n A^2)
+//   phase B4 block 0: per-task (N_i, S_i, Q_i) as a fixed-order sum over groups
+//   [C1 NCCL all-reduce of the 3*n_tasks doubles -- second launch starts here]
+//   phase C  token-parallel: mu_i = S_i/N_i, sigma_i = sqrt(max(Q_i/N_i - mu_i^2, 0)),
+//            adv_tok[t] = mask ? (A_hat_g - mu)/max(sigma, eps) : 0, stable compaction
+//            idx[] / adv_c[] for part 2; block 0 writes task_stats and N.
+// Every reduction has a fixed order, so results are bitwise run-to-run deterministic.
+#include <cooperative_groups.h>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace agentrl {
+
+constexpr int COOP_THREADS = 256;
+
+struct AdvParams {
+    int64_t T;
+    int32_t n_traj, n_groups, n_tasks;
+    int64_t n_chunks;
+    const int64_t* off;
+    const int32_t* task_id;
+    const int32_t* group_id;
+    const float* rewards;
+    const uint8_t* mask;
+    double eps_std;
+    int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task;
+    double *adv_hat, *grp_nsq, *stats;
+    int64_t* meta;
+    int32_t* d_status;
+    float* adv_tok;
+    int32_t* idx;
+    float* adv_c;
+    double* task_stats_out;
+    int64_t* n_mask_global_out;
+};
+
+__device__ __forceinline__ int32_t coop_find_traj(const int64_t* __restrict__ off,
+                                                  int32_t n_traj, int64_t t) {
+    int32_t lo = 0, hi = n_traj;
+    while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (off[mid] <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo < n_traj ? lo : n_traj - 1;
+}
+
+__device__ __forceinline__ void coop_mask16(const uint8_t* __restrict__ mask, int64_t T,
+                                            int64_t t0, bool any_traj, uint8_t (&m)[16]) {
+    if (any_traj && t0 + 16 <= T && (reinterpret_cast<uintptr_t>(mask + t0) & 15) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + t0));
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m[i] = b[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m[i] = (any_traj && t0 + i < T) ? mask[t0 + i] : 0;
+    }
+}
+
+// exclusive scan of one int per thread over a 256-thread block (returns prefix; total out)
+__device__ __forceinline__ int32_t coop_block_exscan(int32_t v, int32_t* s_w, int32_t& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int32_t w = lane < 8 ? s_w[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < 8) s_w[lane] = w;
+    }
+    __syncthreads();
+    const int32_t base = wid > 0 ? s_w[wid - 1] : 0;
+    total = s_w[7];
+    __syncthreads();
+    return base + x - v;
+}
+
+// in-place exclusive scan of a[0..n) by one block of 256 threads (contiguous per-thread
+// segments, then a block scan of segment sums); returns the total
+__device__ int64_t coop_block_scan_array(int32_t* a, int64_t n, int64_t* s_seg) {
+    const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
+    const int64_t lo = min(n, (int64_t)threadIdx.x * per), hi = min(n, lo + per);
+    int64_t s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += a[i];
+    // block scan of 64-bit segment sums
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_seg[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = lane < 8 ? s_seg[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < 8) s_seg[lane] = w;
+    }
+    __syncthreads();
+    int64_t run = (wid > 0 ? s_seg[wid - 1] : 0) + x - s;
+    const int64_t total = s_seg[7];
+    for (int64_t i = lo; i < hi; ++i) {
+        const int32_t v = a[i];
+        a[i] = (int32_t)run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ double coop_block_sum(double v, double* s_red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) s_red[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < COOP_THREADS / 32; ++w) r += s_red[w];
+    __syncthreads();
+    return r;  // thread 0
+}
+
+// ------------------------------------------------------------------ phases 0 .. B4
+__device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
+    __shared__ int32_t s_w[8];
+    __shared__ int64_t s_seg[8];
+    __shared__ double s_red[8];
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    int32_t st = 0;
+
+    // phase 0
+    for (int64_t i = gtid; i < p.n_traj; i += gstride) p.n_g[i] = 0;
+    for (int64_t i = gtid; i < p.n_groups; i += gstride) {
+        p.grp_cnt[i] = 0;
+        p.grp_fill[i] = 0;
+    }
+    grid.sync();
+
+    // phase A
+    const bool any_traj = p.n_traj > 0;
+    for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
+        const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
+        uint8_t m[16];
+        coop_mask16(p.mask, p.T, t0, any_traj, m);
+        int32_t mine = 0;
+        if (t0 < p.T && any_traj) {
+            int32_t g = coop_find_traj(p.off, p.n_traj, t0);
+            int64_t end = p.off[g + 1];
+            int32_t cnt = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t t = t0 + i;
+                if (t >= p.T) break;
+                while (t >= end && g + 1 < p.n_traj) {
+                    if (cnt) atomicAdd(&p.n_g[g], cnt);
+                    cnt = 0;
+                    ++g;
+                    end = p.off[g + 1];
+                }
+                const int32_t bit = m[i] != 0;
+                cnt += bit;
+                mine += bit;
+            }
+            if (cnt) atomicAdd(&p.n_g[g], cnt);
+        }
+        int32_t total;
+        coop_block_exscan(mine, s_w, total);
+        if (threadIdx.x == 0) p.chunk[c] = total;
+    }
+    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
+        const int32_t j = p.group_id[g], i = p.task_id[g];
+        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
+            st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+            continue;
+        }
+        atomicAdd(&p.grp_cnt[j], 1);
+        if (p.off[g + 1] < p.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
+    }
+    if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
+    grid.sync();
+
+    // phase B1 (block 0)
+    if (blockIdx.x == 0) {
+        const int64_t n_mask = coop_block_scan_array(p.chunk, p.n_chunks, s_seg);
+        for (int64_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) p.grp_start[j] = p.grp_cnt[j];
+        __syncthreads();
+        coop_block_scan_array(p.grp_start, p.n_groups, s_seg);
+        if (threadIdx.x == 0) p.meta[0] = n_mask;
+    }
+    grid.sync();
+
+    // phase B2
+    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
+        const int32_t j = p.group_id[g], i = p.task_id[g];
+        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) continue;
+        const int32_t slot = atomicAdd(&p.grp_fill[j], 1);
+        p.members[p.grp_start[j] + slot] = (int32_t)g;
+    }
+    grid.sync();
+
+    // phase B3: per group (GRPO advantage; readings R1, R2, R14)
+    for (int64_t j = gtid; j < p.n_groups; j += gstride) {
+        const int32_t K = p.grp_cnt[j];
+        int32_t* mb = p.members + p.grp_start[j];
+        for (int a = 1; a < K; ++a) {
+            const int32_t x = mb[a];
+            int b = a - 1;
+            while (b >= 0 && mb[b] > x) {
+                mb[b + 1] = mb[b];
+                --b;
+            }
+            mb[b + 1] = x;
+        }
+        double N = 0.0, S = 0.0, Q = 0.0;
+        int32_t task0 = -1;
+        if (K > 0) {
+            if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+            task0 = p.task_id[mb[0]];
+            double sum = 0.0, rmax = p.rewards[mb[0]], rmin = rmax;
+            for (int a = 0; a < K; ++a) {
+                const double r = p.rewards[mb[a]];
+                if (p.task_id[mb[a]] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                sum += r;
+                rmax = fmax(rmax, r);
+                rmin = fmin(rmin, r);
+            }
+            const bool flat = rmax == rmin;
+            const double mean = sum / (double)K;
+            double ss = 0.0;
+            if (!flat)
+                for (int a = 0; a < K; ++a) {
+                    const double dlt = (double)p.rewards[mb[a]] - mean;
+                    ss += dlt * dlt;
+                }
+            const double sd = sqrt(ss / (double)K);
+            const double den = sd > p.eps_std ? sd : p.eps_std;
+            for (int a = 0; a < K; ++a) {
+                const int32_t g = mb[a];
+                const double ah = flat ? 0.0 : ((double)p.rewards[g] - mean) / den;
+                p.adv_hat[g] = ah;
+                const double n = (double)p.n_g[g];
+                N += n;
+                S += n * ah;
+                Q += n * ah * ah;
+            }
+        }
+        p.grp_task[j] = task0;
+        p.grp_nsq[3 * j + 0] = N;
+        p.grp_nsq[3 * j + 1] = S;
+        p.grp_nsq[3 * j + 2] = Q;
+    }
+    if (st) atomicOr(p.d_status, st);
+    grid.sync();
+
+    // phase B4 (block 0): per-task moments over the token set, fixed order
+    if (blockIdx.x == 0) {
+        const int64_t per = (p.n_groups + COOP_THREADS - 1) / COOP_THREADS;
+        const int64_t lo = min((int64_t)p.n_groups, (int64_t)threadIdx.x * per);
+        const int64_t hi = min((int64_t)p.n_groups, lo + per);
+        for (int32_t i = 0; i < p.n_tasks; ++i) {
+            double N = 0.0, S = 0.0, Q = 0.0;
+            for (int64_t j = lo; j < hi; ++j)
+                if (p.grp_task[j] == i) {
+                    N += p.grp_nsq[3 * j];
+                    S += p.grp_nsq[3 * j + 1];
+                    Q += p.grp_nsq[3 * j + 2];
+                }
+            N = coop_block_sum(N, s_red);
+            S = coop_block_sum(S, s_red);
+            Q = coop_block_sum(Q, s_red);
+            if (threadIdx.x == 0) {
+                p.stats[3 * i] = N;
+                p.stats[3 * i + 1] = S;
+                p.stats[3 * i + 2] = Q;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ phase C
+__device__ void coop_apply_phase(const AdvParams& p) {
+    extern __shared__ double s_task[];  // [2*n_tasks]: mu, 1/den (as den)
+    __shared__ int32_t s_w[8];
+    for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
+        const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
+        const double mu = N > 0.0 ? S / N : 0.0;
+        const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
+        s_task[2 * i] = mu;
+        s_task[2 * i + 1] = sd > p.eps_std ? sd : p.eps_std;
+        if (blockIdx.x == 0 && p.task_stats_out) {
+            p.task_stats_out[3 * i] = N;
+            p.task_stats_out[3 * i + 1] = mu;
+            p.task_stats_out[3 * i + 2] = sd;
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        double nsum = 0.0;
+        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
+        if (threadIdx.x == 0) {
+            const int64_t n = (int64_t)nsum;
+            p.meta[1] = n;
+            if (p.n_mask_global_out) *p.n_mask_global_out = n;
+            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
+        }
+    }
+    const bool any_traj = p.n_traj > 0;
+    for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
+        const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
+        uint8_t m[16];
+        coop_mask16(p.mask, p.T, t0, any_traj, m);
+        int32_t mine = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mine += m[i] != 0;
+        int32_t total;
+        int32_t pos = p.chunk[c] + coop_block_exscan(mine, s_w, total);
+        float outv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) outv[i] = 0.f;
+        if (t0 < p.T && any_traj && mine > 0) {
+            int32_t g = coop_find_traj(p.off, p.n_traj, t0);
+            int64_t end = p.off[g + 1];
+            int32_t cur = -1;
+            float at = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t t = t0 + i;
+                if (t >= p.T) break;
+                while (t >= end && g + 1 < p.n_traj) {
+                    ++g;
+                    end = p.off[g + 1];
+                }
+                if (m[i]) {
+                    if (g != cur) {  // Eq.1 for this trajectory
+                        cur = g;
+                        const int32_t ti = p.task_id[g];
+                        at = (ti >= 0 && ti < p.n_tasks)
+                                 ? (float)((p.adv_hat[g] - s_task[2 * ti]) / s_task[2 * ti + 1])
+                                 : 0.f;
+                    }
+                    outv[i] = at;
+                    p.idx[pos] = (int32_t)t;
+                    p.adv_c[pos] = at;
+                    ++pos;
+                }
+            }
+        }
+        if (t0 < p.T) {
+            if (t0 + 16 <= p.T && (reinterpret_cast<uintptr_t>(p.adv_tok + t0) & 15) == 0) {
+                float4* o4 = reinterpret_cast<float4*>(p.adv_tok + t0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    o4[i] = make_float4(outv[4 * i], outv[4 * i + 1], outv[4 * i + 2], outv[4 * i + 3]);
+            } else {
+                for (int i = 0; i < 16; ++i)
+                    if (t0 + i < p.T) p.adv_tok[t0 + i] = outv[i];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_all(const AdvParams p) {
+    cg::grid_group grid = cg::this_grid();
+    coop_stats_phases(p, grid);
+    grid.sync();
+    coop_apply_phase(p);
+}
+
+__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_stats(const AdvParams p) {
+    cg::grid_group grid = cg::this_grid();
+    coop_stats_phases(p, grid);
+}
+
+__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_apply(const AdvParams p) {
+    coop_apply_phase(p);
+}
+
+static int coop_grid(const void* kern, size_t smem, int64_t want) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, COOP_THREADS, smem) !=
+            cudaSuccess ||
+        per_sm <= 0)
+        return 0;
+    const int64_t cap = (int64_t)per_sm * num_sms();
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cap, want));
+}
+
+int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
+                         double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
+                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream) {
+    int dev = 0;
+    int coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop) return AGENTRL_ERR_UNSUPPORTED;
+    AdvParams p;
+    p.T = b->T;
+    p.n_traj = b->n_traj;
+    p.n_groups = b->n_groups;
+    p.n_tasks = b->n_tasks;
+    p.n_chunks = ceil_div(b->T, CHUNK_TOKENS);
+    p.off = b->traj_offsets;
+    p.task_id = b->task_id;
+    p.group_id = b->group_id;
+    p.rewards = b->rewards;
+    p.mask = b->loss_mask;
+    p.eps_std = eps_std;
+    p.n_g = reinterpret_cast<int32_t*>(ws + w.n_g);
+    p.chunk = reinterpret_cast<int32_t*>(ws + w.chunk_cnt);
+    p.grp_cnt = reinterpret_cast<int32_t*>(ws + w.grp_cnt);
+    p.grp_start = reinterpret_cast<int32_t*>(ws + w.grp_start);
+    p.grp_fill = reinterpret_cast<int32_t*>(ws + w.grp_fill);
+    p.members = reinterpret_cast<int32_t*>(ws + w.members);
+    p.grp_task = reinterpret_cast<int32_t*>(ws + w.grp_task);
+    p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
+    p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
+    p.stats = reinterpret_cast<double*>(ws + w.stats);
+    p.meta = reinterpret_cast<int64_t*>(ws + w.meta);
+    p.d_status = d_status;
+    p.adv_tok = adv_tok;
+    p.idx = reinterpret_cast<int32_t*>(ws + w.idx);
+    p.adv_c = reinterpret_cast<float*>(ws + w.adv_c);
+    p.task_stats_out = task_stats;
+    p.n_mask_global_out = n_mask_global;
+    const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks);
+    if (smem > 48 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    const int64_t want = std::max<int64_t>(
+        {p.n_chunks, ceil_div(p.n_traj, COOP_THREADS), ceil_div(p.n_groups, COOP_THREADS), 1});
+    void* args[] = {&p};
+    if (!comm) {
+        const int grid = coop_grid((const void*)k_adv_coop_all, smem, want);
+        if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+        ProfScope ps(KID_STATS, stream);
+        AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_coop_all, grid, COOP_THREADS, args,
+                                            smem, stream));
+        count_launch();
+        return AGENTRL_OK;
+    }
+    const int grid = coop_grid((const void*)k_adv_coop_stats, 0, want);
+    if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+    {
+        ProfScope ps(KID_STATS, stream);
+        AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_coop_stats, grid, COOP_THREADS, args,
+                                            0, stream));
+        count_launch();
+    }
+    int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks, stream);
+    if (rc != AGENTRL_OK) return rc;
+    ProfScope ps(KID_APPLY, stream);
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_chunks, (int64_t)num_sms() * 8));
+    k_adv_coop_apply<<<g2, COOP_THREADS, smem, stream>>>(p);
+    count_launch();
+    AG_CUDA(cudaGetLastError());
+    return AGENTRL_OK;
+}
+
+}  // namespace agentrl

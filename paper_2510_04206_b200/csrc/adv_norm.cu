@@ -17,6 +17,7 @@
 // masked tokens; per trajectory ~40 B.  The kernels are launch-latency bound at the paper's
 // batch sizes.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -398,6 +399,8 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.grp_start = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.members = p.take(sizeof(int32_t) * (size_t)(n_traj + 1));
     w.adv_hat = p.take(sizeof(double) * (size_t)(n_traj + 1));
+    w.grp_task = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
+    w.grp_nsq = p.take(sizeof(double) * 3 * (size_t)(n_groups + 1));
     w.stats = p.take(sizeof(double) * (size_t)(3 * n_tasks + 1));
     w.meta = p.take(sizeof(int64_t) * 4);
     w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
@@ -409,6 +412,14 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
 int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
                     int64_t* n_mask_global, uint8_t* ws, const AdvWs& w, agentrl_comm comm,
                     int32_t* d_status, cudaStream_t stream) {
+    {
+        const char* e = getenv("AGENTRL_ADV_COOP");
+        if (!(e && e[0] == '0')) {
+            int rc = launch_adv_norm_coop(b, eps_std, adv_tok, task_stats, n_mask_global, ws, w,
+                                          comm, d_status, stream);
+            if (rc != AGENTRL_ERR_UNSUPPORTED) return rc;
+        }
+    }
     const int64_t T = b->T;
     const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
     int32_t* n_g = reinterpret_cast<int32_t*>(ws + w.n_g);

@@ -30,6 +30,8 @@ struct WsPlan {
 struct AdvWs {
     size_t n_g, chunk_cnt, chunk_base, grp_cnt, grp_start, grp_fill, members;  // int32
     size_t adv_hat;                                                               // double
+    size_t grp_task;  // int32 [n_groups] task of each group (cooperative path)
+    size_t grp_nsq;   // double [3*n_groups] per-group (N, S, Q) partials (cooperative path)
     size_t stats;     // double [3*n_tasks]: N_i, S_i, Q_i (local, then global)
     size_t meta;      // int64 [4]: n_mask_local, n_mask_global, pad
     size_t idx;       // int32 [T] compacted token positions
@@ -37,6 +39,12 @@ struct AdvWs {
     size_t total;
 };
 AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, size_t base = 0);
+
+// Cooperative single-kernel path (adv_coop.cu); returns AGENTRL_ERR_UNSUPPORTED if the grid
+// cannot be co-resident (caller falls back to the 3-kernel path).
+int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
+                         double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
+                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream);
 
 // Enqueue part 1.  Returns AGENTRL_* code.  comm may be null.
 int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
