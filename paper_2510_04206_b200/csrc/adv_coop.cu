@@ -37,7 +37,7 @@ struct AdvParams {
     const float* rewards;
     const uint8_t* mask;
     double eps_std;
-    int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task;
+    int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
     double *adv_hat, *grp_nsq, *stats;
     int64_t* meta;
     int32_t* d_status;
@@ -70,6 +70,42 @@ __device__ __forceinline__ void coop_mask16(const uint8_t* __restrict__ mask, in
 #pragma unroll
         for (int i = 0; i < 16; ++i) m[i] = (any_traj && t0 + i < T) ? mask[t0 + i] : 0;
     }
+}
+
+// Token -> trajectory lookup for one 4096-token chunk: the block stages off[first .. last+1]
+// of the trajectories that overlap the chunk into shared memory (one coalesced load) and every
+// thread binary-searches there, instead of ~log2(n_traj) dependent global loads per phase.
+constexpr int SOFF_CAP = 1024;
+struct ChunkTraj {
+    int32_t first, cnt;  // cnt = number of staged offsets (trajectories + 1); 0 = not staged
+};
+__device__ __forceinline__ ChunkTraj stage_chunk_offsets(const int64_t* __restrict__ off,
+                                                         const int32_t* __restrict__ chunk_first,
+                                                         int32_t n_traj, int64_t c,
+                                                         int64_t n_chunks, int64_t* s_off) {
+    ChunkTraj r{0, 0};
+    int32_t f = chunk_first[c];
+    int32_t l = (c + 1 < n_chunks) ? chunk_first[c + 1] : n_traj - 1;
+    f = min(max(f, 0), n_traj - 1);
+    l = min(max(l, f), n_traj - 1);
+    const int32_t cnt = l - f + 2;
+    r.first = f;
+    if (cnt <= SOFF_CAP) {
+        for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) s_off[i] = off[f + i];
+        r.cnt = cnt;
+    }
+    __syncthreads();
+    return r;
+}
+// local index k with s_off[k] <= t < s_off[k+1] (clamped)
+__device__ __forceinline__ int32_t smem_find(const int64_t* s_off, int32_t cnt, int64_t t) {
+    int32_t lo = 0, hi = cnt - 1;
+    while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (s_off[mid] <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // exclusive scan of one int per thread over a 256-thread block (returns prefix; total out)
@@ -165,18 +201,35 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         p.grp_cnt[i] = 0;
         p.grp_fill[i] = 0;
     }
+    for (int64_t g = gtid; g < p.n_traj; g += gstride) {  // chunks whose first token is in g
+        const int64_t a = p.off[g], b = p.off[g + 1];
+        const int64_t c_lo = (a + CHUNK_TOKENS - 1) / CHUNK_TOKENS;
+        const int64_t c_hi = min((b + CHUNK_TOKENS - 1) / CHUNK_TOKENS, p.n_chunks);
+        for (int64_t c = max(c_lo, (int64_t)0); c < c_hi; ++c) p.chunk_first[c] = (int32_t)g;
+    }
     grid.sync();
 
     // phase A
     const bool any_traj = p.n_traj > 0;
+    __shared__ int64_t s_off[SOFF_CAP];
     for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
         const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
+        ChunkTraj ct{0, 0};
+        if (any_traj) ct = stage_chunk_offsets(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_off);
         int32_t mine = 0;
         if (t0 < p.T && any_traj) {
-            int32_t g = coop_find_traj(p.off, p.n_traj, t0);
-            int64_t end = p.off[g + 1];
+            int32_t g, k = 0;
+            int64_t end;
+            if (ct.cnt) {
+                k = smem_find(s_off, ct.cnt, t0);
+                g = ct.first + k;
+                end = s_off[k + 1];
+            } else {
+                g = coop_find_traj(p.off, p.n_traj, t0);
+                end = p.off[g + 1];
+            }
             int32_t cnt = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -186,7 +239,8 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
                     if (cnt) atomicAdd(&p.n_g[g], cnt);
                     cnt = 0;
                     ++g;
-                    end = p.off[g + 1];
+                    ++k;
+                    end = (ct.cnt && k + 1 < ct.cnt) ? s_off[k + 1] : p.off[g + 1];
                 }
                 const int32_t bit = m[i] != 0;
                 cnt += bit;
@@ -195,7 +249,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
             if (cnt) atomicAdd(&p.n_g[g], cnt);
         }
         int32_t total;
-        coop_block_exscan(mine, s_w, total);
+        coop_block_exscan(mine, s_w, total);  // (its barriers also retire s_off for the next chunk)
         if (threadIdx.x == 0) p.chunk[c] = total;
     }
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
@@ -338,10 +392,13 @@ __device__ void coop_apply_phase(const AdvParams& p) {
         }
     }
     const bool any_traj = p.n_traj > 0;
+    __shared__ int64_t s_off[SOFF_CAP];
     for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
         const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
+        ChunkTraj ct{0, 0};
+        if (any_traj) ct = stage_chunk_offsets(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_off);
         int32_t mine = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) mine += m[i] != 0;
@@ -351,8 +408,16 @@ __device__ void coop_apply_phase(const AdvParams& p) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) outv[i] = 0.f;
         if (t0 < p.T && any_traj && mine > 0) {
-            int32_t g = coop_find_traj(p.off, p.n_traj, t0);
-            int64_t end = p.off[g + 1];
+            int32_t g, k = 0;
+            int64_t end;
+            if (ct.cnt) {
+                k = smem_find(s_off, ct.cnt, t0);
+                g = ct.first + k;
+                end = s_off[k + 1];
+            } else {
+                g = coop_find_traj(p.off, p.n_traj, t0);
+                end = p.off[g + 1];
+            }
             int32_t cur = -1;
             float at = 0.f;
 #pragma unroll
@@ -361,7 +426,8 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                 if (t >= p.T) break;
                 while (t >= end && g + 1 < p.n_traj) {
                     ++g;
-                    end = p.off[g + 1];
+                    ++k;
+                    end = (ct.cnt && k + 1 < ct.cnt) ? s_off[k + 1] : p.off[g + 1];
                 }
                 if (m[i]) {
                     if (g != cur) {  // Eq.1 for this trajectory
@@ -389,6 +455,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                     if (t0 + i < p.T) p.adv_tok[t0 + i] = outv[i];
             }
         }
+        __syncthreads();  // s_off is restaged by the next chunk
     }
 }
 
@@ -445,6 +512,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.grp_fill = reinterpret_cast<int32_t*>(ws + w.grp_fill);
     p.members = reinterpret_cast<int32_t*>(ws + w.members);
     p.grp_task = reinterpret_cast<int32_t*>(ws + w.grp_task);
+    p.chunk_first = reinterpret_cast<int32_t*>(ws + w.chunk_first);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
     p.stats = reinterpret_cast<double*>(ws + w.stats);

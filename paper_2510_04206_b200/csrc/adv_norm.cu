@@ -401,6 +401,7 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.adv_hat = p.take(sizeof(double) * (size_t)(n_traj + 1));
     w.grp_task = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.grp_nsq = p.take(sizeof(double) * 3 * (size_t)(n_groups + 1));
+    w.chunk_first = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.stats = p.take(sizeof(double) * (size_t)(3 * n_tasks + 1));
     w.meta = p.take(sizeof(int64_t) * 4);
     w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
