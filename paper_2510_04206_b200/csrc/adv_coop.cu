@@ -26,6 +26,7 @@ namespace cg = cooperative_groups;
 namespace agentrl {
 
 constexpr int COOP_THREADS = 256;
+constexpr int GMAX_BLOCKS = 2048;  // cap on the cooperative grid (per-block scratch arrays)
 
 struct AdvParams {
     int64_t T;
@@ -38,6 +39,8 @@ struct AdvParams {
     const uint8_t* mask;
     double eps_std;
     int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
+    int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
+    double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
     int64_t* meta;
     int32_t* d_status;
@@ -186,16 +189,45 @@ __device__ __forceinline__ double coop_block_sum(double v, double* s_red) {
     return r;  // thread 0
 }
 
+// ------------------------------------------------------------------ helpers
+// balanced contiguous partition of [0, n) over G blocks
+__device__ __forceinline__ int64_t part_lo(int64_t n, int64_t b, int64_t G) { return n * b / G; }
+// block owning item j under part_lo
+__device__ __forceinline__ int64_t part_owner(int64_t n, int64_t j, int64_t G) {
+    return ((j + 1) * G + n - 1) / n - 1;
+}
+// exclusive prefix over blocks of a per-block int array, computed by every block into smem
+__device__ void block_prefix_smem(const int32_t* __restrict__ blk, int64_t G, int32_t* s_pre,
+                                  int32_t* s_w) {
+    // G <= GMAX_BLOCKS; each thread scans a contiguous segment
+    const int64_t per = (G + COOP_THREADS - 1) / COOP_THREADS;
+    const int64_t lo = min(G, (int64_t)threadIdx.x * per), hi = min(G, lo + per);
+    int32_t sum = 0;
+    for (int64_t b = lo; b < hi; ++b) sum += blk[b];
+    int32_t total;
+    int32_t run = coop_block_exscan(sum, s_w, total);
+    for (int64_t b = lo; b < hi; ++b) {
+        s_pre[b] = run;
+        run += blk[b];
+    }
+    if (threadIdx.x == 0) s_pre[G] = total;
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ phases 0 .. B4
 __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     __shared__ int32_t s_w[8];
-    __shared__ int64_t s_seg[8];
     __shared__ double s_red[8];
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
+    __shared__ int64_t s_off[SOFF_CAP];
+    const int64_t G = gridDim.x, B = blockIdx.x;
+    const int64_t gtid = B * blockDim.x + threadIdx.x;
+    const int64_t gstride = G * blockDim.x;
     int32_t st = 0;
+    const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
+    const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
 
-    // phase 0
+    // phase 0: zero scratch; chunk -> first-trajectory table
     for (int64_t i = gtid; i < p.n_traj; i += gstride) p.n_g[i] = 0;
     for (int64_t i = gtid; i < p.n_groups; i += gstride) {
         p.grp_cnt[i] = 0;
@@ -203,16 +235,16 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     }
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {  // chunks whose first token is in g
         const int64_t a = p.off[g], b = p.off[g + 1];
-        const int64_t c_lo = (a + CHUNK_TOKENS - 1) / CHUNK_TOKENS;
-        const int64_t c_hi = min((b + CHUNK_TOKENS - 1) / CHUNK_TOKENS, p.n_chunks);
-        for (int64_t c = max(c_lo, (int64_t)0); c < c_hi; ++c) p.chunk_first[c] = (int32_t)g;
+        const int64_t lo = (a + CHUNK_TOKENS - 1) / CHUNK_TOKENS;
+        const int64_t hi = min((b + CHUNK_TOKENS - 1) / CHUNK_TOKENS, p.n_chunks);
+        for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
     }
     grid.sync();
 
-    // phase A
+    // phase A: this block's contiguous chunks: n_g (atomics), per-chunk counts, block total
     const bool any_traj = p.n_traj > 0;
-    __shared__ int64_t s_off[SOFF_CAP];
-    for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
+    int32_t blk_total = 0;
+    for (int64_t c = c_lo; c < c_hi; ++c) {
         const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
@@ -251,7 +283,9 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         int32_t total;
         coop_block_exscan(mine, s_w, total);  // (its barriers also retire s_off for the next chunk)
         if (threadIdx.x == 0) p.chunk[c] = total;
+        blk_total += total;
     }
+    if (threadIdx.x == 0) p.blk_chunk[B] = blk_total;
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int32_t j = p.group_id[g], i = p.task_id[g];
         if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
@@ -264,29 +298,40 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     grid.sync();
 
-    // phase B1 (block 0)
-    if (blockIdx.x == 0) {
-        const int64_t n_mask = coop_block_scan_array(p.chunk, p.n_chunks, s_seg);
-        for (int64_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) p.grp_start[j] = p.grp_cnt[j];
-        __syncthreads();
-        coop_block_scan_array(p.grp_start, p.n_groups, s_seg);
-        if (threadIdx.x == 0) p.meta[0] = n_mask;
+    // phase B1: local exclusive scan of K_j over this block's groups; block total
+    {
+        const int64_t n = j_hi - j_lo;
+        const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
+        const int64_t lo = j_lo + min(n, (int64_t)threadIdx.x * per);
+        const int64_t hi = min(j_hi, lo + per);
+        int32_t sum = 0;
+        for (int64_t j = lo; j < hi; ++j) sum += p.grp_cnt[j];
+        int32_t total;
+        int32_t run = coop_block_exscan(sum, s_w, total);
+        for (int64_t j = lo; j < hi; ++j) {
+            p.grp_start[j] = run;  // local start within this block's member range
+            run += p.grp_cnt[j];
+        }
+        if (threadIdx.x == 0) p.blk_grp[B] = total;
     }
     grid.sync();
 
-    // phase B2
+    // phase B2: global group starts = block prefix + local; scatter member lists
+    block_prefix_smem(p.blk_grp, G, s_pre, s_w);
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int32_t j = p.group_id[g], i = p.task_id[g];
         if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) continue;
+        const int64_t owner = part_owner(p.n_groups, j, G);
         const int32_t slot = atomicAdd(&p.grp_fill[j], 1);
-        p.members[p.grp_start[j] + slot] = (int32_t)g;
+        p.members[s_pre[owner] + p.grp_start[j] + slot] = (int32_t)g;
     }
     grid.sync();
 
-    // phase B3: per group (GRPO advantage; readings R1, R2, R14)
-    for (int64_t j = gtid; j < p.n_groups; j += gstride) {
+    // phase B3: this block's groups (GRPO advantage; readings R1, R2, R14), then the
+    // block's per-task partial (N, S, Q) in a fixed order
+    for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
         const int32_t K = p.grp_cnt[j];
-        int32_t* mb = p.members + p.grp_start[j];
+        int32_t* mb = p.members + s_pre[B] + p.grp_start[j];
         for (int a = 1; a < K; ++a) {
             const int32_t x = mb[a];
             int b = a - 1;
@@ -334,26 +379,47 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         p.grp_nsq[3 * j + 1] = S;
         p.grp_nsq[3 * j + 2] = Q;
     }
+    __syncthreads();
+    for (int32_t i = 0; i < p.n_tasks; ++i) {
+        double N = 0.0, S = 0.0, Q = 0.0;
+        for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS)
+            if (p.grp_task[j] == i) {
+                N += p.grp_nsq[3 * j];
+                S += p.grp_nsq[3 * j + 1];
+                Q += p.grp_nsq[3 * j + 2];
+            }
+        N = coop_block_sum(N, s_red);
+        S = coop_block_sum(S, s_red);
+        Q = coop_block_sum(Q, s_red);
+        if (threadIdx.x == 0) {
+            double* bp = p.blk_part + 3 * ((int64_t)B * p.n_tasks + i);
+            bp[0] = N;
+            bp[1] = S;
+            bp[2] = Q;
+        }
+    }
     if (st) atomicOr(p.d_status, st);
     grid.sync();
 
-    // phase B4 (block 0): per-task moments over the token set, fixed order
-    if (blockIdx.x == 0) {
-        const int64_t per = (p.n_groups + COOP_THREADS - 1) / COOP_THREADS;
-        const int64_t lo = min((int64_t)p.n_groups, (int64_t)threadIdx.x * per);
-        const int64_t hi = min((int64_t)p.n_groups, lo + per);
-        for (int32_t i = 0; i < p.n_tasks; ++i) {
+    // phase B4 (block 0): per-task moments over the token set = fixed-order sum
+    // of the block partials (warp w handles tasks w, w+8, ...; lanes stride over blocks)
+    if (B == 0) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int32_t i = wid; i < p.n_tasks; i += COOP_THREADS / 32) {
             double N = 0.0, S = 0.0, Q = 0.0;
-            for (int64_t j = lo; j < hi; ++j)
-                if (p.grp_task[j] == i) {
-                    N += p.grp_nsq[3 * j];
-                    S += p.grp_nsq[3 * j + 1];
-                    Q += p.grp_nsq[3 * j + 2];
-                }
-            N = coop_block_sum(N, s_red);
-            S = coop_block_sum(S, s_red);
-            Q = coop_block_sum(Q, s_red);
-            if (threadIdx.x == 0) {
+            for (int64_t b = lane; b < G; b += 32) {
+                const double* bp = p.blk_part + 3 * (b * p.n_tasks + i);
+                N += bp[0];
+                S += bp[1];
+                Q += bp[2];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                N += __shfl_down_sync(0xffffffffu, N, o);
+                S += __shfl_down_sync(0xffffffffu, S, o);
+                Q += __shfl_down_sync(0xffffffffu, Q, o);
+            }
+            if (lane == 0) {
                 p.stats[3 * i] = N;
                 p.stats[3 * i + 1] = S;
                 p.stats[3 * i + 2] = Q;
@@ -363,37 +429,43 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
 }
 
 // ------------------------------------------------------------------ phase C
+// (needs gridDim.x == the stats launch's grid: it owns the same contiguous chunk ranges)
 __device__ void coop_apply_phase(const AdvParams& p) {
-    extern __shared__ double s_task[];  // [2*n_tasks]: mu, 1/den (as den)
+    extern __shared__ double s_task[];  // [2*n_tasks]: mu, max(sigma, eps)
     __shared__ int32_t s_w[8];
+    __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
+    __shared__ int64_t s_off[SOFF_CAP];
+    const int64_t G = gridDim.x, B = blockIdx.x;
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
         const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
         const double mu = N > 0.0 ? S / N : 0.0;
         const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
         s_task[2 * i] = mu;
         s_task[2 * i + 1] = sd > p.eps_std ? sd : p.eps_std;
-        if (blockIdx.x == 0 && p.task_stats_out) {
+        if (B == 0 && p.task_stats_out) {
             p.task_stats_out[3 * i] = N;
             p.task_stats_out[3 * i + 1] = mu;
             p.task_stats_out[3 * i + 2] = sd;
         }
     }
-    __syncthreads();
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // also orders s_task writes
+    if (B == 0 && threadIdx.x < 32) {
         double nsum = 0.0;
         for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
         if (threadIdx.x == 0) {
             const int64_t n = (int64_t)nsum;
-            p.meta[1] = n;
+            p.meta[0] = s_pre[G];  // local masked rows
+            p.meta[1] = n;         // global N
             if (p.n_mask_global_out) *p.n_mask_global_out = n;
             if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
         }
     }
     const bool any_traj = p.n_traj > 0;
-    __shared__ int64_t s_off[SOFF_CAP];
-    for (int64_t c = blockIdx.x; c < p.n_chunks; c += gridDim.x) {
+    const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
+    int32_t base = s_pre[B];
+    for (int64_t c = c_lo; c < c_hi; ++c) {
         const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
@@ -403,7 +475,8 @@ __device__ void coop_apply_phase(const AdvParams& p) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) mine += m[i] != 0;
         int32_t total;
-        int32_t pos = p.chunk[c] + coop_block_exscan(mine, s_w, total);
+        int32_t pos = base + coop_block_exscan(mine, s_w, total);
+        base += total;
         float outv[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) outv[i] = 0.f;
@@ -482,7 +555,7 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
         per_sm <= 0)
         return 0;
     const int64_t cap = (int64_t)per_sm * num_sms();
-    return (int)std::max<int64_t>(1, std::min<int64_t>(cap, want));
+    return (int)std::max<int64_t>(1, std::min<int64_t>({cap, want, (int64_t)GMAX_BLOCKS}));
 }
 
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
@@ -513,6 +586,9 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.members = reinterpret_cast<int32_t*>(ws + w.members);
     p.grp_task = reinterpret_cast<int32_t*>(ws + w.grp_task);
     p.chunk_first = reinterpret_cast<int32_t*>(ws + w.chunk_first);
+    p.blk_chunk = reinterpret_cast<int32_t*>(ws + w.blk_chunk);
+    p.blk_grp = reinterpret_cast<int32_t*>(ws + w.blk_grp);
+    p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
     p.stats = reinterpret_cast<double*>(ws + w.stats);
@@ -548,8 +624,8 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks, stream);
     if (rc != AGENTRL_OK) return rc;
     ProfScope ps(KID_APPLY, stream);
-    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_chunks, (int64_t)num_sms() * 8));
-    k_adv_coop_apply<<<g2, COOP_THREADS, smem, stream>>>(p);
+    // same grid as the stats launch: phase C reuses its contiguous chunk partition
+    k_adv_coop_apply<<<grid, COOP_THREADS, smem, stream>>>(p);
     count_launch();
     AG_CUDA(cudaGetLastError());
     return AGENTRL_OK;

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace agentrl {
@@ -402,6 +404,9 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.grp_task = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.grp_nsq = p.take(sizeof(double) * 3 * (size_t)(n_groups + 1));
     w.chunk_first = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
+    w.blk_chunk = p.take(sizeof(int32_t) * 2048);
+    w.blk_grp = p.take(sizeof(int32_t) * 2048);
+    w.blk_part = p.take(sizeof(double) * 3 * 2048 * (size_t)std::max(n_tasks, 1));
     w.stats = p.take(sizeof(double) * (size_t)(3 * n_tasks + 1));
     w.meta = p.take(sizeof(int64_t) * 4);
     w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
