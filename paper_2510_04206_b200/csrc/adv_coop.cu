@@ -27,6 +27,9 @@ namespace agentrl {
 
 constexpr int COOP_THREADS = 256;
 constexpr int GMAX_BLOCKS = 2048;  // cap on the cooperative grid (per-block scratch arrays)
+constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 tokens)
+constexpr int WOFF_CAP = 64;       // trajectory offsets staged per warp chunk
+constexpr int NWARPS = COOP_THREADS / 32;
 
 struct AdvParams {
     int64_t T;
@@ -109,6 +112,34 @@ __device__ __forceinline__ int32_t smem_find(const int64_t* s_off, int32_t cnt, 
         else hi = mid;
     }
     return lo;
+}
+
+// warp-level staging of the offsets of the trajectories overlapping warp chunk c; returns the
+// number staged (0: too many, use the global binary search)
+__device__ __forceinline__ int32_t warp_stage(const int64_t* __restrict__ off,
+                                              const int32_t* __restrict__ wfirst, int32_t n_traj,
+                                              int64_t c, int64_t n_wchunks, int64_t* s_offw,
+                                              int32_t& first) {
+    const int lane = threadIdx.x & 31;
+    int32_t f = wfirst[c];
+    int32_t l = (c + 1 < n_wchunks) ? wfirst[c + 1] : n_traj - 1;
+    f = min(max(f, 0), n_traj - 1);
+    l = min(max(l, f), n_traj - 1);
+    const int32_t cnt = l - f + 2;
+    first = f;
+    if (cnt > WOFF_CAP) return 0;
+    for (int32_t i = lane; i < cnt; i += 32) s_offw[i] = off[f + i];
+    __syncwarp();
+    return cnt;
+}
+__device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
 }
 
 // exclusive scan of one int per thread over a 256-thread block (returns prefix; total out)
@@ -219,7 +250,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     __shared__ int32_t s_w[8];
     __shared__ double s_red[8];
     __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
-    __shared__ int64_t s_off[SOFF_CAP];
+    __shared__ int64_t s_off[NWARPS * WOFF_CAP];
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t gtid = B * blockDim.x + threadIdx.x;
     const int64_t gstride = G * blockDim.x;
@@ -235,29 +266,32 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     }
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {  // chunks whose first token is in g
         const int64_t a = p.off[g], b = p.off[g + 1];
-        const int64_t lo = (a + CHUNK_TOKENS - 1) / CHUNK_TOKENS;
-        const int64_t hi = min((b + CHUNK_TOKENS - 1) / CHUNK_TOKENS, p.n_chunks);
+        const int64_t lo = (a + WCHUNK - 1) / WCHUNK;
+        const int64_t hi = min((b + WCHUNK - 1) / WCHUNK, p.n_chunks);
         for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
     }
     grid.sync();
 
-    // phase A: this block's contiguous chunks: n_g (atomics), per-chunk counts, block total
+    // phase A: this block's contiguous warp chunks (512 tokens each, one warp per chunk):
+    // n_g (atomics), per-chunk counts, block total
     const bool any_traj = p.n_traj > 0;
-    int32_t blk_total = 0;
-    for (int64_t c = c_lo; c < c_hi; ++c) {
-        const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t* s_offw = s_off + warp * WOFF_CAP;
+    int32_t warp_total = 0;
+    for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
+        const int64_t t0 = c * WCHUNK + lane * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
-        ChunkTraj ct{0, 0};
-        if (any_traj) ct = stage_chunk_offsets(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_off);
+        int32_t first = 0, cnt_st = 0;
+        if (any_traj) cnt_st = warp_stage(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_offw, first);
         int32_t mine = 0;
         if (t0 < p.T && any_traj) {
             int32_t g, k = 0;
             int64_t end;
-            if (ct.cnt) {
-                k = smem_find(s_off, ct.cnt, t0);
-                g = ct.first + k;
-                end = s_off[k + 1];
+            if (cnt_st) {
+                k = smem_find(s_offw, cnt_st, t0);
+                g = first + k;
+                end = s_offw[k + 1];
             } else {
                 g = coop_find_traj(p.off, p.n_traj, t0);
                 end = p.off[g + 1];
@@ -272,7 +306,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
                     cnt = 0;
                     ++g;
                     ++k;
-                    end = (ct.cnt && k + 1 < ct.cnt) ? s_off[k + 1] : p.off[g + 1];
+                    end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
                 }
                 const int32_t bit = m[i] != 0;
                 cnt += bit;
@@ -280,11 +314,17 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
             }
             if (cnt) atomicAdd(&p.n_g[g], cnt);
         }
-        int32_t total;
-        coop_block_exscan(mine, s_w, total);  // (its barriers also retire s_off for the next chunk)
-        if (threadIdx.x == 0) p.chunk[c] = total;
-        blk_total += total;
+        const int32_t total = __shfl_sync(0xffffffffu, warp_incl_scan(mine), 31);
+        if (lane == 0) p.chunk[c] = total;
+        warp_total += total;
+        __syncwarp();  // s_offw restaged by this warp's next chunk
     }
+    if (lane == 0) s_w[warp] = warp_total;
+    __syncthreads();
+    int32_t blk_total = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < NWARPS; ++w) blk_total += s_w[w];
+    __syncthreads();
     if (threadIdx.x == 0) p.blk_chunk[B] = blk_total;
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int32_t j = p.group_id[g], i = p.task_id[g];
@@ -434,7 +474,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     extern __shared__ double s_task[];  // [2*n_tasks]: mu, max(sigma, eps)
     __shared__ int32_t s_w[8];
     __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
-    __shared__ int64_t s_off[SOFF_CAP];
+    __shared__ int64_t s_off[NWARPS * WOFF_CAP];
     const int64_t G = gridDim.x, B = blockIdx.x;
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
         const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
@@ -464,29 +504,45 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     }
     const bool any_traj = p.n_traj > 0;
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t* s_offw = s_off + warp * WOFF_CAP;
+    __shared__ int32_t s_cnt[2][NWARPS];
     int32_t base = s_pre[B];
-    for (int64_t c = c_lo; c < c_hi; ++c) {
-        const int64_t t0 = c * CHUNK_TOKENS + threadIdx.x * 16;
+    for (int64_t r = 0; c_lo + r * NWARPS < c_hi; ++r) {
+        // one barrier per round of NWARPS chunks: exchange their masked counts (double buffer)
+        const int64_t c = c_lo + r * NWARPS + warp;
+        const bool valid = c < c_hi;
+        int32_t* sc = s_cnt[r & 1];
+        if (lane == 0) sc[warp] = valid ? p.chunk[c] : 0;
+        __syncthreads();
+        int32_t wbase = base, round_total = 0;
+#pragma unroll
+        for (int w = 0; w < NWARPS; ++w) {
+            const int32_t v = sc[w];
+            if (w < warp) wbase += v;
+            round_total += v;
+        }
+        base += round_total;
+        if (!valid) continue;
+        const int64_t t0 = c * WCHUNK + lane * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
-        ChunkTraj ct{0, 0};
-        if (any_traj) ct = stage_chunk_offsets(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_off);
+        int32_t first = 0, cnt_st = 0;
+        if (any_traj) cnt_st = warp_stage(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_offw, first);
         int32_t mine = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) mine += m[i] != 0;
-        int32_t total;
-        int32_t pos = base + coop_block_exscan(mine, s_w, total);
-        base += total;
+        int32_t pos = wbase + warp_incl_scan(mine) - mine;
         float outv[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) outv[i] = 0.f;
         if (t0 < p.T && any_traj && mine > 0) {
             int32_t g, k = 0;
             int64_t end;
-            if (ct.cnt) {
-                k = smem_find(s_off, ct.cnt, t0);
-                g = ct.first + k;
-                end = s_off[k + 1];
+            if (cnt_st) {
+                k = smem_find(s_offw, cnt_st, t0);
+                g = first + k;
+                end = s_offw[k + 1];
             } else {
                 g = coop_find_traj(p.off, p.n_traj, t0);
                 end = p.off[g + 1];
@@ -500,7 +556,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                 while (t >= end && g + 1 < p.n_traj) {
                     ++g;
                     ++k;
-                    end = (ct.cnt && k + 1 < ct.cnt) ? s_off[k + 1] : p.off[g + 1];
+                    end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
                 }
                 if (m[i]) {
                     if (g != cur) {  // Eq.1 for this trajectory
@@ -528,7 +584,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                     if (t0 + i < p.T) p.adv_tok[t0 + i] = outv[i];
             }
         }
-        __syncthreads();  // s_off is restaged by the next chunk
+        __syncwarp();  // s_offw restaged by this warp's next chunk
     }
 }
 
@@ -571,7 +627,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.n_traj = b->n_traj;
     p.n_groups = b->n_groups;
     p.n_tasks = b->n_tasks;
-    p.n_chunks = ceil_div(b->T, CHUNK_TOKENS);
+    p.n_chunks = ceil_div(b->T, WCHUNK);
     p.off = b->traj_offsets;
     p.task_id = b->task_id;
     p.group_id = b->group_id;

@@ -391,7 +391,7 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     WsPlan p;
     p.off = base;
     AdvWs w;
-    const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    const int64_t n_chunks = ceil_div(T, 512);  // warp chunks (cooperative path; >= legacy)
     // the int32 scratch that must start zeroed is contiguous: n_g, grp_cnt, grp_fill
     w.n_g = p.take(sizeof(int32_t) * (size_t)(n_traj + 1));
     w.grp_cnt = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
