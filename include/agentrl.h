@@ -207,6 +207,10 @@ int agentrl_last_launch_count(void);
 int agentrl_profile_start(int max_pairs);
 int agentrl_profile_stop(double* host_ms_sum, int* host_counts, int n_ids);
 const char* agentrl_kernel_name(int id);
+/* Debug: %globaltimer stamps (ns) of the last single-GPU part-1 launch at its phase
+ * boundaries: [0] start, [1] after zero/table, [2] counts, [3] group scans, [4] member lists,
+ * [5] group advantages + task partials, [6] task moments, [7] apply/compaction end. */
+int agentrl_debug_adv_phase_ns(unsigned long long host_ns8[8]);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,7 @@ EXPORTED = (
     "agentrl_comm_unique_id", "agentrl_comm_init", "agentrl_comm_destroy",
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
+    "agentrl_debug_adv_phase_ns",
 )
 NUM_KERNEL_IDS = 10
 
@@ -188,6 +189,13 @@ def profile_stop() -> dict:
                                      NUM_KERNEL_IDS), "agentrl_profile_stop")
     return {_lib.agentrl_kernel_name(i).decode(): (float(ms[i]), int(cnt[i]))
             for i in range(NUM_KERNEL_IDS)}
+
+
+def debug_adv_phase_ns():
+    """Phase boundary timestamps (ns) of the last single-GPU agentrl_task_adv_norm launch."""
+    buf = (C.c_ulonglong * 8)()
+    _check(_lib.agentrl_debug_adv_phase_ns(buf), "agentrl_debug_adv_phase_ns")
+    return [int(x) for x in buf]
 
 
 def alloc_workspace(nbytes: int, device="cuda"):

@@ -31,6 +31,17 @@ constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 token
 constexpr int WOFF_CAP = 64;       // trajectory offsets staged per warp chunk
 constexpr int NWARPS = COOP_THREADS / 32;
 
+// phase timestamps of the last cooperative launch (block 0, after each grid barrier), read by
+// agentrl_debug_adv_phase_ns(); 8 x %globaltimer ns
+__device__ unsigned long long g_adv_phase_ns[8];
+__device__ __forceinline__ void phase_mark(int i) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_adv_phase_ns[i] = t;
+    }
+}
+
 struct AdvParams {
     int64_t T;
     int32_t n_traj, n_groups, n_tasks;
@@ -255,6 +266,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     const int64_t gtid = B * blockDim.x + threadIdx.x;
     const int64_t gstride = G * blockDim.x;
     int32_t st = 0;
+    phase_mark(0);
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
 
@@ -271,6 +283,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
     }
     grid.sync();
+    phase_mark(1);
 
     // phase A: this block's contiguous warp chunks (512 tokens each, one warp per chunk):
     // n_g (atomics), per-chunk counts, block total
@@ -337,6 +350,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     }
     if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     grid.sync();
+    phase_mark(2);
 
     // phase B1: local exclusive scan of K_j over this block's groups; block total
     {
@@ -355,6 +369,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         if (threadIdx.x == 0) p.blk_grp[B] = total;
     }
     grid.sync();
+    phase_mark(3);
 
     // phase B2: global group starts = block prefix + local; scatter member lists
     block_prefix_smem(p.blk_grp, G, s_pre, s_w);
@@ -366,6 +381,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         p.members[s_pre[owner] + p.grp_start[j] + slot] = (int32_t)g;
     }
     grid.sync();
+    phase_mark(4);
 
     // phase B3: this block's groups (GRPO advantage; readings R1, R2, R14), then the
     // block's per-task partial (N, S, Q) in a fixed order
@@ -440,6 +456,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     }
     if (st) atomicOr(p.d_status, st);
     grid.sync();
+    phase_mark(5);
 
     // phase B4 (block 0): per-task moments over the token set = fixed-order sum
     // of the block partials (warp w handles tasks w, w+8, ...; lanes stride over blocks)
@@ -592,7 +609,10 @@ __global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_all(const AdvParams p
     cg::grid_group grid = cg::this_grid();
     coop_stats_phases(p, grid);
     grid.sync();
+    phase_mark(6);
     coop_apply_phase(p);
+    grid.sync();
+    phase_mark(7);
 }
 
 __global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_stats(const AdvParams p) {
@@ -685,6 +705,13 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     count_launch();
     AG_CUDA(cudaGetLastError());
     return AGENTRL_OK;
+}
+
+int debug_adv_phase_ns(unsigned long long* host8) {
+    return cudaMemcpyFromSymbol(host8, g_adv_phase_ns, sizeof(unsigned long long) * 8) ==
+                   cudaSuccess
+               ? AGENTRL_OK
+               : AGENTRL_ERR_CUDA;
 }
 
 }  // namespace agentrl

@@ -298,6 +298,10 @@ const char* agentrl_status_string(int code) {
 
 int agentrl_version(void) { return 100; }
 
+int agentrl_debug_adv_phase_ns(unsigned long long* host_ns8) {
+    return host_ns8 ? debug_adv_phase_ns(host_ns8) : AGENTRL_ERR_INVALID_ARG;
+}
+
 int agentrl_profile_start(int max_pairs) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (max_pairs <= 0) return AGENTRL_ERR_INVALID_ARG;

@@ -100,6 +100,7 @@ struct ProfScope {
     ~ProfScope() { prof_mark(kid, false, s); }
 };
 int num_sms();
+int debug_adv_phase_ns(unsigned long long* host8);
 int check_device();  // AGENTRL_OK or AGENTRL_ERR_UNSUPPORTED / _CUDA
 
 }  // namespace agentrl

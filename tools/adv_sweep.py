@@ -69,7 +69,9 @@ def time_adv(b, iters=20, graph=False):
             times.append(e0.elapsed_time(e1))
     times.sort()
     ms = times[len(times) // 2]
-    return ms, int(nm.item())
+    ph = ag.debug_adv_phase_ns()
+    phases = [round((ph[i + 1] - ph[i]) / 1e3, 1) for i in range(7)]
+    return ms, int(nm.item()), phases
 
 
 def main():
@@ -86,12 +88,12 @@ def main():
     cases += [(c, synth.make_structure(synth.CONFIGS[c])) for c in a.configs.split(",") if c]
     for name, b in cases:
         for graph in (False, True):
-            ms, nm = time_adv(b, a.iters, graph)
+            ms, nm, phases = time_adv(b, a.iters, graph)
             by = alg_bytes(b)
             print(json.dumps({"case": name, "T": int(b["T"]), "n_traj": len(b["task_id"]),
                               "graph": graph, "latency_us": ms * 1e3, "alg_bytes": by,
                               "GBps": by / (ms / 1e3) / 1e9, "frac_hbm": by / (ms / 1e3) / 1e9 / hbm,
-                              "n_mask": nm}), flush=True)
+                              "n_mask": nm, "phase_us": phases}), flush=True)
 
 
 if __name__ == "__main__":
