@@ -30,6 +30,7 @@ constexpr int GMAX_BLOCKS = 2048;  // cap on the cooperative grid (per-block scr
 constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 tokens)
 constexpr int WOFF_CAP = 64;       // trajectory offsets staged per warp chunk
 constexpr int NWARPS = COOP_THREADS / 32;
+constexpr int TASK_BATCH = 16;  // tasks reduced per barrier in the per-block partials
 
 // phase timestamps of the last cooperative launch (block 0, after each grid barrier), read by
 // agentrl_debug_adv_phase_ns(); 8 x %globaltimer ns
@@ -54,6 +55,7 @@ struct AdvParams {
     double eps_std;
     int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
+    int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
     double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
     int64_t* meta;
@@ -334,11 +336,24 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     }
     if (lane == 0) s_w[warp] = warp_total;
     __syncthreads();
-    int32_t blk_total = 0;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < NWARPS; ++w) blk_total += s_w[w];
-    __syncthreads();
-    if (threadIdx.x == 0) p.blk_chunk[B] = blk_total;
+    // block-local exclusive scan of this block's chunk counts -> chunk_base (local), so that the
+    // apply phase can place every chunk without block-wide exchanges
+    {
+        const int64_t n = c_hi - c_lo;
+        const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
+        const int64_t lo = c_lo + min(n, (int64_t)threadIdx.x * per);
+        const int64_t hi = min(c_hi, lo + per);
+        int32_t sum = 0;
+        for (int64_t c = lo; c < hi; ++c) sum += p.chunk[c];
+        int32_t total;
+        int32_t run = coop_block_exscan(sum, s_w, total);
+        for (int64_t c = lo; c < hi; ++c) {
+            const int32_t v = p.chunk[c];
+            p.chunk_base[c] = run;
+            run += v;
+        }
+        if (threadIdx.x == 0) p.blk_chunk[B] = total;
+    }
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int32_t j = p.group_id[g], i = p.task_id[g];
         if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
@@ -436,22 +451,41 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         p.grp_nsq[3 * j + 2] = Q;
     }
     __syncthreads();
-    for (int32_t i = 0; i < p.n_tasks; ++i) {
-        double N = 0.0, S = 0.0, Q = 0.0;
-        for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS)
-            if (p.grp_task[j] == i) {
-                N += p.grp_nsq[3 * j];
-                S += p.grp_nsq[3 * j + 1];
-                Q += p.grp_nsq[3 * j + 2];
+    // per-task partials of this block: warp shuffles (fixed tree) + one barrier, tasks in
+    // batches of TASK_BATCH
+    {
+        __shared__ double s_wp[NWARPS][TASK_BATCH][3];
+        const int warp_b = threadIdx.x >> 5, lane_b = threadIdx.x & 31;
+        for (int32_t i0 = 0; i0 < p.n_tasks; i0 += TASK_BATCH) {
+            const int32_t nb = min(TASK_BATCH, p.n_tasks - i0);
+            for (int32_t ii = 0; ii < nb; ++ii) {
+                double N = 0.0, S = 0.0, Q = 0.0;
+                for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS)
+                    if (p.grp_task[j] == i0 + ii) {
+                        N += p.grp_nsq[3 * j];
+                        S += p.grp_nsq[3 * j + 1];
+                        Q += p.grp_nsq[3 * j + 2];
+                    }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    N += __shfl_down_sync(0xffffffffu, N, o);
+                    S += __shfl_down_sync(0xffffffffu, S, o);
+                    Q += __shfl_down_sync(0xffffffffu, Q, o);
+                }
+                if (lane_b == 0) {
+                    s_wp[warp_b][ii][0] = N;
+                    s_wp[warp_b][ii][1] = S;
+                    s_wp[warp_b][ii][2] = Q;
+                }
             }
-        N = coop_block_sum(N, s_red);
-        S = coop_block_sum(S, s_red);
-        Q = coop_block_sum(Q, s_red);
-        if (threadIdx.x == 0) {
-            double* bp = p.blk_part + 3 * ((int64_t)B * p.n_tasks + i);
-            bp[0] = N;
-            bp[1] = S;
-            bp[2] = Q;
+            __syncthreads();
+            if (threadIdx.x < 3 * nb) {
+                const int ii = threadIdx.x / 3, k = threadIdx.x % 3;
+                double v = 0.0;
+                for (int w = 0; w < NWARPS; ++w) v += s_wp[w][ii][k];
+                p.blk_part[3 * ((int64_t)B * p.n_tasks + i0 + ii) + k] = v;
+            }
+            __syncthreads();
         }
     }
     if (st) atomicOr(p.d_status, st);
@@ -523,24 +557,11 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t* s_offw = s_off + warp * WOFF_CAP;
-    __shared__ int32_t s_cnt[2][NWARPS];
-    int32_t base = s_pre[B];
-    for (int64_t r = 0; c_lo + r * NWARPS < c_hi; ++r) {
-        // one barrier per round of NWARPS chunks: exchange their masked counts (double buffer)
-        const int64_t c = c_lo + r * NWARPS + warp;
-        const bool valid = c < c_hi;
-        int32_t* sc = s_cnt[r & 1];
-        if (lane == 0) sc[warp] = valid ? p.chunk[c] : 0;
-        __syncthreads();
-        int32_t wbase = base, round_total = 0;
-#pragma unroll
-        for (int w = 0; w < NWARPS; ++w) {
-            const int32_t v = sc[w];
-            if (w < warp) wbase += v;
-            round_total += v;
-        }
-        base += round_total;
-        if (!valid) continue;
+    const int32_t blk_base = s_pre[B];
+    // every warp walks its own chunks with no block-wide exchange: the chunk's compaction base
+    // is the block prefix plus the local base stored by the counting phase
+    for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
+        const int32_t wbase = blk_base + p.chunk_base[c];
         const int64_t t0 = c * WCHUNK + lane * 16;
         uint8_t m[16];
         coop_mask16(p.mask, p.T, t0, any_traj, m);
@@ -663,6 +684,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.grp_task = reinterpret_cast<int32_t*>(ws + w.grp_task);
     p.chunk_first = reinterpret_cast<int32_t*>(ws + w.chunk_first);
     p.blk_chunk = reinterpret_cast<int32_t*>(ws + w.blk_chunk);
+    p.chunk_base = reinterpret_cast<int32_t*>(ws + w.wchunk_base);
     p.blk_grp = reinterpret_cast<int32_t*>(ws + w.blk_grp);
     p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
@@ -677,8 +699,9 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.n_mask_global_out = n_mask_global;
     const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks);
     if (smem > 48 * 1024) return AGENTRL_ERR_UNSUPPORTED;
-    const int64_t want = std::max<int64_t>(
-        {p.n_chunks, ceil_div(p.n_traj, COOP_THREADS), ceil_div(p.n_groups, COOP_THREADS), 1});
+    const int64_t want = std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
+                                            ceil_div(p.n_traj, COOP_THREADS),
+                                            ceil_div(p.n_groups, COOP_THREADS), 1});
     void* args[] = {&p};
     if (!comm) {
         const int grid = coop_grid((const void*)k_adv_coop_all, smem, want);
