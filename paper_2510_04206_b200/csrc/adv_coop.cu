@@ -155,6 +155,49 @@ __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
     return v;
 }
 
+// ---- software-pipelined chunk inputs: the mask bytes and trajectory range of the NEXT chunk
+// are loaded while the current chunk is processed (breaks the per-warp dependent-load chain)
+struct ChunkIn {
+    uint4 mk;
+    int32_t f, l, base;
+};
+__device__ __forceinline__ ChunkIn chunk_fetch(const AdvParams& p, int64_t c, bool any_traj,
+                                               bool want_base) {
+    ChunkIn r;
+    const int lane = threadIdx.x & 31;
+    const int64_t t0 = c * WCHUNK + lane * 16;
+    if (any_traj && t0 + 16 <= p.T && (reinterpret_cast<uintptr_t>(p.mask + t0) & 15) == 0) {
+        r.mk = __ldg(reinterpret_cast<const uint4*>(p.mask + t0));
+    } else {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        for (int i = 0; i < 16; ++i)
+            if (any_traj && t0 + i < p.T) w[i >> 2] |= (uint32_t)p.mask[t0 + i] << (8 * (i & 3));
+        r.mk = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    r.f = any_traj ? p.chunk_first[c] : 0;
+    r.l = (any_traj && c + 1 < p.n_chunks) ? p.chunk_first[c + 1] : p.n_traj - 1;
+    r.base = want_base ? p.chunk_base[c] : 0;
+    return r;
+}
+__device__ __forceinline__ void unpack16(const uint4& v, uint8_t (&m)[16]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+}
+__device__ __forceinline__ int32_t warp_stage_fl(const int64_t* __restrict__ off, int32_t f,
+                                                 int32_t l, int32_t n_traj, int64_t* s_offw,
+                                                 int32_t& first) {
+    const int lane = threadIdx.x & 31;
+    f = min(max(f, 0), n_traj - 1);
+    l = min(max(l, f), n_traj - 1);
+    const int32_t cnt = l - f + 2;
+    first = f;
+    if (cnt > WOFF_CAP) return 0;
+    for (int32_t i = lane; i < cnt; i += 32) s_offw[i] = off[f + i];
+    __syncwarp();
+    return cnt;
+}
+
 // exclusive scan of one int per thread over a 256-thread block (returns prefix; total out)
 __device__ __forceinline__ int32_t coop_block_exscan(int32_t v, int32_t* s_w, int32_t& total) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -293,12 +336,16 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t* s_offw = s_off + warp * WOFF_CAP;
     int32_t warp_total = 0;
+    ChunkIn nxt{};
+    if (c_lo + warp < c_hi) nxt = chunk_fetch(p, c_lo + warp, any_traj, false);
     for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
+        const ChunkIn cur = nxt;
+        if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, false);
         const int64_t t0 = c * WCHUNK + lane * 16;
         uint8_t m[16];
-        coop_mask16(p.mask, p.T, t0, any_traj, m);
+        unpack16(cur.mk, m);
         int32_t first = 0, cnt_st = 0;
-        if (any_traj) cnt_st = warp_stage(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_offw, first);
+        if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
         int32_t mine = 0;
         if (t0 < p.T && any_traj) {
             int32_t g, k = 0;
@@ -560,13 +607,17 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     const int32_t blk_base = s_pre[B];
     // every warp walks its own chunks with no block-wide exchange: the chunk's compaction base
     // is the block prefix plus the local base stored by the counting phase
+    ChunkIn nxt{};
+    if (c_lo + warp < c_hi) nxt = chunk_fetch(p, c_lo + warp, any_traj, true);
     for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
-        const int32_t wbase = blk_base + p.chunk_base[c];
+        const ChunkIn cur = nxt;
+        if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, true);
+        const int32_t wbase = blk_base + cur.base;
         const int64_t t0 = c * WCHUNK + lane * 16;
         uint8_t m[16];
-        coop_mask16(p.mask, p.T, t0, any_traj, m);
+        unpack16(cur.mk, m);
         int32_t first = 0, cnt_st = 0;
-        if (any_traj) cnt_st = warp_stage(p.off, p.chunk_first, p.n_traj, c, p.n_chunks, s_offw, first);
+        if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
         int32_t mine = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) mine += m[i] != 0;
@@ -626,7 +677,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     }
 }
 
-__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_all(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_all(const AdvParams p) {
     cg::grid_group grid = cg::this_grid();
     coop_stats_phases(p, grid);
     grid.sync();
@@ -636,12 +687,12 @@ __global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_all(const AdvParams p
     phase_mark(7);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_stats(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_stats(const AdvParams p) {
     cg::grid_group grid = cg::this_grid();
     coop_stats_phases(p, grid);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS) k_adv_coop_apply(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_apply(const AdvParams p) {
     coop_apply_phase(p);
 }
 
