@@ -65,6 +65,7 @@ struct AdvParams {
     float* adv_c;
     double* task_stats_out;
     int64_t* n_mask_global_out;
+    int32_t compact;  // write idx[] / adv_c[] (needed by the fused step only)
 };
 
 __device__ __forceinline__ int32_t coop_find_traj(const int64_t* __restrict__ off,
@@ -656,8 +657,10 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                                  : 0.f;
                     }
                     outv[i] = at;
-                    p.idx[pos] = (int32_t)t;
-                    p.adv_c[pos] = at;
+                    if (p.compact) {
+                        p.idx[pos] = (int32_t)t;
+                        p.adv_c[pos] = at;
+                    }
                     ++pos;
                 }
             }
@@ -708,7 +711,7 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
 
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
                          double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
-                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream) {
+                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream, bool compact) {
     int dev = 0;
     int coop = 0;
     cudaGetDevice(&dev);
@@ -748,6 +751,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.adv_c = reinterpret_cast<float*>(ws + w.adv_c);
     p.task_stats_out = task_stats;
     p.n_mask_global_out = n_mask_global;
+    p.compact = compact ? 1 : 0;
     const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks);
     if (smem > 48 * 1024) return AGENTRL_ERR_UNSUPPORTED;
     const int64_t want = std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),

@@ -418,12 +418,12 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
 
 int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
                     int64_t* n_mask_global, uint8_t* ws, const AdvWs& w, agentrl_comm comm,
-                    int32_t* d_status, cudaStream_t stream) {
+                    int32_t* d_status, cudaStream_t stream, bool compact) {
     {
         const char* e = getenv("AGENTRL_ADV_COOP");
         if (!(e && e[0] == '0')) {
             int rc = launch_adv_norm_coop(b, eps_std, adv_tok, task_stats, n_mask_global, ws, w,
-                                          comm, d_status, stream);
+                                          comm, d_status, stream, compact);
             if (rc != AGENTRL_ERR_UNSUPPORTED) return rc;
         }
     }

@@ -187,7 +187,7 @@ int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok
     if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
     return launch_adv_norm(b, eps_std, adv_tok, task_stats, n_mask_global,
                            static_cast<uint8_t*>(ws), w, comm, d_status,
-                           reinterpret_cast<cudaStream_t>(stream));
+                           reinterpret_cast<cudaStream_t>(stream), /*compact=*/false);
 }
 
 size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V) {

@@ -47,12 +47,14 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
 // cannot be co-resident (caller falls back to the 3-kernel path).
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
                          double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
-                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream);
+                         agentrl_comm comm, int32_t* d_status, cudaStream_t stream,
+                         bool compact);
 
 // Enqueue part 1.  Returns AGENTRL_* code.  comm may be null.
+// compact: also write the compaction (idx / adv_c) that part 2 consumes (fused step only)
 int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
                     int64_t* n_mask_global, uint8_t* ws, const AdvWs& w, agentrl_comm comm,
-                    int32_t* d_status, cudaStream_t stream);
+                    int32_t* d_status, cudaStream_t stream, bool compact = true);
 
 // ---- part 2 workspace (see lmhead.cu) ----
 struct LossWs {
