@@ -606,6 +606,9 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t* s_offw = s_off + warp * WOFF_CAP;
     const int32_t blk_base = s_pre[B];
+    // compaction staging (dynamic smem after s_task; present only when p.compact)
+    int32_t(*s_cidx)[WCHUNK] = reinterpret_cast<int32_t(*)[WCHUNK]>(s_task + 2 * p.n_tasks);
+    float(*s_cadv)[WCHUNK] = reinterpret_cast<float(*)[WCHUNK]>(s_task + 2 * p.n_tasks) + NWARPS;
     // every warp walks its own chunks with no block-wide exchange: the chunk's compaction base
     // is the block prefix plus the local base stored by the counting phase
     ChunkIn nxt{};
@@ -622,7 +625,9 @@ __device__ void coop_apply_phase(const AdvParams& p) {
         int32_t mine = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) mine += m[i] != 0;
-        int32_t pos = wbase + warp_incl_scan(mine) - mine;
+        const int32_t incl = warp_incl_scan(mine);
+        const int32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
+        int32_t pos = incl - mine;  // position within this warp chunk's compacted range
         float outv[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) outv[i] = 0.f;
@@ -657,9 +662,9 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                                  : 0.f;
                     }
                     outv[i] = at;
-                    if (p.compact) {
-                        p.idx[pos] = (int32_t)t;
-                        p.adv_c[pos] = at;
+                    if (p.compact) {  // staged in smem, written coalesced below
+                        s_cidx[warp][pos] = (int32_t)t;
+                        s_cadv[warp][pos] = at;
                     }
                     ++pos;
                 }
@@ -676,7 +681,14 @@ __device__ void coop_apply_phase(const AdvParams& p) {
                     if (t0 + i < p.T) p.adv_tok[t0 + i] = outv[i];
             }
         }
-        __syncwarp();  // s_offw restaged by this warp's next chunk
+        __syncwarp();  // s_offw restaged by this warp's next chunk; s_c* complete
+        if (p.compact) {
+            for (int32_t i = lane; i < wtotal; i += 32) {
+                p.idx[wbase + i] = s_cidx[warp][i];
+                p.adv_c[wbase + i] = s_cadv[warp][i];
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -752,8 +764,17 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.task_stats_out = task_stats;
     p.n_mask_global_out = n_mask_global;
     p.compact = compact ? 1 : 0;
-    const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks);
-    if (smem > 48 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks) +
+                        (compact ? (size_t)NWARPS * WCHUNK * 8 : 0);
+    if (smem > 96 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute((const void*)k_adv_coop_all,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute((const void*)k_adv_coop_apply,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        attr = true;
+    }
     const int64_t want = std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
                                             ceil_div(p.n_traj, COOP_THREADS),
                                             ceil_div(p.n_groups, COOP_THREADS), 1});
