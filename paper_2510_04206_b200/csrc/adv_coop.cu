@@ -712,11 +712,28 @@ __global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_apply(const AdvPar
 }
 
 static int coop_grid(const void* kern, size_t smem, int64_t want) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, COOP_THREADS, smem) !=
-            cudaSuccess ||
-        per_sm <= 0)
-        return 0;
+    // occupancy per (kernel, dynamic smem, device), cached: keeps the per-call host work small
+    struct Key {
+        const void* k;
+        size_t smem;
+        int dev;
+        int per_sm;
+    };
+    static thread_local Key cache[8];
+    static thread_local int n_cache = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = -1;
+    for (int i = 0; i < n_cache; ++i)
+        if (cache[i].k == kern && cache[i].smem == smem && cache[i].dev == dev) per_sm = cache[i].per_sm;
+    if (per_sm < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, COOP_THREADS, smem) !=
+            cudaSuccess)
+            per_sm = 0;
+        cache[n_cache % 8] = Key{kern, smem, dev, per_sm};
+        n_cache = n_cache < 8 ? n_cache + 1 : 8;
+    }
+    if (per_sm <= 0) return 0;
     const int64_t cap = (int64_t)per_sm * num_sms();
     return (int)std::max<int64_t>(1, std::min<int64_t>({cap, want, (int64_t)GMAX_BLOCKS}));
 }
@@ -724,10 +741,13 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
                          double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
                          agentrl_comm comm, int32_t* d_status, cudaStream_t stream, bool compact) {
+    static thread_local int coop = -1, coop_dev = -1;
     int dev = 0;
-    int coop = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (dev != coop_dev) {
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        coop_dev = dev;
+    }
     if (!coop) return AGENTRL_ERR_UNSUPPORTED;
     AdvParams p;
     p.T = b->T;

@@ -62,11 +62,14 @@ int num_sms() {
 int check_device() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return AGENTRL_ERR_CUDA;
+    static thread_local int ok_dev = -1;  // last device that passed the check
+    if (dev == ok_dev) return AGENTRL_OK;
     int major = 0, minor = 0;
     if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
         return AGENTRL_ERR_CUDA;
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     if (major != 10 || minor != 0) return AGENTRL_ERR_UNSUPPORTED;  // built for sm_100a only
+    ok_dev = dev;
     return AGENTRL_OK;
 }
 
