@@ -345,8 +345,32 @@ def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
             times.append(e0.elapsed_time(e1))
     times.sort()
     ms = times[len(times) // 2]
+    # the same call replayed from a CUDA graph (no host submission in the timed interval)
+    gms = None
+    try:
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s)
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s)
+            gt = []
+            for i in range(iters):
+                flush.fill_(float(i))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                g.replay()
+                e1.record(s)
+                e1.synchronize()
+                gt.append(e0.elapsed_time(e1))
+            gt.sort()
+            gms = gt[len(gt) // 2]
+    except Exception:  # graph capture unavailable: report the direct number only
+        gms = None
     by = 5 * T + 20 * n_traj
-    return {"latency_us": ms * 1e3, "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
+    return {"latency_us": ms * 1e3, "graph_latency_us": None if gms is None else gms * 1e3,
+            "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
             "frac_hbm": by / (ms / 1e3) / 1e9 / hbm_gbs, "cold_l2": True,
             "note": "launch-latency bound at this size; see profiles/*adv_sweep* for the T sweep"}
 

@@ -345,15 +345,14 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             s_f[j] = c_t * ex2_approx((pr[j].x - lse) * LOG2E);
         __syncthreads();
         const int32_t y = tgt_c[p];
-        for (int c = threadIdx.x; c < nvec; c += MERGE_THREADS) {
-            const int v0 = c * 8;
+        // 16-byte vectors, MERGE_UNROLL loads in flight per thread before any store
+        auto conv = [&](const uint4& in, int v0) -> uint4 {
             const float f = s_f[v0 >> 8];  // 256-column tiles
-            uint4 in = row4[c];
             const __half2* h2 = reinterpret_cast<const __half2*>(&in);
             float g[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                float2 x = __half22float2(h2[k]);
+                const float2 x = __half22float2(h2[k]);
                 g[2 * k] = f * x.x;
                 g[2 * k + 1] = f * x.y;
             }
@@ -365,8 +364,19 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             out.y = pack_bf162(g[2], g[3]);
             out.z = pack_bf162(g[4], g[5]);
             out.w = pack_bf162(g[6], g[7]);
-            row4[c] = out;
+            return out;
+        };
+        constexpr int MERGE_UNROLL = 4;
+        int c = threadIdx.x;
+        for (; c + (MERGE_UNROLL - 1) * MERGE_THREADS < nvec; c += MERGE_UNROLL * MERGE_THREADS) {
+            uint4 in[MERGE_UNROLL];
+#pragma unroll
+            for (int u = 0; u < MERGE_UNROLL; ++u) in[u] = row4[c + u * MERGE_THREADS];
+#pragma unroll
+            for (int u = 0; u < MERGE_UNROLL; ++u)
+                row4[c + u * MERGE_THREADS] = conv(in[u], (c + u * MERGE_THREADS) * 8);
         }
+        for (; c < nvec; c += MERGE_THREADS) row4[c] = conv(row4[c], c * 8);
         __syncthreads();
     }
 }
