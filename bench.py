@@ -237,26 +237,50 @@ def run_native(args, cfg, world, rank, local_rank):
         h2d = sum(x.numel() * x.element_size() for x in [hid_h, tgt_h, old_h, *meta_h.values()])
         d2h = loss_h.numel() * loss_h.element_size()
         stats_dev = torch.empty(5, dtype=torch.float64, device=dev)
+        # double-buffered device inputs: step k+1's host->device copy runs on a copy stream
+        # while step k computes (every copy is still inside the timed region)
+        sets = [dict(hid=hid, target=target, old=old, bd=bd),
+                dict(hid=torch.empty_like(hid), target=torch.empty_like(target),
+                     old=torch.empty_like(old),
+                     bd={k: (v.clone() if torch.is_tensor(v) else v) for k, v in bd.items()})]
+        main_s = torch.cuda.current_stream()
+        copy_s = torch.cuda.Stream(device=dev)
 
-        def e2e_step():
-            hid.copy_(hid_h, non_blocking=True)
-            target.copy_(tgt_h, non_blocking=True)
-            old.copy_(old_h, non_blocking=True)
+        def h2d(S):
+            S["hid"].copy_(hid_h, non_blocking=True)
+            S["target"].copy_(tgt_h, non_blocking=True)
+            S["old"].copy_(old_h, non_blocking=True)
             for k, v in meta_h.items():
-                bd[k].copy_(v, non_blocking=True)
-            one_step()
-            stats_dev[0:1].copy_(step.loss)
-            stats_dev[1:5].copy_(step.loss_stats)
-            loss_h.copy_(stats_dev, non_blocking=True)
+                S["bd"][k].copy_(v, non_blocking=True)
 
-        for _ in range(2):
-            e2e_step()
+        def run_e2e(n):
+            copy_s.wait_stream(main_s)
+            done, ready = [None, None], [None, None]
+            with torch.cuda.stream(copy_s):
+                h2d(sets[0])
+                ready[0] = copy_s.record_event()
+            for k in range(n):
+                i, j = k % 2, 1 - k % 2
+                if k + 1 < n:
+                    with torch.cuda.stream(copy_s):
+                        if done[j] is not None:
+                            copy_s.wait_event(done[j])
+                        h2d(sets[j])
+                        ready[j] = copy_s.record_event()
+                main_s.wait_event(ready[i])
+                S = sets[i]
+                step(S["bd"], S["hid"], W, S["target"], S["old"])
+                stats_dev[0:1].copy_(step.loss)
+                stats_dev[1:5].copy_(step.loss_stats)
+                loss_h.copy_(stats_dev, non_blocking=True)
+                done[i] = main_s.record_event()
+
+        run_e2e(2)
         torch.cuda.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        for _ in range(args.steps):
-            e2e_step()
+        run_e2e(args.steps)
         f1.record()
         torch.cuda.synchronize()
         barrier()
@@ -266,7 +290,9 @@ def run_native(args, cfg, world, rank, local_rank):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms_e2e = float(tt.item())
         e2e = {"value": T_global / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
+               "pipelining": "inputs double-buffered; step k+1's pinned H2D copy overlaps "
+                             "step k on a copy stream; loss/stats D2H after each step"}
 
     # ---- roofline of the dominant kernel (events recorded by the library, same stream)
     pk = peaks()
