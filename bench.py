@@ -246,7 +246,7 @@ def run_native(args, cfg, world, rank, local_rank):
         main_s = torch.cuda.current_stream()
         copy_s = torch.cuda.Stream(device=dev)
 
-        def h2d(S):
+        def copy_inputs(S):
             S["hid"].copy_(hid_h, non_blocking=True)
             S["target"].copy_(tgt_h, non_blocking=True)
             S["old"].copy_(old_h, non_blocking=True)
@@ -257,7 +257,7 @@ def run_native(args, cfg, world, rank, local_rank):
             copy_s.wait_stream(main_s)
             done, ready = [None, None], [None, None]
             with torch.cuda.stream(copy_s):
-                h2d(sets[0])
+                copy_inputs(sets[0])
                 ready[0] = copy_s.record_event()
             for k in range(n):
                 i, j = k % 2, 1 - k % 2
@@ -265,7 +265,7 @@ def run_native(args, cfg, world, rank, local_rank):
                     with torch.cuda.stream(copy_s):
                         if done[j] is not None:
                             copy_s.wait_event(done[j])
-                        h2d(sets[j])
+                        copy_inputs(sets[j])
                         ready[j] = copy_s.record_event()
                 main_s.wait_event(ready[i])
                 S = sets[i]
