@@ -189,6 +189,19 @@ int agentrl_comm_unique_id(unsigned char host_id[128]);
 int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned char host_id[128]);
 int agentrl_comm_destroy(agentrl_comm comm);
 
+/* Callback communicator: every all-reduce (sum, in place on the device buffer, ordered on
+ * `stream`) is delegated to fn(user, dev_buf, count, dtype, stream), called on the host at
+ * enqueue time in the same order on every rank; fn returns 0 on success.  For hosts without
+ * NCCL between the ranks (e.g. several ranks sharing one GPU in tests, or a custom fabric).
+ * dtype: AGENTRL_DTYPE_*. */
+#define AGENTRL_DTYPE_F64 0
+#define AGENTRL_DTYPE_F32 1
+#define AGENTRL_DTYPE_I64 2
+typedef int (*agentrl_allreduce_fn)(void* user, void* dev_buf, size_t count, int dtype,
+                                    agentrl_stream stream);
+int agentrl_comm_init_callback(agentrl_comm* out, int world, int rank, agentrl_allreduce_fn fn,
+                               void* user);
+
 /* ---- misc -------------------------------------------------------------- */
 const char* agentrl_status_string(int code); /* text for a return code or status bit */
 int agentrl_version(void);                    /* major*10000 + minor*100 + patch */

@@ -39,7 +39,7 @@ EXPORTED = (
     "agentrl_comm_unique_id", "agentrl_comm_init", "agentrl_comm_destroy",
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
-    "agentrl_debug_adv_phase_ns",
+    "agentrl_debug_adv_phase_ns", "agentrl_comm_init_callback",
 )
 NUM_KERNEL_IDS = 10
 
@@ -79,6 +79,8 @@ _lib.agentrl_grpo_step.argtypes = [C.POINTER(Batch), _f64, C.POINTER(LossArgs),
 _lib.agentrl_comm_unique_id.argtypes = [C.c_char_p]
 _lib.agentrl_comm_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_char_p]
 _lib.agentrl_comm_destroy.argtypes = [_P]
+_lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p]
 _lib.agentrl_status_string.argtypes = [C.c_int]
 _lib.agentrl_status_string.restype = C.c_char_p
 _lib.agentrl_version.restype = C.c_int
@@ -237,6 +239,66 @@ class Comm:
         if self.handle:
             _lib.agentrl_comm_destroy(self.handle)
             self.handle = None
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+
+
+class CallbackComm(Comm):
+    """Communicator whose all-reduces call back into Python (plumbing for hosts without NCCL
+    between the ranks, e.g. several test ranks sharing one GPU).  ``fn(dev_ptr, count, dtype,
+    stream_handle) -> None`` must all-reduce (sum) the device buffer in place, ordered on the
+    stream; dtype is 0 = f64, 1 = f32, 2 = i64."""
+
+    def __init__(self, world: int, rank: int, fn):
+        def _tramp(user, buf, n, dtype, stream):
+            try:
+                fn(buf, int(n), int(dtype), stream)
+                return 0
+            except Exception:  # noqa: BLE001 -- report failure through the C return code
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._cb = ALLREDUCE_FN(_tramp)  # keep alive
+        h = C.c_void_p()
+        _check(_lib.agentrl_comm_init_callback(C.byref(h), int(world), int(rank), self._cb, None),
+               "agentrl_comm_init_callback")
+        self.handle = h
+
+
+def gloo_allreduce_fn(group=None):
+    """Callback for CallbackComm: stream sync, device->host copy, torch.distributed
+    all_reduce (any backend, e.g. gloo), host->device copy (test plumbing)."""
+    import torch
+    import torch.distributed as dist
+    cudart = _cudart()
+    tmap = {0: torch.float64, 1: torch.float32, 2: torch.int64}
+
+    def fn(buf, n, dtype, stream):
+        torch.cuda.ExternalStream(stream).synchronize()
+        host = torch.empty(n, dtype=tmap[dtype])
+        nbytes = n * host.element_size()
+        if cudart.cudaMemcpy(C.c_void_p(host.data_ptr()), C.c_void_p(buf), C.c_size_t(nbytes), 2):
+            raise RuntimeError("cudaMemcpy D2H failed")
+        dist.all_reduce(host, group=group)
+        if cudart.cudaMemcpy(C.c_void_p(buf), C.c_void_p(host.data_ptr()), C.c_size_t(nbytes), 1):
+            raise RuntimeError("cudaMemcpy H2D failed")
+    return fn
+
+
+def _cudart():
+    import glob
+    import torch
+    cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime",
+                                   "lib", "libcudart.so*")) + ["libcudart.so.12"]
+    for c in cands:
+        try:
+            lib = C.CDLL(c)
+            lib.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+            return lib
+        except OSError:
+            continue
+    raise OSError("libcudart not found")
 
 
 class Step:

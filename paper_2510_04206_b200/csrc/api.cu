@@ -117,13 +117,24 @@ static NcclApi* nccl() {
 struct agentrl_comm_s {
     agentrl::nccl_comm_t comm;
     int world, rank;
+    agentrl_allreduce_fn fn;  // callback backend (non-null) instead of NCCL
+    void* user;
 };
 
 namespace agentrl {
 static int allreduce(agentrl_comm c, void* buf, size_t n, int dtype, cudaStream_t s) {
-    NcclApi* api = nccl();
-    if (!api || !c) return AGENTRL_ERR_NCCL;
+    if (!c) return AGENTRL_ERR_NCCL;
     if (n == 0) return AGENTRL_OK;
+    if (c->fn) {  // callback backend: dtype codes of include/agentrl.h
+        const int code = dtype == NCCL_FLOAT64 ? AGENTRL_DTYPE_F64
+                                               : (dtype == NCCL_FLOAT32 ? AGENTRL_DTYPE_F32
+                                                                        : AGENTRL_DTYPE_I64);
+        return c->fn(c->user, buf, n, code, reinterpret_cast<agentrl_stream>(s)) == 0
+                   ? AGENTRL_OK
+                   : AGENTRL_ERR_NCCL;
+    }
+    NcclApi* api = nccl();
+    if (!api) return AGENTRL_ERR_NCCL;
     return api->allReduce(buf, buf, n, dtype, NCCL_SUM, c->comm, s) == 0 ? AGENTRL_OK
                                                                          : AGENTRL_ERR_NCCL;
 }
@@ -262,7 +273,7 @@ int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned cha
     if (!api) return AGENTRL_ERR_NCCL;
     nccl_uid_t id;
     memcpy(id.internal, host_id, 128);
-    agentrl_comm c = new agentrl_comm_s{nullptr, world, rank};
+    agentrl_comm c = new agentrl_comm_s{nullptr, world, rank, nullptr, nullptr};
     if (api->commInitRank(&c->comm, world, id, rank) != 0) {
         delete c;
         return AGENTRL_ERR_NCCL;
@@ -271,8 +282,19 @@ int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned cha
     return AGENTRL_OK;
 }
 
+int agentrl_comm_init_callback(agentrl_comm* out, int world, int rank, agentrl_allreduce_fn fn,
+                               void* user) {
+    if (!out || world <= 0 || rank < 0 || rank >= world || !fn) return AGENTRL_ERR_INVALID_ARG;
+    *out = new agentrl_comm_s{nullptr, world, rank, fn, user};
+    return AGENTRL_OK;
+}
+
 int agentrl_comm_destroy(agentrl_comm comm) {
     if (!comm) return AGENTRL_OK;
+    if (comm->fn) {
+        delete comm;
+        return AGENTRL_OK;
+    }
     NcclApi* api = nccl();
     int rc = AGENTRL_OK;
     if (api && comm->comm && api->commDestroy(comm->comm) != 0) rc = AGENTRL_ERR_NCCL;

@@ -1,0 +1,105 @@
+"""Two ranks on one GPU: the sharded data path of the library (split cooperative adv-norm
+launches around the statistics all-reduce, the loss all-reduce, the grad_W all-reduce on the
+side stream) against the fp64 oracle on the GLOBAL batch (R6).  NCCL cannot place two ranks
+on one device, so the ranks use the callback communicator with a gloo all-reduce; the
+library-side collective placement is the same as with NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, out_dir, cfg_name):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import synth
+    import paper_2510_04206_b200 as ag
+    from gpu_util import batch_dev, bf16_dev, f64, t
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = synth.CONFIGS[cfg_name]
+    gb = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=gb["loss_mask"])
+    h, W = f64(hb), f64(Wb)
+    lp = oracle.logprob(h, W, y, gb["loss_mask"])
+    old = (lp + synth.make_deltas(cfg.T, 23)).astype(np.float32)
+    off = gb["traj_offsets"]
+    cs = np.concatenate([[0], np.cumsum(gb["loss_mask"].astype(np.int64))])
+    ng = cs[off[1:]] - cs[off[:-1]]
+    rog = synth.shard_groups_lpt(np.bincount(gb["group_id"], weights=ng,
+                                             minlength=gb["n_groups"]), world)
+    lb = synth.shard_batch(gb, rog, rank)
+    tok = lb["token_index"]
+    comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn())
+    step = ag.Step(lb["T"], len(lb["task_id"]), lb["n_groups"], lb["n_tasks"], cfg.d, cfg.V,
+                   comm=comm)
+    step(batch_dev(lb), bf16_dev(hb[tok]), bf16_dev(Wb), t(y[tok], torch.int32),
+         t(old[tok], torch.float32))
+    torch.cuda.synchronize()
+    res = dict(loss=step.loss.item(), adv=step.adv_tok.cpu().numpy(),
+               gh=step.grad_hidden.float().cpu().numpy(), gw=step.grad_W.cpu().numpy(),
+               ts=step.task_stats.cpu().numpy(), st=int(step.status.item()), tok=tok)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), **res)
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_name", ["tiny", "ragged"])
+def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    import oracle
+    import synth
+    from gpu_util import adv_close, f64, max_abs_rel
+
+    mp.spawn(_rank, args=(2, _port(), str(tmp_path), cfg_name), nprocs=2, join=True)
+    cfg = synth.CONFIGS[cfg_name]
+    gb = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=gb["loss_mask"])
+    h, W = f64(hb), f64(Wb)
+    lp = oracle.logprob(h, W, y, gb["loss_mask"])
+    old = (lp + synth.make_deltas(cfg.T, 23)).astype(np.float32)
+    ref = oracle.grpo_step(gb, h, W, y, old.astype(np.float64))
+    r = [dict(np.load(tmp_path / f"r{k}.npz")) for k in range(2)]
+    N = int((gb["loss_mask"] != 0).sum())
+    for k in range(2):
+        assert r[k]["st"] & ~16 == 0
+        # global (all-reduced) results are identical on both ranks
+        assert abs(r[k]["loss"] - ref["loss"]) <= 1e-3 * max(abs(ref["loss"]), 1.0 / N) + 1e-9
+        assert max_abs_rel(r[k]["gw"], ref["grad_W"]) <= 2e-2
+        np.testing.assert_array_equal(r[k]["ts"][:, 0], ref["task_stats"][:, 0])
+        np.testing.assert_allclose(r[k]["ts"][:, 1:], ref["task_stats"][:, 1:], rtol=1e-9,
+                                   atol=1e-12)
+        # rank-local rows
+        tok = r[k]["tok"]
+        assert adv_close(r[k]["adv"], ref["adv_tok"][tok])
+    np.testing.assert_array_equal(r[0]["gw"], r[1]["gw"])
+    gh = np.zeros_like(ref["grad_hidden"])
+    for k in range(2):
+        gh[r[k]["tok"]] = r[k]["gh"]
+    assert max_abs_rel(gh, ref["grad_hidden"]) <= 2e-2
