@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libagentrl.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} not built: run `python -m paper_2510_04206_b200.build` "
+        f"{LIB_PATH} not built: run `python paper_2510_04206_b200/build.py` "
         "(there is no CPU fallback for this package)")
 
 _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)

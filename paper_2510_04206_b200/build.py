@@ -1,6 +1,9 @@
 """Build libagentrl.so (sm_100a) in-tree with nvcc.
 
-    python -m paper_2510_04206_b200.build [--force] [--verbose]
+    python paper_2510_04206_b200/build.py [--force] [--verbose] [--ptxas-v]
+
+(run as a script or load by path: importing it through the package would run the package
+__init__, which refuses to load without the library)
 
 Every .cu under csrc/ is compiled with
     -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo

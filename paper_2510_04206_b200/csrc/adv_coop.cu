@@ -305,7 +305,6 @@ __device__ void block_prefix_smem(const int32_t* __restrict__ blk, int64_t G, in
 // ------------------------------------------------------------------ phases 0 .. B4
 __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     __shared__ int32_t s_w[8];
-    __shared__ double s_red[8];
     __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
     __shared__ int64_t s_off[NWARPS * WOFF_CAP];
     const int64_t G = gridDim.x, B = blockIdx.x;

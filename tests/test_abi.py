@@ -21,8 +21,20 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def libpath():
-    from paper_2510_04206_b200 import build
-    return build.build()
+    import __graft_entry__
+    return __graft_entry__._load_builder().build()
+
+
+def test_build_works_without_prebuilt_library(tmp_path):
+    """A fresh checkout has no .so: the builder (loaded by path, never through the package,
+    whose __init__ refuses to load without the library) must produce one from scratch."""
+    import __graft_entry__
+    b = __graft_entry__._load_builder()
+    b.LIB = str(tmp_path / "libagentrl.so")
+    b.BUILD = str(tmp_path / "obj")
+    out = b.build(force=True)
+    lib = ctypes.CDLL(out)
+    assert hasattr(lib, "agentrl_grpo_step")
 
 
 def test_library_exports_every_declared_symbol(libpath):
