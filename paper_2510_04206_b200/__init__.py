@@ -275,7 +275,10 @@ def gloo_allreduce_fn(group=None):
     tmap = {0: torch.float64, 1: torch.float32, 2: torch.int64}
 
     def fn(buf, n, dtype, stream):
-        torch.cuda.ExternalStream(stream).synchronize()
+        if stream:  # a null handle is the legacy default stream
+            torch.cuda.ExternalStream(stream).synchronize()
+        else:
+            torch.cuda.synchronize()
         host = torch.empty(n, dtype=tmap[dtype])
         nbytes = n * host.element_size()
         if cudart.cudaMemcpy(C.c_void_p(host.data_ptr()), C.c_void_p(buf), C.c_size_t(nbytes), 2):
