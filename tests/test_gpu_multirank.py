@@ -66,6 +66,35 @@ def _rank(rank, world, port, out_dir, cfg_name):
     dist.destroy_process_group()
 
 
+def test_nccl_world1_matches_no_comm():
+    """The real NCCL communicator (dlopen'd libnccl, unique id, init, all-reduces incl. the
+    grad_W one on the side stream) at world size 1 gives bitwise the single-GPU result."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import synth
+    import paper_2510_04206_b200 as ag
+    from gpu_util import batch_dev, bf16_dev, t
+
+    cfg = synth.CONFIGS["ragged"]
+    b = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
+    old = synth.make_old_logp_free(cfg.T, 5)
+    args = (batch_dev(b), bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32), t(old, torch.float32))
+    s0 = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V)
+    s0(*args)
+    comm = ag.Comm(1, 0, ag.Comm.unique_id())
+    s1 = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V, comm=comm)
+    s1(*args)
+    torch.cuda.synchronize()
+    for a, c in ((s0.loss, s1.loss), (s0.adv_tok, s1.adv_tok), (s0.grad_W, s1.grad_W),
+                 (s0.grad_hidden, s1.grad_hidden), (s0.task_stats, s1.task_stats)):
+        assert torch.equal(a, c)
+    comm.destroy()
+
+
 @pytest.mark.parametrize("cfg_name", ["tiny", "ragged"])
 def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name):
     torch = pytest.importorskip("torch")
