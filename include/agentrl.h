@@ -180,6 +180,31 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
                       void* ws, size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                       agentrl_stream stream);
 
+/*
+ * Forward-only token log-probs and entropies (no backward): the
+ * trainer's recomputation of behaviour / reference log-probs pi_old and the policy
+ * entropy that DAPO's clip-higher targets.  For every masked token t:
+ *   logp[t]    = z_{t,y_t} - logsumexp_v z_{t,v},  z = logit_scale * <hidden_t, W_v>
+ *   entropy[t] = -sum_v p_{t,v} log p_{t,v}        (optional output)
+ * Unmasked tokens get 0.  Same shapes/alignment rules as part 2; status bits
+ * AGENTRL_ST_BAD_TARGET / AGENTRL_ST_NONFINITE.
+ */
+typedef struct {
+    int64_t T;
+    int32_t d, V;
+    const void* hidden;  /* __nv_bfloat16 [T,d] */
+    const void* W_head;  /* __nv_bfloat16 [V,d] */
+    const int32_t* target;
+    const uint8_t* loss_mask;
+    float logit_scale;
+    int32_t reserved;
+} agentrl_logprob_args;
+
+size_t agentrl_logprob_workspace_size(int64_t T, int32_t d, int32_t V);
+int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp /*[T]*/,
+                        float* entropy /*[T] or NULL*/, void* ws, size_t ws_bytes,
+                        int32_t* d_status, agentrl_stream stream);
+
 /* ---- communicator (NCCL over NVLink; loaded lazily with dlopen) ----------
  * Rank 0 calls agentrl_comm_unique_id, the caller broadcasts the 128 bytes
  * (e.g. over a torch.distributed process group), then every rank calls
@@ -215,8 +240,8 @@ int agentrl_last_launch_count(void);
  * on), up to n pairs.  agentrl_profile_stop synchronises those events and
  * writes, per kernel id, the summed milliseconds and the launch count.  Kernel
  * ids: 0 count, 1 stats, 2 apply, 3 compact, 4 gather, 5 fwd GEMM, 6 merge+G,
- * 7 loss reduce, 8 grad_W GEMM, 9 grad_hidden GEMM. */
-#define AGENTRL_NUM_KERNEL_IDS 10
+ * 7 loss reduce, 8 grad_W GEMM, 9 grad_hidden GEMM, 10 log-prob GEMM, 11 log-prob merge. */
+#define AGENTRL_NUM_KERNEL_IDS 12
 int agentrl_profile_start(int max_pairs);
 int agentrl_profile_stop(double* host_ms_sum, int* host_counts, int n_ids);
 const char* agentrl_kernel_name(int id);

@@ -63,6 +63,7 @@ def lib():
         L.oracle_logprob.argtypes = [i64, i32, i32, P, P, P, P, f64, P]
         L.oracle_grpo_step.argtypes = [i64, i32, i32, i32, P, P, P, P, P, f64, i32, i32, P, P, P,
                                        P, f64, f64, f64, P, P, P, P, P, P, P]
+        L.oracle_logprob_entropy.argtypes = [i64, i32, i32, P, P, P, P, f64, P, P]
         L.oracle_num_threads.restype = C.c_int
         L.oracle_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -192,6 +193,21 @@ def logprob(hidden, W, target, loss_mask, logit_scale=1.0):
     if st != 0:
         raise ValueError(f"oracle_logprob status {st}")
     return out
+
+
+def logprob_entropy(hidden, W, target, loss_mask, logit_scale=1.0):
+    """(logp, entropy) of every masked token; plain definitions."""
+    h = _c(hidden, np.float64)
+    w = _c(W, np.float64)
+    T, d = h.shape
+    lp = np.zeros(T, np.float64)
+    ent = np.zeros(T, np.float64)
+    st = lib().oracle_logprob_entropy(T, d, w.shape[0], _p(h), _p(w), _p(_c(target, np.int32)),
+                                      _p(_c(loss_mask, np.uint8)), float(logit_scale), _p(lp),
+                                      _p(ent))
+    if st != 0:
+        raise ValueError(f"oracle_logprob_entropy status {st}")
+    return lp, ent
 
 
 def grpo_step(b, hidden, W, target, old_logp, eps_std=1e-6, eps_lo=0.2, eps_hi=0.2,

@@ -514,3 +514,41 @@ int oracle_grpo_step(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_task
     free(at);
     return st;
 }
+
+/*
+ * Forward-only log-prob and entropy of every masked token (the token
+ * distribution of P:1186-1190).  Plain definitions in fp64:
+ *   p_v = exp(z_v - lse),  logp_t = z_y - lse,  H_t = -sum_v p_v log p_v = -sum_v p_v (z_v - lse)
+ * Unmasked tokens get 0.
+ */
+int oracle_logprob_entropy(int64_t T, int32_t d, int32_t V, const double* hidden,
+                           const double* W, const int32_t* target, const uint8_t* loss_mask,
+                           double logit_scale, double* logp_out /*[T]*/,
+                           double* ent_out /*[T]*/) {
+    if (T < 0 || d <= 0 || V <= 0 || !(logit_scale > 0)) return OR_ERR_ARG;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t t = 0; t < T; ++t) {
+        if (!loss_mask[t]) {
+            logp_out[t] = 0.0;
+            ent_out[t] = 0.0;
+            continue;
+        }
+        double* z = (double*)malloc(sizeof(double) * (size_t)V);
+        token_logits(d, V, hidden + (size_t)t * (size_t)d, W, logit_scale, z);
+        double m = z[0];
+        for (int32_t v = 1; v < V; ++v)
+            if (z[v] > m) m = z[v];
+        double se = 0.0;
+        for (int32_t v = 0; v < V; ++v) se += exp(z[v] - m);
+        const double lse = m + log(se);
+        double H = 0.0;
+        for (int32_t v = 0; v < V; ++v) {
+            const double lp = z[v] - lse;
+            H -= exp(lp) * lp;
+        }
+        logp_out[t] = z[target[t]] - lse;
+        ent_out[t] = H;
+        free(z);
+    }
+    return 0;
+}

@@ -40,8 +40,15 @@ EXPORTED = (
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
     "agentrl_debug_adv_phase_ns", "agentrl_comm_init_callback",
+    "agentrl_logprob_workspace_size", "agentrl_logprob_fwd",
 )
-NUM_KERNEL_IDS = 10
+NUM_KERNEL_IDS = 12
+
+
+class LogprobArgs(C.Structure):
+    _fields_ = [("T", C.c_int64), ("d", C.c_int32), ("V", C.c_int32), ("hidden", C.c_void_p),
+                ("W_head", C.c_void_p), ("target", C.c_void_p), ("loss_mask", C.c_void_p),
+                ("logit_scale", C.c_float), ("reserved", C.c_int32)]
 
 
 class Batch(C.Structure):
@@ -81,6 +88,9 @@ _lib.agentrl_comm_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_
 _lib.agentrl_comm_destroy.argtypes = [_P]
 _lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p,
                                             C.c_void_p]
+_lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i32, _i32]
+_lib.agentrl_logprob_workspace_size.restype = _sz
+_lib.agentrl_logprob_fwd.argtypes = [C.POINTER(LogprobArgs), _P, _P, _P, _sz, _P, _P]
 _lib.agentrl_status_string.argtypes = [C.c_int]
 _lib.agentrl_status_string.restype = C.c_char_p
 _lib.agentrl_version.restype = C.c_int
@@ -171,6 +181,20 @@ def agentrl_grpo_step(batch: Batch, eps_std, args: LossArgs, out: LossOut, adv_t
                                   _ptr(adv_tok_out), _ptr(task_stats), _ptr(ws),
                                   ws.numel() * ws.element_size(), comm, _ptr(d_status),
                                   _stream(stream))
+
+
+def agentrl_logprob_workspace_size(T, d, V) -> int:
+    return int(_lib.agentrl_logprob_workspace_size(T, d, V))
+
+
+def agentrl_logprob_fwd(T, hidden, W_head, target, loss_mask, logp, entropy, ws, d_status,
+                        logit_scale=1.0, stream=None) -> int:
+    """Forward-only log-probs (and entropies if ``entropy`` is a tensor) of the masked tokens."""
+    a = LogprobArgs(int(T), int(hidden.shape[1]), int(W_head.shape[0]), _ptr(hidden),
+                    _ptr(W_head), _ptr(target), _ptr(loss_mask), float(logit_scale), 0)
+    return _lib.agentrl_logprob_fwd(C.byref(a), _ptr(logp), _ptr(entropy), _ptr(ws),
+                                    ws.numel() * ws.element_size(), _ptr(d_status),
+                                    _stream(stream))
 
 
 def last_launch_count() -> int:

@@ -222,6 +222,27 @@ int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_o
                               nullptr, comm, d_status, reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t agentrl_logprob_workspace_size(int64_t T, int32_t d, int32_t V) {
+    return plan_logp(T, d, V).total;
+}
+
+int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp, float* entropy, void* ws,
+                        size_t ws_bytes, int32_t* d_status, agentrl_stream stream) {
+    g_launches = 0;
+    if (!a || !logp || !d_status || !ws || !a->hidden || !a->W_head || !a->target ||
+        !a->loss_mask || !(a->logit_scale > 0.f))
+        return AGENTRL_ERR_INVALID_ARG;
+    if (a->T < 0 || a->T >= (int64_t)1 << 31 || a->d <= 0 || a->d % 64 != 0 || a->V < 8 ||
+        a->V % 8 != 0 || !aligned(a->hidden, 16) || !aligned(a->W_head, 16))
+        return AGENTRL_ERR_SHAPE;
+    int rc = check_device();
+    if (rc) return rc;
+    LogpWs w = plan_logp(a->T, a->d, a->V);
+    if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
+    return launch_logprob(a, logp, entropy, static_cast<uint8_t*>(ws), w, d_status,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t agentrl_grpo_step_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
                                         int32_t n_tasks, int32_t d, int32_t V) {
     AdvWs wa = plan_adv(T, n_traj, n_groups, n_tasks);
@@ -372,7 +393,8 @@ int agentrl_profile_stop(double* ms_sum, int* counts, int n_ids) {
 const char* agentrl_kernel_name(int id) {
     static const char* names[KID_N] = {"k_count", "k_stats", "k_apply", "k_compact",
                                        "k_gather", "gemm_fwd", "k_merge_g", "k_loss_reduce",
-                                       "gemm_grad_W", "gemm_grad_hidden"};
+                                       "gemm_grad_W", "gemm_grad_hidden", "gemm_logp",
+                                       "k_logp_merge"};
     return (id >= 0 && id < KID_N) ? names[id] : "unknown";
 }
 int agentrl_last_launch_count(void) { return g_launches; }

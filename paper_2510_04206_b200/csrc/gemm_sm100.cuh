@@ -56,7 +56,9 @@ struct GemmCfg {
     static constexpr int TX_BYTES = (GEMM_A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
 
-enum { EPI_FWD = 0, EPI_GRADH = 1, EPI_GRADW = 2 };
+// EPI_LOGP: forward-only log-prob/entropy statistics (no P~ store): per (row, tile)
+// (m, l', u = sum exp(z - m) z)
+enum { EPI_FWD = 0, EPI_GRADH = 1, EPI_GRADW = 2, EPI_LOGP = 3 };
 
 struct GemmArgs {
     // problem: rows M (dynamic if m_dev), cols N, reduction K (dynamic if k_dev)
@@ -72,7 +74,8 @@ struct GemmArgs {
     const int32_t* tgt;  // [rows] target token of each compacted row
     __half* P;           // [rows, ldP] exp(z - m), fp16
     int64_t ldP;
-    float2* part;  // [rows, n_tiles] (m, l')
+    float2* part;   // [rows, n_tiles] (m, l')             (EPI_FWD)
+    float4* part4;  // [rows, n_tiles] (m, l', u, 0)       (EPI_LOGP)
     int32_t n_tiles;
     float* zy;  // [rows]
     // EPI_GRADH
@@ -149,7 +152,8 @@ template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                           const GemmArgs& p) {
     using Cfg = GemmCfg<PAIR, NSPLIT>;
-    static_assert(EPI != EPI_FWD || NSPLIT == 1, "forward statistics are per 256-column tile");
+    static_assert((EPI != EPI_FWD && EPI != EPI_LOGP) || NSPLIT == 1,
+                  "forward statistics are per 256-column tile");
     constexpr int STAGES = Cfg::STAGES;
     constexpr int ACC_BUFS = Cfg::ACC_BUFS;
     extern __shared__ uint8_t smem_raw[];
@@ -369,7 +373,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 const uint32_t taddr =
                     tmem_base + lane_base + (uint32_t)(acc * GEMM_BN + h * GEMM_BN);
 
-                if constexpr (EPI == EPI_FWD) {
+                if constexpr (EPI == EPI_FWD || EPI == EPI_LOGP) {
+                    constexpr bool kStoreP = EPI == EPI_FWD;  // EPI_LOGP: statistics only
                     const float s = p.scale;
                     const float LOG2E = 1.4426950408889634f;
                     // pass 1: tile max over valid columns
@@ -387,10 +392,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     // relative precision when the tile max dominates -- p_y close to 1), z_y
                     const int32_t y = row_ok ? p.tgt[row] : -1;
                     const int32_t yl = y - col0;
-                    float l = 0.f;
+                    float l = 0.f, u = 0.f;  // u (EPI_LOGP): sum exp(z - m) * z
                     bool max_seen = false;
                     const float mb = m * LOG2E;
-                    __half* prow = p.P + (row_ok ? row : 0) * p.ldP + col0;
+                    __half* prow = kStoreP ? p.P + (row_ok ? row : 0) * p.ldP + col0 : nullptr;
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
                         tmem_ld_32x32b_x32(taddr + c * 32, r);
@@ -405,9 +410,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             max_seen |= is_max;
                             if (is_max) e[j] = 1.f;
                             l += is_max ? 0.f : e[j];
+                            if constexpr (!kStoreP) u = fmaf(e[j], ok ? z : 0.f, u);
                             if (c * 32 + j == yl && row_ok) p.zy[row] = z;
                         }
-                        if (row_ok) {
+                        if (kStoreP && row_ok) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 8) {
                                 if (c * 32 + j < ncol) {
@@ -421,7 +427,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             }
                         }
                     }
-                    if (row_ok) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
+                    if (row_ok) {
+                        if constexpr (kStoreP) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
+                        else p.part4[row * p.n_tiles + n_blk] = make_float4(m, l, u, 0.f);
+                    }
                 } else if constexpr (EPI == EPI_GRADH) {
                     const float s = p.scale;
                     __nv_bfloat16* orow =

@@ -82,6 +82,15 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
                        const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
                        int32_t* d_status, cudaStream_t stream);
 
+// ---- forward-only log-prob / entropy (lmhead.cu) ----
+struct LogpWs {
+    size_t idx, meta, chunk, tgt_c, H, part4, zy, sched, total;
+    int32_t n_tiles;
+};
+LogpWs plan_logp(int64_t T, int32_t d, int32_t V, size_t base = 0);
+int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, uint8_t* ws,
+                   const LogpWs& w, int32_t* d_status, cudaStream_t stream);
+
 // ---- comm (comm.cpp) ----
 int comm_allreduce_f64(agentrl_comm c, double* buf, size_t n, cudaStream_t s);
 int comm_allreduce_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
@@ -93,7 +102,7 @@ void count_launch(int n = 1);
 // per-kernel event timing (agentrl_profile_start/stop)
 enum KernelId {
     KID_COUNT = 0, KID_STATS, KID_APPLY, KID_COMPACT, KID_GATHER, KID_FWD, KID_MERGE,
-    KID_REDUCE, KID_GRADW, KID_GRADH, KID_N
+    KID_REDUCE, KID_GRADW, KID_GRADH, KID_LOGP_GEMM, KID_LOGP_MERGE, KID_N
 };
 void prof_mark(int kid, bool begin, cudaStream_t s);
 struct ProfScope {

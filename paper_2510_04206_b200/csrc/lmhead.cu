@@ -114,7 +114,11 @@ static bool gemm_wide_n() {
 template <int EPI, bool A_MN, bool B_MN, int NSPLIT>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream) {
-    ProfScope ps(EPI == EPI_FWD ? KID_FWD : (EPI == EPI_GRADW ? KID_GRADW : KID_GRADH), stream);
+    ProfScope ps(EPI == EPI_FWD    ? KID_FWD
+                 : EPI == EPI_GRADW ? KID_GRADW
+                 : EPI == EPI_LOGP  ? KID_LOGP_GEMM
+                                    : KID_GRADH,
+                 stream);
     // max_tiles is counted in 128 x 256 tiles (an upper bound of the CTAs worth launching)
     if (gemm_use_pair()) {
         auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT>;
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS)
         const int64_t t = t0 + i;
         if (t < T && mask[t]) {
             idx[pos] = (int32_t)t;
-            adv_c[pos] = adv_tok[t];
+            if (adv_c) adv_c[pos] = adv_tok[t];
             ++pos;
         }
     }
@@ -234,13 +238,13 @@ __global__ void __launch_bounds__(256)
                     y = 0;
                 }
                 tgt_c[p] = y;
-                old_c[p] = old_logp[t];
+                if (old_c) old_c[p] = old_logp[t];
             }
         } else {
             for (int c = lane; c < chunks; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
             if (lane == 0) {
                 tgt_c[p] = 0;
-                old_c[p] = 0.f;
+                if (old_c) old_c[p] = 0.f;
             }
         }
     }
@@ -644,6 +648,147 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         if (rc) return rc;
     }
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
+    return AGENTRL_OK;
+}
+
+}  // namespace agentrl
+
+// ============================================================================ log-prob forward
+// agentrl_logprob_fwd: forward-only token log-probs and entropies (the
+// trainer's recomputation of pi_old / pi_ref log-probs, and the entropy that DAPO
+// monitors).  Same compaction / gather / forward GEMM as part 2, with the EPI_LOGP
+// epilogue (no P~ store: per (row, tile) max m, l' = sum exp(z-m) - 1, u = sum exp(z-m) z),
+// then one warp per row:
+//   lse = M + log1p(L'),  logp = z_y - lse,  entropy = lse - sum_j exp(m_j - lse) u_j
+//   (= -sum_v p_v log p_v).
+namespace agentrl {
+
+__global__ void __launch_bounds__(256)
+    k_logp_merge(const int64_t* __restrict__ rows_dev, int32_t n_tiles,
+                 const float4* __restrict__ part4, const float* __restrict__ zy,
+                 const int32_t* __restrict__ idx, float* __restrict__ logp_out,
+                 float* __restrict__ ent_out, int32_t* d_status) {
+    const int64_t rows = *rows_dev;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float LOG2E = 1.4426950408889634f;
+    for (int64_t p = (int64_t)blockIdx.x * 8 + warp; p < rows; p += (int64_t)gridDim.x * 8) {
+        const float4* pr = part4 + p * (int64_t)n_tiles;
+        float M = -INFINITY;
+        for (int j = lane; j < n_tiles; j += 32) M = fmaxf(M, pr[j].x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        int jm = 0x7fffffff;
+        for (int j = lane; j < n_tiles; j += 32)
+            if (pr[j].x == M) jm = min(jm, j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) jm = min(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+        float Lm1 = 0.f;
+        for (int j = lane; j < n_tiles; j += 32) {
+            const float4 t = pr[j];
+            Lm1 += j == jm ? t.y : (1.f + t.y) * ex2_approx((t.x - M) * LOG2E);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) Lm1 += __shfl_xor_sync(0xffffffffu, Lm1, o);
+        const float lse = M + log1pf(Lm1);
+        float Ez = 0.f;
+        for (int j = lane; j < n_tiles; j += 32) {
+            const float4 t = pr[j];
+            Ez += expf(t.x - lse) * t.z;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) Ez += __shfl_xor_sync(0xffffffffu, Ez, o);
+        if (lane == 0) {
+            const float logp = zy[p] - lse;
+            const int64_t t = idx[p];
+            logp_out[t] = logp;
+            if (ent_out) ent_out[t] = fmaxf(lse - Ez, 0.f);
+            if (!isfinite(logp)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
+        }
+    }
+}
+
+LogpWs plan_logp(int64_t T, int32_t d, int32_t V, size_t base) {
+    WsPlan p;
+    p.off = base;
+    LogpWs w;
+    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    w.n_tiles = (int32_t)ceil_div(V, GEMM_BN);
+    w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
+    w.meta = p.take(sizeof(int64_t) * 4);
+    w.chunk = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
+    w.tgt_c = p.take(sizeof(int32_t) * (size_t)rows_cap);
+    w.H = p.take((size_t)rows_cap * d * 2, 1024);
+    w.part4 = p.take(sizeof(float4) * (size_t)rows_cap * w.n_tiles);
+    w.zy = p.take(sizeof(float) * (size_t)rows_cap);
+    w.sched = p.take(sizeof(int) * 16);
+    w.total = p.off;
+    return w;
+}
+
+int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, uint8_t* ws,
+                   const LogpWs& w, int32_t* d_status, cudaStream_t stream) {
+    const int64_t T = a->T;
+    const int32_t d = a->d, V = a->V;
+    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    int64_t* meta = reinterpret_cast<int64_t*>(ws + w.meta);
+    int32_t* idx = reinterpret_cast<int32_t*>(ws + w.idx);
+    int32_t* chunk = reinterpret_cast<int32_t*>(ws + w.chunk);
+    int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + w.tgt_c);
+    __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(ws + w.H);
+    float4* part4 = reinterpret_cast<float4*>(ws + w.part4);
+    float* zy = reinterpret_cast<float*>(ws + w.zy);
+    int* sched = reinterpret_cast<int*>(ws + w.sched);
+    AG_CUDA(cudaMemsetAsync(meta, 0, 4 * sizeof(int64_t), stream));
+    AG_CUDA(cudaMemsetAsync(sched, 0, 16 * sizeof(int), stream));
+    AG_CUDA(cudaMemsetAsync(logp, 0, (size_t)T * sizeof(float), stream));
+    if (entropy) AG_CUDA(cudaMemsetAsync(entropy, 0, (size_t)T * sizeof(float), stream));
+    const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    if (n_chunks > 0) {
+        ProfScope ps(KID_COMPACT, stream);
+        k_mask_count<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, chunk);
+        k_chunk_scan<<<1, 32, 0, stream>>>(n_chunks, chunk, meta);
+        k_compact<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(T, a->loss_mask, nullptr,
+                                                                     chunk, idx, nullptr);
+        count_launch(3);
+    }
+    {
+        ProfScope ps(KID_GATHER, stream);
+        k_gather<<<num_sms() * 4, 256, 0, stream>>>(
+            meta, T, d, V, reinterpret_cast<const __nv_bfloat16*>(a->hidden), a->target, nullptr,
+            idx, H, tgt_c, nullptr, d_status);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
+    }
+    CUtensorMap mH_K, mW_K;
+    int rc;
+    if ((rc = make_map(&mH_K, H, d, rows_cap, d, 64, 128))) return rc;
+    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, gemm_use_pair() ? 128 : 256))) return rc;
+    {
+        GemmArgs g{};
+        g.m_dev = meta;
+        g.N = V;
+        g.K_static = d;
+        g.group_m = gemm_group_m();
+        g.pol_a = l2_policy(0, 2);
+        g.pol_b = l2_policy(1, 1);
+        g.tile_counter = gemm_dynamic() ? sched : nullptr;
+        g.scale = a->logit_scale;
+        g.tgt = tgt_c;
+        g.part4 = part4;
+        g.n_tiles = w.n_tiles;
+        g.zy = zy;
+        if ((rc = launch_gemm<EPI_LOGP, false, false, 1>(mH_K, mW_K, g,
+                                                          (rows_cap / GEMM_BM) * w.n_tiles, stream)))
+            return rc;
+    }
+    {
+        ProfScope ps(KID_LOGP_MERGE, stream);
+        k_logp_merge<<<num_sms() * 8, 256, 0, stream>>>(meta, w.n_tiles, part4, zy, idx, logp,
+                                                        entropy, d_status);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
+    }
     return AGENTRL_OK;
 }
 

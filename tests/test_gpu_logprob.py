@@ -1,0 +1,91 @@
+"""GPU parity of agentrl_logprob_fwd (forward-only log-prob + entropy)
+against the fp64 oracle.  Tolerances: logp <= 1e-3 absolute;
+entropy <= 1e-3 absolute (same fp32 softmax statistics)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+from gpu_util import bf16_dev, f64, t  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ag():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_04206_b200 as m
+    return m
+
+
+def _run(ag, hb, Wb, y, mask, scale=1.0, with_entropy=True):
+    T, d = hb.shape
+    V = Wb.shape[0]
+    ws = ag.alloc_workspace(ag.agentrl_logprob_workspace_size(T, d, V))
+    logp = torch.full((T,), float("nan"), device="cuda")
+    ent = torch.full((T,), float("nan"), device="cuda") if with_entropy else None
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rc = ag.agentrl_logprob_fwd(T, bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32),
+                                t(mask, torch.uint8), logp, ent, ws, st, logit_scale=scale)
+    assert rc == 0, ag.status_string(rc)
+    torch.cuda.synchronize()
+    return logp.cpu().numpy(), (ent.cpu().numpy() if ent is not None else None), int(st.item())
+
+
+@pytest.mark.parametrize("cfg_name,scale", [("tiny", 1.0), ("ragged", 1.0), ("ragged", 1.25)])
+def test_logprob_entropy_parity(ag, cfg_name, scale):
+    cfg = synth.CONFIGS[cfg_name]
+    b = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
+    lp_ref, ent_ref = oracle.logprob_entropy(f64(hb), f64(Wb), y, b["loss_mask"], scale)
+    lp, ent, st = _run(ag, hb, Wb, y, b["loss_mask"], scale)
+    assert st == 0
+    m = b["loss_mask"] != 0
+    assert np.abs(lp[m] - lp_ref[m]).max() <= 1e-3
+    assert np.abs(ent[m] - ent_ref[m]).max() <= 1e-3
+    assert np.all(lp[~m] == 0) and np.all(ent[~m] == 0)
+    # without the entropy output
+    lp2, _, _ = _run(ag, hb, Wb, y, b["loss_mask"], scale, with_entropy=False)
+    np.testing.assert_array_equal(lp2, lp)
+
+
+def test_logprob_matches_grpo_step_logp(ag):
+    """The forward-only path and the fused step's logp output agree bitwise (same GEMM,
+    same epilogue statistics, same merge arithmetic)."""
+    cfg = synth.CONFIGS["ragged"]
+    b = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
+    lp, _, _ = _run(ag, hb, Wb, y, b["loss_mask"])
+    from gpu_util import batch_dev
+    step = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V)
+    old = synth.make_old_logp_free(cfg.T, 3)
+    step(batch_dev(b), bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32), t(old, torch.float32))
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(step.logp.cpu().numpy(), lp, atol=2e-6)
+
+
+def test_logprob_uniform_head(ag):
+    """W = 0: logp = -ln V and entropy = ln V for every masked token."""
+    cfg = synth.CONFIGS["ragged"]
+    b = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
+    lp, ent, _ = _run(ag, hb, np.zeros_like(Wb), y, b["loss_mask"])
+    m = b["loss_mask"] != 0
+    assert np.abs(lp[m] + np.log(cfg.V)).max() < 1e-5
+    assert np.abs(ent[m] - np.log(cfg.V)).max() < 1e-5
+
+
+@pytest.mark.slow
+def test_logprob_full_size_spot_rows(ag):
+    cfg = synth.CONFIGS["qwen7b"]
+    b = synth.make_structure(cfg)
+    hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
+    lp, ent, st = _run(ag, hb, Wb, y, b["loss_mask"])
+    assert st == 0
+    rows = np.random.default_rng(2).choice(np.nonzero(b["loss_mask"])[0], 24, replace=False)
+    lr, er = oracle.logprob_entropy(f64(hb[rows]), f64(Wb), y[rows], np.ones(24, np.uint8))
+    assert np.abs(lp[rows] - lr).max() <= 1e-3
+    assert np.abs(ent[rows] - er).max() <= 1e-3

@@ -271,3 +271,43 @@ def test_grpo_step_composes():
     assert st["loss"] == sep["loss"]
     np.testing.assert_array_equal(st["grad_W"], sep["grad_W"])
     np.testing.assert_array_equal(st["adv_tok"], an["adv_tok"])
+
+
+# --------------------------------------------------------------------------- entropy
+def test_entropy_uniform_is_log_V():
+    T, d, V = 6, 4, 512
+    h, _, y = _rand_head(T, d, V, 31)
+    lp, H = oracle.logprob_entropy(h, np.zeros((V, d)), y, np.ones(T, np.uint8))
+    np.testing.assert_allclose(H, math.log(V), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(lp, -math.log(V), rtol=0, atol=1e-12)
+
+
+def test_entropy_two_logit_closed_form():
+    """d=1, W=[[1],[0]], h=[x]: z=(s x, 0), p = sigmoid(s x), H = binary entropy."""
+    xs = np.linspace(-6, 6, 13)
+    h = xs[:, None]
+    W = np.asarray([[1.0], [0.0]])
+    y = np.zeros(len(xs), np.int32)
+    for s in (1.0, 1.25):
+        lp, H = oracle.logprob_entropy(h, W, y, np.ones(len(xs), np.uint8), logit_scale=s)
+        p = 1.0 / (1.0 + np.exp(-s * xs))
+        np.testing.assert_allclose(H, -(p * np.log(p) + (1 - p) * np.log(1 - p)), atol=1e-13)
+        np.testing.assert_allclose(lp, np.log(p), atol=1e-13)
+
+
+def test_entropy_bruteforce_and_bounds():
+    T, d, V = 10, 8, 64
+    h, W, y = _rand_head(T, d, V, 33, scale=2.0)
+    mask = (np.arange(T) % 3 != 0).astype(np.uint8)
+    lp, H = oracle.logprob_entropy(h, W, y, mask)
+    for t in range(T):
+        if not mask[t]:
+            assert H[t] == 0.0 and lp[t] == 0.0
+            continue
+        z = [sum(np.longdouble(h[t, k]) * np.longdouble(W[v, k]) for k in range(d))
+             for v in range(V)]
+        Z = sum(np.exp(zz) for zz in z)
+        ref = -sum((np.exp(zz) / Z) * (zz - np.log(Z)) for zz in z)
+        assert abs(float(ref) - H[t]) < 1e-12
+        assert 0.0 <= H[t] <= math.log(V) + 1e-12
+    np.testing.assert_allclose(lp, oracle.logprob(h, W, y, mask), atol=1e-13)
