@@ -19,6 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "agentrl_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_variants.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 # data-dependent status bits
@@ -32,9 +33,10 @@ S_NO_TOKENS = 32
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain -O2, no fast-math: IEEE fp64)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(
+            os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
-               "-ffp-contract=off", _SRC, "-o", _LIB + ".tmp", "-lm"]
+               "-ffp-contract=off", *_SRCS, "-o", _LIB + ".tmp", "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
     return _LIB
@@ -64,6 +66,10 @@ def lib():
         L.oracle_grpo_step.argtypes = [i64, i32, i32, i32, P, P, P, P, P, f64, i32, i32, P, P, P,
                                        P, f64, f64, f64, P, P, P, P, P, P, P]
         L.oracle_logprob_entropy.argtypes = [i64, i32, i32, P, P, P, P, f64, P, P]
+        L.oracle_seq_mean_weights.argtypes = [i64, i32, P, P, P]
+        L.oracle_seq_mean_weights.restype = i64
+        L.oracle_policy_loss_ex.argtypes = [i64, i32, i32, P, P, P, P, P, P, f64, f64, f64, i64,
+                                            f64, P, P, P, P, P, P, P]
         L.oracle_num_threads.restype = C.c_int
         L.oracle_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -193,6 +199,42 @@ def logprob(hidden, W, target, loss_mask, logit_scale=1.0):
     if st != 0:
         raise ValueError(f"oracle_logprob status {st}")
     return out
+
+
+def seq_mean_weights(b):
+    """w_t = 1/(n_seq n_g(t)) of the sequence-level aggregation (R7b)."""
+    T = int(b["T"])
+    off = _c(b["traj_offsets"], np.int64)
+    w = np.zeros(T, np.float64)
+    n_seq = lib().oracle_seq_mean_weights(T, len(off) - 1, _p(off),
+                                          _p(_c(b["loss_mask"], np.uint8)), _p(w))
+    return w, int(n_seq)
+
+
+def policy_loss_ex(hidden, W, target, adv_tok, old_logp, loss_mask, n_mask_global,
+                   eps_lo=0.2, eps_hi=0.2, logit_scale=1.0, kl_beta=0.0, ref_logp=None,
+                   weights=None, grads=True):
+    """Loss variants (oracle_variants.c): KL penalty (k3) and per-token
+    weights (token mean by default; sequence mean via seq_mean_weights)."""
+    h = _c(hidden, np.float64)
+    w = _c(W, np.float64)
+    T, d = h.shape
+    V = w.shape[0]
+    loss = np.zeros(1, np.float64)
+    logp = np.zeros(T, np.float64)
+    gh = np.zeros((T, d), np.float64) if grads else None
+    gw = np.zeros((V, d), np.float64) if grads else None
+    stats = np.zeros(5, np.float64)
+    ref = None if ref_logp is None else _c(ref_logp, np.float64)
+    wt = None if weights is None else _c(weights, np.float64)
+    st = lib().oracle_policy_loss_ex(T, d, V, _p(h), _p(w), _p(_c(target, np.int32)),
+                                     _p(_c(adv_tok, np.float64)), _p(_c(old_logp, np.float64)),
+                                     _p(_c(loss_mask, np.uint8)), float(eps_lo), float(eps_hi),
+                                     float(logit_scale), int(n_mask_global), float(kl_beta),
+                                     _p(ref), _p(wt), _p(loss), _p(logp), _p(gh), _p(gw),
+                                     _p(stats))
+    return dict(status=st, loss=float(loss[0]), logp=logp, grad_hidden=gh, grad_W=gw,
+                loss_stats=stats)
 
 
 def logprob_entropy(hidden, W, target, loss_mask, logit_scale=1.0):
