@@ -233,10 +233,10 @@ def run_native(args, cfg, world, rank, local_rank):
         old_h = old.cpu().pin_memory()
         meta_h = {k: bd[k].cpu().pin_memory() for k in
                   ("traj_offsets", "task_id", "group_id", "rewards", "loss_mask")}
-        loss_h = torch.empty(5, dtype=torch.float64).pin_memory()
+        loss_h = torch.empty(6, dtype=torch.float64).pin_memory()
         h2d = sum(x.numel() * x.element_size() for x in [hid_h, tgt_h, old_h, *meta_h.values()])
         d2h = loss_h.numel() * loss_h.element_size()
-        stats_dev = torch.empty(5, dtype=torch.float64, device=dev)
+        stats_dev = torch.empty(6, dtype=torch.float64, device=dev)
         # double-buffered device inputs: step k+1's host->device copy runs on a copy stream
         # while step k computes (every copy is still inside the timed region)
         sets = [dict(hid=hid, target=target, old=old, bd=bd),
@@ -271,7 +271,7 @@ def run_native(args, cfg, world, rank, local_rank):
                 S = sets[i]
                 step(S["bd"], S["hid"], W, S["target"], S["old"])
                 stats_dev[0:1].copy_(step.loss)
-                stats_dev[1:5].copy_(step.loss_stats)
+                stats_dev[1:6].copy_(step.loss_stats)
                 loss_h.copy_(stats_dev, non_blocking=True)
                 done[i] = main_s.record_event()
 

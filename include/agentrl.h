@@ -148,6 +148,21 @@ typedef struct {
     const int64_t* n_mask_global;      /* device [1] */
     int32_t grad_W_mode;               /* 0 = local sum only, 1 = all-reduce over comm */
     int32_t reserved;
+    /* ---- objective variants; all-zero = the base objective above ----
+     * KL penalty (the "- beta D_KL" of P:1103 / P:1119; beta unstated in the paper, R11):
+     *   loss += sum_t w_t * beta * KL_t,  KL_t = exp(ref_t - logp_t) - (ref_t - logp_t) - 1
+     *   (k3 estimator, >= 0); needs ref_logp [T] when kl_beta > 0.
+     * Aggregation weights w_t (loss = sum_t w_t (-term_t + beta KL_t)):
+     *   tok_weight != NULL : w_t = tok_weight[t] (any caller-defined aggregation)
+     *   else loss_agg == 0 : w_t = 1 / N (token-level mean; default)
+     *   else loss_agg == 1 : w_t = 1 / (n_seq * n_g(t)), n_seq = trajectories with masked
+     *                        tokens (global), n_g = the trajectory's masked tokens: mean over
+     *                        sequences of per-sequence token means (GRPO's 1/K).
+     *                        agentrl_grpo_step only (needs the batch descriptor). */
+    float kl_beta;                     /* >= 0 */
+    int32_t loss_agg;                  /* 0 or 1 */
+    const float* ref_logp;             /* [T] or NULL */
+    const float* tok_weight;           /* [T] or NULL */
 } agentrl_loss_args;
 
 /* Outputs.  loss and grad_hidden / grad_W are required; the others may be NULL.
@@ -156,8 +171,8 @@ typedef struct {
  *   logp        [T] float: logp_t on masked tokens, 0 elsewhere
  *   grad_hidden [T,d] bf16 (overwritten)
  *   grad_W      [V,d] float (overwritten)
- *   loss_stats  [4] double: clip fraction, mean rho, mean logp, masked tokens
- *               (local) */
+ *   loss_stats  [5] double: clip fraction, mean rho, mean logp, masked tokens,
+ *               mean KL (all local) */
 typedef struct {
     double* loss;
     float* logp;

@@ -63,7 +63,9 @@ class LossArgs(C.Structure):
                 ("old_logp", C.c_void_p), ("loss_mask", C.c_void_p),
                 ("clip_eps_low", C.c_float), ("clip_eps_high", C.c_float),
                 ("logit_scale", C.c_float), ("n_mask_global", C.c_void_p),
-                ("grad_W_mode", C.c_int32), ("reserved", C.c_int32)]
+                ("grad_W_mode", C.c_int32), ("reserved", C.c_int32),
+                ("kl_beta", C.c_float), ("loss_agg", C.c_int32), ("ref_logp", C.c_void_p),
+                ("tok_weight", C.c_void_p)]
 
 
 class LossOut(C.Structure):
@@ -136,12 +138,14 @@ def make_batch(b) -> Batch:
 
 def make_loss_args(T, hidden, W_head, target, old_logp, loss_mask, adv_tok=None,
                    n_mask_global=None, eps_low=0.2, eps_high=0.2, logit_scale=1.0,
-                   grad_W_mode=0) -> LossArgs:
+                   grad_W_mode=0, kl_beta=0.0, loss_agg=0, ref_logp=None,
+                   tok_weight=None) -> LossArgs:
     d = int(hidden.shape[1])
     V = int(W_head.shape[0])
     return LossArgs(int(T), d, V, _ptr(hidden), _ptr(W_head), _ptr(target), _ptr(adv_tok),
                     _ptr(old_logp), _ptr(loss_mask), float(eps_low), float(eps_high),
-                    float(logit_scale), _ptr(n_mask_global), int(grad_W_mode), 0)
+                    float(logit_scale), _ptr(n_mask_global), int(grad_W_mode), 0,
+                    float(kl_beta), int(loss_agg), _ptr(ref_logp), _ptr(tok_weight))
 
 
 def make_loss_out(loss, grad_hidden, grad_W, logp=None, loss_stats=None) -> LossOut:
@@ -337,10 +341,11 @@ class Step:
 
     def __init__(self, T, n_traj, n_groups, n_tasks, d, V, device="cuda", eps_std=1e-6,
                  eps_low=0.2, eps_high=0.2, logit_scale=1.0, comm: Comm | None = None,
-                 grad_W_mode=None):
+                 grad_W_mode=None, kl_beta=0.0, loss_agg=0):
         import torch
         self.T, self.d, self.V = int(T), int(d), int(V)
         self.eps_std, self.eps_low, self.eps_high, self.scale = eps_std, eps_low, eps_high, logit_scale
+        self.kl_beta, self.loss_agg = float(kl_beta), int(loss_agg)
         self.comm = comm
         self.grad_W_mode = (1 if comm is not None else 0) if grad_W_mode is None else grad_W_mode
         self.ws = alloc_workspace(agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks,
@@ -352,16 +357,19 @@ class Step:
         self.logp = torch.empty(T, dtype=torch.float32, device=device)
         self.grad_hidden = torch.empty(T, d, dtype=torch.bfloat16, device=device)
         self.grad_W = torch.empty(V, d, dtype=torch.float32, device=device)
-        self.loss_stats = torch.zeros(4, dtype=torch.float64, device=device)
+        self.loss_stats = torch.zeros(5, dtype=torch.float64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
 
-    def __call__(self, batch, hidden, W_head, target, old_logp, stream=None, zero_status=True):
+    def __call__(self, batch, hidden, W_head, target, old_logp, stream=None, zero_status=True,
+                 ref_logp=None, tok_weight=None):
         if zero_status:
             self.status.zero_()
         b = make_batch(batch)
         a = make_loss_args(self.T, hidden, W_head, target, old_logp, batch["loss_mask"],
                            eps_low=self.eps_low, eps_high=self.eps_high,
-                           logit_scale=self.scale, grad_W_mode=self.grad_W_mode)
+                           logit_scale=self.scale, grad_W_mode=self.grad_W_mode,
+                           kl_beta=self.kl_beta, loss_agg=self.loss_agg, ref_logp=ref_logp,
+                           tok_weight=tok_weight)
         o = make_loss_out(self.loss, self.grad_hidden, self.grad_W, self.logp, self.loss_stats)
         rc = agentrl_grpo_step(b, self.eps_std, a, o, self.adv_tok, self.task_stats, self.ws,
                                self.comm.handle if self.comm else None, self.status, stream)

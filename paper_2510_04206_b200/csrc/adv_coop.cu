@@ -316,6 +316,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
 
     // phase 0: zero scratch; chunk -> first-trajectory table
+    if (gtid == 0) p.meta[3] = 0;  // local count of trajectories with masked tokens (n_seq)
     for (int64_t i = gtid; i < p.n_traj; i += gstride) p.n_g[i] = 0;
     for (int64_t i = gtid; i < p.n_groups; i += gstride) {
         p.grp_cnt[i] = 0;
@@ -447,6 +448,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
 
     // phase B3: this block's groups (GRPO advantage; readings R1, R2, R14), then the
     // block's per-task partial (N, S, Q) in a fixed order
+    unsigned long long nz = 0;  // trajectories with masked tokens (sequence-mean weights)
     for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
         const int32_t K = p.grp_cnt[j];
         int32_t* mb = p.members + s_pre[B] + p.grp_start[j];
@@ -490,6 +492,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
                 N += n;
                 S += n * ah;
                 Q += n * ah * ah;
+                nz += p.n_g[g] > 0;
             }
         }
         p.grp_task[j] = task0;
@@ -497,6 +500,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         p.grp_nsq[3 * j + 1] = S;
         p.grp_nsq[3 * j + 2] = Q;
     }
+    if (nz) atomicAdd(reinterpret_cast<unsigned long long*>(&p.meta[3]), nz);  // integer: exact
     __syncthreads();
     // per-task partials of this block: warp shuffles (fixed tree) + one barrier, tasks in
     // batches of TASK_BATCH
@@ -563,6 +567,7 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
                 p.stats[3 * i + 2] = Q;
             }
         }
+        if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)p.meta[3];  // n_seq (local)
     }
 }
 
@@ -596,6 +601,7 @@ __device__ void coop_apply_phase(const AdvParams& p) {
             const int64_t n = (int64_t)nsum;
             p.meta[0] = s_pre[G];  // local masked rows
             p.meta[1] = n;         // global N
+            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global n_seq
             if (p.n_mask_global_out) *p.n_mask_global_out = n;
             if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
         }
@@ -815,7 +821,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
                                             0, stream));
         count_launch();
     }
-    int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks, stream);
+    int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks + 1, stream);
     if (rc != AGENTRL_OK) return rc;
     ProfScope ps(KID_APPLY, stream);
     // same grid as the stats launch: phase C reuses its contiguous chunk partition

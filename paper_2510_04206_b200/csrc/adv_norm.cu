@@ -267,6 +267,12 @@ __global__ void __launch_bounds__(STATS_THREADS)
             stats[3 * i + 2] = Q;
         }
     }
+    {  // trajectories with masked tokens (sequence-mean weights), local
+        double nz = 0.0;
+        for (int64_t g = threadIdx.x; g < n_traj; g += blockDim.x) nz += n_g[g] > 0 ? 1.0 : 0.0;
+        nz = block_sum_f64(nz, s_red);
+        if (threadIdx.x == 0) stats[3 * n_tasks] = nz;
+    }
     if (threadIdx.x == 0) {
         meta[0] = n_mask_local;
         if (s_status) atomicOr(d_status, s_status);
@@ -358,6 +364,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS)
         if (threadIdx.x == 0) {
             const int64_t n = (int64_t)nsum;
             meta[1] = n;
+            meta[2] = (int64_t)stats[3 * n_tasks];
             if (n_mask_global_out) *n_mask_global_out = n;
             if (n == 0) atomicOr(d_status, AGENTRL_ST_NO_TOKENS);
         }
@@ -381,6 +388,7 @@ __global__ void k_adv_empty(int32_t n_tasks, double* task_stats_out, int64_t* n_
         }
         meta[0] = 0;
         meta[1] = (int64_t)nsum;
+        meta[2] = (int64_t)stats[3 * n_tasks];
         if (n_mask_global_out) *n_mask_global_out = (int64_t)nsum;
         if (nsum == 0.0) atomicOr(d_status, AGENTRL_ST_NO_TOKENS);
     }
@@ -461,7 +469,7 @@ int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, doub
     count_launch();
     AG_CUDA(cudaGetLastError());
     if (comm) {
-        int rc = comm_allreduce_f64(comm, stats, (size_t)3 * b->n_tasks, stream);
+        int rc = comm_allreduce_f64(comm, stats, (size_t)3 * b->n_tasks + 1, stream);
         if (rc != AGENTRL_OK) return rc;
     }
     ProfScope ps_apply(KID_APPLY, stream);

@@ -175,6 +175,12 @@ static int check_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, boo
         !aligned(o->grad_W, 16))
         return AGENTRL_ERR_SHAPE;
     if (a->grad_W_mode < 0 || a->grad_W_mode > 1) return AGENTRL_ERR_INVALID_ARG;
+    // objective variants: beta >= 0 (ref log-probs needed when > 0); loss_agg 0/1, the
+    // sequence mean only in the fused step (it needs the batch descriptor) unless the caller
+    // supplies the weights
+    if (!(a->kl_beta >= 0.f) || (a->kl_beta > 0.f && !a->ref_logp)) return AGENTRL_ERR_INVALID_ARG;
+    if (a->loss_agg < 0 || a->loss_agg > 1) return AGENTRL_ERR_INVALID_ARG;
+    if (!fused && a->loss_agg == 1 && !a->tok_weight) return AGENTRL_ERR_INVALID_ARG;
     return AGENTRL_OK;
 }
 
@@ -270,10 +276,12 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
                               d_status, s)))
         return rc;
     const int before = g_launches;
+    const FusedExtras fx{b->traj_offsets, b->n_traj, reinterpret_cast<const int32_t*>(w8 + wa.n_g),
+                         meta + 2 /* global n_seq */};
     rc = launch_policy_loss(a, o, w8, wl, reinterpret_cast<const int32_t*>(w8 + wa.idx),
                             meta /* [0] local rows */,
                             reinterpret_cast<const float*>(w8 + wa.adv_c),
-                            meta + 1 /* global N */, comm, d_status, s);
+                            meta + 1 /* global N */, comm, d_status, s, &fx);
     (void)before;
     return rc;
 }

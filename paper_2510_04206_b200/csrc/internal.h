@@ -67,6 +67,7 @@ struct LossWs {
     size_t zy;                              // float [T_pad]
     size_t row_term, row_rho, row_logp;     // double/float per row
     size_t row_clip;                        // int32 per row
+    size_t row_kl, w_c, ref_c;              // float per row: KL_t, weight w_t, ref log-prob
     size_t red;                             // double [8] loss reduction output
     size_t sched;                           // int [16] GEMM tile counters (dynamic scheduler)
     size_t total;
@@ -77,10 +78,18 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0);
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:
 //   idx_dev  int32 [T] compacted token positions, rows_dev -> int64 number of rows (local T_eff),
 //   adv_c    float [T] compacted advantages, nglob -> int64 global masked count.
+// batch information the fused step hands to part 2 (sequence-mean weights, loss_agg == 1)
+struct FusedExtras {
+    const int64_t* off;   // traj_offsets [n_traj+1]
+    int32_t n_traj;
+    const int32_t* n_g;   // masked tokens per trajectory (part 1 workspace)
+    const int64_t* nseq;  // global number of trajectories with masked tokens (device)
+};
 int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
                        const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
                        const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
-                       int32_t* d_status, cudaStream_t stream);
+                       int32_t* d_status, cudaStream_t stream,
+                       const FusedExtras* fx = nullptr);
 
 // ---- forward-only log-prob / entropy (lmhead.cu) ----
 struct LogpWs {

@@ -259,9 +259,12 @@ __global__ void __launch_bounds__(MERGE_THREADS)
               const float* __restrict__ zy, const int32_t* __restrict__ tgt_c,
               const float* __restrict__ old_c, const float* __restrict__ adv_c,
               const int32_t* __restrict__ idx, float eps_lo, float eps_hi,
-              uint16_t* __restrict__ PG /* fp16 P~ in, bf16 G out, [rows, V] */,
-              double* __restrict__ row_term, float* __restrict__ row_rho,
-              float* __restrict__ row_logp, int32_t* __restrict__ row_clip,
+              const float* __restrict__ w_c /* per-row weight w_t */,
+              const float* __restrict__ ref_c /* per-row ref log-prob or null */,
+              float kl_beta, uint16_t* __restrict__ PG /* fp16 P~ in, bf16 G out, [rows, V] */,
+              double* __restrict__ row_term /* w (-term + beta KL) */,
+              float* __restrict__ row_rho, float* __restrict__ row_logp,
+              int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
               float* __restrict__ logp_out) {
     extern __shared__ float s_f[];  // [n_tiles] scale per tile
     __shared__ float s_red[MERGE_THREADS / 32];
@@ -330,11 +333,22 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             const double u = (double)rho * (double)A, cl = (double)rc * (double)A;
             const double term = u < cl ? u : cl;
             const bool clipped = (A > 0.f && rho > hi) || (A < 0.f && rho < lo);
-            c_t = clipped ? 0.f : (float)((double)rho * (double)A / Nd);
-            row_term[p] = term;
+            // weight w_t (1/N token mean by default) and the k3 KL penalty (8(f) variants):
+            //   loss_t = w (-term + beta KL),  c_t = w ([unclipped] rho A - beta (1 - e^r))
+            const double w = w_c ? (double)w_c[p] : 1.0 / Nd;
+            double kl = 0.0, dkl = 0.0;
+            if (kl_beta > 0.f && ref_c) {
+                const double r = (double)ref_c[p] - (double)logp;
+                const double er = exp(r);
+                kl = er - r - 1.0;
+                dkl = 1.0 - er;
+            }
+            c_t = (float)(w * ((clipped ? 0.0 : (double)rho * (double)A) - (double)kl_beta * dkl));
+            row_term[p] = w * (-term + (double)kl_beta * kl);
             row_rho[p] = rho;
             row_logp[p] = logp;
             row_clip[p] = clipped ? 1 : 0;
+            row_kl[p] = (float)kl;
             if (logp_out) logp_out[idx[p]] = logp;
             s_bc[0] = lse;
             s_bc[1] = c_t;
@@ -390,20 +404,21 @@ __global__ void __launch_bounds__(1024)
     k_loss_reduce(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
                   const double* __restrict__ row_term, const float* __restrict__ row_rho,
                   const float* __restrict__ row_logp, const int32_t* __restrict__ row_clip,
-                  double* __restrict__ loss_out, double* __restrict__ stats_out,
-                  int32_t* d_status) {
-    __shared__ double s[4][32];
+                  const float* __restrict__ row_kl, double* __restrict__ loss_out,
+                  double* __restrict__ stats_out, int32_t* d_status) {
+    __shared__ double s[5][32];
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
-    double a = 0.0, b = 0.0, c = 0.0, e = 0.0;
+    double a = 0.0, b = 0.0, c = 0.0, e = 0.0, k = 0.0;
     // contiguous per-thread segments, fixed order
     const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
     const int64_t lo = min(rows, (int64_t)threadIdx.x * per), hi = min(rows, lo + per);
     for (int64_t p = lo; p < hi; ++p) {
-        a += row_term[p];
+        a += row_term[p];  // w_t (-term_t + beta KL_t)
         b += (double)row_rho[p];
         c += (double)row_logp[p];
         e += (double)row_clip[p];
+        k += (double)row_kl[p];
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -412,23 +427,26 @@ __global__ void __launch_bounds__(1024)
         b += __shfl_down_sync(0xffffffffu, b, o);
         c += __shfl_down_sync(0xffffffffu, c, o);
         e += __shfl_down_sync(0xffffffffu, e, o);
+        k += __shfl_down_sync(0xffffffffu, k, o);
     }
     if (lane == 0) {
         s[0][wid] = a;
         s[1][wid] = b;
         s[2][wid] = c;
         s[3][wid] = e;
+        s[4][wid] = k;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double A = 0, B = 0, Cc = 0, E = 0;
+        double A = 0, B = 0, Cc = 0, E = 0, K = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
             A += s[0][w];
             B += s[1][w];
             Cc += s[2][w];
             E += s[3][w];
+            K += s[4][w];
         }
-        const double loss = N > 0.0 ? -A / N : 0.0;
+        const double loss = N > 0.0 ? A : 0.0;
         *loss_out = loss;
         if (!isfinite(loss) || !isfinite(Cc)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
         if (stats_out) {
@@ -437,6 +455,7 @@ __global__ void __launch_bounds__(1024)
             stats_out[1] = B / r;
             stats_out[2] = Cc / r;
             stats_out[3] = (double)rows;
+            stats_out[4] = K / r;
         }
     }
 }
@@ -464,10 +483,46 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.row_rho = p.take(sizeof(float) * (size_t)rows_cap);
     w.row_logp = p.take(sizeof(float) * (size_t)rows_cap);
     w.row_clip = p.take(sizeof(int32_t) * (size_t)rows_cap);
+    w.row_kl = p.take(sizeof(float) * (size_t)rows_cap);
+    w.w_c = p.take(sizeof(float) * (size_t)rows_cap);
+    w.ref_c = p.take(sizeof(float) * (size_t)rows_cap);
     w.red = p.take(sizeof(double) * 8);
     w.sched = p.take(sizeof(int) * 16);
     w.total = p.off;
     return w;
+}
+
+// per-row aggregation weight w_t and reference log-prob (objective variants):
+//   w_t = tok_weight[t] | 1/(n_seq n_g(t)) (sequence mean) | 1/N (token mean)
+__global__ void __launch_bounds__(256)
+    k_row_weights(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
+                  const int32_t* __restrict__ idx, const float* __restrict__ tok_weight,
+                  const float* __restrict__ ref_logp, int32_t agg,
+                  const int64_t* __restrict__ off, int32_t n_traj,
+                  const int32_t* __restrict__ n_g, const int64_t* __restrict__ nseq_dev,
+                  float* __restrict__ w_c, float* __restrict__ ref_c) {
+    const int64_t rows = *rows_dev;
+    const double N = (double)*nglob_dev;
+    const double nseq = nseq_dev ? (double)*nseq_dev : 0.0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < rows;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = idx[p];
+        double w = N > 0.0 ? 1.0 / N : 0.0;
+        if (tok_weight) {
+            w = tok_weight[t];
+        } else if (agg == 1 && off && n_g && nseq > 0.0) {
+            int32_t lo = 0, hi = n_traj;  // trajectory of token t
+            while (hi - lo > 1) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (off[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            const int32_t ng = n_g[lo];
+            w = ng > 0 ? 1.0 / (nseq * (double)ng) : 0.0;
+        }
+        w_c[p] = (float)w;
+        if (ref_c) ref_c[p] = ref_logp ? ref_logp[t] : 0.f;
+    }
 }
 
 struct SideStream {
@@ -487,7 +542,7 @@ static SideStream& side_stream() {
 int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
                        const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
                        const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
-                       int32_t* d_status, cudaStream_t stream) {
+                       int32_t* d_status, cudaStream_t stream, const FusedExtras* fx) {
     const int64_t T = a->T;
     const int32_t d = a->d, V = a->V;
     const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
@@ -504,6 +559,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float* row_rho = reinterpret_cast<float*>(ws + w.row_rho);
     float* row_logp = reinterpret_cast<float*>(ws + w.row_logp);
     int32_t* row_clip = reinterpret_cast<int32_t*>(ws + w.row_clip);
+    float* row_kl = reinterpret_cast<float*>(ws + w.row_kl);
+    float* w_c = reinterpret_cast<float*>(ws + w.w_c);
+    float* ref_c = reinterpret_cast<float*>(ws + w.ref_c);
     int* sched = reinterpret_cast<int*>(ws + w.sched);
     int* ctr_fwd = gemm_dynamic() ? sched + 0 : nullptr;
     int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
@@ -541,7 +599,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
                                            reinterpret_cast<const __nv_bfloat16*>(a->hidden),
                                            a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
                                            d_status);
-        count_launch();
+        k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
+            rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
+            fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
+            fx ? fx->nseq : nullptr, w_c, ref_c);
+        count_launch(2);
         AG_CUDA(cudaGetLastError());
     }
 
@@ -585,8 +647,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         ProfScope ps(KID_MERGE, stream);
         k_merge_g<<<grid, MERGE_THREADS, smem, stream>>>(
             rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
-            a->clip_eps_low, a->clip_eps_high, PG, row_term, row_rho, row_logp, row_clip,
-            o->logp);
+            a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
+            a->kl_beta, PG, row_term, row_rho, row_logp, row_clip, row_kl, o->logp);
         count_launch();
         AG_CUDA(cudaGetLastError());
     }
@@ -594,7 +656,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     {
         ProfScope ps(KID_REDUCE, stream);
         k_loss_reduce<<<1, 1024, 0, stream>>>(rows_dev, nglob_dev, row_term, row_rho, row_logp,
-                                              row_clip, o->loss, o->loss_stats, d_status);
+                                              row_clip, row_kl, o->loss, o->loss_stats, d_status);
     }
     count_launch();
     AG_CUDA(cudaGetLastError());

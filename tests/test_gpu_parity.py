@@ -141,7 +141,7 @@ def test_policy_loss_parity(ag, cfg_name, eps, scale):
     logp = torch.full((T,), float("nan"), device="cuda")
     gh = torch.full((T, d), float("nan"), dtype=torch.bfloat16, device="cuda")
     gw = torch.full((V, d), float("nan"), device="cuda")
-    stats = torch.zeros(4, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(5, dtype=torch.float64, device="cuda")
     nm = torch.tensor([an["n_mask"]], dtype=torch.int64, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     args = ag.make_loss_args(T, hidden, Wd, t(y, torch.int32), t(old, torch.float32), mask,
