@@ -420,20 +420,12 @@ def cpu_baseline(cfg, gb, seconds=15.0, rows=None):
     an = oracle.task_adv_norm(gb)
     t_adv = time.perf_counter() - t0
     d, V = cfg.d, cfg.V
-    # per-token oracle cost ~ 3*V*d fp64 MACs; pick rows to fit `seconds`
+    # per-token oracle cost ~ 3*V*d fp64 MACs; the oracle parallelises across tokens, so the
+    # sample holds 4 tokens per host thread (~10 s at the paper's head sizes)
     if rows is None:
-        rows = 1
-        rng = np.random.default_rng(1)
-        W = rng.standard_normal((V, d)) * (3.0 / math.sqrt(d))
-        h = rng.standard_normal((rows, d))
-        t1 = time.perf_counter()
-        oracle.policy_loss_fwd_bwd(h, W, np.zeros(rows, np.int32), np.ones(rows), np.zeros(rows),
-                                   np.ones(rows, np.uint8), rows)
-        per = time.perf_counter() - t1
-        rows = int(max(1, min(256, (seconds - per) / max(per, 1e-3))))
-    else:
-        rng = np.random.default_rng(1)
-        W = rng.standard_normal((V, d)) * (3.0 / math.sqrt(d))
+        rows = 4 * max(cores, 1)
+    rng = np.random.default_rng(1)
+    W = rng.standard_normal((V, d)) * (3.0 / math.sqrt(d))
     h = rng.standard_normal((rows, d))
     t1 = time.perf_counter()
     oracle.policy_loss_fwd_bwd(h, W, rng.integers(0, V, size=rows).astype(np.int32),
@@ -455,7 +447,9 @@ def run_reference(args, cfg, world, rank):
     gb = synth.make_structure(cfg)
     samples = []
     for i in range(max(args.warmup, 0) + args.steps):
-        cb = cpu_baseline(cfg, gb, seconds=min(args.cpu_seconds, 10.0), rows=2 if i else None)
+        import oracle
+        cb = cpu_baseline(cfg, gb, seconds=min(args.cpu_seconds, 10.0),
+                          rows=2 * max(oracle.num_threads(), 1))
         if i >= args.warmup:
             samples.append(cb)
     v = statistics.median([s["value"] for s in samples])
