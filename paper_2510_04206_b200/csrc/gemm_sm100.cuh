@@ -40,20 +40,27 @@ constexpr int GEMM_BM = 128;  // rows per CTA
 constexpr int GEMM_BN = 256;  // columns per MMA (and per FWD statistics tile)
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 192;
-constexpr int GEMM_A_STAGE = GEMM_BM * GEMM_BK * 2;  // 16 KB
 
-template <bool PAIR, int NSPLIT>
+// KSUB: 64-wide K atoms per pipeline stage (K-major operands only).  KSUB = 2 stages 128 K
+// per k-block: 8 MMAs per barrier round trip instead of 4, for the short-K forward GEMM whose
+// 4-MMA k-blocks left the tensor pipe ~12% idle (profiles/r01_fwd_ksub.txt).
+template <bool PAIR, int NSPLIT, int KSUB = 1>
 struct GemmCfg {
     static_assert(NSPLIT == 1 || (NSPLIT == 2 && PAIR), "512-column tiles need a CTA pair");
+    static_assert(KSUB == 1 || KSUB == 2, "one or two K atoms per stage");
+    static constexpr int BK = GEMM_BK * KSUB;                    // K per stage
+    static constexpr int A_ATOM = GEMM_BM * GEMM_BK * 2;         // 16 KB: 128 rows x 64 K
+    static constexpr int A_STAGE = A_ATOM * KSUB;
     static constexpr int B_ROWS = PAIR ? GEMM_BN / 2 : GEMM_BN;  // B rows per CTA per MMA
-    static constexpr int B_HALF = B_ROWS * GEMM_BK * 2;          // bytes per MMA's B slice
+    static constexpr int B_ATOM = B_ROWS * GEMM_BK * 2;
+    static constexpr int B_HALF = B_ATOM * KSUB;                 // bytes per MMA's B slice
     static constexpr int B_STAGE = NSPLIT * B_HALF;
-    static constexpr int STAGES = PAIR ? (NSPLIT == 1 ? 6 : 4) : 4;
+    static constexpr int STAGES = (PAIR ? (NSPLIT == 1 ? 6 : 4) : 4) / KSUB;
     static constexpr int TILE_M = PAIR ? 2 * GEMM_BM : GEMM_BM;  // rows per tile
     static constexpr int TILE_N = GEMM_BN * NSPLIT;              // columns per tile
     static constexpr int ACC_BUFS = NSPLIT == 1 ? 2 : 1;
-    static constexpr int SMEM = STAGES * (GEMM_A_STAGE + B_STAGE) + 1024 + 1024;
-    static constexpr int TX_BYTES = (GEMM_A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
+    static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024;
+    static constexpr int TX_BYTES = (A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
 
 // EPI_LOGP: forward-only log-prob/entropy statistics (no P~ store): per (row, tile)
@@ -64,6 +71,7 @@ struct GemmArgs {
     // problem: rows M (dynamic if m_dev), cols N, reduction K (dynamic if k_dev)
     int64_t M_static;
     const int64_t* m_dev;
+    const int64_t* m_range;  // optional [r0, r1): only rows r0 .. r1-1 (r0 a multiple of 256)
     int32_t N;
     int64_t K_static;
     const int64_t* k_dev;
@@ -118,19 +126,21 @@ __device__ __forceinline__ void advance_acc(int& acc, uint32_t& acc_phase) {
 }
 
 // TMA loads of one k-block: A (128 rows of this CTA) and B (per MMA half: B_ROWS rows)
-template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT>
+template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB>
 __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                            uint64_t* full_bar, uint32_t full_bar_leader,
                                            uint8_t* a_dst, uint8_t* b_dst, int32_t m0,
                                            int32_t n0, int32_t k0, uint64_t pol_a,
                                            uint64_t pol_b) {
-    using Cfg = GemmCfg<PAIR, NSPLIT>;
+    using Cfg = GemmCfg<PAIR, NSPLIT, KSUB>;
+    static_assert(KSUB == 1 || (!A_MN && !B_MN), "K atoms are stacked for K-major operands");
     auto ld = [&](const CUtensorMap& m, uint8_t* dst, int32_t x, int32_t y, uint64_t pol) {
         if constexpr (PAIR) tma_load_2d_pair(&m, full_bar_leader, dst, x, y, pol);
         else tma_load_2d(&m, full_bar, dst, x, y, pol);
     };
     if constexpr (!A_MN) {
-        ld(tmA, a_dst, k0, m0, pol_a);
+#pragma unroll
+        for (int a = 0; a < KSUB; ++a) ld(tmA, a_dst + a * Cfg::A_ATOM, k0 + a * GEMM_BK, m0, pol_a);
     } else {
 #pragma unroll
         for (int i = 0; i < GEMM_BM / 64; ++i) ld(tmA, a_dst + i * 8192, m0 + i * 64, k0, pol_a);
@@ -140,7 +150,8 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
         const int32_t nh = n0 + h * GEMM_BN;
         uint8_t* bd = b_dst + h * Cfg::B_HALF;
         if constexpr (!B_MN) {
-            ld(tmB, bd, k0, nh, pol_b);
+#pragma unroll
+            for (int a = 0; a < KSUB; ++a) ld(tmB, bd + a * Cfg::B_ATOM, k0 + a * GEMM_BK, nh, pol_b);
         } else {
 #pragma unroll
             for (int i = 0; i < Cfg::B_ROWS / 64; ++i) ld(tmB, bd + i * 8192, nh + i * 64, k0, pol_b);
@@ -148,10 +159,10 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
     }
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT>
+template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                           const GemmArgs& p) {
-    using Cfg = GemmCfg<PAIR, NSPLIT>;
+    using Cfg = GemmCfg<PAIR, NSPLIT, KSUB>;
     static_assert((EPI != EPI_FWD && EPI != EPI_LOGP) || NSPLIT == 1,
                   "forward statistics are per 256-column tile");
     constexpr int STAGES = Cfg::STAGES;
@@ -160,7 +171,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * GEMM_A_STAGE;
+    uint8_t* sB = smem + STAGES * Cfg::A_STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_STAGE);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
@@ -179,12 +190,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     const int64_t unit = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
     const int64_t n_units = PAIR ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
-    const int64_t M = p.m_dev ? *p.m_dev : p.M_static;
+    const int64_t r0 = p.m_range ? p.m_range[0] : 0;
+    const int64_t M = p.m_range ? p.m_range[1] : (p.m_dev ? *p.m_dev : p.M_static);
     const int64_t K = p.k_dev ? *p.k_dev : p.K_static;
-    const int64_t num_m = (M + Cfg::TILE_M - 1) / Cfg::TILE_M;
+    const int64_t num_m = M > r0 ? (M - r0 + Cfg::TILE_M - 1) / Cfg::TILE_M : 0;
     const int64_t num_n = (p.N + Cfg::TILE_N - 1) / Cfg::TILE_N;
     const int64_t num_tiles = num_m * num_n;
-    const int64_t num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+    const int64_t num_kb = (K + Cfg::BK - 1) / Cfg::BK;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -252,7 +264,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 if (tile >= num_tiles) break;
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
-                const int32_t m0 = (int32_t)(m_blk * Cfg::TILE_M + rank * GEMM_BM);
+                const int32_t m0 = (int32_t)(r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM);
                 const int32_t n0 = (int32_t)(n_blk * Cfg::TILE_N + rank * Cfg::B_ROWS);
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -265,9 +277,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     } else {
                         mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
                     }
-                    load_stage<A_MN, B_MN, PAIR, NSPLIT>(
-                        tmA, tmB, &full[stage], fb, sA + stage * GEMM_A_STAGE,
-                        sB + stage * Cfg::B_STAGE, m0, n0, (int32_t)(kb * GEMM_BK), pol_a, pol_b);
+                    load_stage<A_MN, B_MN, PAIR, NSPLIT, KSUB>(
+                        tmA, tmB, &full[stage], fb, sA + stage * Cfg::A_STAGE,
+                        sB + stage * Cfg::B_STAGE, m0, n0, (int32_t)(kb * Cfg::BK), pol_a, pol_b);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -301,20 +313,23 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + stage * GEMM_A_STAGE);
+                    const uint32_t a_base = smem_u32(sA + stage * Cfg::A_STAGE);
                     const uint32_t b_base = smem_u32(sB + stage * Cfg::B_STAGE);
 #pragma unroll
-                    for (int k = 0; k < GEMM_BK / 16; ++k) {
+                    for (int k = 0; k < Cfg::BK / 16; ++k) {
+                        // K-major: atom k/4 (stacked), +32 B per K=16 inside the 128 B row
+                        const uint32_t ka = (uint32_t)((k >> 2) * Cfg::A_ATOM + (k & 3) * 32);
+                        const uint32_t kb_off = (uint32_t)((k >> 2) * Cfg::B_ATOM + (k & 3) * 32);
                         const uint64_t adesc =
                             A_MN ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
+                                 : umma_desc_sw128(a_base + ka, 16, 1024);
                         const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
 #pragma unroll
                         for (int h = 0; h < NSPLIT; ++h) {
                             const uint32_t bh = b_base + h * Cfg::B_HALF;
                             const uint64_t bdesc =
                                 B_MN ? umma_desc_sw128(bh + k * 2048, 8192, 1024)
-                                     : umma_desc_sw128(bh + k * 32, 16, 1024);
+                                     : umma_desc_sw128(bh + kb_off, 16, 1024);
                             const uint32_t dh = d_tmem + (uint32_t)(h * GEMM_BN);
                             if constexpr (PAIR) tc_mma_f16_pair(dh, adesc, bdesc, idesc, accum);
                             else tc_mma_f16(dh, adesc, bdesc, idesc, accum);
@@ -361,7 +376,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             if (tile >= num_tiles) break;
             int64_t m_blk, n_blk;
             tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
-            const int64_t row = m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
+            const int64_t row = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
             const bool row_ok = row < M;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -504,18 +519,18 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     }
 }
 
-template <int EPI, bool A_MN, bool B_MN, int NSPLIT>
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, true, NSPLIT>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, true, NSPLIT, KSUB>(tmA, tmB, p);
 }
 
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, false, 1>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, false, 1, 1>(tmA, tmB, p);
 }
 
 }  // namespace agentrl

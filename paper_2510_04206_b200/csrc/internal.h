@@ -69,10 +69,12 @@ struct LossWs {
     size_t row_clip;                        // int32 per row
     size_t row_kl, w_c, ref_c;              // float per row: KL_t, weight w_t, ref log-prob
     size_t red;                             // double [8] loss reduction output
-    size_t sched;                           // int [16] GEMM tile counters (dynamic scheduler)
+    size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
+    size_t fbnd;                            // int64 [MAX_FWD_CHUNKS + 1] forward row chunks
     size_t total;
     int32_t n_tiles;
 };
+constexpr int MAX_FWD_CHUNKS = 8;
 LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0);
 
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:

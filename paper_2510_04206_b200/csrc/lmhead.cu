@@ -111,7 +111,17 @@ static bool gemm_wide_n() {
     return v == 1 && gemm_use_pair();
 }
 
-template <int EPI, bool A_MN, bool B_MN, int NSPLIT>
+// forward/log-prob GEMMs stage two 64-wide K atoms per k-block unless AGENTRL_FWD_KSUB=1
+static bool gemm_fwd_ksub2() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("AGENTRL_FWD_KSUB");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB = 1>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream) {
     ProfScope ps(EPI == EPI_FWD    ? KID_FWD
@@ -121,8 +131,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
                  stream);
     // max_tiles is counted in 128 x 256 tiles (an upper bound of the CTAs worth launching)
     if (gemm_use_pair()) {
-        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT>;
-        constexpr int smem = GemmCfg<true, NSPLIT>::SMEM;
+        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB>;
+        constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM;
         static bool attr_done = false;  // per instantiation
         if (!attr_done) {
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -265,7 +275,8 @@ __global__ void __launch_bounds__(MERGE_THREADS)
               double* __restrict__ row_term /* w (-term + beta KL) */,
               float* __restrict__ row_rho, float* __restrict__ row_logp,
               int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
-              float* __restrict__ logp_out) {
+              float* __restrict__ logp_out,
+              const int64_t* __restrict__ rng /* optional row range [r0, r1) */) {
     extern __shared__ float s_f[];  // [n_tiles] scale per tile
     __shared__ float s_red[MERGE_THREADS / 32];
     __shared__ int s_jm[MERGE_THREADS / 32];
@@ -275,8 +286,11 @@ __global__ void __launch_bounds__(MERGE_THREADS)
     const double Nd = (double)*nglob_dev;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float LOG2E = 1.4426950408889634f;
+    // row range of this launch; the one ending at rows also zeroes the padding rows
+    const int64_t p_lo = rng ? rng[0] : 0;
+    const int64_t p_hi = rng ? (rng[1] >= rows ? rows_pad : rng[1]) : rows_pad;
 
-    for (int64_t p = blockIdx.x; p < rows_pad; p += gridDim.x) {
+    for (int64_t p = p_lo + blockIdx.x; p < p_hi; p += gridDim.x) {
         uint4* row4 = reinterpret_cast<uint4*>(PG + p * (int64_t)V);
         const int nvec = V / 8;
         if (p >= rows) {  // padding rows inside GEMM3's K range: zero
@@ -487,7 +501,8 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.w_c = p.take(sizeof(float) * (size_t)rows_cap);
     w.ref_c = p.take(sizeof(float) * (size_t)rows_cap);
     w.red = p.take(sizeof(double) * 8);
-    w.sched = p.take(sizeof(int) * 16);
+    w.sched = p.take(sizeof(int) * 32);
+    w.fbnd = p.take(sizeof(int64_t) * (MAX_FWD_CHUNKS + 1));
     w.total = p.off;
     return w;
 }
@@ -500,9 +515,16 @@ __global__ void __launch_bounds__(256)
                   const float* __restrict__ ref_logp, int32_t agg,
                   const int64_t* __restrict__ off, int32_t n_traj,
                   const int32_t* __restrict__ n_g, const int64_t* __restrict__ nseq_dev,
-                  float* __restrict__ w_c, float* __restrict__ ref_c) {
+                  float* __restrict__ w_c, float* __restrict__ ref_c, int32_t n_fchunks,
+                  int64_t* __restrict__ fbnd) {
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
+    if (blockIdx.x == 0 && threadIdx.x <= n_fchunks) {
+        // forward row chunks [fbnd[c], fbnd[c+1]): 256-row aligned, the last ends at rows
+        const int64_t per = (rows + n_fchunks - 1) / n_fchunks;
+        const int64_t R = (per + 255) / 256 * 256;
+        fbnd[threadIdx.x] = min(rows, (int64_t)threadIdx.x * R);
+    }
     const double nseq = nseq_dev ? (double)*nseq_dev : 0.0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < rows;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -539,6 +561,33 @@ static SideStream& side_stream() {
     return ss;
 }
 
+// forward row chunks (AGENTRL_FWD_CHUNKS, default 4, 1 = no overlap of the merge)
+static int fwd_chunks() {
+    static int v = -1;
+    if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 4), MAX_FWD_CHUNKS);
+    return v;
+}
+struct ForkStreams {
+    cudaStream_t hi = nullptr, lo = nullptr;  // forward chunks / merges
+    cudaEvent_t fork = nullptr, join = nullptr, ev[MAX_FWD_CHUNKS] = {};
+};
+static ForkStreams& fork_streams() {
+    static thread_local ForkStreams fs[16];  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ForkStreams& f = fs[dev & 15];
+    if (!f.hi) {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        cudaStreamCreateWithPriority(&f.hi, cudaStreamNonBlocking, greatest);
+        cudaStreamCreateWithPriority(&f.lo, cudaStreamNonBlocking, least);
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
+        for (auto& e : f.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    return f;
+}
+
 int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
                        const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
                        const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
@@ -563,10 +612,12 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float* w_c = reinterpret_cast<float*>(ws + w.w_c);
     float* ref_c = reinterpret_cast<float*>(ws + w.ref_c);
     int* sched = reinterpret_cast<int*>(ws + w.sched);
+    int64_t* fbnd = reinterpret_cast<int64_t*>(ws + w.fbnd);
+    const int n_fc = fwd_chunks();
     int* ctr_fwd = gemm_dynamic() ? sched + 0 : nullptr;
     int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
     int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
-    AG_CUDA(cudaMemsetAsync(sched, 0, 16 * sizeof(int), stream));
+    AG_CUDA(cudaMemsetAsync(sched, 0, 32 * sizeof(int), stream));
 
     // ---- compaction (standalone) or reuse of part 1's
     if (!idx_dev) {
@@ -602,7 +653,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
             rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
             fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
-            fx ? fx->nseq : nullptr, w_c, ref_c);
+            fx ? fx->nseq : nullptr, w_c, ref_c, n_fc, fbnd);
         count_launch(2);
         AG_CUDA(cudaGetLastError());
     }
@@ -619,16 +670,28 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     if ((rc = make_map(&mG_MN, PG, V, rows_cap, V, 64, 64))) return rc;
 
     const int64_t max_m_tiles = rows_cap / GEMM_BM;
-    // ---- K5 forward GEMM + softmax-statistics epilogue
-    {
+    // ---- K5 forward GEMM + softmax-statistics epilogue, K6 merge.  With n_fc > 1 row chunks
+    // the forward runs chunk by chunk on a high-priority stream and the (HBM-bound) merge of
+    // chunk c runs on a low-priority stream beside the (tensor-bound) forward of chunk c+1.
+    ForkStreams* fs = n_fc > 1 ? &fork_streams() : nullptr;
+    cudaStream_t s_fwd = stream, s_mrg = stream;
+    if (fs) {
+        s_fwd = fs->hi;
+        s_mrg = fs->lo;
+        AG_CUDA(cudaEventRecord(fs->fork, stream));
+        AG_CUDA(cudaStreamWaitEvent(s_fwd, fs->fork, 0));
+        AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->fork, 0));
+    }
+    for (int c = 0; c < n_fc; ++c) {
         GemmArgs g{};
+        g.m_range = n_fc > 1 ? fbnd + c : nullptr;
         g.m_dev = rows_dev;
         g.N = V;
         g.K_static = d;
         g.group_m = gemm_group_m();
         g.pol_a = l2_policy(0, 2);  // H rows of the current row group: reused by every column
         g.pol_b = l2_policy(1, 1);  // W: streamed, shared only by the concurrent row tiles
-        g.tile_counter = ctr_fwd;
+        g.tile_counter = ctr_fwd ? ctr_fwd + 16 * (c > 0) + c : nullptr;
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
         g.P = reinterpret_cast<__half*>(PG);
@@ -636,21 +699,30 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.part = part;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
-        if ((rc = launch_gemm<EPI_FWD, false, false, 1>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
-                                                      stream)))
-            return rc;
-    }
-    // ---- K6 merge + loss terms + G (in place)
-    {
+        rc = gemm_fwd_ksub2()
+                 ? launch_gemm<EPI_FWD, false, false, 1, 2>(mH_K, mW_K, g, max_m_tiles * w.n_tiles, s_fwd)
+                 : launch_gemm<EPI_FWD, false, false, 1, 1>(mH_K, mW_K, g, max_m_tiles * w.n_tiles, s_fwd);
+        if (rc) return rc;
+        if (fs) {
+            AG_CUDA(cudaEventRecord(fs->ev[c], s_fwd));
+            AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->ev[c], 0));
+        }
+        // merge + loss terms + G (in place) of this chunk; chunks merged beside the next
+        // forward chunk keep a small footprint (2 blocks per SM next to the GEMM CTA)
         size_t smem = sizeof(float) * (size_t)w.n_tiles;
-        int grid = num_sms() * 8;
-        ProfScope ps(KID_MERGE, stream);
-        k_merge_g<<<grid, MERGE_THREADS, smem, stream>>>(
+        int grid = num_sms() * (c + 1 < n_fc ? 2 : 8);
+        ProfScope ps(KID_MERGE, s_mrg);
+        k_merge_g<<<grid, MERGE_THREADS, smem, s_mrg>>>(
             rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
             a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
-            a->kl_beta, PG, row_term, row_rho, row_logp, row_clip, row_kl, o->logp);
+            a->kl_beta, PG, row_term, row_rho, row_logp, row_clip, row_kl, o->logp,
+            n_fc > 1 ? fbnd + c : nullptr);
         count_launch();
         AG_CUDA(cudaGetLastError());
+    }
+    if (fs) {  // join: the last merge waited on the last forward chunk
+        AG_CUDA(cudaEventRecord(fs->join, s_mrg));
+        AG_CUDA(cudaStreamWaitEvent(stream, fs->join, 0));
     }
     // ---- K7 loss reduction (+ C2)
     {
@@ -670,7 +742,10 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.N = d;
         g.k_dev = rows_dev;
         g.group_m = gemm_group_m_bwd();
-        g.pol_a = l2_policy(2, 1);  // G^T: each column block read by one wave only
+        // G^T column blocks are shared by the d/512 pairs of one row block, which drift apart
+        // over the K = T_eff loop: evict_first made the laggards re-read G from HBM (DRAM
+        // 160 -> 131 GB at glm9b with evict_normal, profiles/r01_l2pol_dyn.txt)
+        g.pol_a = l2_policy(2, 0);
         g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
         g.tile_counter = ctr_gw;
         g.scale = a->logit_scale;
@@ -697,7 +772,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.N = d;
         g.K_static = V;
         g.group_m = gemm_group_m_bwd();
-        g.pol_a = l2_policy(4, 1);  // G rows: read by one wave only
+        g.pol_a = l2_policy(4, 0);  // G rows: shared by the pairs of one row block (as above)
         g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
         g.tile_counter = ctr_gh;
         g.scale = a->logit_scale;
@@ -840,9 +915,10 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
         g.part4 = part4;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
-        if ((rc = launch_gemm<EPI_LOGP, false, false, 1>(mH_K, mW_K, g,
-                                                          (rows_cap / GEMM_BM) * w.n_tiles, stream)))
-            return rc;
+        const int64_t mt = (rows_cap / GEMM_BM) * w.n_tiles;
+        rc = gemm_fwd_ksub2() ? launch_gemm<EPI_LOGP, false, false, 1, 2>(mH_K, mW_K, g, mt, stream)
+                              : launch_gemm<EPI_LOGP, false, false, 1, 1>(mH_K, mW_K, g, mt, stream);
+        if (rc) return rc;
     }
     {
         ProfScope ps(KID_LOGP_MERGE, stream);

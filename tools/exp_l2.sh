@@ -1,7 +1,7 @@
 #!/bin/bash
 # L2 policy experiment: DRAM bytes (ncu, first step's GEMMs) and live step time per setting.
-for pol in 000000 210100 210102 220102 110100; do
-  AGENTRL_L2POL=$pol timeout 600 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum -k regex:gemm -c 3 --csv \
+for pol in ${POLS:-211010 210000 210202 212020 211212 210101}; do
+  AGENTRL_L2POL=$pol timeout 600 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum -k regex:gemm --launch-skip ${SKIP:-0} -c 3 --csv \
      --log-file gpurun_out/l2_$pol.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
   AGENTRL_L2POL=$pol timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/l2b_$pol.json 2>/dev/null
   python - "$pol" <<'PY'
