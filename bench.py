@@ -301,7 +301,8 @@ def run_native(args, cfg, world, rank, local_rank):
     dom_name, (dom_ms, dom_n) = dom
     kernel_ms = {k: (v[0] / max(v[1], 1), v[1]) for k, v in prof.items() if v[1] > 0}
     if dom_name in gemm_names and dom_n > 0:
-        flop = 2.0 * T_eff_local * V * d
+        # each GEMM does 2 T_eff V d per step, over dom_n / steps launches (row-chunked forward)
+        flop = 2.0 * T_eff_local * V * d * args.steps / dom_n
         achieved = flop / (dom_ms / dom_n / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved,
                 "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
@@ -407,7 +408,10 @@ def traffic_from_profiles(config, kernel):
         return None
     with open(p) as f:
         j = json.load(f)
-    return j.get(config, {}).get(kernel)
+    e = j.get(config, {}).get(kernel)
+    if isinstance(e, dict):  # per launch = per step / launches per step
+        return e["bytes_per_step"] / max(e["launches_per_step"], 1)
+    return e
 
 
 # --------------------------------------------------------------------------- oracle timing

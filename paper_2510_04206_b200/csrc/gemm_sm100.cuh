@@ -95,7 +95,46 @@ struct GemmArgs {
     // dynamic tile scheduler: zeroed int counter (tiles claimed in global order), or null for
     // the static persistent schedule (tile = unit + i * units)
     int* tile_counter;
+    // optional progress throttle (dynamic scheduler only): int64 [units], preset to -1.  Each
+    // pair leader publishes its position wave * num_kb + kb every prog_every k-blocks and waits
+    // while it is more than prog_lead k-blocks ahead of the slowest active pair, so pairs that
+    // share operand slices stay within an L2-resident window instead of drifting apart.
+    int64_t* prog;
+    int32_t prog_every, prog_lead;
 };
+
+__device__ __forceinline__ void prog_store(int64_t* p, int64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void prog_load2(const int64_t* p, int64_t& a, int64_t& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+// min position over the units that have started and not finished (-1: not started,
+// INT64_MAX: finished); 8 loads in flight per round (n_units padded to even by the -1 preset)
+__device__ __forceinline__ int64_t prog_min(const int64_t* prog, int64_t n_units) {
+    int64_t mn = INT64_MAX;
+    for (int64_t u = 0; u < n_units; u += 8) {
+        int64_t v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) prog_load2(prog + u + 2 * i, v[2 * i], v[2 * i + 1]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (u + i < n_units && v[i] >= 0 && v[i] < mn) mn = v[i];
+    }
+    return mn;
+}
+// wait until this unit is at most `lead` k-blocks ahead of the slowest active unit.  Positions
+// only grow, so a stale minimum is a lower bound: re-read only when it says we may be ahead.
+// The slowest unit never waits.
+__device__ __forceinline__ void prog_throttle(const int64_t* prog, int64_t n_units, int64_t mine,
+                                              int32_t lead, int64_t& cached_min) {
+    if (mine - cached_min <= (int64_t)lead) return;
+    for (;;) {
+        cached_min = prog_min(prog, n_units);
+        if (mine - cached_min <= (int64_t)lead) return;
+        __nanosleep(100);
+    }
+}
 
 constexpr int QD = 4;  // tile-queue depth (dynamic scheduler)
 
@@ -237,6 +276,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             const uint64_t pol_b = make_policy(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
+            const bool throttle = dyn && leader && p.prog != nullptr && p.prog_every > 0;
+            int64_t prog_cached_min = INT64_MIN / 2;
             for (int64_t it = 0;; ++it) {
                 int64_t tile;
                 if (!dyn) {
@@ -261,12 +302,20 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
                     }
                 }
-                if (tile >= num_tiles) break;
+                if (tile >= num_tiles) {
+                    if (throttle) prog_store(p.prog + unit, INT64_MAX);
+                    break;
+                }
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int32_t m0 = (int32_t)(r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM);
                 const int32_t n0 = (int32_t)(n_blk * Cfg::TILE_N + rank * Cfg::B_ROWS);
+                const int64_t wave_pos = (tile / n_units) * num_kb;
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    if (throttle && kb % p.prog_every == 0) {
+                        prog_store(p.prog + unit, wave_pos + kb);
+                        prog_throttle(p.prog, n_units, wave_pos + kb, p.prog_lead, prog_cached_min);
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint32_t fb = 0;
                     if constexpr (PAIR) {

@@ -71,10 +71,12 @@ struct LossWs {
     size_t red;                             // double [8] loss reduction output
     size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
     size_t fbnd;                            // int64 [MAX_FWD_CHUNKS + 1] forward row chunks
+    size_t prog;                            // int64 [2][PROG_UNITS] backward GEMM progress
     size_t total;
     int32_t n_tiles;
 };
 constexpr int MAX_FWD_CHUNKS = 8;
+constexpr int PROG_UNITS = 256;  // >= GEMM units (SMs, or SM pairs)
 LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0);
 
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:

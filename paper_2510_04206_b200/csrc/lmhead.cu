@@ -503,6 +503,7 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.red = p.take(sizeof(double) * 8);
     w.sched = p.take(sizeof(int) * 32);
     w.fbnd = p.take(sizeof(int64_t) * (MAX_FWD_CHUNKS + 1));
+    w.prog = p.take(sizeof(int64_t) * 2 * PROG_UNITS);
     w.total = p.off;
     return w;
 }
@@ -561,6 +562,20 @@ static SideStream& side_stream() {
     return ss;
 }
 
+// backward-GEMM progress throttle: max lead in k-blocks over the slowest pair
+// (AGENTRL_THROTTLE_LEAD, default 192, 0 = off) checked every AGENTRL_THROTTLE_EVERY k-blocks.
+// glm9b: grad GEMM HBM reads 144/151 -> 67/64 GB, +3% cycles, step 157 -> 150 ms on the
+// power-capped part (profiles/r01_throttle.txt)
+static int throttle_lead() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("AGENTRL_THROTTLE_LEAD");
+        v = e ? atoi(e) : 192;
+    }
+    return gemm_dynamic() ? v : 0;
+}
+static int throttle_every() { return env_int("AGENTRL_THROTTLE_EVERY", 8); }
+
 // forward row chunks (AGENTRL_FWD_CHUNKS, default 4, 1 = no overlap of the merge)
 static int fwd_chunks() {
     static int v = -1;
@@ -618,6 +633,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
     int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
     AG_CUDA(cudaMemsetAsync(sched, 0, 32 * sizeof(int), stream));
+    int64_t* prog = reinterpret_cast<int64_t*>(ws + w.prog);  // [2][PROG_UNITS] backward GEMMs
+    const int lead = throttle_lead();
+    if (lead > 0) AG_CUDA(cudaMemsetAsync(prog, 0xff, 2 * PROG_UNITS * sizeof(int64_t), stream));
 
     // ---- compaction (standalone) or reuse of part 1's
     if (!idx_dev) {
@@ -748,6 +766,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.pol_a = l2_policy(2, 0);
         g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
         g.tile_counter = ctr_gw;
+        if (lead > 0) {
+            g.prog = prog;
+            g.prog_every = throttle_every();
+            g.prog_lead = lead;
+        }
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
         g.ldo = d;
@@ -775,6 +798,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.pol_a = l2_policy(4, 0);  // G rows: shared by the pairs of one row block (as above)
         g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
         g.tile_counter = ctr_gh;
+        if (lead > 0) {
+            g.prog = prog + PROG_UNITS;
+            g.prog_every = throttle_every();
+            g.prog_lead = lead;
+        }
         g.scale = a->logit_scale;
         g.idx = idx_dev;
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);

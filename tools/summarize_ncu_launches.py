@@ -11,9 +11,9 @@ def short(name):
     m = re.search(r"agentrl::(\w+)", name)
     if m:
         base = m.group(1)
-        t = re.search(r"gemm_sm100_kernel<(\d)", name)
+        t = re.search(r"gemm_sm100_(?:pair_)?kernel<(\d)", name)
         if t:
-            base += {"0": "<FWD>", "1": "<GRADH>", "2": "<GRADW>"}[t.group(1)]
+            base += {"0": "<FWD>", "1": "<GRADH>", "2": "<GRADW>", "3": "<LOGP>"}[t.group(1)]
         return base
     return "other:" + name.split("(")[0][-60:]
 
@@ -28,10 +28,13 @@ def main(path, last_steps=None):
         rows.append((short(r["Kernel Name"]), float(r["Metric Value"]), r["Metric Unit"]))
     ours = [r for r in rows if not r[0].startswith("other:")]
     if last_steps:
-        # k_count starts each step
-        starts = [i for i, r in enumerate(ours) if r[0] == "k_count"]
-        if len(starts) >= last_steps:
-            ours = ours[starts[-last_steps]:]
+        # the advantage normalisation (k_adv_coop_all, or k_count on the 3-kernel path)
+        # starts each step
+        starts = [i for i, r in enumerate(ours) if r[0] in ("k_adv_coop_all", "k_count")]
+        segs = [ours[a:b] for a, b in zip(starts, starts[1:] + [len(ours)])]
+        segs = [sg for sg in segs if any("gemm" in r[0] for r in sg)]  # fused steps only
+        if len(segs) >= last_steps:
+            ours = [r for sg in segs[-last_steps:] for r in sg]
     agg = OrderedDict()
     for n, v, u in ours:
         scale = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(u, 1e-6)
