@@ -129,7 +129,8 @@ int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok
  * strictly active: A>0 & rho>1+eps_high or A<0 & rho<1-eps_low):
  *   G_{t,v} = c_t (softmax_v - [v=y_t]),  c_t = unclipped ? rho_t A_t / N : 0
  *   grad_hidden = logit_scale * G W        (rows of unmasked tokens are 0)
- *   grad_W      = logit_scale * G^T hidden (summed over ranks if grad_W_mode=1)
+ *   grad_W      = logit_scale * G^T hidden (summed over ranks if grad_W_mode=1; the rank's
+ *                 row shard summed if grad_W_mode=2)
  * Shapes: d % 64 == 0, V % 8 == 0, 1 <= V.  Arithmetic: bf16 operands on
  * tcgen05 tensor cores with fp32 accumulation; softmax statistics fp32; loss
  * and statistics reductions fp64.
@@ -146,7 +147,13 @@ typedef struct {
     float clip_eps_low, clip_eps_high; /* [0,1) and >= 0; default 0.2, 0.2 */
     float logit_scale;                 /* > 0; default 1.0 */
     const int64_t* n_mask_global;      /* device [1] */
-    int32_t grad_W_mode;               /* 0 = local sum only, 1 = all-reduce over comm */
+    int32_t grad_W_mode;               /* 0 = local sum only, 1 = all-reduce over comm,
+                                          2 = reduce-scatter over comm (FSDP-style shard,
+                                          P:1357): rows [rank*V/world, (rank+1)*V/world) of
+                                          grad_W hold the global sum, the other rows are
+                                          scratch; needs V % world == 0 (else
+                                          AGENTRL_ERR_SHAPE).  A callback communicator
+                                          without a reduce-scatter sums every row. */
     int32_t reserved;
     /* ---- objective variants; all-zero = the base objective above ----
      * KL penalty (the "- beta D_KL" of P:1103 / P:1119; beta unstated in the paper, R11):
@@ -241,6 +248,13 @@ typedef int (*agentrl_allreduce_fn)(void* user, void* dev_buf, size_t count, int
                                     agentrl_stream stream);
 int agentrl_comm_init_callback(agentrl_comm* out, int world, int rank, agentrl_allreduce_fn fn,
                                void* user);
+/* Optional in-place reduce-scatter for a callback communicator (grad_W_mode = 2): dev_buf holds
+ * world * recv_count elements; afterwards block [rank*recv_count, (rank+1)*recv_count) holds
+ * the sum over ranks (other blocks unspecified), ordered on `stream`.  Without it the
+ * communicator's all-reduce is used (a superset).  INVALID_ARG for an NCCL communicator. */
+typedef int (*agentrl_reduce_scatter_fn)(void* user, void* dev_buf, size_t recv_count, int dtype,
+                                         agentrl_stream stream);
+int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn fn);
 
 /* ---- misc -------------------------------------------------------------- */
 const char* agentrl_status_string(int code); /* text for a return code or status bit */

@@ -40,7 +40,7 @@ EXPORTED = (
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
     "agentrl_debug_adv_phase_ns", "agentrl_comm_init_callback",
-    "agentrl_logprob_workspace_size", "agentrl_logprob_fwd",
+    "agentrl_logprob_workspace_size", "agentrl_logprob_fwd", "agentrl_comm_set_reduce_scatter",
 )
 NUM_KERNEL_IDS = 12
 
@@ -88,6 +88,7 @@ _lib.agentrl_grpo_step.argtypes = [C.POINTER(Batch), _f64, C.POINTER(LossArgs),
 _lib.agentrl_comm_unique_id.argtypes = [C.c_char_p]
 _lib.agentrl_comm_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_char_p]
 _lib.agentrl_comm_destroy.argtypes = [_P]
+_lib.agentrl_comm_set_reduce_scatter.argtypes = [_P, C.c_void_p]
 _lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p,
                                             C.c_void_p]
 _lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i32, _i32]
@@ -276,9 +277,10 @@ class CallbackComm(Comm):
     """Communicator whose all-reduces call back into Python (plumbing for hosts without NCCL
     between the ranks, e.g. several test ranks sharing one GPU).  ``fn(dev_ptr, count, dtype,
     stream_handle) -> None`` must all-reduce (sum) the device buffer in place, ordered on the
-    stream; dtype is 0 = f64, 1 = f32, 2 = i64."""
+    stream; dtype is 0 = f64, 1 = f32, 2 = i64.  Optional ``rs_fn(dev_ptr, recv_count, dtype,
+    stream_handle)``: in-place reduce-scatter (grad_W_mode=2); else the all-reduce is used."""
 
-    def __init__(self, world: int, rank: int, fn):
+    def __init__(self, world: int, rank: int, fn, rs_fn=None):
         def _tramp(user, buf, n, dtype, stream):
             try:
                 fn(buf, int(n), int(dtype), stream)
@@ -292,6 +294,43 @@ class CallbackComm(Comm):
         _check(_lib.agentrl_comm_init_callback(C.byref(h), int(world), int(rank), self._cb, None),
                "agentrl_comm_init_callback")
         self.handle = h
+        self._rs = None
+        if rs_fn is not None:
+            def _rs_tramp(user, buf, n, dtype, stream):
+                try:
+                    rs_fn(buf, int(n), int(dtype), stream)
+                    return 0
+                except Exception:  # noqa: BLE001
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            self._rs = ALLREDUCE_FN(_rs_tramp)  # same C signature
+            _check(_lib.agentrl_comm_set_reduce_scatter(h, self._rs),
+                   "agentrl_comm_set_reduce_scatter")
+
+
+def gloo_reduce_scatter_fn(world, rank, group=None):
+    """Reduce-scatter callback (in place, block `rank` of world blocks gets the sum) over
+    torch.distributed reduce_scatter_tensor through host memory (test plumbing)."""
+    import torch
+    import torch.distributed as dist
+    cudart = _cudart()
+    tmap = {0: torch.float64, 1: torch.float32, 2: torch.int64}
+
+    def fn(buf, m, dtype, stream):
+        if stream:
+            torch.cuda.ExternalStream(stream).synchronize()
+        else:
+            torch.cuda.synchronize()
+        host = torch.empty(world * m, dtype=tmap[dtype])
+        es = host.element_size()
+        if cudart.cudaMemcpy(C.c_void_p(host.data_ptr()), C.c_void_p(buf), C.c_size_t(host.numel() * es), 2):
+            raise RuntimeError("cudaMemcpy D2H failed")
+        out = torch.empty(m, dtype=tmap[dtype])
+        dist.reduce_scatter_tensor(out, host, group=group)
+        if cudart.cudaMemcpy(C.c_void_p(buf + rank * m * es), C.c_void_p(out.data_ptr()), C.c_size_t(m * es), 1):
+            raise RuntimeError("cudaMemcpy H2D failed")
+    return fn
 
 
 def gloo_allreduce_fn(group=None):

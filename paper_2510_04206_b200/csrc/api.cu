@@ -83,6 +83,8 @@ typedef int (*fn_commInitRank)(nccl_comm_t*, int, nccl_uid_t, int);
 typedef int (*fn_commDestroy)(nccl_comm_t);
 typedef int (*fn_allReduce)(const void*, void*, size_t, int /*dtype*/, int /*op*/, nccl_comm_t,
                             cudaStream_t);
+typedef int (*fn_reduceScatter)(const void*, void*, size_t /*recvcount*/, int, int, nccl_comm_t,
+                                cudaStream_t);
 enum { NCCL_INT64 = 4, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
 
 struct NcclApi {
@@ -91,6 +93,7 @@ struct NcclApi {
     fn_commInitRank commInitRank = nullptr;
     fn_commDestroy commDestroy = nullptr;
     fn_allReduce allReduce = nullptr;
+    fn_reduceScatter reduceScatter = nullptr;
 };
 static NcclApi* nccl() {
     static NcclApi api;
@@ -106,6 +109,7 @@ static NcclApi* nccl() {
         api.commInitRank = (fn_commInitRank)dlsym(h, "ncclCommInitRank");
         api.commDestroy = (fn_commDestroy)dlsym(h, "ncclCommDestroy");
         api.allReduce = (fn_allReduce)dlsym(h, "ncclAllReduce");
+        api.reduceScatter = (fn_reduceScatter)dlsym(h, "ncclReduceScatter");
     });
     if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.allReduce)
         return nullptr;
@@ -119,6 +123,7 @@ struct agentrl_comm_s {
     int world, rank;
     agentrl_allreduce_fn fn;  // callback backend (non-null) instead of NCCL
     void* user;
+    agentrl_reduce_scatter_fn rs;  // optional callback reduce-scatter
 };
 
 namespace agentrl {
@@ -147,6 +152,28 @@ int comm_allreduce_f32(agentrl_comm c, float* b, size_t n, cudaStream_t s) {
 int comm_allreduce_i64(agentrl_comm c, int64_t* b, size_t n, cudaStream_t s) {
     return allreduce(c, b, n, NCCL_INT64, s);
 }
+// in-place sum reduce-scatter of n = world * m floats: rank r's block [r m, (r+1) m) receives
+// the global sum.  The callback backend has only an all-reduce, which is a superset.
+int comm_reduce_scatter_f32(agentrl_comm c, float* b, size_t n, cudaStream_t s) {
+    if (!c) return AGENTRL_ERR_NCCL;
+    if (n == 0) return AGENTRL_OK;
+    if (c->fn && c->rs) {
+        if (c->world <= 0 || n % (size_t)c->world != 0) return AGENTRL_ERR_NCCL;
+        return c->rs(c->user, b, n / (size_t)c->world, AGENTRL_DTYPE_F32,
+                     reinterpret_cast<agentrl_stream>(s)) == 0
+                   ? AGENTRL_OK
+                   : AGENTRL_ERR_NCCL;
+    }
+    if (c->fn) return allreduce(c, b, n, NCCL_FLOAT32, s);
+    NcclApi* api = nccl();
+    if (!api || !api->reduceScatter || c->world <= 0 || n % (size_t)c->world != 0)
+        return AGENTRL_ERR_NCCL;
+    const size_t m = n / (size_t)c->world;
+    return api->reduceScatter(b, b + (size_t)c->rank * m, m, NCCL_FLOAT32, NCCL_SUM, c->comm, s) == 0
+               ? AGENTRL_OK
+               : AGENTRL_ERR_NCCL;
+}
+int comm_world(agentrl_comm c) { return c ? c->world : 1; }
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -174,7 +201,7 @@ static int check_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, boo
     if (!aligned(a->hidden, 16) || !aligned(a->W_head, 16) || !aligned(o->grad_hidden, 16) ||
         !aligned(o->grad_W, 16))
         return AGENTRL_ERR_SHAPE;
-    if (a->grad_W_mode < 0 || a->grad_W_mode > 1) return AGENTRL_ERR_INVALID_ARG;
+    if (a->grad_W_mode < 0 || a->grad_W_mode > 2) return AGENTRL_ERR_INVALID_ARG;
     // objective variants: beta >= 0 (ref log-probs needed when > 0); loss_agg 0/1, the
     // sequence mean only in the fused step (it needs the batch descriptor) unless the caller
     // supplies the weights
@@ -219,6 +246,7 @@ int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_o
                                 agentrl_stream stream) {
     g_launches = 0;
     int rc = check_loss(a, o, false);
+    if (!rc && a->grad_W_mode == 2 && comm && a->V % comm_world(comm) != 0) rc = AGENTRL_ERR_SHAPE;
     if (rc) return rc;
     if (!d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
     if ((rc = check_device())) return rc;
@@ -263,6 +291,7 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
     int rc = check_batch(b, eps_std);
     if (rc) return rc;
     if ((rc = check_loss(a, o, true))) return rc;
+    if (a->grad_W_mode == 2 && comm && a->V % comm_world(comm) != 0) return AGENTRL_ERR_SHAPE;
     if (a->T != b->T || a->loss_mask != b->loss_mask) return AGENTRL_ERR_INVALID_ARG;
     if ((b->T > 0 && !adv_tok_out) || !d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
     if ((rc = check_device())) return rc;
@@ -302,7 +331,7 @@ int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned cha
     if (!api) return AGENTRL_ERR_NCCL;
     nccl_uid_t id;
     memcpy(id.internal, host_id, 128);
-    agentrl_comm c = new agentrl_comm_s{nullptr, world, rank, nullptr, nullptr};
+    agentrl_comm c = new agentrl_comm_s{nullptr, world, rank, nullptr, nullptr, nullptr};
     if (api->commInitRank(&c->comm, world, id, rank) != 0) {
         delete c;
         return AGENTRL_ERR_NCCL;
@@ -314,7 +343,13 @@ int agentrl_comm_init(agentrl_comm* out, int world, int rank, const unsigned cha
 int agentrl_comm_init_callback(agentrl_comm* out, int world, int rank, agentrl_allreduce_fn fn,
                                void* user) {
     if (!out || world <= 0 || rank < 0 || rank >= world || !fn) return AGENTRL_ERR_INVALID_ARG;
-    *out = new agentrl_comm_s{nullptr, world, rank, fn, user};
+    *out = new agentrl_comm_s{nullptr, world, rank, fn, user, nullptr};
+    return AGENTRL_OK;
+}
+
+int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn fn) {
+    if (!comm || !comm->fn) return AGENTRL_ERR_INVALID_ARG;
+    comm->rs = fn;
     return AGENTRL_OK;
 }
 

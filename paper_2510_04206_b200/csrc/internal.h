@@ -108,6 +108,8 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
 int comm_allreduce_f64(agentrl_comm c, double* buf, size_t n, cudaStream_t s);
 int comm_allreduce_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
 int comm_allreduce_i64(agentrl_comm c, int64_t* buf, size_t n, cudaStream_t s);
+int comm_reduce_scatter_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
+int comm_world(agentrl_comm c);
 
 // launch counter for the bench's gpu_launches claim
 void count_launch(int n = 1);

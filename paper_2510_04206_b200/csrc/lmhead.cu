@@ -781,11 +781,14 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     }
     // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
     SideStream* ss = nullptr;
-    if (comm && a->grad_W_mode == 1) {
+    if (comm && a->grad_W_mode >= 1) {
         ss = &side_stream();
         AG_CUDA(cudaEventRecord(ss->e0, stream));
         AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
-        if ((rc = comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s))) return rc;
+        rc = a->grad_W_mode == 1
+                 ? comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s)
+                 : comm_reduce_scatter_f32(comm, o->grad_W, (size_t)V * d, ss->s);  // FSDP shard
+        if (rc) return rc;
         AG_CUDA(cudaEventRecord(ss->e1, ss->s));
     }
     // ---- K8 grad_hidden = s G W   (M = T_eff, N = d, K = V), scattered to idx rows

@@ -102,3 +102,24 @@ def test_missing_library_fails_loudly(tmp_path):
                        capture_output=True, text=True)
     assert r.returncode != 0 and "ImportError" in r.stderr
     del code
+
+
+def test_reduce_scatter_mode_contract(libpath):
+    """grad_W_mode 2 (reduce-scatter row shards) needs V % world == 0: SHAPE before any device
+    work; mode 3 is INVALID_ARG.  Host-side checks only (fake, aligned, never-dereferenced
+    pointers; the call returns before touching the device)."""
+    import paper_2510_04206_b200 as m
+    comm = m.CallbackComm(3, 0, lambda *a: None)
+    fake = 1 << 20
+    args = m.LossArgs(T=16, d=64, V=2000, hidden=fake, W_head=fake, target=fake, adv_tok=fake,
+                      old_logp=fake, loss_mask=fake, clip_eps_low=0.2, clip_eps_high=0.2,
+                      logit_scale=1.0, n_mask_global=fake, grad_W_mode=2)
+    out = m.LossOut(loss=fake, grad_hidden=fake, grad_W=fake)
+    call = lambda: m._lib.agentrl_policy_loss_fwd_bwd(ctypes.byref(args), ctypes.byref(out), fake,
+                                                      1 << 30, comm.handle, fake, None)
+    assert call() == m.ERR_SHAPE          # 2000 % 3 != 0
+    args.V = 2016                          # divisible: passes this check, fails later (no GPU)
+    assert call() not in (m.ERR_SHAPE, m.ERR_INVALID_ARG, 0)
+    args.grad_W_mode = 3
+    assert call() == m.ERR_INVALID_ARG
+    comm.destroy()

@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, out_dir, cfg_name):
+def _rank(rank, world, port, out_dir, cfg_name, mode=1):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -51,9 +51,10 @@ def _rank(rank, world, port, out_dir, cfg_name):
                                              minlength=gb["n_groups"]), world)
     lb = synth.shard_batch(gb, rog, rank)
     tok = lb["token_index"]
-    comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn())
+    comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn(),
+                           rs_fn=ag.gloo_reduce_scatter_fn(world, rank) if mode == 2 else None)
     step = ag.Step(lb["T"], len(lb["task_id"]), lb["n_groups"], lb["n_tasks"], cfg.d, cfg.V,
-                   comm=comm)
+                   comm=comm, grad_W_mode=mode)
     step(batch_dev(lb), bf16_dev(hb[tok]), bf16_dev(Wb), t(y[tok], torch.int32),
          t(old[tok], torch.float32))
     torch.cuda.synchronize()
@@ -88,15 +89,22 @@ def test_nccl_world1_matches_no_comm():
     comm = ag.Comm(1, 0, ag.Comm.unique_id())
     s1 = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V, comm=comm)
     s1(*args)
+    # grad_W_mode 2: ncclReduceScatter in place (world 1: the whole buffer is rank 0's shard)
+    s2 = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V, comm=comm,
+                 grad_W_mode=2)
+    s2(*args)
     torch.cuda.synchronize()
-    for a, c in ((s0.loss, s1.loss), (s0.adv_tok, s1.adv_tok), (s0.grad_W, s1.grad_W),
-                 (s0.grad_hidden, s1.grad_hidden), (s0.task_stats, s1.task_stats)):
-        assert torch.equal(a, c)
+    for s in (s1, s2):
+        for a, c in ((s0.loss, s.loss), (s0.adv_tok, s.adv_tok), (s0.grad_W, s.grad_W),
+                     (s0.grad_hidden, s.grad_hidden), (s0.task_stats, s.task_stats)):
+            assert torch.equal(a, c)
     comm.destroy()
 
 
-@pytest.mark.parametrize("cfg_name", ["tiny", "ragged"])
-def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name):
+@pytest.mark.parametrize("cfg_name,mode", [("tiny", 1), ("ragged", 1), ("ragged", 2)])
+def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name, mode):
+    """mode 1: grad_W all-reduced (replicated head); mode 2: reduce-scattered (FSDP-style row
+    shard): each rank's rows [r V/2, (r+1) V/2) hold the global sum."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -106,7 +114,7 @@ def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name):
     import synth
     from gpu_util import adv_close, f64, max_abs_rel
 
-    mp.spawn(_rank, args=(2, _port(), str(tmp_path), cfg_name), nprocs=2, join=True)
+    mp.spawn(_rank, args=(2, _port(), str(tmp_path), cfg_name, mode), nprocs=2, join=True)
     cfg = synth.CONFIGS[cfg_name]
     gb = synth.make_structure(cfg)
     hb, Wb, y = synth.make_head(cfg, mask=gb["loss_mask"])
@@ -120,14 +128,20 @@ def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name):
         assert r[k]["st"] & ~16 == 0
         # global (all-reduced) results are identical on both ranks
         assert abs(r[k]["loss"] - ref["loss"]) <= 1e-3 * max(abs(ref["loss"]), 1.0 / N) + 1e-9
-        assert max_abs_rel(r[k]["gw"], ref["grad_W"]) <= 2e-2
+        if mode == 1:
+            assert max_abs_rel(r[k]["gw"], ref["grad_W"]) <= 2e-2
+        else:
+            sh = slice(k * cfg.V // 2, (k + 1) * cfg.V // 2)
+            gmax = np.abs(ref["grad_W"]).max()
+            assert np.abs(r[k]["gw"][sh] - ref["grad_W"][sh]).max() <= 2e-2 * gmax
         np.testing.assert_array_equal(r[k]["ts"][:, 0], ref["task_stats"][:, 0])
         np.testing.assert_allclose(r[k]["ts"][:, 1:], ref["task_stats"][:, 1:], rtol=1e-9,
                                    atol=1e-12)
         # rank-local rows
         tok = r[k]["tok"]
         assert adv_close(r[k]["adv"], ref["adv_tok"][tok])
-    np.testing.assert_array_equal(r[0]["gw"], r[1]["gw"])
+    if mode == 1:
+        np.testing.assert_array_equal(r[0]["gw"], r[1]["gw"])
     gh = np.zeros_like(ref["grad_hidden"])
     for k in range(2):
         gh[r[k]["tok"]] = r[k]["gh"]

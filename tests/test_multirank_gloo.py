@@ -71,10 +71,16 @@ def _worker(rank, world, port, out_dir):
     # C2, C3
     loss = torch.tensor([out["loss"]], dtype=torch.float64)
     dist.all_reduce(loss)
-    gw = torch.from_numpy(out["grad_W"])
+    gw_local = torch.from_numpy(out["grad_W"])
+    # C3 as a reduce-scatter (grad_W_mode 2, FSDP-style row shard): block `rank` of the rows
+    shard = torch.empty(gw_local.shape[0] // world, gw_local.shape[1], dtype=gw_local.dtype)
+    dist.reduce_scatter_tensor(shard, gw_local.clone())
+    gw = gw_local.clone()
     dist.all_reduce(gw)
+    np.save(os.path.join(out_dir, f"shard{rank}.npy"), shard.numpy())
     if rank == 0:
         ref = oracle.grpo_step(gb, h, W, y, old)
+        np.save(os.path.join(out_dir, "gw_ref.npy"), ref["grad_W"])
         np.save(os.path.join(out_dir, "res.npy"),
                 np.asarray([loss.item(), ref["loss"],
                             float(np.abs(gw.numpy() - ref["grad_W"]).max()),
@@ -98,3 +104,7 @@ def test_two_rank_protocol_matches_global(tmp_path):
     np.testing.assert_allclose(adv[0], adv[1], atol=1e-12)
     gh = np.load(tmp_path / "gh.npy")
     np.testing.assert_allclose(gh[0], gh[1], atol=1e-14)
+    # reduce-scatter shards tile the global grad_W
+    shards = np.concatenate([np.load(tmp_path / f"shard{k}.npy") for k in range(2)])
+    ref = np.load(tmp_path / "gw_ref.npy")
+    assert np.abs(shards - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1.0)
