@@ -71,7 +71,7 @@ struct LossWs {
     size_t red;                             // double [8] loss reduction output
     size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
     size_t fbnd;                            // int64 [MAX_FWD_CHUNKS + 1] forward row chunks
-    size_t prog;                            // int64 [2][PROG_UNITS] backward GEMM progress
+    size_t prog;                            // int64 [2 + MAX_FWD_CHUNKS][PROG_UNITS] GEMM progress
     size_t total;
     int32_t n_tiles;
 };

@@ -503,7 +503,7 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.red = p.take(sizeof(double) * 8);
     w.sched = p.take(sizeof(int) * 32);
     w.fbnd = p.take(sizeof(int64_t) * (MAX_FWD_CHUNKS + 1));
-    w.prog = p.take(sizeof(int64_t) * 2 * PROG_UNITS);
+    w.prog = p.take(sizeof(int64_t) * (2 + MAX_FWD_CHUNKS) * PROG_UNITS);
     w.total = p.off;
     return w;
 }
@@ -575,6 +575,15 @@ static int throttle_lead() {
     return gemm_dynamic() ? v : 0;
 }
 static int throttle_every() { return env_int("AGENTRL_THROTTLE_EVERY", 8); }
+// forward GEMM throttle (AGENTRL_THROTTLE_LEAD_FWD, k-blocks of 128 K; 0 = off)
+static int throttle_lead_fwd() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("AGENTRL_THROTTLE_LEAD_FWD");
+        v = e ? atoi(e) : 0;
+    }
+    return gemm_dynamic() ? v : 0;
+}
 
 // forward row chunks (AGENTRL_FWD_CHUNKS, default 4, 1 = no overlap of the merge)
 static int fwd_chunks() {
@@ -633,9 +642,12 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
     int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
     AG_CUDA(cudaMemsetAsync(sched, 0, 32 * sizeof(int), stream));
-    int64_t* prog = reinterpret_cast<int64_t*>(ws + w.prog);  // [2][PROG_UNITS] backward GEMMs
-    const int lead = throttle_lead();
-    if (lead > 0) AG_CUDA(cudaMemsetAsync(prog, 0xff, 2 * PROG_UNITS * sizeof(int64_t), stream));
+    // progress arrays: [0] grad_W, [1] grad_hidden, [2 + c] forward chunk c
+    int64_t* prog = reinterpret_cast<int64_t*>(ws + w.prog);
+    const int lead = throttle_lead(), lead_fwd = throttle_lead_fwd();
+    if (lead > 0 || lead_fwd > 0)
+        AG_CUDA(cudaMemsetAsync(prog, 0xff, (2 + MAX_FWD_CHUNKS) * PROG_UNITS * sizeof(int64_t),
+                                stream));
 
     // ---- compaction (standalone) or reuse of part 1's
     if (!idx_dev) {
@@ -710,6 +722,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.pol_a = l2_policy(0, 2);  // H rows of the current row group: reused by every column
         g.pol_b = l2_policy(1, 1);  // W: streamed, shared only by the concurrent row tiles
         g.tile_counter = ctr_fwd ? ctr_fwd + 16 * (c > 0) + c : nullptr;
+        if (lead_fwd > 0) {
+            g.prog = prog + (2 + c) * PROG_UNITS;
+            g.prog_every = throttle_every();
+            g.prog_lead = lead_fwd;
+        }
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
         g.P = reinterpret_cast<__half*>(PG);
