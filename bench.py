@@ -178,7 +178,11 @@ def run_native(args, cfg, world, rank, local_rank):
         bd[k] = bd[k].to(torch.int32)
     bd["rewards"] = bd["rewards"].to(torch.float32)
     bd["loss_mask"] = bd["loss_mask"].to(torch.uint8)
-    step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm)
+    # C3 as the FSDP-style reduce-scatter of grad_W rows (the paper's trainer shards the head,
+    # P:1357) when V divides evenly, else the all-reduce of a replicated head
+    gw_mode = (2 if V % world == 0 else 1) if comm is not None else 0
+    step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm,
+                   grad_W_mode=gw_mode)
     # behaviour log-probs: one untimed forward (old = 0), then old = logp + delta
     old = torch.zeros(T, dtype=torch.float32, device=dev)
     step(bd, hid, W, target, old)
@@ -321,6 +325,7 @@ def run_native(args, cfg, world, rank, local_rank):
         "config": {"workload": cfg.name, "T": T_global, "T_eff": T_eff_global, "d": d, "V": V,
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
+                   "grad_W_collective": {0: "none", 1: "all-reduce", 2: "reduce-scatter"}[gw_mode],
                    "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
         "masked_tokens_per_s": T_eff_global / (ms / 1e3),

@@ -123,7 +123,7 @@ static bool gemm_fwd_ksub2() {
 
 template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB = 1>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
-                       int64_t max_tiles, cudaStream_t stream) {
+                       int64_t max_tiles, cudaStream_t stream, int reserve_sms = 0) {
     ProfScope ps(EPI == EPI_FWD    ? KID_FWD
                  : EPI == EPI_GRADW ? KID_GRADW
                  : EPI == EPI_LOGP  ? KID_LOGP_GEMM
@@ -138,8 +138,10 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             attr_done = true;
         }
-        int64_t grid = gemm_full_grid() ? 2 * std::max<int64_t>(max_tiles, 1)
-                                        : std::min<int64_t>(num_sms() & ~1, std::max<int64_t>(max_tiles, 2));
+        int64_t grid = gemm_full_grid()
+                           ? 2 * std::max<int64_t>(max_tiles, 1)
+                           : std::min<int64_t>((num_sms() - reserve_sms) & ~1,
+                                               std::max<int64_t>(max_tiles, 2));
         grid &= ~int64_t(1);
         kern<<<(unsigned)grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     } else {
@@ -150,7 +152,7 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             attr_done = true;
         }
-        int grid = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(max_tiles, 1));
+        int grid = (int)std::min<int64_t>(num_sms() - reserve_sms, std::max<int64_t>(max_tiles, 1));
         kern<<<grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     }
     count_launch();
@@ -585,6 +587,17 @@ static int throttle_lead_fwd() {
     return gemm_dynamic() ? v : 0;
 }
 
+// SMs left free for NCCL while grad_hidden overlaps C3 (AGENTRL_COMM_SMS, default 16), only
+// when the communicator spans more than one rank
+static int comm_reserve_sms() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("AGENTRL_COMM_SMS");
+        v = e ? std::max(0, atoi(e)) : 16;
+    }
+    return std::min(v, num_sms() / 2);
+}
+
 // forward row chunks (AGENTRL_FWD_CHUNKS, default 4, 1 = no overlap of the merge)
 static int fwd_chunks() {
     static int v = -1;
@@ -828,8 +841,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
         g.ldo = d;
         const int64_t tiles = max_m_tiles * ceil_div(d, GEMM_BN);
-        rc = gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream)
-                           : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream);
+        // with C3 in flight on the side stream, leave SMs for the NCCL kernel so the
+        // collective overlaps this GEMM instead of queueing behind its persistent CTAs
+        const int rsv = ss && comm_world(comm) > 1 ? comm_reserve_sms() : 0;
+        rc = gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream, rsv)
+                           : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream, rsv);
         if (rc) return rc;
     }
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
