@@ -27,6 +27,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
+# extra nvcc flags for A/B builds (e.g. AGENTRL_NVCC_EXTRA="-DADV_MIN_BLOCKS=2")
+FLAGS += os.environ.get("AGENTRL_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -26,11 +26,25 @@ namespace cg = cooperative_groups;
 namespace agentrl {
 
 constexpr int COOP_THREADS = 256;
+#ifndef ADV_MIN_BLOCKS
+#define ADV_MIN_BLOCKS 3  // resident blocks per SM the register budget is cut for
+#endif
 constexpr int GMAX_BLOCKS = 2048;  // cap on the cooperative grid (per-block scratch arrays)
 constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 tokens)
 constexpr int WOFF_CAP = 64;       // trajectory offsets staged per warp chunk
 constexpr int NWARPS = COOP_THREADS / 32;
 constexpr int TASK_BATCH = 16;  // tasks reduced per barrier in the per-block partials
+constexpr int BT_CAP = 2048;    // trajectories a block stages in smem for its token range
+
+// static shared memory of the cooperative kernels (one arena for all phases)
+struct CoopSmem {
+    int32_t s_w[8];
+    int32_t s_pre[GMAX_BLOCKS + 1];
+    // the offsets of the trajectories overlapping this block's tokens (or, on the fallback path
+    // for blocks spanning more than BT_CAP trajectories, per-warp offset staging)
+    int64_t s_boff[BT_CAP + 1];
+    int32_t s_aux[BT_CAP];  // phase A: masked count per staged trajectory; C: its A~ (f32 bits)
+};
 
 // phase timestamps of the last cooperative launch (block 0, after each grid barrier), read by
 // agentrl_debug_adv_phase_ns(); 8 x %globaltimer ns
@@ -77,6 +91,33 @@ __device__ __forceinline__ int32_t coop_find_traj(const int64_t* __restrict__ of
         else hi = mid;
     }
     return lo < n_traj ? lo : n_traj - 1;
+}
+
+// trajectories [bf, bf + n) overlap this block's warp chunks [c_lo, c_hi) (clamped; 0 if none)
+__device__ __forceinline__ int32_t block_traj_range(const AdvParams& p, int64_t c_lo, int64_t c_hi,
+                                                    int32_t& bf) {
+    bf = 0;
+    if (p.n_traj <= 0 || c_lo >= c_hi) return 0;
+    int32_t f = p.chunk_first[c_lo];
+    int32_t l = c_hi < p.n_chunks ? p.chunk_first[c_hi] : p.n_traj - 1;
+    f = min(max(f, 0), p.n_traj - 1);
+    l = min(max(l, f), p.n_traj - 1);
+    bf = f;
+    return l - f + 1;
+}
+// k in [lo, hi) with s[k] <= t < s[k+1] (clamped to lo / hi - 1)
+__device__ __forceinline__ int32_t smem_find_in(const int64_t* s, int32_t lo, int32_t hi, int64_t t) {
+    while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (s[mid] <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+// mask byte i (compile-time after unrolling) of a 16-byte vector, as 0/1
+__device__ __forceinline__ int32_t mbit(const uint4& v, int i) {
+    const uint32_t w = i < 4 ? v.x : (i < 8 ? v.y : (i < 12 ? v.z : v.w));
+    return ((w >> (8 * (i & 3))) & 0xffu) != 0u;
 }
 
 __device__ __forceinline__ void coop_mask16(const uint8_t* __restrict__ mask, int64_t T,
@@ -303,10 +344,11 @@ __device__ void block_prefix_smem(const int32_t* __restrict__ blk, int64_t G, in
 }
 
 // ------------------------------------------------------------------ phases 0 .. B4
-__device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
-    __shared__ int32_t s_w[8];
-    __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
-    __shared__ int64_t s_off[NWARPS * WOFF_CAP];
+__device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid, CoopSmem& sm) {
+    static_assert(NWARPS * WOFF_CAP <= BT_CAP + 1, "fallback staging fits the arena");
+    int32_t* s_w = sm.s_w;
+    int32_t* s_pre = sm.s_pre;
+    int64_t* s_off = sm.s_boff;  // fallback path: per-warp staging
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t gtid = B * blockDim.x + threadIdx.x;
     const int64_t gstride = G * blockDim.x;
@@ -332,9 +374,21 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
     phase_mark(1);
 
     // phase A: this block's contiguous warp chunks (512 tokens each, one warp per chunk):
-    // n_g (atomics), per-chunk counts, block total
+    // n_g, per-chunk counts, block total.  Fast path: the block stages the offsets of the
+    // trajectories its tokens cover once (one coalesced load) and counts per trajectory with
+    // shared atomics; the chunk loop then has no dependent global loads.
     const bool any_traj = p.n_traj > 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t bf = 0;
+    const int32_t nbt = any_traj ? block_traj_range(p, c_lo, c_hi, bf) : 0;
+    const bool staged = nbt > 0 && nbt <= BT_CAP;
+    if (staged) {
+        for (int32_t k = threadIdx.x; k <= nbt; k += COOP_THREADS) {
+            sm.s_boff[k] = p.off[bf + k];
+            if (k < nbt) sm.s_aux[k] = 0;
+        }
+    }
+    __syncthreads();
     int64_t* s_offw = s_off + warp * WOFF_CAP;
     int32_t warp_total = 0;
     ChunkIn nxt{};
@@ -343,44 +397,73 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
         const ChunkIn cur = nxt;
         if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, false);
         const int64_t t0 = c * WCHUNK + lane * 16;
-        uint8_t m[16];
-        unpack16(cur.mk, m);
-        int32_t first = 0, cnt_st = 0;
-        if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
         int32_t mine = 0;
-        if (t0 < p.T && any_traj) {
-            int32_t g, k = 0;
-            int64_t end;
-            if (cnt_st) {
-                k = smem_find(s_offw, cnt_st, t0);
-                g = first + k;
-                end = s_offw[k + 1];
-            } else {
-                g = coop_find_traj(p.off, p.n_traj, t0);
-                end = p.off[g + 1];
-            }
-            int32_t cnt = 0;
+        if (staged) {
+            if (t0 < p.T) {
+                const int32_t klo = min(max(cur.f - bf, 0), nbt - 1);
+                const int32_t khi = min(max(cur.l - bf + 1, klo + 1), nbt);
+                int32_t k = smem_find_in(sm.s_boff, klo, khi, t0);
+                int64_t end = sm.s_boff[k + 1];
+                int32_t cnt = 0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t t = t0 + i;
-                if (t >= p.T) break;
-                while (t >= end && g + 1 < p.n_traj) {
-                    if (cnt) atomicAdd(&p.n_g[g], cnt);
-                    cnt = 0;
-                    ++g;
-                    ++k;
-                    end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t t = t0 + i;
+                    while (t >= end && k + 1 < nbt) {
+                        if (cnt) atomicAdd(&sm.s_aux[k], cnt);
+                        cnt = 0;
+                        ++k;
+                        end = sm.s_boff[k + 1];
+                    }
+                    const int32_t bit = mbit(cur.mk, i);  // 0 past T (zero-filled load)
+                    cnt += bit;
+                    mine += bit;
                 }
-                const int32_t bit = m[i] != 0;
-                cnt += bit;
-                mine += bit;
+                if (cnt) atomicAdd(&sm.s_aux[k], cnt);
             }
-            if (cnt) atomicAdd(&p.n_g[g], cnt);
+        } else {
+            uint8_t m[16];
+            unpack16(cur.mk, m);
+            int32_t first = 0, cnt_st = 0;
+            if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
+            if (t0 < p.T && any_traj) {
+                int32_t g, k = 0;
+                int64_t end;
+                if (cnt_st) {
+                    k = smem_find(s_offw, cnt_st, t0);
+                    g = first + k;
+                    end = s_offw[k + 1];
+                } else {
+                    g = coop_find_traj(p.off, p.n_traj, t0);
+                    end = p.off[g + 1];
+                }
+                int32_t cnt = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t t = t0 + i;
+                    if (t >= p.T) break;
+                    while (t >= end && g + 1 < p.n_traj) {
+                        if (cnt) atomicAdd(&p.n_g[g], cnt);
+                        cnt = 0;
+                        ++g;
+                        ++k;
+                        end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
+                    }
+                    const int32_t bit = m[i] != 0;
+                    cnt += bit;
+                    mine += bit;
+                }
+                if (cnt) atomicAdd(&p.n_g[g], cnt);
+            }
         }
         const int32_t total = __shfl_sync(0xffffffffu, warp_incl_scan(mine), 31);
         if (lane == 0) p.chunk[c] = total;
         warp_total += total;
         __syncwarp();  // s_offw restaged by this warp's next chunk
+    }
+    if (staged) {  // per-trajectory block counts -> n_g (integer atomics: exact, order-free)
+        __syncthreads();
+        for (int32_t k = threadIdx.x; k < nbt; k += COOP_THREADS)
+            if (sm.s_aux[k]) atomicAdd(&p.n_g[bf + k], sm.s_aux[k]);
     }
     if (lane == 0) s_w[warp] = warp_total;
     __syncthreads();
@@ -573,11 +656,11 @@ __device__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid) {
 
 // ------------------------------------------------------------------ phase C
 // (needs gridDim.x == the stats launch's grid: it owns the same contiguous chunk ranges)
-__device__ void coop_apply_phase(const AdvParams& p) {
+__device__ __forceinline__ void coop_apply_phase(const AdvParams& p, CoopSmem& sm) {
     extern __shared__ double s_task[];  // [2*n_tasks]: mu, max(sigma, eps)
-    __shared__ int32_t s_w[8];
-    __shared__ int32_t s_pre[GMAX_BLOCKS + 1];
-    __shared__ int64_t s_off[NWARPS * WOFF_CAP];
+    int32_t* s_w = sm.s_w;
+    int32_t* s_pre = sm.s_pre;
+    int64_t* s_off = sm.s_boff;  // fallback path: per-warp staging
     const int64_t G = gridDim.x, B = blockIdx.x;
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
         const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
@@ -614,6 +697,25 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     // compaction staging (dynamic smem after s_task; present only when p.compact)
     int32_t(*s_cidx)[WCHUNK] = reinterpret_cast<int32_t(*)[WCHUNK]>(s_task + 2 * p.n_tasks);
     float(*s_cadv)[WCHUNK] = reinterpret_cast<float(*)[WCHUNK]>(s_task + 2 * p.n_tasks) + NWARPS;
+    // Fast path: the block stages the offsets and final values A~_g = (A^_g - mu_i) / max(sigma_i,
+    // eps) (Eq.1) of the trajectories its tokens cover; the chunk loop then streams
+    // mask -> adv_tok with smem lookups only.
+    int32_t bf = 0;
+    const int32_t nbt = any_traj ? block_traj_range(p, c_lo, c_hi, bf) : 0;
+    const bool staged = nbt > 0 && nbt <= BT_CAP;
+    if (staged) {
+        for (int32_t k = threadIdx.x; k <= nbt; k += COOP_THREADS) {
+            sm.s_boff[k] = p.off[bf + k];
+            if (k < nbt) {
+                const int32_t ti = p.task_id[bf + k];
+                const float at = (ti >= 0 && ti < p.n_tasks)
+                                     ? (float)((p.adv_hat[bf + k] - s_task[2 * ti]) / s_task[2 * ti + 1])
+                                     : 0.f;
+                sm.s_aux[k] = __float_as_int(at);
+            }
+        }
+    }
+    __syncthreads();
     // every warp walks its own chunks with no block-wide exchange: the chunk's compaction base
     // is the block prefix plus the local base stored by the counting phase
     ChunkIn nxt{};
@@ -623,55 +725,79 @@ __device__ void coop_apply_phase(const AdvParams& p) {
         if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, true);
         const int32_t wbase = blk_base + cur.base;
         const int64_t t0 = c * WCHUNK + lane * 16;
-        uint8_t m[16];
-        unpack16(cur.mk, m);
-        int32_t first = 0, cnt_st = 0;
-        if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
         int32_t mine = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) mine += m[i] != 0;
+        for (int i = 0; i < 16; ++i) mine += mbit(cur.mk, i);
         const int32_t incl = warp_incl_scan(mine);
         const int32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
         int32_t pos = incl - mine;  // position within this warp chunk's compacted range
         float outv[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) outv[i] = 0.f;
-        if (t0 < p.T && any_traj && mine > 0) {
-            int32_t g, k = 0;
-            int64_t end;
-            if (cnt_st) {
-                k = smem_find(s_offw, cnt_st, t0);
-                g = first + k;
-                end = s_offw[k + 1];
-            } else {
-                g = coop_find_traj(p.off, p.n_traj, t0);
-                end = p.off[g + 1];
-            }
-            int32_t cur = -1;
-            float at = 0.f;
+        if (staged) {
+            if (t0 < p.T && mine > 0) {
+                const int32_t klo = min(max(cur.f - bf, 0), nbt - 1);
+                const int32_t khi = min(max(cur.l - bf + 1, klo + 1), nbt);
+                int32_t k = smem_find_in(sm.s_boff, klo, khi, t0);
+                int64_t end = sm.s_boff[k + 1];
+                float at = __int_as_float(sm.s_aux[k]);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t t = t0 + i;
-                if (t >= p.T) break;
-                while (t >= end && g + 1 < p.n_traj) {
-                    ++g;
-                    ++k;
-                    end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
-                }
-                if (m[i]) {
-                    if (g != cur) {  // Eq.1 for this trajectory
-                        cur = g;
-                        const int32_t ti = p.task_id[g];
-                        at = (ti >= 0 && ti < p.n_tasks)
-                                 ? (float)((p.adv_hat[g] - s_task[2 * ti]) / s_task[2 * ti + 1])
-                                 : 0.f;
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t t = t0 + i;
+                    while (t >= end && k + 1 < nbt) {
+                        ++k;
+                        end = sm.s_boff[k + 1];
+                        at = __int_as_float(sm.s_aux[k]);
                     }
-                    outv[i] = at;
-                    if (p.compact) {  // staged in smem, written coalesced below
+                    const bool on = mbit(cur.mk, i);
+                    outv[i] = on ? at : 0.f;
+                    if (p.compact && on) {  // staged in smem, written coalesced below
                         s_cidx[warp][pos] = (int32_t)t;
                         s_cadv[warp][pos] = at;
+                        ++pos;
                     }
-                    ++pos;
+                }
+            }
+        } else {  // fallback: per-warp offset staging (warp-collective), global lookups
+            int32_t first = 0, cnt_st = 0;
+            if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
+            if (t0 < p.T && any_traj && mine > 0) {
+                int32_t g, k = 0;
+                int64_t end;
+                if (cnt_st) {
+                    k = smem_find(s_offw, cnt_st, t0);
+                    g = first + k;
+                    end = s_offw[k + 1];
+                } else {
+                    g = coop_find_traj(p.off, p.n_traj, t0);
+                    end = p.off[g + 1];
+                }
+                int32_t gcur = -1;
+                float at = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t t = t0 + i;
+                    while (t >= end && g + 1 < p.n_traj) {
+                        ++g;
+                        ++k;
+                        end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
+                    }
+                    const bool on = t < p.T && mbit(cur.mk, i);
+                    if (on) {
+                        if (g != gcur) {  // Eq.1 for this trajectory
+                            gcur = g;
+                            const int32_t ti = p.task_id[g];
+                            at = (ti >= 0 && ti < p.n_tasks)
+                                     ? (float)((p.adv_hat[g] - s_task[2 * ti]) / s_task[2 * ti + 1])
+                                     : 0.f;
+                        }
+                        outv[i] = at;
+                        if (p.compact) {
+                            s_cidx[warp][pos] = (int32_t)t;
+                            s_cadv[warp][pos] = at;
+                            ++pos;
+                        }
+                    }
                 }
             }
         }
@@ -697,23 +823,26 @@ __device__ void coop_apply_phase(const AdvParams& p) {
     }
 }
 
-__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_all(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_all(const AdvParams p) {
+    __shared__ CoopSmem sm;
     cg::grid_group grid = cg::this_grid();
-    coop_stats_phases(p, grid);
+    coop_stats_phases(p, grid, sm);
     grid.sync();
     phase_mark(6);
-    coop_apply_phase(p);
+    coop_apply_phase(p, sm);
     grid.sync();
     phase_mark(7);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_stats(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_stats(const AdvParams p) {
+    __shared__ CoopSmem sm;
     cg::grid_group grid = cg::this_grid();
-    coop_stats_phases(p, grid);
+    coop_stats_phases(p, grid, sm);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS, 4) k_adv_coop_apply(const AdvParams p) {
-    coop_apply_phase(p);
+__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_apply(const AdvParams p) {
+    __shared__ CoopSmem sm;
+    coop_apply_phase(p, sm);
 }
 
 static int coop_grid(const void* kern, size_t smem, int64_t want) {
