@@ -2,49 +2,56 @@
 // sec 3.2 Eq.1) as ONE cooperative persistent kernel with grid-wide barriers
 // between its phases (two launches around the NCCL all-reduce when a communicator is given).
 //
-//   phase 0  zero the integer scratch (n_g, K_j, fill counters)
-//   phase A  token-parallel (4096-token chunks, 16 B mask loads): n_g via integer atomics,
-//            per-chunk masked counts; trajectory-parallel: K_j, offsets validation
-//   phase B1 block 0: exclusive scans of chunk counts (-> compaction bases) and K_j
-//   phase B2 trajectory-parallel: group member lists (atomic slots)
-//   phase B3 group-parallel: sort members (-> deterministic order), exact-equal rule,
-//            population std, A_hat_g (fp64); per-group (N, S, Q) = (sum n, sum n A, sum n A^2)
-//   phase B4 block 0: per-task (N_i, S_i, Q_i) as a fixed-order sum over groups
-//   [C1 NCCL all-reduce of the 3*n_tasks doubles -- second launch starts here]
-//   phase C  token-parallel: mu_i = S_i/N_i, sigma_i = sqrt(max(Q_i/N_i - mu_i^2, 0)),
-//            adv_tok[t] = mask ? (A_hat_g - mu)/max(sigma, eps) : 0, stable compaction
-//            idx[] / adv_c[] for part 2; block 0 writes task_stats and N.
-// Every reduction has a fixed order, so results are bitwise run-to-run deterministic.
+// Token streaming (phases A and C).  Each block owns a contiguous range of 512-token warp
+// chunks; warp w takes chunks w, w+8, ... of it.  The mask bytes reach shared memory through a
+// per-warp ring of RING slots filled by 1-D bulk copies (cp.async.bulk, one 512 B copy per
+// chunk, completion on an mbarrier), so every warp keeps RING-1 chunks in flight without
+// spending registers.  Trajectory offsets are staged per block in windows of 64 chunks.
+//   phase A  per-trajectory masked counts n_g: each lane counts its 16 tokens, a segmented
+//            warp scan sums the lanes of one trajectory, and one lane per trajectory adds to a
+//            shared counter (no same-address atomics inside a warp); per-chunk counts.
+//   phase C  adv_tok[t] = mask ? A~_g(t) : 0 with the staged A~ of the window; the 16 values of
+//            each lane go through a swizzled shared-memory transpose so that the stores are
+//            512 B contiguous per warp instruction; optional stable compaction idx[] / adv_c[].
+//
+// Two drivers:
+//   small  (n_traj <= 2048, n_groups <= 1024; every BASELINE config): all offsets staged per
+//          block; A -> grid barrier -> block 0 does the group/task statistics in shared memory
+//          -> grid barrier -> C.  Per-block trajectory counts are written to disjoint slots
+//          (index g + block) and summed in block order: no zeroing pass, exact integers.
+//   large  phase 0 (zero, chunk -> first-trajectory table) | A | B1 K_j scans | B2 member lists
+//          | B3 group advantages (members of groups of <= 16 sorted in registers) | B4 task
+//          moments | C.
+// Every floating-point reduction has a fixed order: results are bitwise run-to-run
+// deterministic.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <climits>
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace agentrl {
 
 constexpr int COOP_THREADS = 256;
-#ifndef ADV_MIN_BLOCKS
-#define ADV_MIN_BLOCKS 3  // resident blocks per SM the register budget is cut for
-#endif
+constexpr int NWARPS = COOP_THREADS / 32;
 constexpr int GMAX_BLOCKS = 2048;  // cap on the cooperative grid (per-block scratch arrays)
 constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 tokens)
-constexpr int WOFF_CAP = 64;       // trajectory offsets staged per warp chunk
-constexpr int NWARPS = COOP_THREADS / 32;
+#ifndef ADV_RING
+#define ADV_RING 8
+#endif
+constexpr int RING = ADV_RING;          // bulk-copy slots per warp
+constexpr int WIN_CHUNKS = 8 * NWARPS;  // warp chunks per offset-staging window (large path)
+constexpr int WIN_TRAJ = 2048;          // trajectories a block stages at once (more: windows,
+                                        // then global lookups)
+constexpr int KC_CAP = 2048;            // chunks per staged window (chunk -> trajectory table)
+constexpr int SMALL_TRAJ = 2048;        // small driver: all offsets staged in every block
+constexpr int SMALL_GROUPS = 512;
 constexpr int TASK_BATCH = 16;  // tasks reduced per barrier in the per-block partials
-constexpr int BT_CAP = 2048;    // trajectories a block stages in smem for its token range
-
-// static shared memory of the cooperative kernels (one arena for all phases)
-struct CoopSmem {
-    int32_t s_w[8];
-    int32_t s_pre[GMAX_BLOCKS + 1];
-    // the offsets of the trajectories overlapping this block's tokens (or, on the fallback path
-    // for blocks spanning more than BT_CAP trajectories, per-warp offset staging)
-    int64_t s_boff[BT_CAP + 1];
-    int32_t s_aux[BT_CAP];  // phase A: masked count per staged trajectory; C: its A~ (f32 bits)
-};
+constexpr int REG_K = 16;       // groups up to this size are handled in registers (phase B3)
 
 // phase timestamps of the last cooperative launch (block 0, after each grid barrier), read by
 // agentrl_debug_adv_phase_ns(); 8 x %globaltimer ns
@@ -55,6 +62,63 @@ __device__ __forceinline__ void phase_mark(int i) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_adv_phase_ns[i] = t;
     }
+}
+
+// dynamic shared memory layout (byte offsets), identical on host and device
+struct Lay {
+    uint32_t ring, bars, ostage, soff, srel, saux, skc, stask, cidx, cadv;
+    uint32_t sng, sgid, stid, srew, smem, sah, gcnt, gstart, gfill, gtask, gnsq;  // small: block 0
+    uint32_t total;
+};
+__host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
+    o = (o + 127u) & ~127u;
+    const uint32_t r = o;
+    o += bytes;
+    return r;
+}
+__host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, int n_traj,
+                                        int n_groups) {
+    Lay L;
+    uint32_t o = 0;
+    L.bars = lay_take(o, NWARPS * RING * 8);
+    const uint32_t stream_begin = (o + 127u) & ~127u;
+    L.ring = lay_take(o, NWARPS * RING * WCHUNK);
+    L.ostage = lay_take(o, NWARPS * WCHUNK * 4);
+    L.cidx = lay_take(o, compact ? NWARPS * WCHUNK * 4 : 0);
+    L.cadv = lay_take(o, compact ? NWARPS * WCHUNK * 4 : 0);
+    const uint32_t stream_end = o;
+    const int nst = small ? n_traj : WIN_TRAJ;
+    L.soff = lay_take(o, small ? 8u * (uint32_t)(n_traj + 1) : 0u);  // all offsets (small)
+    L.srel = lay_take(o, 4u * (uint32_t)(nst + 1));
+    L.saux = lay_take(o, 4u * (uint32_t)(nst + 1));
+    L.skc = lay_take(o, 4u * KC_CAP);
+    L.stask = lay_take(o, 16u * (uint32_t)(n_tasks > 0 ? n_tasks : 1));
+    const uint32_t fixed_end = o;
+    // the small driver's statistics block (block 0) never streams tokens: its group arrays
+    // alias its streaming buffers (ring, transpose and compaction staging)
+    uint32_t b = stream_begin;
+    const uint32_t nt = small ? (uint32_t)n_traj : 0u, ng = small ? (uint32_t)n_groups + 1 : 0u;
+    L.sng = lay_take(b, 4u * nt);
+    L.sgid = lay_take(b, 4u * nt);
+    L.stid = lay_take(b, 4u * nt);
+    L.srew = lay_take(b, 4u * nt);
+    L.smem = lay_take(b, 4u * nt);
+    L.sah = lay_take(b, 8u * nt);
+    L.gcnt = lay_take(b, 4u * ng);
+    L.gstart = lay_take(b, 4u * ng);
+    L.gfill = lay_take(b, 4u * ng);
+    L.gtask = lay_take(b, 4u * ng);
+    L.gnsq = lay_take(b, 24u * ng);
+    if (b <= stream_end) {
+        L.total = fixed_end;
+    } else {  // does not fit the streaming buffers: place after the fixed arrays
+        const uint32_t shift = ((fixed_end + 127u) & ~127u) - stream_begin;
+        uint32_t* f[] = {&L.sng, &L.sgid, &L.stid, &L.srew, &L.smem, &L.sah,
+                         &L.gcnt, &L.gstart, &L.gfill, &L.gtask, &L.gnsq};
+        for (uint32_t* x : f) *x += shift;
+        L.total = b + shift;
+    }
+    return L;
 }
 
 struct AdvParams {
@@ -70,8 +134,10 @@ struct AdvParams {
     int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
     int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
+    int32_t* blk_cnt;              // small driver: per-block trajectory counts at [g + block]
     double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
+    float* atilde;  // small driver without comm: A~_g published by the statistics block
     int64_t* meta;
     int32_t* d_status;
     float* adv_tok;
@@ -80,8 +146,10 @@ struct AdvParams {
     double* task_stats_out;
     int64_t* n_mask_global_out;
     int32_t compact;  // write idx[] / adv_c[] (needed by the fused step only)
+    Lay lay;
 };
 
+// ------------------------------------------------------------------ small helpers
 __device__ __forceinline__ int32_t coop_find_traj(const int64_t* __restrict__ off,
                                                   int32_t n_traj, int64_t t) {
     int32_t lo = 0, hi = n_traj;
@@ -91,19 +159,6 @@ __device__ __forceinline__ int32_t coop_find_traj(const int64_t* __restrict__ of
         else hi = mid;
     }
     return lo < n_traj ? lo : n_traj - 1;
-}
-
-// trajectories [bf, bf + n) overlap this block's warp chunks [c_lo, c_hi) (clamped; 0 if none)
-__device__ __forceinline__ int32_t block_traj_range(const AdvParams& p, int64_t c_lo, int64_t c_hi,
-                                                    int32_t& bf) {
-    bf = 0;
-    if (p.n_traj <= 0 || c_lo >= c_hi) return 0;
-    int32_t f = p.chunk_first[c_lo];
-    int32_t l = c_hi < p.n_chunks ? p.chunk_first[c_hi] : p.n_traj - 1;
-    f = min(max(f, 0), p.n_traj - 1);
-    l = min(max(l, f), p.n_traj - 1);
-    bf = f;
-    return l - f + 1;
 }
 // k in [lo, hi) with s[k] <= t < s[k+1] (clamped to lo / hi - 1)
 __device__ __forceinline__ int32_t smem_find_in(const int64_t* s, int32_t lo, int32_t hi, int64_t t) {
@@ -119,73 +174,11 @@ __device__ __forceinline__ int32_t mbit(const uint4& v, int i) {
     const uint32_t w = i < 4 ? v.x : (i < 8 ? v.y : (i < 12 ? v.z : v.w));
     return ((w >> (8 * (i & 3))) & 0xffu) != 0u;
 }
-
-__device__ __forceinline__ void coop_mask16(const uint8_t* __restrict__ mask, int64_t T,
-                                            int64_t t0, bool any_traj, uint8_t (&m)[16]) {
-    if (any_traj && t0 + 16 <= T && (reinterpret_cast<uintptr_t>(mask + t0) & 15) == 0) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + t0));
-        const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+__device__ __forceinline__ int32_t mcount(const uint4& v) {
+    int32_t n = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) m[i] = b[i];
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) m[i] = (any_traj && t0 + i < T) ? mask[t0 + i] : 0;
-    }
-}
-
-// Token -> trajectory lookup for one 4096-token chunk: the block stages off[first .. last+1]
-// of the trajectories that overlap the chunk into shared memory (one coalesced load) and every
-// thread binary-searches there, instead of ~log2(n_traj) dependent global loads per phase.
-constexpr int SOFF_CAP = 1024;
-struct ChunkTraj {
-    int32_t first, cnt;  // cnt = number of staged offsets (trajectories + 1); 0 = not staged
-};
-__device__ __forceinline__ ChunkTraj stage_chunk_offsets(const int64_t* __restrict__ off,
-                                                         const int32_t* __restrict__ chunk_first,
-                                                         int32_t n_traj, int64_t c,
-                                                         int64_t n_chunks, int64_t* s_off) {
-    ChunkTraj r{0, 0};
-    int32_t f = chunk_first[c];
-    int32_t l = (c + 1 < n_chunks) ? chunk_first[c + 1] : n_traj - 1;
-    f = min(max(f, 0), n_traj - 1);
-    l = min(max(l, f), n_traj - 1);
-    const int32_t cnt = l - f + 2;
-    r.first = f;
-    if (cnt <= SOFF_CAP) {
-        for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) s_off[i] = off[f + i];
-        r.cnt = cnt;
-    }
-    __syncthreads();
-    return r;
-}
-// local index k with s_off[k] <= t < s_off[k+1] (clamped)
-__device__ __forceinline__ int32_t smem_find(const int64_t* s_off, int32_t cnt, int64_t t) {
-    int32_t lo = 0, hi = cnt - 1;
-    while (hi - lo > 1) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (s_off[mid] <= t) lo = mid;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// warp-level staging of the offsets of the trajectories overlapping warp chunk c; returns the
-// number staged (0: too many, use the global binary search)
-__device__ __forceinline__ int32_t warp_stage(const int64_t* __restrict__ off,
-                                              const int32_t* __restrict__ wfirst, int32_t n_traj,
-                                              int64_t c, int64_t n_wchunks, int64_t* s_offw,
-                                              int32_t& first) {
-    const int lane = threadIdx.x & 31;
-    int32_t f = wfirst[c];
-    int32_t l = (c + 1 < n_wchunks) ? wfirst[c + 1] : n_traj - 1;
-    f = min(max(f, 0), n_traj - 1);
-    l = min(max(l, f), n_traj - 1);
-    const int32_t cnt = l - f + 2;
-    first = f;
-    if (cnt > WOFF_CAP) return 0;
-    for (int32_t i = lane; i < cnt; i += 32) s_offw[i] = off[f + i];
-    __syncwarp();
-    return cnt;
+    for (int i = 0; i < 16; ++i) n += mbit(v, i);
+    return n;
 }
 __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
     const int lane = threadIdx.x & 31;
@@ -196,48 +189,15 @@ __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
     }
     return v;
 }
-
-// ---- software-pipelined chunk inputs: the mask bytes and trajectory range of the NEXT chunk
-// are loaded while the current chunk is processed (breaks the per-warp dependent-load chain)
-struct ChunkIn {
-    uint4 mk;
-    int32_t f, l, base;
-};
-__device__ __forceinline__ ChunkIn chunk_fetch(const AdvParams& p, int64_t c, bool any_traj,
-                                               bool want_base) {
-    ChunkIn r;
-    const int lane = threadIdx.x & 31;
+// the 16 mask bytes of lane `lane` of chunk c, zero past T (direct loads; tail / misaligned)
+__device__ __forceinline__ uint4 mask_direct(const AdvParams& p, int64_t c, int lane) {
     const int64_t t0 = c * WCHUNK + lane * 16;
-    if (any_traj && t0 + 16 <= p.T && (reinterpret_cast<uintptr_t>(p.mask + t0) & 15) == 0) {
-        r.mk = __ldg(reinterpret_cast<const uint4*>(p.mask + t0));
-    } else {
-        uint32_t w[4] = {0u, 0u, 0u, 0u};
-        for (int i = 0; i < 16; ++i)
-            if (any_traj && t0 + i < p.T) w[i >> 2] |= (uint32_t)p.mask[t0 + i] << (8 * (i & 3));
-        r.mk = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-    r.f = any_traj ? p.chunk_first[c] : 0;
-    r.l = (any_traj && c + 1 < p.n_chunks) ? p.chunk_first[c + 1] : p.n_traj - 1;
-    r.base = want_base ? p.chunk_base[c] : 0;
-    return r;
-}
-__device__ __forceinline__ void unpack16(const uint4& v, uint8_t (&m)[16]) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 16; ++i) m[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
-}
-__device__ __forceinline__ int32_t warp_stage_fl(const int64_t* __restrict__ off, int32_t f,
-                                                 int32_t l, int32_t n_traj, int64_t* s_offw,
-                                                 int32_t& first) {
-    const int lane = threadIdx.x & 31;
-    f = min(max(f, 0), n_traj - 1);
-    l = min(max(l, f), n_traj - 1);
-    const int32_t cnt = l - f + 2;
-    first = f;
-    if (cnt > WOFF_CAP) return 0;
-    for (int32_t i = lane; i < cnt; i += 32) s_offw[i] = off[f + i];
-    __syncwarp();
-    return cnt;
+    if (t0 + 16 <= p.T && (reinterpret_cast<uintptr_t>(p.mask + t0) & 15) == 0)
+        return __ldg(reinterpret_cast<const uint4*>(p.mask + t0));
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int i = 0; i < 16; ++i)
+        if (t0 + i < p.T) w[i >> 2] |= (uint32_t)p.mask[t0 + i] << (8 * (i & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // exclusive scan of one int per thread over a 256-thread block (returns prefix; total out)
@@ -252,73 +212,37 @@ __device__ __forceinline__ int32_t coop_block_exscan(int32_t v, int32_t* s_w, in
     if (lane == 31) s_w[wid] = x;
     __syncthreads();
     if (wid == 0) {
-        int32_t w = lane < 8 ? s_w[lane] : 0;
+        int32_t w = lane < NWARPS ? s_w[lane] : 0;
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
+        for (int o = 1; o < NWARPS; o <<= 1) {
             const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= o) w += y;
         }
-        if (lane < 8) s_w[lane] = w;
+        if (lane < NWARPS) s_w[lane] = w;
     }
     __syncthreads();
     const int32_t base = wid > 0 ? s_w[wid - 1] : 0;
-    total = s_w[7];
+    total = s_w[NWARPS - 1];
     __syncthreads();
     return base + x - v;
 }
-
-// in-place exclusive scan of a[0..n) by one block of 256 threads (contiguous per-thread
-// segments, then a block scan of segment sums); returns the total
-__device__ int64_t coop_block_scan_array(int32_t* a, int64_t n, int64_t* s_seg) {
+// in-place exclusive scan of a[0..n) by the block (contiguous per-thread segments); total out
+__device__ int32_t coop_block_scan_array(int32_t* a, int64_t n, int32_t* s_w) {
     const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
     const int64_t lo = min(n, (int64_t)threadIdx.x * per), hi = min(n, lo + per);
-    int64_t s = 0;
+    int32_t s = 0;
     for (int64_t i = lo; i < hi; ++i) s += a[i];
-    // block scan of 64-bit segment sums
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int64_t x = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_seg[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        int64_t w = lane < 8 ? s_seg[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        if (lane < 8) s_seg[lane] = w;
-    }
-    __syncthreads();
-    int64_t run = (wid > 0 ? s_seg[wid - 1] : 0) + x - s;
-    const int64_t total = s_seg[7];
+    int32_t total;
+    int32_t run = coop_block_exscan(s, s_w, total);
     for (int64_t i = lo; i < hi; ++i) {
         const int32_t v = a[i];
-        a[i] = (int32_t)run;
+        a[i] = run;
         run += v;
     }
     __syncthreads();
     return total;
 }
 
-__device__ __forceinline__ double coop_block_sum(double v, double* s_red) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (lane == 0) s_red[wid] = v;
-    __syncthreads();
-    double r = 0.0;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < COOP_THREADS / 32; ++w) r += s_red[w];
-    __syncthreads();
-    return r;  // thread 0
-}
-
-// ------------------------------------------------------------------ helpers
 // balanced contiguous partition of [0, n) over G blocks
 __device__ __forceinline__ int64_t part_lo(int64_t n, int64_t b, int64_t G) { return n * b / G; }
 // block owning item j under part_lo
@@ -328,7 +252,6 @@ __device__ __forceinline__ int64_t part_owner(int64_t n, int64_t j, int64_t G) {
 // exclusive prefix over blocks of a per-block int array, computed by every block into smem
 __device__ void block_prefix_smem(const int32_t* __restrict__ blk, int64_t G, int32_t* s_pre,
                                   int32_t* s_w) {
-    // G <= GMAX_BLOCKS; each thread scans a contiguous segment
     const int64_t per = (G + COOP_THREADS - 1) / COOP_THREADS;
     const int64_t lo = min(G, (int64_t)threadIdx.x * per), hi = min(G, lo + per);
     int32_t sum = 0;
@@ -343,12 +266,782 @@ __device__ void block_prefix_smem(const int32_t* __restrict__ blk, int64_t G, in
     __syncthreads();
 }
 
-// ------------------------------------------------------------------ phases 0 .. B4
-__device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_group& grid, CoopSmem& sm) {
-    static_assert(NWARPS * WOFF_CAP <= BT_CAP + 1, "fallback staging fits the arena");
-    int32_t* s_w = sm.s_w;
-    int32_t* s_pre = sm.s_pre;
-    int64_t* s_off = sm.s_boff;  // fallback path: per-warp staging
+// ------------------------------------------------------------------ per-warp bulk-copy ring
+struct WarpRing {
+    uint8_t* buf;   // RING x WCHUNK bytes
+    uint64_t* bar;  // RING mbarriers
+    uint32_t par;   // parity of each slot's next completion
+    bool on;        // mask 16 B aligned: full chunks arrive by bulk copy
+};
+__device__ __forceinline__ WarpRing ring_setup(const AdvParams& p, uint8_t* smem) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpRing r;
+    r.buf = smem + p.lay.ring + warp * RING * WCHUNK;
+    r.bar = reinterpret_cast<uint64_t*>(smem + p.lay.bars) + warp * RING;
+    r.par = 0u;
+    r.on = (reinterpret_cast<uintptr_t>(p.mask) & 15) == 0;
+    if (lane == 0) {
+        for (int s = 0; s < RING; ++s) mbar_init(&r.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    return r;
+}
+__device__ __forceinline__ bool chunk_full(const AdvParams& p, int64_t c) {
+    return (c + 1) * WCHUNK <= p.T;
+}
+// lane 0: start the copy of chunk c into `slot`
+__device__ __forceinline__ void ring_issue(const AdvParams& p, WarpRing& r, int slot, int64_t c) {
+    mbar_arrive_expect_tx(&r.bar[slot], WCHUNK);
+    bulk_g2s(r.buf + slot * WCHUNK, p.mask + c * WCHUNK, WCHUNK, &r.bar[slot]);
+}
+
+// Offset staging of one window of chunks [w0, w1): trajectories [f, f + nbt) cover its
+// tokens; s_rel[k] = off[f + k] - base (clamped to [0, INT_MAX]), k = 0..nbt, with base the
+// window's first token, so the token loops compare 32-bit positions.  staged == false: the
+// window covers more than WIN_TRAJ trajectories and uses global lookups.
+struct Window {
+    int32_t f, nbt;
+    int64_t base;
+    const int32_t* s_rel;
+    bool staged;
+};
+
+// warp-cooperative search: largest k in [0, n) with s[k] <= t (s[0] <= t); 32 probes per
+// round narrow the range 32x (3 rounds for 2048 entries instead of 11 dependent steps)
+__device__ __forceinline__ int32_t warp_find(const int32_t* s, int32_t n, int32_t t) {
+    const int lane = threadIdx.x & 31;
+    int32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int32_t step = (hi - lo + 31) >> 5;
+        const int32_t pos = lo + lane * step;
+        const uint32_t m = __ballot_sync(0xffffffffu, pos < hi && s[pos] <= t);
+        lo += (31 - __clz(m | 1u)) * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+// the lane's trajectory (window-local) from the chunk's first one: short forward walk
+__device__ __forceinline__ int32_t lane_traj(const Window& w, int32_t kc, int32_t tr0) {
+    int32_t k = kc;
+    while (k + 1 < w.nbt && w.s_rel[k + 1] <= tr0) ++k;
+    return k;
+}
+
+// ------------------------------------------------------------------ phase A: counting
+// lane: 16 tokens from tr0 (window-relative); counts of trajectories after the lane's first
+// one go straight to the shared counters (rare: a boundary inside the lane's 16 tokens); the
+// first trajectory's count is summed over lanes by a segmented warp scan and added once per
+// trajectory.
+__device__ __forceinline__ int32_t count_chunk_staged(const uint4& mk, int32_t tr0, int32_t kc,
+                                                      const Window& w, int32_t* s_cnt) {
+    const int lane = threadIdx.x & 31;
+    int32_t k = lane_traj(w, kc, tr0);
+    int32_t end = w.s_rel[k + 1];
+    const int32_t key = k;
+    int32_t head = 0, cnt = 0, mine = 0;
+    bool crossed = false;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int32_t t = tr0 + i;
+        while (t >= end && k + 1 < w.nbt) {
+            if (!crossed) head = cnt;
+            else if (cnt) atomicAdd(&s_cnt[k], cnt);
+            crossed = true;
+            cnt = 0;
+            ++k;
+            end = w.s_rel[k + 1];
+        }
+        const int32_t bit = mbit(mk, i);
+        cnt += bit;
+        mine += bit;
+    }
+    if (!crossed) head = cnt;
+    else if (cnt) atomicAdd(&s_cnt[k], cnt);
+    // keys are nondecreasing over lanes: segmented inclusive sum, one add per trajectory
+    int32_t v = head;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        const int32_t ky = __shfl_up_sync(0xffffffffu, key, o);
+        if (lane >= o && ky == key) v += y;
+    }
+    const int32_t kn = __shfl_down_sync(0xffffffffu, key, 1);
+    if ((lane == 31 || kn != key) && v) atomicAdd(&s_cnt[key], v);
+    return mine;
+}
+// unstaged window: global binary search per lane, global integer atomics on n_g
+__device__ __forceinline__ int32_t count_chunk_global(const AdvParams& p, const uint4& mk,
+                                                      int64_t t0) {
+    int32_t mine = 0;
+    if (t0 < p.T && p.n_traj > 0) {
+        int32_t g = coop_find_traj(p.off, p.n_traj, t0);
+        int64_t end = p.off[g + 1];
+        int32_t cnt = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int64_t t = t0 + i;
+            while (t >= end && g + 1 < p.n_traj) {
+                if (cnt) atomicAdd(&p.n_g[g], cnt);
+                cnt = 0;
+                ++g;
+                end = p.off[g + 1];
+            }
+            const int32_t bit = mbit(mk, i);
+            cnt += bit;
+            mine += bit;
+        }
+        if (cnt) atomicAdd(&p.n_g[g], cnt);
+    }
+    return mine;
+}
+
+// ------------------------------------------------------------------ phase C: apply
+// writes the 16 values of each lane through a swizzled transpose: lane L stores its q-th
+// float4 at word L*16 + 4*(q ^ ((L>>1)&3)) (conflict-free), then reads back the float4 of tokens
+// i*128 + 4L (conflict-free) and stores it -- 512 contiguous bytes per warp instruction
+__device__ __forceinline__ void store_transposed(const AdvParams& p, float* os, int64_t c,
+                                                 const float (&v)[16], bool vec_ok) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(os + lane * 16 + 4 * (q ^ ((lane >> 1) & 3))) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int tok = i * 128 + lane * 4;
+        const int lp = tok >> 4, q = lane & 3;
+        const float4 x = *reinterpret_cast<const float4*>(os + lp * 16 + 4 * (q ^ ((lp >> 1) & 3)));
+        const int64_t t = c * WCHUNK + tok;
+        if (vec_ok && t + 4 <= p.T) {
+            *reinterpret_cast<float4*>(p.adv_tok + t) = x;
+        } else {
+            if (t < p.T) p.adv_tok[t] = x.x;
+            if (t + 1 < p.T) p.adv_tok[t + 1] = x.y;
+            if (t + 2 < p.T) p.adv_tok[t + 2] = x.z;
+            if (t + 3 < p.T) p.adv_tok[t + 3] = x.w;
+        }
+    }
+    __syncwarp();
+}
+
+// Eq.1 for trajectory g with the block's per-task (mu, max(sigma, eps))
+__device__ __forceinline__ float adv_tilde(const AdvParams& p, const double2* s_task, int32_t g) {
+    const int32_t ti = p.task_id[g];
+    return (ti >= 0 && ti < p.n_tasks)
+               ? (float)((p.adv_hat[g] - s_task[ti].x) / s_task[ti].y)
+               : 0.f;
+}
+
+// ------------------------------------------------------------------ the streaming loop
+// PH 0: counting (phase A); PH 1: apply (phase C).  small: one window = the block's range,
+// offsets from s_offall (all trajectories staged); else windows of WIN_CHUNKS chunks staged
+// from the chunk -> first-trajectory table.
+// ------------------------------------------------------------------ bit-parallel chunk code
+// The 16 mask bytes of a lane -> a per-byte 0xFF/0x00 mask (4 words) and a 16-bit token mask.
+struct LaneMask {
+    uint32_t byte[4];  // 0xFF in every byte whose mask byte is nonzero (reading R18)
+    uint32_t bits;     // bit i = token i of the lane is an assistant token
+};
+__device__ __forceinline__ LaneMask lane_mask(const uint4& mk) {
+    const uint32_t w[4] = {mk.x, mk.y, mk.z, mk.w};
+    LaneMask m;
+    m.bits = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        // high bit of each byte set iff the byte is nonzero
+        const uint32_t hb = ((((w[q] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w[q]) & 0x80808080u) >> 7;
+        m.byte[q] = hb * 0xFFu;
+        m.bits |= ((hb * 0x01020408u) >> 24) << (4 * q);
+    }
+    return m;
+}
+
+// phase A, staged window: per-trajectory masked counts of chunk c (window-relative start tc,
+// first trajectory kc).  With E the exclusive prefix of the lanes' popcounts, the count below
+// a boundary x is P(x) = E[x/16] + popc(bits[x/16] & low(x%16)); lane j handles the segment
+// that ends at the chunk's j-th trajectory start (and adds it once: no intra-warp conflicts).
+__device__ __forceinline__ int32_t count_chunk_bits(const LaneMask& m, int32_t tc, int32_t kc,
+                                                    const Window& w, int32_t* s_cnt) {
+    const int lane = threadIdx.x & 31;
+    const int32_t pc = __popc(m.bits);
+    const int32_t E = warp_incl_scan(pc) - pc;
+    const int32_t total = __shfl_sync(0xffffffffu, E + pc, 31);
+    int32_t prevP = 0;
+    for (int32_t jb = 0;; jb += 32) {
+        const int32_t kb = kc + 1 + jb + lane;  // trajectory starting at boundary jb + lane
+        const int32_t b = kb < w.nbt ? w.s_rel[kb] : INT_MAX;
+        const bool in = b < tc + WCHUNK;
+        const int32_t nb = __popc(__ballot_sync(0xffffffffu, in));
+        const int32_t x = in ? b - tc : 0;
+        const int32_t o = x >> 4;
+        const int32_t Eo = __shfl_sync(0xffffffffu, E, o);
+        const uint32_t bo = __shfl_sync(0xffffffffu, m.bits, o);
+        const int32_t P = in ? Eo + __popc(bo & ((1u << (x & 15)) - 1u)) : total;
+        int32_t Pm = __shfl_up_sync(0xffffffffu, P, 1);
+        if (lane == 0) Pm = prevP;
+        const int32_t cnt = P - Pm;
+        if (lane <= nb && cnt > 0) atomicAdd(&s_cnt[kc + jb + lane], cnt);
+        if (nb < 32) break;
+        prevP = __shfl_sync(0xffffffffu, P, 31);
+    }
+    return pc;
+}
+
+// phase C, staged window: the lane's 16 advantages (as bits, 0 on unmasked tokens).  Start
+// from the chunk's first trajectory, then every trajectory start b inside the chunk overwrites
+// the tokens at or after b (uniform loop over the chunk's few boundaries).
+__device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, int32_t kc,
+                                                 const Window& w, const int32_t* s_val,
+                                                 uint32_t (&out)[16]) {
+    const int lane = threadIdx.x & 31;
+    const int32_t tr0 = tc + lane * 16;
+    const uint32_t v0 = (uint32_t)s_val[kc];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = v0;
+    for (int32_t jb = 0;; jb += 32) {
+        const int32_t kb = kc + 1 + jb + lane;
+        const int32_t b = kb < w.nbt ? w.s_rel[kb] : INT_MAX;
+        const uint32_t av = kb < w.nbt ? (uint32_t)s_val[kb] : 0u;
+        const int32_t nb = __popc(__ballot_sync(0xffffffffu, b < tc + WCHUNK));
+        for (int32_t j = 0; j < nb; ++j) {
+            const int32_t rel = __shfl_sync(0xffffffffu, b, j) - tr0;
+            const uint32_t v = __shfl_sync(0xffffffffu, av, j);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) out[i] = i >= rel ? v : out[i];
+        }
+        if (nb < 32) break;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] &= __byte_perm(m.byte[i >> 2], 0u, (i & 3) * 0x1111u);
+}
+
+// resident (PH 1): the warp's chunks are still in its ring slots from phase A (same kernel,
+// at most RING chunks per warp) and are not copied again.  from_atilde (PH 1): stage the
+// published A~_g instead of computing Eq.1 per trajectory.
+template <int PH>
+__device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int64_t c_lo,
+                             int64_t c_hi, bool small, const int64_t* s_offall, int32_t blk_base,
+                             int32_t& warp_total, bool resident = false, bool from_atilde = false) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t B = blockIdx.x;
+    int32_t* s_rel = reinterpret_cast<int32_t*>(smem + p.lay.srel);
+    int32_t* s_aux = reinterpret_cast<int32_t*>(smem + p.lay.saux);
+    const double2* s_task = reinterpret_cast<const double2*>(smem + p.lay.stask);
+    float* os = reinterpret_cast<float*>(smem + p.lay.ostage) + warp * WCHUNK;
+    int32_t* s_cidx = reinterpret_cast<int32_t*>(smem + p.lay.cidx) + warp * WCHUNK;
+    float* s_cadv = reinterpret_cast<float*>(smem + p.lay.cadv) + warp * WCHUNK;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(p.adv_tok) & 15) == 0;
+    const bool any_traj = p.n_traj > 0;
+    const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
+    const bool res = resident && n_mine <= RING;  // warp-uniform
+    if (lane == 0 && r.on && !res) {
+        for (int s = 0; s < RING; ++s) {
+            const int64_t c = c_lo + warp + (int64_t)s * NWARPS;
+            if (c < c_hi && chunk_full(p, c)) ring_issue(p, r, s, c);
+        }
+    }
+    // staging plan: the block's whole range if its trajectories fit, else 64-chunk windows
+    int64_t wlen = max(c_hi - c_lo, (int64_t)1);
+    if (wlen > KC_CAP) wlen = WIN_CHUNKS;
+    if (!small && any_traj && c_lo < c_hi) {
+        const int32_t f = p.chunk_first[c_lo];
+        const int32_t l = c_hi < p.n_chunks ? p.chunk_first[c_hi] : p.n_traj - 1;
+        if (l - f + 1 > WIN_TRAJ) wlen = WIN_CHUNKS;
+    }
+    int32_t* s_kc = reinterpret_cast<int32_t*>(smem + p.lay.skc);
+    int64_t kseq = 0;
+    for (int64_t w0 = c_lo; w0 < c_hi; w0 += wlen) {
+        const int64_t w1 = min(c_hi, w0 + wlen);
+        // ---- stage the window's trajectories (block-wide)
+        Window w{0, 0, w0 * WCHUNK, s_rel, false};
+        if (any_traj) {
+            int32_t f, l;
+            if (small) {
+                f = smem_find_in(s_offall, 0, p.n_traj, w0 * WCHUNK);
+                l = smem_find_in(s_offall, 0, p.n_traj, min(w1 * WCHUNK, p.T) - 1);
+            } else {
+                f = p.chunk_first[w0];
+                l = w1 < p.n_chunks ? p.chunk_first[w1] : p.n_traj - 1;
+            }
+            f = min(max(f, 0), p.n_traj - 1);
+            l = min(max(l, f), p.n_traj - 1);
+            w.f = f;
+            w.nbt = l - f + 1;
+            w.staged = small || w.nbt <= WIN_TRAJ;
+            if (w.staged) {
+                for (int32_t k = threadIdx.x; k <= w.nbt; k += COOP_THREADS) {
+                    const int64_t o = (small ? s_offall[f + k] : p.off[f + k]) - w.base;
+                    s_rel[k] = (int32_t)min(max(o, (int64_t)0), (int64_t)INT_MAX);
+                    if (k < w.nbt)
+                        s_aux[k] = PH == 0 ? 0
+                                           : (from_atilde ? __float_as_int(p.atilde[f + k])
+                                                          : __float_as_int(adv_tilde(p, s_task, f + k)));
+                }
+            }
+        }
+        __syncthreads();
+        if (w.staged) {  // chunk -> first trajectory of the window (no searches)
+            const int32_t nwc = (int32_t)(w1 - w0);
+            for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
+                const int32_t lo = (w.s_rel[k] + WCHUNK - 1) / WCHUNK;
+                const int32_t hi = min((int32_t)(((int64_t)w.s_rel[k + 1] + WCHUNK - 1) / WCHUNK), nwc);
+                for (int32_t q = lo; q < hi; ++q) s_kc[q] = k;
+            }
+            __syncthreads();
+        }
+        // ---- this warp's chunks of the window
+        for (int64_t c = w0 + warp; c < w1; c += NWARPS, ++kseq) {
+            const int slot = (int)(kseq % RING);
+            uint4 mk;
+            if (r.on && chunk_full(p, c)) {
+                if (!res) {
+                    mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
+                    r.par ^= 1u << slot;
+                }
+                mk = *reinterpret_cast<const uint4*>(r.buf + slot * WCHUNK + lane * 16);
+            } else {
+                mk = mask_direct(p, c, lane);
+            }
+            const int64_t t0 = c * WCHUNK + lane * 16;
+            const int32_t tc = (int32_t)(c * WCHUNK - w.base);  // chunk start, window-relative
+            const int32_t kc = (any_traj && w.staged) ? s_kc[c - w0] : 0;
+            if (PH == 0) {
+                int32_t mine;
+                if (!any_traj) mine = 0;
+                else if (w.staged) mine = count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux);
+                else mine = count_chunk_global(p, mk, t0);
+                int32_t tot = mine;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                if (lane == 0) p.chunk[c] = tot;
+                warp_total += tot;
+            } else {
+                const LaneMask lm = lane_mask(mk);
+                const int32_t mine = any_traj ? __popc(lm.bits) : 0;
+                const int32_t incl = warp_incl_scan(mine);
+                const int32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
+                int32_t pos = incl - mine;
+                float outv[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) outv[i] = 0.f;
+                if (any_traj && w.staged) {
+                    uint32_t ob[16];
+                    apply_chunk_bits(lm, tc, kc, w, s_aux, ob);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) outv[i] = __uint_as_float(ob[i]);
+                    if (p.compact) {  // staged in smem, written coalesced below
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if ((lm.bits >> i) & 1u) {
+                                s_cidx[pos] = (int32_t)(t0 + i);
+                                s_cadv[pos] = outv[i];
+                                ++pos;
+                            }
+                    }
+                } else if (mine > 0 && t0 < p.T) {
+                    int32_t g = coop_find_traj(p.off, p.n_traj, t0);
+                    int64_t end = p.off[g + 1];
+                    float at = adv_tilde(p, s_task, g);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int64_t t = t0 + i;
+                        while (t >= end && g + 1 < p.n_traj) {
+                            ++g;
+                            end = p.off[g + 1];
+                            at = adv_tilde(p, s_task, g);
+                        }
+                        const bool on = mbit(mk, i);
+                        outv[i] = on ? at : 0.f;
+                        if (p.compact && on) {
+                            s_cidx[pos] = (int32_t)t;
+                            s_cadv[pos] = at;
+                            ++pos;
+                        }
+                    }
+                }
+                if (c * WCHUNK < p.T) store_transposed(p, os, c, outv, vec_ok);
+                if (p.compact) {
+                    __syncwarp();
+                    const int32_t wbase = blk_base + p.chunk_base[c];
+                    for (int32_t i = lane; i < wtotal; i += 32) {
+                        p.idx[wbase + i] = s_cidx[i];
+                        p.adv_c[wbase + i] = s_cadv[i];
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && r.on && !res) {
+                const int64_t c2 = c + (int64_t)RING * NWARPS;
+                if (c2 < c_hi && chunk_full(p, c2)) ring_issue(p, r, slot, c2);
+            }
+        }
+        __syncthreads();
+        // ---- window epilogue (counting): per-trajectory counts out
+        if (PH == 0 && w.staged) {
+            for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
+                if (small) p.blk_cnt[w.f + B + k] = s_aux[k];  // disjoint slot g + block
+                else if (s_aux[k]) atomicAdd(&p.n_g[w.f + k], s_aux[k]);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// per-task (mu, max(sigma, eps)) into smem from the (global) stats; block 0 publishes
+// task_stats, N, n_seq
+__device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w) {
+    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
+    const int64_t G = gridDim.x, B = blockIdx.x;
+    for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
+        const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
+        const double mu = N > 0.0 ? S / N : 0.0;
+        const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
+        s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
+        if (B == 0 && p.task_stats_out) {
+            p.task_stats_out[3 * i] = N;
+            p.task_stats_out[3 * i + 1] = mu;
+            p.task_stats_out[3 * i + 2] = sd;
+        }
+    }
+    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // also orders the s_task writes
+    if (B == 0 && threadIdx.x < 32) {
+        double nsum = 0.0;
+        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
+        if (threadIdx.x == 0) {
+            const int64_t n = (int64_t)nsum;
+            p.meta[0] = s_pre[G];  // local masked rows
+            p.meta[1] = n;         // global N
+            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global n_seq
+            if (p.n_mask_global_out) *p.n_mask_global_out = n;
+            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
+        }
+    }
+}
+
+// block-local exclusive scan of the block's chunk counts -> chunk_base; block total
+__device__ void chunk_bases(const AdvParams& p, int64_t c_lo, int64_t c_hi, int32_t* s_w) {
+    __syncthreads();  // chunk counts of all warps written
+    const int64_t n = c_hi - c_lo;
+    const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
+    const int64_t lo = c_lo + min(n, (int64_t)threadIdx.x * per);
+    const int64_t hi = min(c_hi, lo + per);
+    int32_t sum = 0;
+    for (int64_t c = lo; c < hi; ++c) sum += p.chunk[c];
+    int32_t total;
+    int32_t run = coop_block_exscan(sum, s_w, total);
+    for (int64_t c = lo; c < hi; ++c) {
+        const int32_t v = p.chunk[c];
+        p.chunk_base[c] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) p.blk_chunk[blockIdx.x] = total;
+}
+
+// ------------------------------------------------------------------ GRPO group advantage
+// (readings R1 population std, R2 exact-equal rule and eps floor, R14 K == 1).
+// mb: the K members sorted by index.  Writes adv_hat; returns (N, S, Q) of the group and
+// its task; nz counts members with masked tokens.
+template <typename GetR, typename GetT, typename GetN>
+__device__ __forceinline__ void group_adv(const AdvParams& p, int32_t K, const int32_t* mb,
+                                          GetR rew, GetT task, GetN ng, double& N, double& S,
+                                          double& Q, int32_t& task0, int32_t& st,
+                                          unsigned long long& nz) {
+    N = S = Q = 0.0;
+    task0 = -1;
+    if (K <= 0) return;
+    if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+    task0 = task(mb[0]);
+    double sum = 0.0, rmax = rew(mb[0]), rmin = rmax;
+    for (int a = 0; a < K; ++a) {
+        const double r = rew(mb[a]);
+        if (task(mb[a]) != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+        sum += r;
+        rmax = fmax(rmax, r);
+        rmin = fmin(rmin, r);
+    }
+    const bool flat = rmax == rmin;
+    const double mean = sum / (double)K;
+    double ss = 0.0;
+    if (!flat)
+        for (int a = 0; a < K; ++a) {
+            const double dlt = (double)rew(mb[a]) - mean;
+            ss += dlt * dlt;
+        }
+    const double sd = sqrt(ss / (double)K);
+    const double den = sd > p.eps_std ? sd : p.eps_std;
+    for (int a = 0; a < K; ++a) {
+        const int32_t g = mb[a];
+        const double ah = flat ? 0.0 : ((double)rew(g) - mean) / den;
+        p.adv_hat[g] = ah;
+        const int32_t nn = ng(g);
+        const double n = (double)nn;
+        N += n;
+        S += n * ah;
+        Q += n * ah * ah;
+        nz += nn > 0;
+    }
+}
+
+// ------------------------------------------------------------------ small driver
+// Block 0 is the statistics block: while blocks 1..G-1 count tokens (phase A) it loads the
+// trajectory table, builds the group member lists and computes every A^_g (none of which
+// depends on the counts); after the grid barrier it only adds the per-block counts and
+// reduces the moments.  Blocks 1..G-1 own contiguous chunk ranges.
+struct SmallArrays {
+    const int64_t* off;
+    int32_t *ng, *gid, *tid, *mem, *gcnt, *gstart, *gfill, *gtask;
+    float* rew;
+    double *ah, *gnsq;
+};
+__device__ __forceinline__ SmallArrays small_arrays(const AdvParams& p, uint8_t* smem) {
+    SmallArrays a;
+    a.off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    a.ng = reinterpret_cast<int32_t*>(smem + p.lay.sng);
+    a.gid = reinterpret_cast<int32_t*>(smem + p.lay.sgid);
+    a.tid = reinterpret_cast<int32_t*>(smem + p.lay.stid);
+    a.rew = reinterpret_cast<float*>(smem + p.lay.srew);
+    a.mem = reinterpret_cast<int32_t*>(smem + p.lay.smem);
+    a.ah = reinterpret_cast<double*>(smem + p.lay.sah);
+    a.gcnt = reinterpret_cast<int32_t*>(smem + p.lay.gcnt);
+    a.gstart = reinterpret_cast<int32_t*>(smem + p.lay.gstart);
+    a.gfill = reinterpret_cast<int32_t*>(smem + p.lay.gfill);
+    a.gtask = reinterpret_cast<int32_t*>(smem + p.lay.gtask);
+    a.gnsq = reinterpret_cast<double*>(smem + p.lay.gnsq);
+    return a;
+}
+
+__device__ void stage_all_offsets(const AdvParams& p, uint8_t* smem) {
+    int64_t* s_off = reinterpret_cast<int64_t*>(smem + p.lay.soff);
+    for (int32_t k = threadIdx.x; k <= p.n_traj; k += COOP_THREADS) s_off[k] = p.off[k];
+    __syncthreads();
+}
+
+// block 0 during phase A: validation, member lists, GRPO advantage (readings R1, R2,
+// R14) of every trajectory into smem and adv_hat
+__device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w) {
+    const SmallArrays a = small_arrays(p, smem);
+    int32_t st = 0;
+    if (threadIdx.x == 0) p.blk_chunk[0] = 0;  // the statistics block streams no tokens
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
+        a.gcnt[j] = 0;
+        a.gfill[j] = 0;
+    }
+    __syncthreads();
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+        if (a.off[g + 1] < a.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
+        const int32_t j = p.group_id[g], i = p.task_id[g];
+        a.rew[g] = p.rewards[g];
+        a.tid[g] = i;
+        a.ah[g] = 0.0;
+        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
+            st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+            a.gid[g] = -1;
+            p.adv_hat[g] = 0.0;
+        } else {
+            a.gid[g] = j;
+            atomicAdd(&a.gcnt[j], 1);
+        }
+    }
+    if (threadIdx.x == 0 && (a.off[0] != 0 || a.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) a.gstart[j] = a.gcnt[j];
+    __syncthreads();
+    coop_block_scan_array(a.gstart, p.n_groups, s_w);
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+        const int32_t j = a.gid[g];
+        if (j >= 0) a.mem[a.gstart[j] + atomicAdd(&a.gfill[j], 1)] = g;
+    }
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
+        const int32_t K = a.gcnt[j];
+        int32_t* mb = a.mem + a.gstart[j];
+        for (int q = 1; q < K; ++q) {  // members in index order (deterministic sums)
+            const int32_t x = mb[q];
+            int b = q - 1;
+            while (b >= 0 && mb[b] > x) {
+                mb[b + 1] = mb[b];
+                --b;
+            }
+            mb[b + 1] = x;
+        }
+        int32_t task0 = -1;
+        if (K > 0) {
+            if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+            task0 = a.tid[mb[0]];
+            double sum = 0.0, rmax = a.rew[mb[0]], rmin = rmax;
+            for (int q = 0; q < K; ++q) {
+                const double r = a.rew[mb[q]];
+                if (a.tid[mb[q]] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                sum += r;
+                rmax = fmax(rmax, r);
+                rmin = fmin(rmin, r);
+            }
+            const bool flat = rmax == rmin;
+            const double mean = sum / (double)K;
+            double ss = 0.0;
+            if (!flat)
+                for (int q = 0; q < K; ++q) {
+                    const double dlt = (double)a.rew[mb[q]] - mean;
+                    ss += dlt * dlt;
+                }
+            const double sd = sqrt(ss / (double)K);
+            const double den = sd > p.eps_std ? sd : p.eps_std;
+            for (int q = 0; q < K; ++q) {
+                const int32_t g = mb[q];
+                const double ah = flat ? 0.0 : ((double)a.rew[g] - mean) / den;
+                a.ah[g] = ah;
+                p.adv_hat[g] = ah;
+            }
+        }
+        a.gtask[j] = task0;
+    }
+    if (st) atomicOr(p.d_status, st);
+}
+
+// block 0 after phase A: n_g (per-block counts summed in block order: exact), per-group and
+// per-task (N, S, Q) in fixed orders; with publish (no communicator) also
+// mu_i, sigma_i, A~_g (Eq.1), task_stats, N and the local masked-row count
+__device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
+                                 bool publish) {
+    const SmallArrays a = small_arrays(p, smem);
+    const int64_t GS = G - 1;  // streaming blocks 1..G-1
+    int32_t rows = 0;          // local masked rows = sum of the streaming blocks' totals
+    for (int64_t b = 1 + threadIdx.x; b < G; b += COOP_THREADS) rows += p.blk_chunk[b];
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+        const int64_t s0 = a.off[g], e = a.off[g + 1];
+        int32_t n = 0;
+        if (e > s0 && s0 >= 0 && GS > 0) {
+            const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
+            const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
+            for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+        }
+        a.ng[g] = n;
+        p.n_g[g] = n;
+    }
+    __syncthreads();
+    unsigned long long nz = 0;
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
+        const int32_t K = a.gcnt[j];
+        const int32_t* mb = a.mem + a.gstart[j];
+        double N = 0.0, S = 0.0, Q = 0.0;
+        for (int q = 0; q < K; ++q) {
+            const int32_t g = mb[q];
+            const double n = (double)a.ng[g], ah = a.ah[g];
+            N += n;
+            S += n * ah;
+            Q += n * ah * ah;
+            nz += a.ng[g] > 0;
+        }
+        a.gnsq[3 * j] = N;
+        a.gnsq[3 * j + 1] = S;
+        a.gnsq[3 * j + 2] = Q;
+    }
+    int32_t nzt = 0, rows_t = 0;
+    (void)coop_block_exscan((int32_t)nz, s_w, nzt);  // also orders the gnsq writes
+    (void)coop_block_exscan(rows, s_w, rows_t);
+    __shared__ double s_st[64 * 3];  // per-task (N, S, Q) for the publish step (n_tasks <= 64)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
+        double N = 0.0, S = 0.0, Q = 0.0;
+        for (int32_t j = lane; j < p.n_groups; j += 32)
+            if (a.gtask[j] == i) {
+                N += a.gnsq[3 * j];
+                S += a.gnsq[3 * j + 1];
+                Q += a.gnsq[3 * j + 2];
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            N += __shfl_down_sync(0xffffffffu, N, o);
+            S += __shfl_down_sync(0xffffffffu, S, o);
+            Q += __shfl_down_sync(0xffffffffu, Q, o);
+        }
+        if (lane == 0) {
+            p.stats[3 * i] = N;
+            p.stats[3 * i + 1] = S;
+            p.stats[3 * i + 2] = Q;
+            if (i < 64) {
+                s_st[3 * i] = N;
+                s_st[3 * i + 1] = S;
+                s_st[3 * i + 2] = Q;
+            }
+        }
+    }
+    if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // n_seq (local)
+    if (!publish) return;
+    __syncthreads();
+    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
+    for (int32_t i = threadIdx.x; i < p.n_tasks; i += COOP_THREADS) {
+        const double N = s_st[3 * i], S = s_st[3 * i + 1], Q = s_st[3 * i + 2];
+        const double mu = N > 0.0 ? S / N : 0.0;
+        const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
+        s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
+        if (p.task_stats_out) {
+            p.task_stats_out[3 * i] = N;
+            p.task_stats_out[3 * i + 1] = mu;
+            p.task_stats_out[3 * i + 2] = sd;
+        }
+    }
+    if (threadIdx.x < 32) {
+        double nsum = 0.0;
+        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += s_st[3 * i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
+        if (threadIdx.x == 0) {
+            const int64_t n = (int64_t)nsum;
+            p.meta[0] = rows_t;  // local masked rows
+            p.meta[1] = n;       // global N
+            p.meta[2] = nzt;     // global n_seq
+            if (p.n_mask_global_out) *p.n_mask_global_out = n;
+            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
+        }
+    }
+    __syncthreads();
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+        const int32_t ti = a.tid[g];
+        p.atilde[g] = (ti >= 0 && ti < p.n_tasks)
+                          ? (float)((a.ah[g] - s_task[ti].x) / s_task[ti].y)
+                          : 0.f;
+    }
+}
+
+__device__ __forceinline__ void small_range(const AdvParams& p, int64_t& c_lo, int64_t& c_hi) {
+    const int64_t GS = gridDim.x - 1, B = (int64_t)blockIdx.x - 1;
+    c_lo = B < 0 ? 0 : part_lo(p.n_chunks, B, GS);
+    c_hi = B < 0 ? 0 : part_lo(p.n_chunks, B + 1, GS);
+}
+
+__device__ __forceinline__ void small_count(const AdvParams& p, uint8_t* smem, WarpRing& r,
+                                            int32_t* s_w) {
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    int32_t warp_total = 0;
+    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total);
+    chunk_bases(p, c_lo, c_hi, s_w);
+}
+
+// phase C of a streaming block.  fused (single kernel, no communicator): the mask is still in
+// the ring and A~ comes from the statistics block; else (second launch after the all-reduce)
+// everything is reloaded and Eq.1 evaluated here.
+__device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
+                                            int32_t* s_pre, int32_t* s_w, bool fused) {
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    if (fused) block_prefix_smem(p.blk_chunk, gridDim.x, s_pre, s_w);
+    else load_task_params(p, smem, s_pre, s_w);
+    int32_t dummy = 0;
+    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused, fused);
+}
+
+// ------------------------------------------------------------------ large driver
+__device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& r,
+                                   cg::grid_group& grid, int32_t* s_w, int32_t* s_pre) {
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t gtid = B * blockDim.x + threadIdx.x;
     const int64_t gstride = G * blockDim.x;
@@ -373,118 +1066,10 @@ __device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_g
     grid.sync();
     phase_mark(1);
 
-    // phase A: this block's contiguous warp chunks (512 tokens each, one warp per chunk):
-    // n_g, per-chunk counts, block total.  Fast path: the block stages the offsets of the
-    // trajectories its tokens cover once (one coalesced load) and counts per trajectory with
-    // shared atomics; the chunk loop then has no dependent global loads.
-    const bool any_traj = p.n_traj > 0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t bf = 0;
-    const int32_t nbt = any_traj ? block_traj_range(p, c_lo, c_hi, bf) : 0;
-    const bool staged = nbt > 0 && nbt <= BT_CAP;
-    if (staged) {
-        for (int32_t k = threadIdx.x; k <= nbt; k += COOP_THREADS) {
-            sm.s_boff[k] = p.off[bf + k];
-            if (k < nbt) sm.s_aux[k] = 0;
-        }
-    }
-    __syncthreads();
-    int64_t* s_offw = s_off + warp * WOFF_CAP;
+    // phase A: counts (n_g via window flushes), per-chunk counts, K_j, validation
     int32_t warp_total = 0;
-    ChunkIn nxt{};
-    if (c_lo + warp < c_hi) nxt = chunk_fetch(p, c_lo + warp, any_traj, false);
-    for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
-        const ChunkIn cur = nxt;
-        if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, false);
-        const int64_t t0 = c * WCHUNK + lane * 16;
-        int32_t mine = 0;
-        if (staged) {
-            if (t0 < p.T) {
-                const int32_t klo = min(max(cur.f - bf, 0), nbt - 1);
-                const int32_t khi = min(max(cur.l - bf + 1, klo + 1), nbt);
-                int32_t k = smem_find_in(sm.s_boff, klo, khi, t0);
-                int64_t end = sm.s_boff[k + 1];
-                int32_t cnt = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t t = t0 + i;
-                    while (t >= end && k + 1 < nbt) {
-                        if (cnt) atomicAdd(&sm.s_aux[k], cnt);
-                        cnt = 0;
-                        ++k;
-                        end = sm.s_boff[k + 1];
-                    }
-                    const int32_t bit = mbit(cur.mk, i);  // 0 past T (zero-filled load)
-                    cnt += bit;
-                    mine += bit;
-                }
-                if (cnt) atomicAdd(&sm.s_aux[k], cnt);
-            }
-        } else {
-            uint8_t m[16];
-            unpack16(cur.mk, m);
-            int32_t first = 0, cnt_st = 0;
-            if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
-            if (t0 < p.T && any_traj) {
-                int32_t g, k = 0;
-                int64_t end;
-                if (cnt_st) {
-                    k = smem_find(s_offw, cnt_st, t0);
-                    g = first + k;
-                    end = s_offw[k + 1];
-                } else {
-                    g = coop_find_traj(p.off, p.n_traj, t0);
-                    end = p.off[g + 1];
-                }
-                int32_t cnt = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t t = t0 + i;
-                    if (t >= p.T) break;
-                    while (t >= end && g + 1 < p.n_traj) {
-                        if (cnt) atomicAdd(&p.n_g[g], cnt);
-                        cnt = 0;
-                        ++g;
-                        ++k;
-                        end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
-                    }
-                    const int32_t bit = m[i] != 0;
-                    cnt += bit;
-                    mine += bit;
-                }
-                if (cnt) atomicAdd(&p.n_g[g], cnt);
-            }
-        }
-        const int32_t total = __shfl_sync(0xffffffffu, warp_incl_scan(mine), 31);
-        if (lane == 0) p.chunk[c] = total;
-        warp_total += total;
-        __syncwarp();  // s_offw restaged by this warp's next chunk
-    }
-    if (staged) {  // per-trajectory block counts -> n_g (integer atomics: exact, order-free)
-        __syncthreads();
-        for (int32_t k = threadIdx.x; k < nbt; k += COOP_THREADS)
-            if (sm.s_aux[k]) atomicAdd(&p.n_g[bf + k], sm.s_aux[k]);
-    }
-    if (lane == 0) s_w[warp] = warp_total;
-    __syncthreads();
-    // block-local exclusive scan of this block's chunk counts -> chunk_base (local), so that the
-    // apply phase can place every chunk without block-wide exchanges
-    {
-        const int64_t n = c_hi - c_lo;
-        const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
-        const int64_t lo = c_lo + min(n, (int64_t)threadIdx.x * per);
-        const int64_t hi = min(c_hi, lo + per);
-        int32_t sum = 0;
-        for (int64_t c = lo; c < hi; ++c) sum += p.chunk[c];
-        int32_t total;
-        int32_t run = coop_block_exscan(sum, s_w, total);
-        for (int64_t c = lo; c < hi; ++c) {
-            const int32_t v = p.chunk[c];
-            p.chunk_base[c] = run;
-            run += v;
-        }
-        if (threadIdx.x == 0) p.blk_chunk[B] = total;
-    }
+    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total);
+    chunk_bases(p, c_lo, c_hi, s_w);
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int32_t j = p.group_id[g], i = p.task_id[g];
         if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
@@ -529,54 +1114,98 @@ __device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_g
     grid.sync();
     phase_mark(4);
 
-    // phase B3: this block's groups (GRPO advantage; readings R1, R2, R14), then the
-    // block's per-task partial (N, S, Q) in a fixed order
-    unsigned long long nz = 0;  // trajectories with masked tokens (sequence-mean weights)
+    // phase B3: this block's groups, then the block's per-task partial (N, S, Q) in a fixed
+    // order.  Groups of <= REG_K members: ids sorted by a register sorting network and their
+    // reward / task / count loads issued together (no dependent global round trips).
+    unsigned long long nz = 0;
     for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
         const int32_t K = p.grp_cnt[j];
-        int32_t* mb = p.members + s_pre[B] + p.grp_start[j];
-        for (int a = 1; a < K; ++a) {
-            const int32_t x = mb[a];
-            int b = a - 1;
-            while (b >= 0 && mb[b] > x) {
-                mb[b + 1] = mb[b];
-                --b;
+        int32_t* mbg = p.members + s_pre[B] + p.grp_start[j];
+        double N, S, Q;
+        int32_t task0;
+        if (K <= REG_K) {
+            int32_t m[REG_K];
+#pragma unroll
+            for (int a = 0; a < REG_K; ++a) m[a] = a < K ? mbg[a] : INT_MAX;
+#pragma unroll
+            for (int k2 = 2; k2 <= REG_K; k2 <<= 1)
+#pragma unroll
+                for (int jj = k2 >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                    for (int i = 0; i < REG_K; ++i) {
+                        const int l = i ^ jj;
+                        if (l > i) {
+                            const bool up = (i & k2) == 0;
+                            const int32_t a0 = m[i], b0 = m[l];
+                            if ((a0 > b0) == up) {
+                                m[i] = b0;
+                                m[l] = a0;
+                            }
+                        }
+                    }
+            float rr[REG_K];
+            int32_t tt[REG_K], nn[REG_K];
+#pragma unroll
+            for (int a = 0; a < REG_K; ++a) {
+                rr[a] = a < K ? p.rewards[m[a]] : 0.f;
+                tt[a] = a < K ? p.task_id[m[a]] : 0;
+                nn[a] = a < K ? p.n_g[m[a]] : 0;
             }
-            mb[b + 1] = x;
-        }
-        double N = 0.0, S = 0.0, Q = 0.0;
-        int32_t task0 = -1;
-        if (K > 0) {
-            if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
-            task0 = p.task_id[mb[0]];
-            double sum = 0.0, rmax = p.rewards[mb[0]], rmin = rmax;
-            for (int a = 0; a < K; ++a) {
-                const double r = p.rewards[mb[a]];
-                if (p.task_id[mb[a]] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-                sum += r;
-                rmax = fmax(rmax, r);
-                rmin = fmin(rmin, r);
-            }
-            const bool flat = rmax == rmin;
-            const double mean = sum / (double)K;
-            double ss = 0.0;
-            if (!flat)
-                for (int a = 0; a < K; ++a) {
-                    const double dlt = (double)p.rewards[mb[a]] - mean;
-                    ss += dlt * dlt;
+            // same arithmetic and order as group_adv, on the register copies
+            N = S = Q = 0.0;
+            task0 = -1;
+            if (K > 0) {
+                if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+                task0 = tt[0];
+                double sum = 0.0, rmax = rr[0], rmin = rmax;
+#pragma unroll
+                for (int a = 0; a < REG_K; ++a)
+                    if (a < K) {
+                        const double rv = rr[a];
+                        if (tt[a] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                        sum += rv;
+                        rmax = fmax(rmax, rv);
+                        rmin = fmin(rmin, rv);
+                    }
+                const bool flat = rmax == rmin;
+                const double mean = sum / (double)K;
+                double ss = 0.0;
+                if (!flat) {
+#pragma unroll
+                    for (int a = 0; a < REG_K; ++a)
+                        if (a < K) {
+                            const double dlt = (double)rr[a] - mean;
+                            ss += dlt * dlt;
+                        }
                 }
-            const double sd = sqrt(ss / (double)K);
-            const double den = sd > p.eps_std ? sd : p.eps_std;
-            for (int a = 0; a < K; ++a) {
-                const int32_t g = mb[a];
-                const double ah = flat ? 0.0 : ((double)p.rewards[g] - mean) / den;
-                p.adv_hat[g] = ah;
-                const double n = (double)p.n_g[g];
-                N += n;
-                S += n * ah;
-                Q += n * ah * ah;
-                nz += p.n_g[g] > 0;
+                const double sd = sqrt(ss / (double)K);
+                const double den = sd > p.eps_std ? sd : p.eps_std;
+#pragma unroll
+                for (int a = 0; a < REG_K; ++a)
+                    if (a < K) {
+                        const double ah = flat ? 0.0 : ((double)rr[a] - mean) / den;
+                        p.adv_hat[m[a]] = ah;
+                        const double n = (double)nn[a];
+                        N += n;
+                        S += n * ah;
+                        Q += n * ah * ah;
+                        nz += nn[a] > 0;
+                    }
             }
+        } else {
+            for (int a = 1; a < K; ++a) {
+                const int32_t x = mbg[a];
+                int b = a - 1;
+                while (b >= 0 && mbg[b] > x) {
+                    mbg[b + 1] = mbg[b];
+                    --b;
+                }
+                mbg[b + 1] = x;
+            }
+            group_adv(
+                p, K, mbg, [&](int32_t g) { return p.rewards[g]; },
+                [&](int32_t g) { return p.task_id[g]; }, [&](int32_t g) { return p.n_g[g]; }, N,
+                S, Q, task0, st, nz);
         }
         p.grp_task[j] = task0;
         p.grp_nsq[3 * j + 0] = N;
@@ -585,8 +1214,6 @@ __device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_g
     }
     if (nz) atomicAdd(reinterpret_cast<unsigned long long*>(&p.meta[3]), nz);  // integer: exact
     __syncthreads();
-    // per-task partials of this block: warp shuffles (fixed tree) + one barrier, tasks in
-    // batches of TASK_BATCH
     {
         __shared__ double s_wp[NWARPS][TASK_BATCH][3];
         const int warp_b = threadIdx.x >> 5, lane_b = threadIdx.x & 31;
@@ -630,7 +1257,7 @@ __device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_g
     // of the block partials (warp w handles tasks w, w+8, ...; lanes stride over blocks)
     if (B == 0) {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int32_t i = wid; i < p.n_tasks; i += COOP_THREADS / 32) {
+        for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
             double N = 0.0, S = 0.0, Q = 0.0;
             for (int64_t b = lane; b < G; b += 32) {
                 const double* bp = p.blk_part + 3 * (b * p.n_tasks + i);
@@ -654,195 +1281,87 @@ __device__ __forceinline__ void coop_stats_phases(const AdvParams& p, cg::grid_g
     }
 }
 
-// ------------------------------------------------------------------ phase C
-// (needs gridDim.x == the stats launch's grid: it owns the same contiguous chunk ranges)
-__device__ __forceinline__ void coop_apply_phase(const AdvParams& p, CoopSmem& sm) {
-    extern __shared__ double s_task[];  // [2*n_tasks]: mu, max(sigma, eps)
-    int32_t* s_w = sm.s_w;
-    int32_t* s_pre = sm.s_pre;
-    int64_t* s_off = sm.s_boff;  // fallback path: per-warp staging
+__device__ __forceinline__ void large_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
+                                            int32_t* s_pre, int32_t* s_w) {
     const int64_t G = gridDim.x, B = blockIdx.x;
-    for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
-        const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
-        const double mu = N > 0.0 ? S / N : 0.0;
-        const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
-        s_task[2 * i] = mu;
-        s_task[2 * i + 1] = sd > p.eps_std ? sd : p.eps_std;
-        if (B == 0 && p.task_stats_out) {
-            p.task_stats_out[3 * i] = N;
-            p.task_stats_out[3 * i + 1] = mu;
-            p.task_stats_out[3 * i + 2] = sd;
-        }
-    }
-    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // also orders s_task writes
-    if (B == 0 && threadIdx.x < 32) {
-        double nsum = 0.0;
-        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
-        if (threadIdx.x == 0) {
-            const int64_t n = (int64_t)nsum;
-            p.meta[0] = s_pre[G];  // local masked rows
-            p.meta[1] = n;         // global N
-            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global n_seq
-            if (p.n_mask_global_out) *p.n_mask_global_out = n;
-            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
-        }
-    }
-    const bool any_traj = p.n_traj > 0;
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t* s_offw = s_off + warp * WOFF_CAP;
-    const int32_t blk_base = s_pre[B];
-    // compaction staging (dynamic smem after s_task; present only when p.compact)
-    int32_t(*s_cidx)[WCHUNK] = reinterpret_cast<int32_t(*)[WCHUNK]>(s_task + 2 * p.n_tasks);
-    float(*s_cadv)[WCHUNK] = reinterpret_cast<float(*)[WCHUNK]>(s_task + 2 * p.n_tasks) + NWARPS;
-    // Fast path: the block stages the offsets and final values A~_g = (A^_g - mu_i) / max(sigma_i,
-    // eps) (Eq.1) of the trajectories its tokens cover; the chunk loop then streams
-    // mask -> adv_tok with smem lookups only.
-    int32_t bf = 0;
-    const int32_t nbt = any_traj ? block_traj_range(p, c_lo, c_hi, bf) : 0;
-    const bool staged = nbt > 0 && nbt <= BT_CAP;
-    if (staged) {
-        for (int32_t k = threadIdx.x; k <= nbt; k += COOP_THREADS) {
-            sm.s_boff[k] = p.off[bf + k];
-            if (k < nbt) {
-                const int32_t ti = p.task_id[bf + k];
-                const float at = (ti >= 0 && ti < p.n_tasks)
-                                     ? (float)((p.adv_hat[bf + k] - s_task[2 * ti]) / s_task[2 * ti + 1])
-                                     : 0.f;
-                sm.s_aux[k] = __float_as_int(at);
-            }
-        }
-    }
-    __syncthreads();
-    // every warp walks its own chunks with no block-wide exchange: the chunk's compaction base
-    // is the block prefix plus the local base stored by the counting phase
-    ChunkIn nxt{};
-    if (c_lo + warp < c_hi) nxt = chunk_fetch(p, c_lo + warp, any_traj, true);
-    for (int64_t c = c_lo + warp; c < c_hi; c += NWARPS) {
-        const ChunkIn cur = nxt;
-        if (c + NWARPS < c_hi) nxt = chunk_fetch(p, c + NWARPS, any_traj, true);
-        const int32_t wbase = blk_base + cur.base;
-        const int64_t t0 = c * WCHUNK + lane * 16;
-        int32_t mine = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) mine += mbit(cur.mk, i);
-        const int32_t incl = warp_incl_scan(mine);
-        const int32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
-        int32_t pos = incl - mine;  // position within this warp chunk's compacted range
-        float outv[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) outv[i] = 0.f;
-        if (staged) {
-            if (t0 < p.T && mine > 0) {
-                const int32_t klo = min(max(cur.f - bf, 0), nbt - 1);
-                const int32_t khi = min(max(cur.l - bf + 1, klo + 1), nbt);
-                int32_t k = smem_find_in(sm.s_boff, klo, khi, t0);
-                int64_t end = sm.s_boff[k + 1];
-                float at = __int_as_float(sm.s_aux[k]);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t t = t0 + i;
-                    while (t >= end && k + 1 < nbt) {
-                        ++k;
-                        end = sm.s_boff[k + 1];
-                        at = __int_as_float(sm.s_aux[k]);
-                    }
-                    const bool on = mbit(cur.mk, i);
-                    outv[i] = on ? at : 0.f;
-                    if (p.compact && on) {  // staged in smem, written coalesced below
-                        s_cidx[warp][pos] = (int32_t)t;
-                        s_cadv[warp][pos] = at;
-                        ++pos;
-                    }
-                }
-            }
-        } else {  // fallback: per-warp offset staging (warp-collective), global lookups
-            int32_t first = 0, cnt_st = 0;
-            if (any_traj) cnt_st = warp_stage_fl(p.off, cur.f, cur.l, p.n_traj, s_offw, first);
-            if (t0 < p.T && any_traj && mine > 0) {
-                int32_t g, k = 0;
-                int64_t end;
-                if (cnt_st) {
-                    k = smem_find(s_offw, cnt_st, t0);
-                    g = first + k;
-                    end = s_offw[k + 1];
-                } else {
-                    g = coop_find_traj(p.off, p.n_traj, t0);
-                    end = p.off[g + 1];
-                }
-                int32_t gcur = -1;
-                float at = 0.f;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t t = t0 + i;
-                    while (t >= end && g + 1 < p.n_traj) {
-                        ++g;
-                        ++k;
-                        end = (cnt_st && k + 1 < cnt_st) ? s_offw[k + 1] : p.off[g + 1];
-                    }
-                    const bool on = t < p.T && mbit(cur.mk, i);
-                    if (on) {
-                        if (g != gcur) {  // Eq.1 for this trajectory
-                            gcur = g;
-                            const int32_t ti = p.task_id[g];
-                            at = (ti >= 0 && ti < p.n_tasks)
-                                     ? (float)((p.adv_hat[g] - s_task[2 * ti]) / s_task[2 * ti + 1])
-                                     : 0.f;
-                        }
-                        outv[i] = at;
-                        if (p.compact) {
-                            s_cidx[warp][pos] = (int32_t)t;
-                            s_cadv[warp][pos] = at;
-                            ++pos;
-                        }
-                    }
-                }
-            }
-        }
-        if (t0 < p.T) {
-            if (t0 + 16 <= p.T && (reinterpret_cast<uintptr_t>(p.adv_tok + t0) & 15) == 0) {
-                float4* o4 = reinterpret_cast<float4*>(p.adv_tok + t0);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    o4[i] = make_float4(outv[4 * i], outv[4 * i + 1], outv[4 * i + 2], outv[4 * i + 3]);
-            } else {
-                for (int i = 0; i < 16; ++i)
-                    if (t0 + i < p.T) p.adv_tok[t0 + i] = outv[i];
-            }
-        }
-        __syncwarp();  // s_offw restaged by this warp's next chunk; s_c* complete
-        if (p.compact) {
-            for (int32_t i = lane; i < wtotal; i += 32) {
-                p.idx[wbase + i] = s_cidx[warp][i];
-                p.adv_c[wbase + i] = s_cadv[warp][i];
-            }
-            __syncwarp();
-        }
-    }
+    load_task_params(p, smem, s_pre, s_w);
+    int32_t dummy = 0;
+    stream_phase<1>(p, smem, r, c_lo, c_hi, false, nullptr, s_pre[B], dummy);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_all(const AdvParams p) {
-    __shared__ CoopSmem sm;
+// static shared memory of the kernels (the rest is the dynamic Lay arena)
+struct CoopStatic {
+    int32_t s_w[NWARPS];
+    int32_t s_pre[GMAX_BLOCKS + 1];
+};
+
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_all(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    coop_stats_phases(p, grid, sm);
+    WarpRing r = ring_setup(p, smem);
+    large_stats_phases(p, smem, r, grid, ss.s_w, ss.s_pre);
     grid.sync();
     phase_mark(6);
-    coop_apply_phase(p, sm);
+    large_apply(p, smem, r, ss.s_pre, ss.s_w);
     grid.sync();
     phase_mark(7);
 }
-
-__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_stats(const AdvParams p) {
-    __shared__ CoopSmem sm;
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_stats(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    coop_stats_phases(p, grid, sm);
+    WarpRing r = ring_setup(p, smem);
+    large_stats_phases(p, smem, r, grid, ss.s_w, ss.s_pre);
+}
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_apply(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
+    WarpRing r = ring_setup(p, smem);
+    large_apply(p, smem, r, ss.s_pre, ss.s_w);
 }
 
-__global__ void __launch_bounds__(COOP_THREADS, ADV_MIN_BLOCKS) k_adv_coop_apply(const AdvParams p) {
-    __shared__ CoopSmem sm;
-    coop_apply_phase(p, sm);
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
+    cg::grid_group grid = cg::this_grid();
+    phase_mark(0);
+    WarpRing r{};
+    stage_all_offsets(p, smem);
+    if (blockIdx.x == 0) {
+        small_group_pre(p, smem, ss.s_w);
+    } else {
+        r = ring_setup(p, smem);
+        small_count(p, smem, r, ss.s_w);
+    }
+    grid.sync();
+    phase_mark(1);
+    if (blockIdx.x == 0) small_group_post(p, smem, gridDim.x, ss.s_w, true);
+    grid.sync();
+    phase_mark(2);
+    if (blockIdx.x != 0) small_apply(p, smem, r, ss.s_pre, ss.s_w, true);
+}
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
+    cg::grid_group grid = cg::this_grid();
+    stage_all_offsets(p, smem);
+    if (blockIdx.x == 0) {
+        small_group_pre(p, smem, ss.s_w);
+    } else {
+        WarpRing r = ring_setup(p, smem);
+        small_count(p, smem, r, ss.s_w);
+    }
+    grid.sync();
+    if (blockIdx.x == 0) small_group_post(p, smem, gridDim.x, ss.s_w, false);
+}
+__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_apply(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CoopStatic ss;
+    stage_all_offsets(p, smem);
+    WarpRing r = ring_setup(p, smem);
+    small_apply(p, smem, r, ss.s_pre, ss.s_w, false);  // block 0 publishes meta / task_stats
 }
 
 static int coop_grid(const void* kern, size_t smem, int64_t want) {
@@ -853,7 +1372,7 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
         int dev;
         int per_sm;
     };
-    static thread_local Key cache[8];
+    static thread_local Key cache[16];
     static thread_local int n_cache = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -864,12 +1383,18 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, COOP_THREADS, smem) !=
             cudaSuccess)
             per_sm = 0;
-        cache[n_cache % 8] = Key{kern, smem, dev, per_sm};
-        n_cache = n_cache < 8 ? n_cache + 1 : 8;
+        cache[n_cache % 16] = Key{kern, smem, dev, per_sm};
+        n_cache = n_cache < 16 ? n_cache + 1 : 16;
     }
     if (per_sm <= 0) return 0;
     const int64_t cap = (int64_t)per_sm * num_sms();
     return (int)std::max<int64_t>(1, std::min<int64_t>({cap, want, (int64_t)GMAX_BLOCKS}));
+}
+
+template <typename K>
+static bool set_smem_attr(K k, size_t bytes) {
+    return cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+           cudaSuccess;
 }
 
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
@@ -906,8 +1431,10 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.blk_chunk = reinterpret_cast<int32_t*>(ws + w.blk_chunk);
     p.chunk_base = reinterpret_cast<int32_t*>(ws + w.wchunk_base);
     p.blk_grp = reinterpret_cast<int32_t*>(ws + w.blk_grp);
+    p.blk_cnt = reinterpret_cast<int32_t*>(ws + w.blk_cnt);
     p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
+    p.atilde = reinterpret_cast<float*>(ws + w.atilde);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
     p.stats = reinterpret_cast<double*>(ws + w.stats);
     p.meta = reinterpret_cast<int64_t*>(ws + w.meta);
@@ -918,45 +1445,55 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.task_stats_out = task_stats;
     p.n_mask_global_out = n_mask_global;
     p.compact = compact ? 1 : 0;
-    const size_t smem = sizeof(double) * 2 * (size_t)std::max(1, b->n_tasks) +
-                        (compact ? (size_t)NWARPS * WCHUNK * 8 : 0);
-    if (smem > 96 * 1024) return AGENTRL_ERR_UNSUPPORTED;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute((const void*)k_adv_coop_all,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        cudaFuncSetAttribute((const void*)k_adv_coop_apply,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        attr = true;
+    bool small = b->n_traj <= SMALL_TRAJ && b->n_groups <= SMALL_GROUPS && b->n_tasks <= 64;
+    {
+        const char* e = getenv("AGENTRL_ADV_SMALL");  // A/B: force the large driver
+        if (e && e[0] == '0') small = false;
     }
-    const int64_t want = std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
-                                            ceil_div(p.n_traj, COOP_THREADS),
-                                            ceil_div(p.n_groups, COOP_THREADS), 1});
+    p.lay = make_lay(b->n_tasks, compact, small, b->n_traj, b->n_groups);
+    const size_t smem = p.lay.total;
+    if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    const void* k_all = small ? (const void*)k_adv_small_all : (const void*)k_adv_large_all;
+    const void* k_stats = small ? (const void*)k_adv_small_stats : (const void*)k_adv_large_stats;
+    const void* k_apply = small ? (const void*)k_adv_small_apply : (const void*)k_adv_large_apply;
+    static thread_local size_t attr_set = 0;
+    if (smem > 48 * 1024 && smem > attr_set) {
+        if (!set_smem_attr(k_adv_small_all, 200 * 1024) ||
+            !set_smem_attr(k_adv_small_stats, 200 * 1024) ||
+            !set_smem_attr(k_adv_small_apply, 200 * 1024) ||
+            !set_smem_attr(k_adv_large_all, 200 * 1024) ||
+            !set_smem_attr(k_adv_large_stats, 200 * 1024) ||
+            !set_smem_attr(k_adv_large_apply, 200 * 1024))
+            return AGENTRL_ERR_UNSUPPORTED;
+        attr_set = 200 * 1024;
+    }
+    // small: one statistics block + one warp chunk per warp
+    const int64_t want = small ? std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1) + 1
+                               : std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
+                                                    ceil_div(p.n_traj, COOP_THREADS),
+                                                    ceil_div(p.n_groups, COOP_THREADS), 1});
     void* args[] = {&p};
     if (!comm) {
-        const int grid = coop_grid((const void*)k_adv_coop_all, smem, want);
-        if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+        const int grid = coop_grid(k_all, smem, want);
+        if (!grid || (small && grid < 2)) return AGENTRL_ERR_UNSUPPORTED;
         ProfScope ps(KID_STATS, stream);
-        AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_coop_all, grid, COOP_THREADS, args,
-                                            smem, stream));
+        AG_CUDA(cudaLaunchCooperativeKernel(k_all, grid, COOP_THREADS, args, smem, stream));
         count_launch();
         return AGENTRL_OK;
     }
-    const int grid = coop_grid((const void*)k_adv_coop_stats, 0, want);
-    if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+    const int grid = std::min(coop_grid(k_stats, smem, want), coop_grid(k_apply, smem, want));
+    if (!grid || (small && grid < 2)) return AGENTRL_ERR_UNSUPPORTED;
     {
         ProfScope ps(KID_STATS, stream);
-        AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_coop_stats, grid, COOP_THREADS, args,
-                                            0, stream));
+        AG_CUDA(cudaLaunchCooperativeKernel(k_stats, grid, COOP_THREADS, args, smem, stream));
         count_launch();
     }
     int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks + 1, stream);
     if (rc != AGENTRL_OK) return rc;
     ProfScope ps(KID_APPLY, stream);
     // same grid as the stats launch: phase C reuses its contiguous chunk partition
-    k_adv_coop_apply<<<grid, COOP_THREADS, smem, stream>>>(p);
+    AG_CUDA(cudaLaunchKernel(k_apply, grid, COOP_THREADS, args, smem, stream));
     count_launch();
-    AG_CUDA(cudaGetLastError());
     return AGENTRL_OK;
 }
 

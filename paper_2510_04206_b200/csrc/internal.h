@@ -30,11 +30,13 @@ struct WsPlan {
 struct AdvWs {
     size_t n_g, chunk_cnt, chunk_base, grp_cnt, grp_start, grp_fill, members;  // int32
     size_t adv_hat;                                                               // double
+    size_t atilde;    // float [n_traj] A~_g (small cooperative driver, no communicator)
     size_t grp_task;  // int32 [n_groups] task of each group (cooperative path)
     size_t grp_nsq;   // double [3*n_groups] per-group (N, S, Q) partials (cooperative path)
     size_t chunk_first;  // int32 [n_chunks] trajectory holding each chunk's first token
     size_t blk_chunk, blk_grp, blk_part;  // per cooperative block: int32, int32, double[3*n_tasks]
     size_t wchunk_base;                   // int32 [n_chunks] local compaction base per chunk
+    size_t blk_cnt;  // int32 [n_traj + 2049] per-block trajectory counts (small coop driver)
     size_t stats;     // double [3*n_tasks]: N_i, S_i, Q_i (local, then global)
     size_t meta;      // int64 [4]: n_mask_local, n_mask_global, pad
     size_t idx;       // int32 [T] compacted token positions

@@ -70,7 +70,8 @@ def time_adv(b, iters=20, graph=False):
     times.sort()
     ms = times[len(times) // 2]
     ph = ag.debug_adv_phase_ns()
-    phases = [round((ph[i + 1] - ph[i]) / 1e3, 1) for i in range(7)]
+    phases = [round((ph[i + 1] - ph[i]) / 1e3, 1) if 0 <= ph[i + 1] - ph[i] < 1e9 else None
+              for i in range(7)]
     return ms, int(nm.item()), phases
 
 
