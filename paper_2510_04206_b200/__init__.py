@@ -17,7 +17,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libagentrl.so")
+# AGENTRL_LIB: an alternative in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("AGENTRL_LIB") or os.path.join(_HERE, "libagentrl.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

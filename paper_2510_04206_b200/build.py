@@ -48,8 +48,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          out: str | None = None) -> str:
+    """out: write an A/B variant library there instead (always rebuilt; objects kept apart)"""
+    global BUILD
+    lib = out or LIB
+    if out:
+        BUILD = os.path.join(BUILD, os.path.basename(out))
+    elif not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     objs = []
@@ -62,17 +68,17 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "--cudart", "static", *objs, "-o", tmp,
            "-ldl", "-lpthread", "-lrt"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv,
-          ptxas_v="--ptxas-v" in sys.argv)
-    print(LIB)
+    out = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")), None)
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv,
+                ptxas_v="--ptxas-v" in sys.argv, out=out))

@@ -43,6 +43,12 @@ constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 token
 #ifndef ADV_RING
 #define ADV_RING 8
 #endif
+#ifndef ADV_LDGSTS
+#define ADV_LDGSTS 1  // ring filled by per-lane cp.async (1) or one cp.async.bulk per chunk (0)
+#endif
+#ifndef ADV_LARGE_MINB
+#define ADV_LARGE_MINB 2  // resident blocks per SM the large driver's register budget is cut for
+#endif
 constexpr int RING = ADV_RING;          // bulk-copy slots per warp
 constexpr int WIN_CHUNKS = 8 * NWARPS;  // warp chunks per offset-staging window (large path)
 constexpr int WIN_TRAJ = 2048;          // trajectories a block stages at once (more: windows,
@@ -295,6 +301,21 @@ __device__ __forceinline__ void ring_issue(const AdvParams& p, WarpRing& r, int 
     mbar_arrive_expect_tx(&r.bar[slot], WCHUNK);
     bulk_g2s(r.buf + slot * WCHUNK, p.mask + c * WCHUNK, WCHUNK, &r.bar[slot]);
 }
+// per-lane variant: every lane copies its own 16 bytes (cp.async, one commit group per chunk;
+// a lane only ever reads its own bytes, so waiting on its own groups is enough)
+__device__ __forceinline__ void lane_issue(const AdvParams& p, WarpRing& r, int slot, int64_t c,
+                                           bool valid) {
+    const int lane = threadIdx.x & 31;
+    if (valid)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         smem_u32(r.buf + slot * WCHUNK + lane * 16)),
+                     "l"(p.mask + c * WCHUNK + lane * 16)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void lane_wait_oldest() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
+}
 
 // Offset staging of one window of chunks [w0, w1): trajectories [f, f + nbt) cover its
 // tokens; s_rel[k] = off[f + k] - base (clamped to [0, INT_MAX]), k = 0..nbt, with base the
@@ -463,7 +484,8 @@ __device__ __forceinline__ LaneMask lane_mask(const uint4& mk) {
 // a boundary x is P(x) = E[x/16] + popc(bits[x/16] & low(x%16)); lane j handles the segment
 // that ends at the chunk's j-th trajectory start (and adds it once: no intra-warp conflicts).
 __device__ __forceinline__ int32_t count_chunk_bits(const LaneMask& m, int32_t tc, int32_t kc,
-                                                    const Window& w, int32_t* s_cnt) {
+                                                    const Window& w, int32_t* s_cnt,
+                                                    int32_t& chunk_total) {
     const int lane = threadIdx.x & 31;
     const int32_t pc = __popc(m.bits);
     const int32_t E = warp_incl_scan(pc) - pc;
@@ -486,6 +508,7 @@ __device__ __forceinline__ int32_t count_chunk_bits(const LaneMask& m, int32_t t
         if (nb < 32) break;
         prevP = __shfl_sync(0xffffffffu, P, 31);
     }
+    chunk_total = total;
     return pc;
 }
 
@@ -520,10 +543,15 @@ __device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, 
 // resident (PH 1): the warp's chunks are still in its ring slots from phase A (same kernel,
 // at most RING chunks per warp) and are not copied again.  from_atilde (PH 1): stage the
 // published A~_g instead of computing Eq.1 per trajectory.
-template <int PH>
+struct NoPre {
+    __device__ void operator()() const {}
+};
+// pre(): work run after the ring's first copies are issued (overlaps their latency)
+template <int PH, typename Pre = NoPre>
 __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int64_t c_lo,
                              int64_t c_hi, bool small, const int64_t* s_offall, int32_t blk_base,
-                             int32_t& warp_total, bool resident = false, bool from_atilde = false) {
+                             int32_t& warp_total, bool resident = false, bool from_atilde = false,
+                             Pre pre = Pre()) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t B = blockIdx.x;
     int32_t* s_rel = reinterpret_cast<int32_t*>(smem + p.lay.srel);
@@ -536,12 +564,18 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     const bool any_traj = p.n_traj > 0;
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
     const bool res = resident && n_mine <= RING;  // warp-uniform
-    if (lane == 0 && r.on && !res) {
+    if (ADV_LDGSTS && r.on && !res) {
+        for (int s = 0; s < RING; ++s) {
+            const int64_t c = c_lo + warp + (int64_t)s * NWARPS;
+            lane_issue(p, r, s, c, c < c_hi && chunk_full(p, c));
+        }
+    } else if (lane == 0 && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
             const int64_t c = c_lo + warp + (int64_t)s * NWARPS;
             if (c < c_hi && chunk_full(p, c)) ring_issue(p, r, s, c);
         }
     }
+    pre();
     // staging plan: the block's whole range if its trajectories fit, else 64-chunk windows
     int64_t wlen = max(c_hi - c_lo, (int64_t)1);
     if (wlen > KC_CAP) wlen = WIN_CHUNKS;
@@ -595,8 +629,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         for (int64_t c = w0 + warp; c < w1; c += NWARPS, ++kseq) {
             const int slot = (int)(kseq % RING);
             uint4 mk;
+            if (ADV_LDGSTS && r.on && !res) lane_wait_oldest();  // this chunk's group
             if (r.on && chunk_full(p, c)) {
-                if (!res) {
+                if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
                     r.par ^= 1u << slot;
                 }
@@ -608,21 +643,25 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             const int32_t tc = (int32_t)(c * WCHUNK - w.base);  // chunk start, window-relative
             const int32_t kc = (any_traj && w.staged) ? s_kc[c - w0] : 0;
             if (PH == 0) {
-                int32_t mine;
-                if (!any_traj) mine = 0;
-                else if (w.staged) mine = count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux);
-                else mine = count_chunk_global(p, mk, t0);
-                int32_t tot = mine;
+                int32_t tot = 0;
+                if (any_traj && w.staged) {
+                    (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
+                } else {
+                    tot = any_traj ? count_chunk_global(p, mk, t0) : 0;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                }
                 if (lane == 0) p.chunk[c] = tot;
                 warp_total += tot;
             } else {
                 const LaneMask lm = lane_mask(mk);
                 const int32_t mine = any_traj ? __popc(lm.bits) : 0;
-                const int32_t incl = warp_incl_scan(mine);
-                const int32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
-                int32_t pos = incl - mine;
+                int32_t wtotal = 0, pos = 0;
+                if (p.compact) {  // positions of the lane's masked tokens in the chunk
+                    const int32_t incl = warp_incl_scan(mine);
+                    wtotal = __shfl_sync(0xffffffffu, incl, 31);
+                    pos = incl - mine;
+                }
                 float outv[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) outv[i] = 0.f;
@@ -673,7 +712,10 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 }
             }
             __syncwarp();
-            if (lane == 0 && r.on && !res) {
+            if (ADV_LDGSTS && r.on && !res) {
+                const int64_t c2 = c + (int64_t)RING * NWARPS;
+                lane_issue(p, r, slot, c2, c2 < c_hi && chunk_full(p, c2));
+            } else if (lane == 0 && r.on && !res) {
                 const int64_t c2 = c + (int64_t)RING * NWARPS;
                 if (c2 < c_hi && chunk_full(p, c2)) ring_issue(p, r, slot, c2);
             }
@@ -1021,7 +1063,9 @@ __device__ __forceinline__ void small_count(const AdvParams& p, uint8_t* smem, W
     small_range(p, c_lo, c_hi);
     const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
     int32_t warp_total = 0;
-    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total);
+    // the offsets are staged while the block's first mask copies are in flight
+    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false, false,
+                    [&]() { stage_all_offsets(p, smem); });
     chunk_bases(p, c_lo, c_hi, s_w);
 }
 
@@ -1068,18 +1112,20 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
 
     // phase A: counts (n_g via window flushes), per-chunk counts, K_j, validation
     int32_t warp_total = 0;
-    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total);
-    chunk_bases(p, c_lo, c_hi, s_w);
-    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
-        const int32_t j = p.group_id[g], i = p.task_id[g];
-        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
-            st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-            continue;
+    auto validate = [&]() {  // K_j and validation, while the first mask copies are in flight
+        for (int64_t g = gtid; g < p.n_traj; g += gstride) {
+            const int32_t j = p.group_id[g], i = p.task_id[g];
+            if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
+                st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                continue;
+            }
+            atomicAdd(&p.grp_cnt[j], 1);
+            if (p.off[g + 1] < p.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
         }
-        atomicAdd(&p.grp_cnt[j], 1);
-        if (p.off[g + 1] < p.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
-    }
-    if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
+        if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
+    };
+    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total, false, false, validate);
+    chunk_bases(p, c_lo, c_hi, s_w);
     grid.sync();
     phase_mark(2);
 
@@ -1212,7 +1258,13 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
         p.grp_nsq[3 * j + 1] = S;
         p.grp_nsq[3 * j + 2] = Q;
     }
-    if (nz) atomicAdd(reinterpret_cast<unsigned long long*>(&p.meta[3]), nz);  // integer: exact
+    {  // one atomic per block (same-address atomics from every thread serialise at L2)
+        int32_t nzt = 0;
+        (void)coop_block_exscan((int32_t)nz, s_w, nzt);
+        if (threadIdx.x == 0 && nzt)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&p.meta[3]),
+                      (unsigned long long)nzt);  // integer: exact
+    }
     __syncthreads();
     {
         __shared__ double s_wp[NWARPS][TASK_BATCH][3];
@@ -1296,7 +1348,7 @@ struct CoopStatic {
     int32_t s_pre[GMAX_BLOCKS + 1];
 };
 
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_all(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_all(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
@@ -1308,14 +1360,14 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_all(const AdvPara
     grid.sync();
     phase_mark(7);
 }
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_stats(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
     WarpRing r = ring_setup(p, smem);
     large_stats_phases(p, smem, r, grid, ss.s_w, ss.s_pre);
 }
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_large_apply(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     WarpRing r = ring_setup(p, smem);
@@ -1328,8 +1380,8 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvPara
     cg::grid_group grid = cg::this_grid();
     phase_mark(0);
     WarpRing r{};
-    stage_all_offsets(p, smem);
     if (blockIdx.x == 0) {
+        stage_all_offsets(p, smem);
         small_group_pre(p, smem, ss.s_w);
     } else {
         r = ring_setup(p, smem);
@@ -1346,8 +1398,8 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvPa
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    stage_all_offsets(p, smem);
     if (blockIdx.x == 0) {
+        stage_all_offsets(p, smem);
         small_group_pre(p, smem, ss.s_w);
     } else {
         WarpRing r = ring_setup(p, smem);
