@@ -347,10 +347,9 @@ def run_native(args, cfg, world, rank, local_rank):
         dist.destroy_process_group()
 
 
-def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
-    """Part 1 alone (agentrl_task_adv_norm) at this rank's batch size, single GPU, cold L2
-    (a 2 x L2 buffer is written before every timed call).  Algorithmic bytes: mask T B +
-    adv_tok 4T B + 20 B per trajectory (offsets, ids, reward)."""
+def _adv_time(ag, bd, lb, dev, iters, graph):
+    """median event time (ms) of agentrl_task_adv_norm on its own stream, cold L2 (a 2 x L2
+    buffer is written before every timed call); optionally replayed from a CUDA graph"""
     import torch
     T = int(lb["T"])
     n_traj = len(lb["task_id"])
@@ -363,48 +362,72 @@ def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
     batch = ag.make_batch(bd)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream(device=dev)
     times = []
-    for i in range(iters + 3):
-        flush.fill_(float(i))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        rc = ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st)
-        e1.record()
-        torch.cuda.synchronize()
-        if rc != 0:
-            return None
-        if i >= 3:
-            times.append(e0.elapsed_time(e1))
-    times.sort()
-    ms = times[len(times) // 2]
-    # the same call replayed from a CUDA graph (no host submission in the timed interval)
-    gms = None
-    try:
-        s = torch.cuda.Stream(device=dev)
-        with torch.cuda.stream(s):
-            ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            if ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s) != 0:
+                return None
+        g = None
+        if graph:
             s.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
                 ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s)
-            gt = []
-            for i in range(iters):
-                flush.fill_(float(i))
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(s)
+        for i in range(iters):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            if g is not None:
                 g.replay()
-                e1.record(s)
-                e1.synchronize()
-                gt.append(e0.elapsed_time(e1))
-            gt.sort()
-            gms = gt[len(gt) // 2]
+            else:
+                ag.agentrl_task_adv_norm(batch, 1e-6, adv, ts, nm, ws, None, st, stream=s)
+            e1.record(s)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    times.sort()
+    return times[len(times) // 2]
+
+
+def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
+    """Part 1 alone (agentrl_task_adv_norm), single GPU, cold L2, at this rank's batch
+    (launch-latency bound) and at the 2^27-token bandwidth point of the DESIGN.md sweep
+    (synth.make_sweep_structure: ~400 tokens/trajectory, 5 tasks, G=8).  Algorithmic bytes:
+    mask T B + adv_tok 4T B + 20 B per trajectory (offsets, ids, reward)."""
+    import torch
+    T = int(lb["T"])
+    n_traj = len(lb["task_id"])
+    ms = _adv_time(ag, bd, lb, dev, iters, False)
+    if ms is None:
+        return None
+    try:
+        gms = _adv_time(ag, bd, lb, dev, iters, True)
     except Exception:  # graph capture unavailable: report the direct number only
         gms = None
     by = 5 * T + 20 * n_traj
-    return {"latency_us": ms * 1e3, "graph_latency_us": None if gms is None else gms * 1e3,
-            "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
-            "frac_hbm": by / (ms / 1e3) / 1e9 / hbm_gbs, "cold_l2": True,
-            "note": "launch-latency bound at this size; see profiles/*adv_sweep* for the T sweep"}
+    out = {"latency_us": ms * 1e3, "graph_latency_us": None if gms is None else gms * 1e3,
+           "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
+           "frac_hbm": by / (ms / 1e3) / 1e9 / hbm_gbs, "cold_l2": True,
+           "note": "launch-latency bound at this size (empty cooperative launch + 2 grid "
+                   "barriers ~8 us); bandwidth_point is the HBM-bound regime"}
+    try:
+        sb = synth.make_sweep_structure(1 << 27)
+        sbd = {k: (torch.from_numpy(np.ascontiguousarray(v)).to(dev) if isinstance(v, np.ndarray)
+                   else v) for k, v in sb.items()}
+        sbd["traj_offsets"] = sbd["traj_offsets"].long()
+        sbd["task_id"] = sbd["task_id"].int()
+        sbd["group_id"] = sbd["group_id"].int()
+        sms = _adv_time(ag, sbd, sb, dev, 10, False)
+        sby = 5 * int(sb["T"]) + 20 * len(sb["task_id"])
+        out["bandwidth_point"] = {"T": int(sb["T"]), "n_traj": len(sb["task_id"]),
+                                  "latency_us": sms * 1e3, "alg_bytes": sby,
+                                  "GBps": sby / (sms / 1e3) / 1e9,
+                                  "frac_hbm": sby / (sms / 1e3) / 1e9 / hbm_gbs}
+        del sbd
+        torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001 -- report, never fail the bench line
+        out["bandwidth_point"] = {"error": str(e)[:200]}
+    return out
 
 
 def traffic_from_profiles(config, kernel):

@@ -874,8 +874,11 @@ __device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w)
         a.gfill[j] = 0;
     }
     __syncthreads();
-    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
-        if (a.off[g + 1] < a.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
+    // the trajectory table and the offsets in one pass (independent loads in flight together)
+    int64_t* s_off = reinterpret_cast<int64_t*>(smem + p.lay.soff);
+    for (int32_t g = threadIdx.x; g <= p.n_traj; g += COOP_THREADS) {
+        s_off[g] = p.off[g];
+        if (g == p.n_traj) break;
         const int32_t j = p.group_id[g], i = p.task_id[g];
         a.rew[g] = p.rewards[g];
         a.tid[g] = i;
@@ -889,8 +892,10 @@ __device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w)
             atomicAdd(&a.gcnt[j], 1);
         }
     }
-    if (threadIdx.x == 0 && (a.off[0] != 0 || a.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     __syncthreads();
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS)
+        if (a.off[g + 1] < a.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
+    if (threadIdx.x == 0 && (a.off[0] != 0 || a.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) a.gstart[j] = a.gcnt[j];
     __syncthreads();
     coop_block_scan_array(a.gstart, p.n_groups, s_w);
@@ -1381,8 +1386,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvPara
     phase_mark(0);
     WarpRing r{};
     if (blockIdx.x == 0) {
-        stage_all_offsets(p, smem);
-        small_group_pre(p, smem, ss.s_w);
+        small_group_pre(p, smem, ss.s_w);  // stages the offsets itself
     } else {
         r = ring_setup(p, smem);
         small_count(p, smem, r, ss.s_w);
@@ -1399,8 +1403,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvPa
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
     if (blockIdx.x == 0) {
-        stage_all_offsets(p, smem);
-        small_group_pre(p, smem, ss.s_w);
+        small_group_pre(p, smem, ss.s_w);  // stages the offsets itself
     } else {
         WarpRing r = ring_setup(p, smem);
         small_count(p, smem, r, ss.s_w);
