@@ -145,11 +145,29 @@ def run_native(args, cfg, world, rank, local_rank):
 
     import paper_2510_04206_b200 as ag
 
+    # AGENTRL_BENCH_SHARED_GPU=1 (flow test only, tests/test_gpu_bench_multirank.py): every
+    # rank on cuda:0 over gloo with the library's callback communicator -- NCCL cannot place
+    # two ranks on one device.  The numbers of such a run are not measurements.
+    shared = os.environ.get("AGENTRL_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    comm = None
+    if world > 1 and shared:
+        dist.init_process_group("gloo")
+        comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn(),
+                               rs_fn=ag.gloo_reduce_scatter_fn(world, rank))
+    elif world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    comm = ag.Comm.from_process_group() if world > 1 else None
+        comm = ag.Comm.from_process_group()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     gb, lb = build_inputs(cfg, rank, world)
     T = int(lb["T"])
@@ -223,10 +241,7 @@ def run_native(args, cfg, world, rank, local_rank):
     prof = ag.profile_stop()
     clocks = clk.stop()
     status = int(step.status.item())
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms)
     value = T_global / (ms / 1e3)
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region
@@ -289,10 +304,7 @@ def run_native(args, cfg, world, rank, local_rank):
         torch.cuda.synchronize()
         barrier()
         ms_e2e = f0.elapsed_time(f1) / args.steps
-        if world > 1:
-            tt = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms_e2e = float(tt.item())
+        ms_e2e = max_over_ranks(ms_e2e)
         e2e = {"value": T_global / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
                "pipelining": "inputs double-buffered; step k+1's pinned H2D copy overlaps "
@@ -338,8 +350,10 @@ def run_native(args, cfg, world, rank, local_rank):
     if world > 1:
         dist.barrier()
     if rank == 0:
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # the oracle baseline: rank 0 at N=1 only
             result["cpu_baseline"] = cpu_baseline(cfg, gb, args.cpu_seconds)
+        if shared:
+            result["note"] = "AGENTRL_BENCH_SHARED_GPU flow test: all ranks on one GPU, not a measurement"
         print(json.dumps(result), flush=True)
     if comm is not None:
         comm.destroy()

@@ -180,12 +180,6 @@ __device__ __forceinline__ int32_t mbit(const uint4& v, int i) {
     const uint32_t w = i < 4 ? v.x : (i < 8 ? v.y : (i < 12 ? v.z : v.w));
     return ((w >> (8 * (i & 3))) & 0xffu) != 0u;
 }
-__device__ __forceinline__ int32_t mcount(const uint4& v) {
-    int32_t n = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) n += mbit(v, i);
-    return n;
-}
 __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -328,69 +322,6 @@ struct Window {
     bool staged;
 };
 
-// warp-cooperative search: largest k in [0, n) with s[k] <= t (s[0] <= t); 32 probes per
-// round narrow the range 32x (3 rounds for 2048 entries instead of 11 dependent steps)
-__device__ __forceinline__ int32_t warp_find(const int32_t* s, int32_t n, int32_t t) {
-    const int lane = threadIdx.x & 31;
-    int32_t lo = 0, hi = n;
-    while (hi - lo > 1) {
-        const int32_t step = (hi - lo + 31) >> 5;
-        const int32_t pos = lo + lane * step;
-        const uint32_t m = __ballot_sync(0xffffffffu, pos < hi && s[pos] <= t);
-        lo += (31 - __clz(m | 1u)) * step;
-        hi = min(hi, lo + step);
-    }
-    return lo;
-}
-// the lane's trajectory (window-local) from the chunk's first one: short forward walk
-__device__ __forceinline__ int32_t lane_traj(const Window& w, int32_t kc, int32_t tr0) {
-    int32_t k = kc;
-    while (k + 1 < w.nbt && w.s_rel[k + 1] <= tr0) ++k;
-    return k;
-}
-
-// ------------------------------------------------------------------ phase A: counting
-// lane: 16 tokens from tr0 (window-relative); counts of trajectories after the lane's first
-// one go straight to the shared counters (rare: a boundary inside the lane's 16 tokens); the
-// first trajectory's count is summed over lanes by a segmented warp scan and added once per
-// trajectory.
-__device__ __forceinline__ int32_t count_chunk_staged(const uint4& mk, int32_t tr0, int32_t kc,
-                                                      const Window& w, int32_t* s_cnt) {
-    const int lane = threadIdx.x & 31;
-    int32_t k = lane_traj(w, kc, tr0);
-    int32_t end = w.s_rel[k + 1];
-    const int32_t key = k;
-    int32_t head = 0, cnt = 0, mine = 0;
-    bool crossed = false;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int32_t t = tr0 + i;
-        while (t >= end && k + 1 < w.nbt) {
-            if (!crossed) head = cnt;
-            else if (cnt) atomicAdd(&s_cnt[k], cnt);
-            crossed = true;
-            cnt = 0;
-            ++k;
-            end = w.s_rel[k + 1];
-        }
-        const int32_t bit = mbit(mk, i);
-        cnt += bit;
-        mine += bit;
-    }
-    if (!crossed) head = cnt;
-    else if (cnt) atomicAdd(&s_cnt[k], cnt);
-    // keys are nondecreasing over lanes: segmented inclusive sum, one add per trajectory
-    int32_t v = head;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
-        const int32_t ky = __shfl_up_sync(0xffffffffu, key, o);
-        if (lane >= o && ky == key) v += y;
-    }
-    const int32_t kn = __shfl_down_sync(0xffffffffu, key, 1);
-    if ((lane == 31 || kn != key) && v) atomicAdd(&s_cnt[key], v);
-    return mine;
-}
 // unstaged window: global binary search per lane, global integer atomics on n_g
 __device__ __forceinline__ int32_t count_chunk_global(const AdvParams& p, const uint4& mk,
                                                       int64_t t0) {
