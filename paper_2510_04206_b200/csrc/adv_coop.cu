@@ -100,8 +100,8 @@ __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, i
     L.skc = lay_take(o, 4u * KC_CAP);
     L.stask = lay_take(o, 16u * (uint32_t)(n_tasks > 0 ? n_tasks : 1));
     const uint32_t fixed_end = o;
-    // the small driver's statistics block (block 0) never streams tokens: its group arrays
-    // alias its streaming buffers (ring, transpose and compaction staging)
+    // small driver: group arrays after the fixed arrays (every block reduces the moments
+    // itself while its mask stays resident in the ring)
     uint32_t b = stream_begin;
     const uint32_t nt = small ? (uint32_t)n_traj : 0u, ng = small ? (uint32_t)n_groups + 1 : 0u;
     L.sng = lay_take(b, 4u * nt);
@@ -115,9 +115,10 @@ __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, i
     L.gfill = lay_take(b, 4u * ng);
     L.gtask = lay_take(b, 4u * ng);
     L.gnsq = lay_take(b, 24u * ng);
-    if (b <= stream_end) {
+    (void)stream_end;
+    if (!small) {
         L.total = fixed_end;
-    } else {  // does not fit the streaming buffers: place after the fixed arrays
+    } else {
         const uint32_t shift = ((fixed_end + 127u) & ~127u) - stream_begin;
         uint32_t* f[] = {&L.sng, &L.sgid, &L.stid, &L.srew, &L.smem, &L.sah,
                          &L.gcnt, &L.gstart, &L.gfill, &L.gtask, &L.gnsq};
@@ -143,7 +144,6 @@ struct AdvParams {
     int32_t* blk_cnt;              // small driver: per-block trajectory counts at [g + block]
     double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
-    float* atilde;  // small driver without comm: A~_g published by the statistics block
     int64_t* meta;
     int32_t* d_status;
     float* adv_tok;
@@ -472,8 +472,7 @@ __device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, 
 }
 
 // resident (PH 1): the warp's chunks are still in its ring slots from phase A (same kernel,
-// at most RING chunks per warp) and are not copied again.  from_atilde (PH 1): stage the
-// published A~_g instead of computing Eq.1 per trajectory.
+// at most RING chunks per warp) and are not copied again.
 struct NoPre {
     __device__ void operator()() const {}
 };
@@ -481,8 +480,7 @@ struct NoPre {
 template <int PH, typename Pre = NoPre>
 __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int64_t c_lo,
                              int64_t c_hi, bool small, const int64_t* s_offall, int32_t blk_base,
-                             int32_t& warp_total, bool resident = false, bool from_atilde = false,
-                             Pre pre = Pre()) {
+                             int32_t& warp_total, bool resident = false, Pre pre = Pre()) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t B = blockIdx.x;
     int32_t* s_rel = reinterpret_cast<int32_t*>(smem + p.lay.srel);
@@ -540,9 +538,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                     const int64_t o = (small ? s_offall[f + k] : p.off[f + k]) - w.base;
                     s_rel[k] = (int32_t)min(max(o, (int64_t)0), (int64_t)INT_MAX);
                     if (k < w.nbt)
-                        s_aux[k] = PH == 0 ? 0
-                                           : (from_atilde ? __float_as_int(p.atilde[f + k])
-                                                          : __float_as_int(adv_tilde(p, s_task, f + k)));
+                        s_aux[k] = PH == 0 ? 0 : __float_as_int(adv_tilde(p, s_task, f + k));
                 }
             }
         }
@@ -877,19 +873,39 @@ __device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w)
             }
         }
         a.gtask[j] = task0;
+        p.grp_task[j] = task0;
+        p.grp_cnt[j] = K;
+        p.grp_start[j] = a.gstart[j];
+        for (int q = 0; q < K; ++q) p.members[a.gstart[j] + q] = mb[q];
     }
     if (st) atomicOr(p.d_status, st);
 }
 
-// block 0 after phase A: n_g (per-block counts summed in block order: exact), per-group and
-// per-task (N, S, Q) in fixed orders; with publish (no communicator) also
-// mu_i, sigma_i, A~_g (Eq.1), task_stats, N and the local masked-row count
-__device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
-                                 bool publish) {
+// After phase A, in every block (identical code and order, so identical results): n_g (the
+// per-block counts of each trajectory summed in block order: exact integers), per-group and
+// per-task (N, S, Q) in fixed orders, then mu_i, max(sigma_i, eps) into the
+// block's s_task.  Streaming blocks first load the group table block 0 published during
+// phase A.  publish (block 0): n_g, task_stats, N, n_seq and the local masked-row count;
+// stats_only (second launch follows the all-reduce): block 0 writes the raw per-task sums.
+__device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
+                            bool publish, bool stats_only) {
     const SmallArrays a = small_arrays(p, smem);
+    const bool blk0 = blockIdx.x == 0;
     const int64_t GS = G - 1;  // streaming blocks 1..G-1
-    int32_t rows = 0;          // local masked rows = sum of the streaming blocks' totals
-    for (int64_t b = 1 + threadIdx.x; b < G; b += COOP_THREADS) rows += p.blk_chunk[b];
+    if (!blk0) {
+        for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
+            a.gcnt[j] = p.grp_cnt[j];
+            a.gstart[j] = p.grp_start[j];
+            a.gtask[j] = p.grp_task[j];
+        }
+        for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+            a.mem[g] = p.members[g];
+            a.ah[g] = p.adv_hat[g];
+        }
+    }
+    int32_t rows = 0;  // local masked rows = sum of the streaming blocks' totals
+    if (blk0 && publish)
+        for (int64_t b = 1 + threadIdx.x; b < G; b += COOP_THREADS) rows += p.blk_chunk[b];
     for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
         const int64_t s0 = a.off[g], e = a.off[g + 1];
         int32_t n = 0;
@@ -899,7 +915,7 @@ __device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, i
             for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
         }
         a.ng[g] = n;
-        p.n_g[g] = n;
+        if (blk0) p.n_g[g] = n;
     }
     __syncthreads();
     unsigned long long nz = 0;
@@ -921,8 +937,8 @@ __device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, i
     }
     int32_t nzt = 0, rows_t = 0;
     (void)coop_block_exscan((int32_t)nz, s_w, nzt);  // also orders the gnsq writes
-    (void)coop_block_exscan(rows, s_w, rows_t);
-    __shared__ double s_st[64 * 3];  // per-task (N, S, Q) for the publish step (n_tasks <= 64)
+    if (blk0 && publish) (void)coop_block_exscan(rows, s_w, rows_t);
+    __shared__ double s_st[64 * 3];  // per-task (N, S, Q) (n_tasks <= 64 on this driver)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
         double N = 0.0, S = 0.0, Q = 0.0;
@@ -939,18 +955,18 @@ __device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, i
             Q += __shfl_down_sync(0xffffffffu, Q, o);
         }
         if (lane == 0) {
-            p.stats[3 * i] = N;
-            p.stats[3 * i + 1] = S;
-            p.stats[3 * i + 2] = Q;
-            if (i < 64) {
-                s_st[3 * i] = N;
-                s_st[3 * i + 1] = S;
-                s_st[3 * i + 2] = Q;
+            s_st[3 * i] = N;
+            s_st[3 * i + 1] = S;
+            s_st[3 * i + 2] = Q;
+            if (blk0 && stats_only) {
+                p.stats[3 * i] = N;
+                p.stats[3 * i + 1] = S;
+                p.stats[3 * i + 2] = Q;
             }
         }
     }
-    if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // n_seq (local)
-    if (!publish) return;
+    if (blk0 && stats_only && threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // n_seq
+    if (stats_only) return;
     __syncthreads();
     double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += COOP_THREADS) {
@@ -958,13 +974,13 @@ __device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, i
         const double mu = N > 0.0 ? S / N : 0.0;
         const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
         s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
-        if (p.task_stats_out) {
+        if (blk0 && publish && p.task_stats_out) {
             p.task_stats_out[3 * i] = N;
             p.task_stats_out[3 * i + 1] = mu;
             p.task_stats_out[3 * i + 2] = sd;
         }
     }
-    if (threadIdx.x < 32) {
+    if (blk0 && publish && threadIdx.x < 32) {
         double nsum = 0.0;
         for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += s_st[3 * i];
 #pragma unroll
@@ -978,13 +994,7 @@ __device__ void small_group_post(const AdvParams& p, uint8_t* smem, int64_t G, i
             if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
         }
     }
-    __syncthreads();
-    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
-        const int32_t ti = a.tid[g];
-        p.atilde[g] = (ti >= 0 && ti < p.n_tasks)
-                          ? (float)((a.ah[g] - s_task[ti].x) / s_task[ti].y)
-                          : 0.f;
-    }
+    __syncthreads();  // s_task visible to the staging
 }
 
 __device__ __forceinline__ void small_range(const AdvParams& p, int64_t& c_lo, int64_t& c_hi) {
@@ -1000,14 +1010,14 @@ __device__ __forceinline__ void small_count(const AdvParams& p, uint8_t* smem, W
     const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
     int32_t warp_total = 0;
     // the offsets are staged while the block's first mask copies are in flight
-    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false, false,
+    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false,
                     [&]() { stage_all_offsets(p, smem); });
     chunk_bases(p, c_lo, c_hi, s_w);
 }
 
 // phase C of a streaming block.  fused (single kernel, no communicator): the mask is still in
-// the ring and A~ comes from the statistics block; else (second launch after the all-reduce)
-// everything is reloaded and Eq.1 evaluated here.
+// the ring and s_task was computed by small_stats; else (second launch after the all-reduce)
+// everything is reloaded and mu, sigma come from the reduced stats.
 __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
                                             int32_t* s_pre, int32_t* s_w, bool fused) {
     int64_t c_lo, c_hi;
@@ -1016,7 +1026,7 @@ __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, W
     if (fused) block_prefix_smem(p.blk_chunk, gridDim.x, s_pre, s_w);
     else load_task_params(p, smem, s_pre, s_w);
     int32_t dummy = 0;
-    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused, fused);
+    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused);
 }
 
 // ------------------------------------------------------------------ large driver
@@ -1060,7 +1070,7 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
         }
         if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     };
-    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total, false, false, validate);
+    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total, false, validate);
     chunk_bases(p, c_lo, c_hi, s_w);
     grid.sync();
     phase_mark(2);
@@ -1324,9 +1334,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvPara
     }
     grid.sync();
     phase_mark(1);
-    if (blockIdx.x == 0) small_group_post(p, smem, gridDim.x, ss.s_w, true);
-    grid.sync();
-    phase_mark(2);
+    small_stats(p, smem, gridDim.x, ss.s_w, true, false);
     if (blockIdx.x != 0) small_apply(p, smem, r, ss.s_pre, ss.s_w, true);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
@@ -1340,7 +1348,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvPa
         small_count(p, smem, r, ss.s_w);
     }
     grid.sync();
-    if (blockIdx.x == 0) small_group_post(p, smem, gridDim.x, ss.s_w, false);
+    if (blockIdx.x == 0) small_stats(p, smem, gridDim.x, ss.s_w, false, true);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1420,7 +1428,6 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.blk_cnt = reinterpret_cast<int32_t*>(ws + w.blk_cnt);
     p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
-    p.atilde = reinterpret_cast<float*>(ws + w.atilde);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
     p.stats = reinterpret_cast<double*>(ws + w.stats);
     p.meta = reinterpret_cast<int64_t*>(ws + w.meta);

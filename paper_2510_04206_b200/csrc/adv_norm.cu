@@ -409,7 +409,6 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.grp_start = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.members = p.take(sizeof(int32_t) * (size_t)(n_traj + 1));
     w.adv_hat = p.take(sizeof(double) * (size_t)(n_traj + 1));
-    w.atilde = p.take(sizeof(float) * (size_t)(n_traj + 1));
     w.grp_task = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.grp_nsq = p.take(sizeof(double) * 3 * (size_t)(n_groups + 1));
     w.chunk_first = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));

@@ -30,7 +30,6 @@ struct WsPlan {
 struct AdvWs {
     size_t n_g, chunk_cnt, chunk_base, grp_cnt, grp_start, grp_fill, members;  // int32
     size_t adv_hat;                                                               // double
-    size_t atilde;    // float [n_traj] A~_g (small cooperative driver, no communicator)
     size_t grp_task;  // int32 [n_groups] task of each group (cooperative path)
     size_t grp_nsq;   // double [3*n_groups] per-group (N, S, Q) partials (cooperative path)
     size_t chunk_first;  // int32 [n_chunks] trajectory holding each chunk's first token
