@@ -243,6 +243,13 @@ def run_native(args, cfg, world, rank, local_rank):
     status = int(step.status.item())
     ms = max_over_ranks(ms)
     value = T_global / (ms / 1e3)
+    imbalance = None
+    if world > 1:  # per-rank load: max / mean of the masked rows (LPT group sharding)
+        mx = max_over_ranks(float(T_eff_local))
+        tot = torch.tensor([float(T_eff_local)], dtype=torch.float64,
+                           device="cpu" if shared else dev)
+        dist.all_reduce(tot)
+        imbalance = mx / (float(tot.item()) / world)
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region
     e2e = None
@@ -324,6 +331,7 @@ def run_native(args, cfg, world, rank, local_rank):
                 "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
                 "peak_kind": f"{pk['src']} sustained bf16 (kernel timed inside a long step)",
                 "frac_of_burst": achieved / pk["bf16"],
+                "frac_of_datasheet": achieved / 2250.0,  # nominal dense bf16 per B200
                 "flop_per_launch": flop, "traffic": traffic_from_profiles(args.config, dom_name)}
     else:
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": None, "peak": pk["hbm"],
@@ -341,6 +349,7 @@ def run_native(args, cfg, world, rank, local_rank):
                    "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
         "masked_tokens_per_s": T_eff_global / (ms / 1e3),
+        "rank_imbalance_masked_rows": imbalance,
         "step_tflops_algorithmic": step_flop / (ms / 1e3) / 1e12,
         "clocks": clocks, "e2e": e2e,
         "gpu_launches": int(launches_per_step * args.steps),
@@ -480,7 +489,14 @@ def cpu_baseline(cfg, gb, seconds=15.0, rows=None):
     t_loss = time.perf_counter() - t1
     n_eff = int(an["n_mask"])
     t_step = t_adv + t_loss / rows * n_eff
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": int(gb["T"]) / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu, "host_cpus": os.cpu_count(),
             "sample": f"adv-norm on the full batch ({t_adv:.3f} s) + loss fwd+bwd of {rows} "
                       f"masked tokens at full V={V}, d={d} ({t_loss:.2f} s), extrapolated to "
                       f"{n_eff} masked tokens"}

@@ -340,8 +340,11 @@ __global__ void __launch_bounds__(MERGE_THREADS)
         if (threadIdx.x == 0) {
             float Lm1 = 0.f;
             for (int w = 0; w < MERGE_THREADS / 32; ++w) Lm1 += s_red[w];
-            const float lse = M + log1pf(Lm1);
-            const float logp = zy[p] - lse;
+            // log p_y = (z_y - M) - log1p(L'), not z_y - lse: lse = M + log1p(L') rounds
+            // log1p(L') to the ulp of M (~2e-6 at |z| ~ 24), which is the whole of 1 - p_y when
+            // p_y -> 1 (the onehot-cancellation rows)
+            const float l1 = log1pf(Lm1);
+            const float logp = (zy[p] - M) - l1;
             const float A = adv_c[p];
             const float rho = expf(logp - old_c[p]);
             const float lo = 1.f - eps_lo, hi = 1.f + eps_hi;
@@ -366,17 +369,18 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             row_clip[p] = clipped ? 1 : 0;
             row_kl[p] = (float)kl;
             if (logp_out) logp_out[idx[p]] = logp;
-            s_bc[0] = lse;
+            s_bc[0] = l1;
             s_bc[1] = c_t;
             // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
             s_bc[2] = c_t * expm1f(logp);
         }
         __syncthreads();
-        const float lse = s_bc[0];
+        const float l1 = s_bc[0];
         c_t = s_bc[1];
         const float g_y = s_bc[2];
+        // exp(m_j - lse) = exp((m_j - M) - log1p(L'))
         for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
-            s_f[j] = c_t * ex2_approx((pr[j].x - lse) * LOG2E);
+            s_f[j] = c_t * ex2_approx(((pr[j].x - M) - l1) * LOG2E);
         __syncthreads();
         const int32_t y = tgt_c[p];
         // 16-byte vectors, MERGE_UNROLL loads in flight per thread before any store
@@ -519,14 +523,23 @@ __global__ void __launch_bounds__(256)
                   const int64_t* __restrict__ off, int32_t n_traj,
                   const int32_t* __restrict__ n_g, const int64_t* __restrict__ nseq_dev,
                   float* __restrict__ w_c, float* __restrict__ ref_c, int32_t n_fchunks,
-                  int64_t* __restrict__ fbnd) {
+                  float fratio, int64_t* __restrict__ fbnd) {
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
     if (blockIdx.x == 0 && threadIdx.x <= n_fchunks) {
-        // forward row chunks [fbnd[c], fbnd[c+1]): 256-row aligned, the last ends at rows
-        const int64_t per = (rows + n_fchunks - 1) / n_fchunks;
-        const int64_t R = (per + 255) / 256 * 256;
-        fbnd[threadIdx.x] = min(rows, (int64_t)threadIdx.x * R);
+        // forward row chunks [fbnd[c], fbnd[c+1]): 256-row aligned, the last ends at rows;
+        // geometric sizes (chunk c+1 = fratio x chunk c) keep the merge of the last chunk,
+        // the one that cannot overlap a forward chunk, short
+        const int c = threadIdx.x;
+        double frac;
+        if (fratio == 1.f) {
+            frac = (double)c / n_fchunks;
+        } else {
+            const double r = fratio;
+            frac = (1.0 - pow(r, (double)c)) / (1.0 - pow(r, (double)n_fchunks));
+        }
+        const int64_t b = (int64_t)ceil(frac * (double)rows / 256.0) * 256;
+        fbnd[c] = c == n_fchunks ? rows : min(rows, b);
     }
     const double nseq = nseq_dev ? (double)*nseq_dev : 0.0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < rows;
@@ -602,6 +615,17 @@ static int comm_reserve_sms() {
 static int fwd_chunks() {
     static int v = -1;
     if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 4), MAX_FWD_CHUNKS);
+    return v;
+}
+// size ratio of consecutive forward row chunks (AGENTRL_FWD_RATIO, default 1 = equal; 0.5 and
+// 0.35 shorten the last, un-overlapped merge but slow the forward as much: same step time)
+static float fwd_ratio() {
+    static float v = -1.f;
+    if (v < 0.f) {
+        const char* e = getenv("AGENTRL_FWD_RATIO");
+        const float x = e ? (float)atof(e) : 0.f;
+        v = (x > 0.f && x <= 1.f) ? x : 1.f;
+    }
     return v;
 }
 struct ForkStreams {
@@ -696,7 +720,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
             rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
             fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
-            fx ? fx->nseq : nullptr, w_c, ref_c, n_fc, fbnd);
+            fx ? fx->nseq : nullptr, w_c, ref_c, n_fc, fwd_ratio(), fbnd);
         count_launch(2);
         AG_CUDA(cudaGetLastError());
     }
@@ -890,7 +914,8 @@ __global__ void __launch_bounds__(256)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) Lm1 += __shfl_xor_sync(0xffffffffu, Lm1, o);
-        const float lse = M + log1pf(Lm1);
+        const float l1 = log1pf(Lm1);
+        const float lse = M + l1;
         float Ez = 0.f;
         for (int j = lane; j < n_tiles; j += 32) {
             const float4 t = pr[j];
@@ -899,7 +924,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) Ez += __shfl_xor_sync(0xffffffffu, Ez, o);
         if (lane == 0) {
-            const float logp = zy[p] - lse;
+            const float logp = (zy[p] - M) - l1;  // see k_merge_g
             const int64_t t = idx[p];
             logp_out[t] = logp;
             if (ent_out) ent_out[t] = fmaxf(lse - Ez, 0.f);

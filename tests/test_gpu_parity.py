@@ -216,9 +216,21 @@ def test_determinism(ag):
         assert torch.equal(a, bb)
 
 
-def _full_size_case(ag, cfg_name, n_spot=24):
+def _full_size_case(ag, cfg_name, n_spot=24, shard_of=None):
+    """shard_of = (world, rank): the rank's LPT shard of the global batch, run as
+    one single-GPU batch -- the per-rank problem size of the multi-GPU configs"""
+    import dataclasses
     cfg = synth.CONFIGS[cfg_name]
     b = synth.make_structure(cfg)
+    if shard_of is not None:
+        world, rank = shard_of
+        off = b["traj_offsets"]
+        cs = np.concatenate([[0], np.cumsum(b["loss_mask"].astype(np.int64))])
+        ng = cs[off[1:]] - cs[off[:-1]]
+        rog = synth.shard_groups_lpt(np.bincount(b["group_id"], weights=ng,
+                                                 minlength=b["n_groups"]), world)
+        b = {k: v for k, v in synth.shard_batch(b, rog, rank).items() if k != "token_index"}
+        cfg = dataclasses.replace(cfg, T=int(b["T"]))
     hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
     old = synth.make_old_logp_free(cfg.T, 99)
     step = _run_step(ag, cfg, b, hb, Wb, y, old)
@@ -273,3 +285,10 @@ def test_full_size_qwen7b_spot_rows(ag):
 @pytest.mark.slow
 def test_full_size_glm9b_spot_rows(ag):
     _full_size_case(ag, "glm9b", n_spot=16)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg_name", ["qwen32b", "skew14b"])
+def test_full_size_rank_shard_spot_rows(ag, cfg_name):
+    """the 8-GPU configs at their per-rank size and head dims (d=5120, V=152064)"""
+    _full_size_case(ag, cfg_name, n_spot=12, shard_of=(8, 0))
