@@ -218,6 +218,9 @@ def run_native(args, cfg, world, rank, local_rank):
     def one_step():
         step(bd, hid, W, target, old)
 
+    # part 1 alone, timed before the power-heavy GEMM steps (the GPU is not yet clocked down
+    # by the power cap; a latency-bound kernel scales with the SM clock)
+    adv = adv_norm_timing(ag, bd, lb, dev, peaks()["hbm"]) if rank == 0 else None
     for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
         one_step()
     torch.cuda.synchronize()
@@ -336,7 +339,6 @@ def run_native(args, cfg, world, rank, local_rank):
     else:
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": None, "peak": pk["hbm"],
                 "unit": "GB/s", "frac": None, "traffic": None}
-    adv = adv_norm_timing(ag, bd, lb, dev, pk["hbm"]) if rank == 0 else None
     step_flop = 6.0 * T_eff_global * V * d
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

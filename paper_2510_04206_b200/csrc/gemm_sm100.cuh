@@ -27,7 +27,7 @@
 // Epilogues (row r = output row; each CTA owns 128 rows of the tile):
 //   EPI_FWD   logits z = s*acc: per (row, 256-col tile) max m and l' = sum exp(z-m) - 1 over
 //             valid columns (the first max element is left out of the sum: no cancellation
-//             later), P~ = exp(z - m) stored as fp16, z_y gathered when the row's target falls
+//             later), P~ = exp(z - m) stored as bf16, z_y gathered when the row's target falls
 //             in the tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
 //   EPI_GRADH grad_hidden[idx[r], :] = bf16(s * acc)   (scatter to the original token row)
 //   EPI_GRADW grad_W[r, :] = s * acc (fp32); zeros if the (dynamic) K extent is 0.
@@ -80,7 +80,8 @@ struct GemmArgs {
     float scale;           // logit_scale s
     // EPI_FWD
     const int32_t* tgt;  // [rows] target token of each compacted row
-    __half* P;           // [rows, ldP] exp(z - m), fp16
+    __nv_bfloat16* P;    // [rows, ldP] exp(z - m), bf16: fp32's exponent range, so entries far
+                         // below the tile max survive (p_y -> 1 rows)
     int64_t ldP;
     float2* part;   // [rows, n_tiles] (m, l')             (EPI_FWD)
     float4* part4;  // [rows, n_tiles] (m, l', u, 0)       (EPI_LOGP)
@@ -459,7 +460,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     float l = 0.f, u = 0.f;  // u (EPI_LOGP): sum exp(z - m) * z
                     bool max_seen = false;
                     const float mb = m * LOG2E;
-                    __half* prow = kStoreP ? p.P + (row_ok ? row : 0) * p.ldP + col0 : nullptr;
+                    __nv_bfloat16* prow =
+                        kStoreP ? p.P + (row_ok ? row : 0) * p.ldP + col0 : nullptr;
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
                         tmem_ld_32x32b_x32(taddr + c * 32, r);
@@ -482,10 +484,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             for (int j = 0; j < 32; j += 8) {
                                 if (c * 32 + j < ncol) {
                                     uint4 v;
-                                    v.x = pack_half2(e[j + 0], e[j + 1]);
-                                    v.y = pack_half2(e[j + 2], e[j + 3]);
-                                    v.z = pack_half2(e[j + 4], e[j + 5]);
-                                    v.w = pack_half2(e[j + 6], e[j + 7]);
+                                    v.x = pack_bf162(e[j + 0], e[j + 1]);
+                                    v.y = pack_bf162(e[j + 2], e[j + 3]);
+                                    v.z = pack_bf162(e[j + 4], e[j + 5]);
+                                    v.w = pack_bf162(e[j + 6], e[j + 7]);
                                     *reinterpret_cast<uint4*>(prow + c * 32 + j) = v;
                                 }
                             }

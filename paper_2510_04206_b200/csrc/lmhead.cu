@@ -5,7 +5,7 @@
 //   K4 k_gather       compacted rows: H[p] = hidden[idx[p]], target/old/adv per row; rows
 //                     [T_eff, pad64) zeroed (they are inside GEMM3's K range)
 //   K5 gemm<FWD>      z = s * H W^T on tcgen05; epilogue: per (row, 256-col tile) max m and
-//                     l = sum exp(z - m), P~ = exp(z - m) -> fp16 [rows, V], z_y gathered
+//                     l = sum exp(z - m), P~ = exp(z - m) -> bf16 [rows, V], z_y gathered
 //   K6 k_merge_g      per row: lse = logsumexp over tiles, logp, rho, PPO-clip term,
 //                     c = unclipped ? rho*A/N : 0; rewrites the row in place as
 //                     G = bf16(c * (P~ * exp(m_tile - lse) - [v == y]))
@@ -14,7 +14,7 @@
 //   C3                NCCL all-reduce of grad_W on a side stream, overlapped with K8
 //   K8 gemm<GRADH>    grad_hidden[idx] = s * G W  (A = G K-major, B = W MN-major, K = V)
 //
-// Executed tensor work is 6 * T_eff * V * d FLOP (three GEMMs; no recompute: the fp16 P~
+// Executed tensor work is 6 * T_eff * V * d FLOP (three GEMMs; no recompute: the bf16 P~
 // written by the forward epilogue replaces the second logits GEMM).  See DESIGN.md.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
               const int32_t* __restrict__ idx, float eps_lo, float eps_hi,
               const float* __restrict__ w_c /* per-row weight w_t */,
               const float* __restrict__ ref_c /* per-row ref log-prob or null */,
-              float kl_beta, uint16_t* __restrict__ PG /* fp16 P~ in, bf16 G out, [rows, V] */,
+              float kl_beta, uint16_t* __restrict__ PG /* bf16 P~ in, bf16 G out, [rows, V] */,
               double* __restrict__ row_term /* w (-term + beta KL) */,
               float* __restrict__ row_rho, float* __restrict__ row_logp,
               int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
@@ -386,11 +386,11 @@ __global__ void __launch_bounds__(MERGE_THREADS)
         // 16-byte vectors, MERGE_UNROLL loads in flight per thread before any store
         auto conv = [&](const uint4& in, int v0) -> uint4 {
             const float f = s_f[v0 >> 8];  // 256-column tiles
-            const __half2* h2 = reinterpret_cast<const __half2*>(&in);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&in);
             float g[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float2 x = __half22float2(h2[k]);
+                const float2 x = __bfloat1622float2(h2[k]);
                 g[2 * k] = f * x.x;
                 g[2 * k + 1] = f * x.y;
             }
@@ -766,7 +766,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         }
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
-        g.P = reinterpret_cast<__half*>(PG);
+        g.P = reinterpret_cast<__nv_bfloat16*>(PG);
         g.ldP = V;
         g.part = part;
         g.n_tiles = w.n_tiles;

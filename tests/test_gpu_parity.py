@@ -159,6 +159,52 @@ def test_policy_loss_parity(ag, cfg_name, eps, scale):
     assert s[3] == an["n_mask"]
 
 
+def test_onehot_cancellation_rows(ag):
+    """Rows with p_y -> 1 at large |z| (z_y ~ 20..32, 1 - p_y ~ 1e-9 .. 1e-4) and a large
+    unclipped coefficient (A < 0, rho = e^3): grad_hidden = c sum_v (p_v - [v=y]) W_v is a
+    difference of nearly equal terms.  Checked per ROW against the oracle (the tensor-level
+    metric would hide it).  Two failure modes this pins: an lse rounded to the ulp of z_y
+    (~2e-6) loses all of 1 - p_y; an fp16 P~ flushes the target tile's other entries
+    (exp(z - z_y) < 6e-8) to zero.  The range stops at 1 - p_y ~ 1e-9: below ~1e-12 the fp64
+    oracle's own p_y - 1 = exp(z_y - lse) - 1 cancels (4% at 8e-14, checked against 80-bit
+    long double), so it would no longer be the arbiter."""
+    rng = np.random.default_rng(2510_04206 + 77)
+    T, d, V = 256, 64, 512
+    Wf = rng.standard_normal((V, d)).astype(np.float32) / np.float32(np.sqrt(d))
+    Wb = synth.to_bf16_bits(Wf)
+    W = f64(Wb)
+    y = rng.integers(0, V, T).astype(np.int32)
+    a = rng.uniform(20.0, 32.0, T)  # target logit
+    wy = W[y]
+    h = a[:, None] * wy / (wy * wy).sum(1, keepdims=True) + 0.05 * rng.standard_normal((T, d))
+    hb = synth.to_bf16_bits(h.astype(np.float32))
+    h = f64(hb)
+    mask = np.ones(T, np.uint8)
+    lp = oracle.logprob(h, W, y, mask)
+    assert lp.max() < -1e-10 and lp.min() > -1e-3  # p_y near 1 on every row, within fp64 reach
+    old = (lp - 3.0).astype(np.float32)  # rho = e^3 > 1 + eps, A < 0: not clipped
+    adv = np.full(T, -1.0, np.float32)
+    ref = oracle.policy_loss_rows(h, W, y, adv.astype(np.float64), old.astype(np.float64), T)
+    assert not ref["clipped"].any()
+    ws = ag.alloc_workspace(ag.agentrl_policy_loss_workspace_size(T, d, V))
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    logp = torch.full((T,), float("nan"), device="cuda")
+    gh = torch.full((T, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    gw = torch.full((V, d), float("nan"), device="cuda")
+    nm = torch.tensor([T], dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    args = ag.make_loss_args(T, bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32),
+                             t(old, torch.float32), t(mask, torch.uint8),
+                             adv_tok=t(adv, torch.float32), n_mask_global=nm)
+    rc = ag.agentrl_policy_loss_fwd_bwd(args, ag.make_loss_out(loss, gh, gw, logp), ws, None, st)
+    assert rc == 0, ag.status_string(rc)
+    torch.cuda.synchronize()
+    got = gh.float().cpu().numpy()
+    want = ref["grad_hidden"]
+    row_err = np.abs(got - want).max(1) / np.abs(want).max(1)
+    assert row_err.max() <= 2e-2, (row_err.max(), -lp[np.argmax(row_err)])
+
+
 def _run_step(ag, cfg, b, hb, Wb, y, old, eps=(0.2, 0.2), scale=1.0):
     step = ag.Step(cfg.T, len(b["task_id"]), b["n_groups"], b["n_tasks"], cfg.d, cfg.V,
                    eps_low=eps[0], eps_high=eps[1], logit_scale=scale)
