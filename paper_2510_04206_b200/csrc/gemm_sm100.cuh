@@ -457,7 +457,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     // relative precision when the tile max dominates -- p_y close to 1), z_y
                     const int32_t y = row_ok ? p.tgt[row] : -1;
                     const int32_t yl = y - col0;
-                    float l = 0.f, u = 0.f;  // u (EPI_LOGP): sum exp(z - m) * z
+                    // u (EPI_LOGP): sum exp(z - m) (m - z) >= 0 -- nonnegative terms, so the
+                    // entropy of a peaked row is not a difference of two ~|z| numbers
+                    float l = 0.f, u = 0.f;
                     bool max_seen = false;
                     const float mb = m * LOG2E;
                     __nv_bfloat16* prow =
@@ -476,7 +478,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             max_seen |= is_max;
                             if (is_max) e[j] = 1.f;
                             l += is_max ? 0.f : e[j];
-                            if constexpr (!kStoreP) u = fmaf(e[j], ok ? z : 0.f, u);
+                            if constexpr (!kStoreP) u = fmaf(e[j], ok ? m - z : 0.f, u);
                             if (c * 32 + j == yl && row_ok) p.zy[row] = z;
                         }
                         if (kStoreP && row_ok) {

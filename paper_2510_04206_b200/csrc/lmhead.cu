@@ -882,10 +882,12 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
 // agentrl_logprob_fwd: forward-only token log-probs and entropies (the
 // trainer's recomputation of pi_old / pi_ref log-probs, and the entropy that DAPO
 // monitors).  Same compaction / gather / forward GEMM as part 2, with the EPI_LOGP
-// epilogue (no P~ store: per (row, tile) max m, l' = sum exp(z-m) - 1, u = sum exp(z-m) z),
-// then one warp per row:
-//   lse = M + log1p(L'),  logp = z_y - lse,  entropy = lse - sum_j exp(m_j - lse) u_j
-//   (= -sum_v p_v log p_v).
+// epilogue (no P~ store: per (row, tile) max m, l' = sum exp(z-m) - 1,
+// u = sum exp(z-m) (m - z) >= 0), then one warp per row, with l1 = log1p(L'):
+//   logp = (z_y - M) - l1,
+//   entropy = -sum_v p_v log p_v = sum_v p_v (lse - z_v)
+//           = l1 + sum_j exp((m_j - M) - l1) [(M - m_j)(1 + l'_j) + u_j]
+//   (every term >= 0: exact to fp32 rounding even for p_y -> 1 rows).
 namespace agentrl {
 
 __global__ void __launch_bounds__(256)
@@ -915,19 +917,18 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) Lm1 += __shfl_xor_sync(0xffffffffu, Lm1, o);
         const float l1 = log1pf(Lm1);
-        const float lse = M + l1;
-        float Ez = 0.f;
+        float Hs = 0.f;  // sum_j w_j [(M - m_j)(1 + l'_j) + u_j]
         for (int j = lane; j < n_tiles; j += 32) {
             const float4 t = pr[j];
-            Ez += expf(t.x - lse) * t.z;
+            Hs += expf((t.x - M) - l1) * fmaf(M - t.x, 1.f + t.y, t.z);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) Ez += __shfl_xor_sync(0xffffffffu, Ez, o);
+        for (int o = 16; o > 0; o >>= 1) Hs += __shfl_xor_sync(0xffffffffu, Hs, o);
         if (lane == 0) {
             const float logp = (zy[p] - M) - l1;  // see k_merge_g
             const int64_t t = idx[p];
             logp_out[t] = logp;
-            if (ent_out) ent_out[t] = fmaxf(lse - Ez, 0.f);
+            if (ent_out) ent_out[t] = l1 + Hs;
             if (!isfinite(logp)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
         }
     }

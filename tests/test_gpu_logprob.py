@@ -89,3 +89,26 @@ def test_logprob_full_size_spot_rows(ag):
     lr, er = oracle.logprob_entropy(f64(hb[rows]), f64(Wb), y[rows], np.ones(24, np.uint8))
     assert np.abs(lp[rows] - lr).max() <= 1e-3
     assert np.abs(ent[rows] - er).max() <= 1e-3
+
+
+def test_entropy_peaked_rows(ag):
+    """p_y -> 1 rows (z_y ~ 20..32 above a random bulk; 1 - p_y ~ 1e-9 .. 1e-4): the entropy is
+    tiny (~1e-8 .. 1e-3) and must come out to a RELATIVE accuracy, not only the 1e-3 absolute
+    bar -- lse - E[z] would be a difference of two ~z_y numbers."""
+    rng = np.random.default_rng(2510_04206 + 78)
+    T, d, V = 256, 64, 512
+    Wf = rng.standard_normal((V, d)).astype(np.float32) / np.float32(np.sqrt(d))
+    Wb = synth.to_bf16_bits(Wf)
+    W = f64(Wb)
+    y = rng.integers(0, V, T).astype(np.int32)
+    a = rng.uniform(20.0, 32.0, T)
+    wy = W[y]
+    h = a[:, None] * wy / (wy * wy).sum(1, keepdims=True) + 0.05 * rng.standard_normal((T, d))
+    hb = synth.to_bf16_bits(h.astype(np.float32))
+    mask = np.ones(T, np.uint8)
+    lp_ref, ent_ref = oracle.logprob_entropy(f64(hb), W, y, mask)
+    assert ent_ref.max() < 1e-2 and ent_ref.min() > 0
+    lp, ent, st = _run(ag, hb, Wb, y, mask)
+    assert st == 0
+    rel = np.abs(ent - ent_ref) / ent_ref
+    assert rel.max() <= 1e-2, (rel.max(), ent_ref[np.argmax(rel)])
