@@ -11,13 +11,14 @@ import sys
 from collections import OrderedDict
 
 sys.path.insert(0, os.path.dirname(__file__))
-from summarize_ncu_launches import short  # noqa: E402
+from summarize_ncu_launches import STEP_START, short  # noqa: E402
 
 BENCH_NAME = {"gemm_sm100_pair_kernel<FWD>": "gemm_fwd", "gemm_sm100_kernel<FWD>": "gemm_fwd",
               "gemm_sm100_pair_kernel<GRADW>": "gemm_grad_W",
               "gemm_sm100_kernel<GRADW>": "gemm_grad_W",
               "gemm_sm100_pair_kernel<GRADH>": "gemm_grad_hidden",
-              "gemm_sm100_kernel<GRADH>": "gemm_grad_hidden", "k_adv_coop_all": "k_adv_coop"}
+              "gemm_sm100_kernel<GRADH>": "gemm_grad_hidden", "k_adv_coop_all": "k_adv_coop",
+              "k_adv_small_all": "k_adv_coop", "k_adv_large_all": "k_adv_coop"}
 
 
 def main(path, config):
@@ -31,11 +32,13 @@ def main(path, config):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r["Metric Unit"], 1)
         launches[key] = launches.get(key, 0.0) + float(r["Metric Value"].replace(",", "")) * scale
     seq = [(k[1], v) for k, v in launches.items() if not k[1].startswith("other:")]
-    starts = [i for i, (n, _) in enumerate(seq) if n in ("k_adv_coop_all", "k_count")]
-    # the first step: from its advantage normalisation to the next one (bench.py's adv-norm
-    # latency probe launches it again after the timed steps)
-    if starts:
-        seq = seq[starts[0]:starts[1] if len(starts) > 1 else None]
+    starts = [i for i, (n, _) in enumerate(seq) if n in STEP_START]
+    # the first fused step: from an advantage normalisation followed by GEMMs to the next one
+    # (bench.py's adv-norm latency probes launch it alone before the steps)
+    segs = [seq[a:b] for a, b in zip(starts, starts[1:] + [len(seq)])]
+    segs = [sg for sg in segs if any(n.startswith("gemm") for n, _ in sg)]
+    if segs:
+        seq = segs[0]
     out = OrderedDict()
     for n, b in seq:
         name = BENCH_NAME.get(n, n)

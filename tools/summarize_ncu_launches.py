@@ -7,6 +7,12 @@ import sys
 from collections import OrderedDict
 
 
+# kernels that start a fused step (the advantage normalisation; bench.py's adv-norm latency
+# probes launch them too, without GEMMs after them)
+STEP_START = ("k_adv_coop_all", "k_adv_small_all", "k_adv_large_all", "k_adv_small_stats",
+              "k_adv_large_stats", "k_count")
+
+
 def short(name):
     m = re.search(r"agentrl::(\w+)", name)
     if m:
@@ -30,7 +36,7 @@ def main(path, last_steps=None):
     if last_steps:
         # the advantage normalisation (k_adv_coop_all, or k_count on the 3-kernel path)
         # starts each step
-        starts = [i for i, r in enumerate(ours) if r[0] in ("k_adv_coop_all", "k_count")]
+        starts = [i for i, r in enumerate(ours) if r[0] in STEP_START]
         segs = [ours[a:b] for a, b in zip(starts, starts[1:] + [len(ours)])]
         segs = [sg for sg in segs if any("gemm" in r[0] for r in sg)]  # fused steps only
         if len(segs) >= last_steps:
