@@ -56,7 +56,7 @@ extern "C" {
 
 /* ---- device status bits (OR-ed into *d_status) -------------------------- */
 #define AGENTRL_ST_BAD_TARGET 1          /* a masked token's target not in [0,V) */
-#define AGENTRL_ST_NONFINITE 2           /* non-finite loss / logp ("abort") */
+#define AGENTRL_ST_NONFINITE 2           /* non-finite loss / logp / ratio ("abort") */
 #define AGENTRL_ST_BAD_OFFSETS 4         /* traj_offsets not 0..T nondecreasing */
 #define AGENTRL_ST_GROUP_SPANS_TASKS 8   /* a group's members have different task_id */
 #define AGENTRL_ST_GROUP_TOO_SMALL 16    /* a group has one trajectory */
@@ -131,6 +131,8 @@ int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok
  *   grad_hidden = logit_scale * G W        (rows of unmasked tokens are 0)
  *   grad_W      = logit_scale * G^T hidden (summed over ranks if grad_W_mode=1; the rank's
  *                 row shard summed if grad_W_mode=2)
+ * Empty batch: T may be 0; the per-token pointers may then be NULL; the call still writes
+ * loss = 0 and a zero grad_W and sets AGENTRL_ST_NO_TOKENS (as it does whenever N == 0).
  * Shapes: d % 64 == 0, V % 8 == 0, 1 <= V.  Arithmetic: bf16 operands on
  * tcgen05 tensor cores with fp32 accumulation; softmax statistics fp32; loss
  * and statistics reductions fp64.

@@ -188,16 +188,18 @@ static int check_batch(const agentrl_batch* b, double eps_std) {
 }
 
 static int check_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, bool fused) {
-    if (!a || !o || !o->loss || !o->grad_hidden || !o->grad_W) return AGENTRL_ERR_INVALID_ARG;
+    if (!a || !o || !o->loss || !o->grad_W || (a->T > 0 && !o->grad_hidden))
+        return AGENTRL_ERR_INVALID_ARG;
     if (!(a->clip_eps_low >= 0.f && a->clip_eps_low < 1.f) || !(a->clip_eps_high >= 0.f) ||
         !(a->logit_scale > 0.f))
         return AGENTRL_ERR_INVALID_ARG;
     if (a->T < 0 || a->T >= (int64_t)1 << 31 || a->d <= 0 || a->d % 64 != 0 || a->V < 8 ||
         a->V % 8 != 0)
         return AGENTRL_ERR_SHAPE;
-    if (!a->hidden || !a->W_head || !a->target || !a->old_logp || !a->loss_mask)
+    // per-token arrays may be empty (null) when T == 0
+    if (!a->W_head || (a->T > 0 && (!a->hidden || !a->target || !a->old_logp || !a->loss_mask)))
         return AGENTRL_ERR_INVALID_ARG;
-    if (!fused && (!a->adv_tok || !a->n_mask_global)) return AGENTRL_ERR_INVALID_ARG;
+    if (!fused && ((a->T > 0 && !a->adv_tok) || !a->n_mask_global)) return AGENTRL_ERR_INVALID_ARG;
     if (!aligned(a->hidden, 16) || !aligned(a->W_head, 16) || !aligned(o->grad_hidden, 16) ||
         !aligned(o->grad_W, 16))
         return AGENTRL_ERR_SHAPE;
@@ -376,7 +378,7 @@ const char* agentrl_status_string(int code) {
         case AGENTRL_ERR_NCCL: return "NCCL error or NCCL unavailable";
         case AGENTRL_ERR_UNSUPPORTED: return "device is not sm_100 (B200)";
         case AGENTRL_ST_BAD_TARGET: return "target token id outside [0, V)";
-        case AGENTRL_ST_NONFINITE: return "non-finite loss or log-prob";
+        case AGENTRL_ST_NONFINITE: return "non-finite loss, log-prob or ratio";
         case AGENTRL_ST_BAD_OFFSETS: return "trajectory offsets inconsistent with T";
         case AGENTRL_ST_GROUP_SPANS_TASKS: return "a group spans tasks (or ids out of range)";
         case AGENTRL_ST_GROUP_TOO_SMALL: return "a group has fewer than 2 trajectories";

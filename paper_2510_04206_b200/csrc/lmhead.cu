@@ -468,7 +468,10 @@ __global__ void __launch_bounds__(1024)
         }
         const double loss = N > 0.0 ? A : 0.0;
         *loss_out = loss;
-        if (!isfinite(loss) || !isfinite(Cc)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
+        // non-finite loss, log-probs or ratios (e.g. a non-finite behaviour log-prob, whose
+        // ratio the clamp would otherwise hide from the loss)
+        if (!isfinite(loss) || !isfinite(Cc) || !isfinite(B)) atomicOr(d_status, AGENTRL_ST_NONFINITE);
+        if (!(N > 0.0)) atomicOr(d_status, AGENTRL_ST_NO_TOKENS);  // S:204 (R16)
         if (stats_out) {
             const double r = rows > 0 ? (double)rows : 1.0;
             stats_out[0] = E / r;
