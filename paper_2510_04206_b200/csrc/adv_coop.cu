@@ -491,12 +491,15 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     float* s_cadv = reinterpret_cast<float*>(smem + p.lay.cadv) + warp * WCHUNK;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(p.adv_tok) & 15) == 0;
     const bool any_traj = p.n_traj > 0;
+    static_assert((RING & (RING - 1)) == 0, "RING is a power of two");
+    // chunk indices fit in 32 bits (T < 2^31): keep the per-chunk bookkeeping 32-bit
+    const int32_t n_full = (int32_t)(p.T / WCHUNK);  // chunks with all 512 tokens < T
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
     const bool res = resident && n_mine <= RING;  // warp-uniform
     if (ADV_LDGSTS && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
-            const int64_t c = c_lo + warp + (int64_t)s * NWARPS;
-            lane_issue(p, r, s, c, c < c_hi && chunk_full(p, c));
+            const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
+            lane_issue(p, r, s, c, c < c_hi && c < n_full);
         }
     } else if (lane == 0 && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
@@ -514,7 +517,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         if (l - f + 1 > WIN_TRAJ) wlen = WIN_CHUNKS;
     }
     int32_t* s_kc = reinterpret_cast<int32_t*>(smem + p.lay.skc);
-    int64_t kseq = 0;
+    int32_t kseq = 0;
     for (int64_t w0 = c_lo; w0 < c_hi; w0 += wlen) {
         const int64_t w1 = min(c_hi, w0 + wlen);
         // ---- stage the window's trajectories (block-wide)
@@ -553,11 +556,11 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             __syncthreads();
         }
         // ---- this warp's chunks of the window
-        for (int64_t c = w0 + warp; c < w1; c += NWARPS, ++kseq) {
-            const int slot = (int)(kseq % RING);
+        for (int32_t c = (int32_t)w0 + warp; c < w1; c += NWARPS, ++kseq) {
+            const int slot = kseq & (RING - 1);
             uint4 mk;
             if (ADV_LDGSTS && r.on && !res) lane_wait_oldest();  // this chunk's group
-            if (r.on && chunk_full(p, c)) {
+            if (r.on && c < n_full) {
                 if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
                     r.par ^= 1u << slot;
@@ -566,9 +569,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             } else {
                 mk = mask_direct(p, c, lane);
             }
-            const int64_t t0 = c * WCHUNK + lane * 16;
-            const int32_t tc = (int32_t)(c * WCHUNK - w.base);  // chunk start, window-relative
-            const int32_t kc = (any_traj && w.staged) ? s_kc[c - w0] : 0;
+            const int64_t t0 = (int64_t)c * WCHUNK + lane * 16;
+            const int32_t tc = (int32_t)((int64_t)c * WCHUNK - w.base);  // window-relative
+            const int32_t kc = (any_traj && w.staged) ? s_kc[c - (int32_t)w0] : 0;
             if (PH == 0) {
                 int32_t tot = 0;
                 if (any_traj && w.staged) {
@@ -627,7 +630,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                         }
                     }
                 }
-                if (c * WCHUNK < p.T) store_transposed(p, os, c, outv, vec_ok);
+                if (t0 - lane * 16 < p.T) store_transposed(p, os, c, outv, vec_ok);
                 if (p.compact) {
                     __syncwarp();
                     const int32_t wbase = blk_base + p.chunk_base[c];
@@ -640,11 +643,11 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             }
             __syncwarp();
             if (ADV_LDGSTS && r.on && !res) {
-                const int64_t c2 = c + (int64_t)RING * NWARPS;
-                lane_issue(p, r, slot, c2, c2 < c_hi && chunk_full(p, c2));
+                const int32_t c2 = c + RING * NWARPS;
+                lane_issue(p, r, slot, c2, c2 < c_hi && c2 < n_full);
             } else if (lane == 0 && r.on && !res) {
-                const int64_t c2 = c + (int64_t)RING * NWARPS;
-                if (c2 < c_hi && chunk_full(p, c2)) ring_issue(p, r, slot, c2);
+                const int32_t c2 = c + RING * NWARPS;
+                if (c2 < c_hi && c2 < n_full) ring_issue(p, r, slot, c2);
             }
         }
         __syncthreads();
