@@ -708,8 +708,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         nglob_dev = a->n_mask_global;
     }
 
-    // ---- outputs that are defined everywhere
-    AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, stream));
+    // ---- outputs that are defined everywhere (grad_hidden's zero rows: below, beside the
+    // forward when the merge stream exists -- only the grad_hidden GEMM reads it back)
+    if (n_fc <= 1 && T > 0) AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, stream));
     if (o->logp) AG_CUDA(cudaMemsetAsync(o->logp, 0, (size_t)T * sizeof(float), stream));
 
     // ---- K4 gather
@@ -751,6 +752,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         AG_CUDA(cudaEventRecord(fs->fork, stream));
         AG_CUDA(cudaStreamWaitEvent(s_fwd, fs->fork, 0));
         AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->fork, 0));
+        // 2 T d bytes of zeros on the low-priority stream, overlapped with the forward GEMM
+        if (T > 0) AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, s_mrg));
     }
     for (int c = 0; c < n_fc; ++c) {
         GemmArgs g{};
