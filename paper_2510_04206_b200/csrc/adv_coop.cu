@@ -142,6 +142,8 @@ struct AdvParams {
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
     int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
     int32_t* blk_cnt;              // small driver: per-block trajectory counts at [g + block]
+    uint8_t* lanecnt;              // large driver: masked tokens of each lane (16 tokens) of
+                                   // each chunk, [n_chunks * 32]
     double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
     int64_t* meta;
@@ -508,10 +510,13 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         }
     }
     pre();
+    // large driver, phase A: a pure popcount stream (per-lane and per-chunk masked counts);
+    // the per-trajectory counts come later from prefix differences at the trajectory bounds
+    const bool pop = PH == 0 && !small;
     // staging plan: the block's whole range if its trajectories fit, else 64-chunk windows
     int64_t wlen = max(c_hi - c_lo, (int64_t)1);
-    if (wlen > KC_CAP) wlen = WIN_CHUNKS;
-    if (!small && any_traj && c_lo < c_hi) {
+    if (wlen > KC_CAP && !pop) wlen = WIN_CHUNKS;
+    if (!small && !pop && any_traj && c_lo < c_hi) {
         const int32_t f = p.chunk_first[c_lo];
         const int32_t l = c_hi < p.n_chunks ? p.chunk_first[c_hi] : p.n_traj - 1;
         if (l - f + 1 > WIN_TRAJ) wlen = WIN_CHUNKS;
@@ -522,7 +527,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         const int64_t w1 = min(c_hi, w0 + wlen);
         // ---- stage the window's trajectories (block-wide)
         Window w{0, 0, w0 * WCHUNK, s_rel, false};
-        if (any_traj) {
+        if (any_traj && !pop) {
             int32_t f, l;
             if (small) {
                 f = smem_find_in(s_offall, 0, p.n_traj, w0 * WCHUNK);
@@ -572,7 +577,13 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             const int64_t t0 = (int64_t)c * WCHUNK + lane * 16;
             const int32_t tc = (int32_t)((int64_t)c * WCHUNK - w.base);  // window-relative
             const int32_t kc = (any_traj && w.staged) ? s_kc[c - (int32_t)w0] : 0;
-            if (PH == 0) {
+            if (pop) {
+                const int32_t pc = any_traj ? __popc(lane_mask(mk).bits) : 0;
+                p.lanecnt[(int64_t)c * 32 + lane] = (uint8_t)pc;  // 32 contiguous bytes
+                const int32_t tot = __reduce_add_sync(0xffffffffu, pc);
+                if (lane == 0) p.chunk[c] = tot;
+                warp_total += tot;
+            } else if (PH == 0) {
                 int32_t tot = 0;
                 if (any_traj && w.staged) {
                     (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
@@ -652,7 +663,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         }
         __syncthreads();
         // ---- window epilogue (counting): per-trajectory counts out
-        if (PH == 0 && w.staged) {
+        if (PH == 0 && !pop && w.staged) {
             for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
                 if (small) p.blk_cnt[w.f + B + k] = s_aux[k];  // disjoint slot g + block
                 else if (s_aux[k]) atomicAdd(&p.n_g[w.f + k], s_aux[k]);
@@ -1032,6 +1043,27 @@ __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, W
     stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused);
 }
 
+// masked tokens before position t (large driver, after phase A): block prefix + the chunk's
+// local base + the lane counts below t's lane + the masked bytes below t in its lane
+__device__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64_t G, int64_t t) {
+    if (t <= 0) return 0;
+    if (t >= p.T) return s_pre[G];
+    const int64_t c = t / WCHUNK;
+    const int r = (int)(t - c * WCHUNK), L = r >> 4, j = r & 15;
+    int32_t P = s_pre[part_owner(p.n_chunks, c, G)] + p.chunk_base[c];
+    const uint4* lc4 = reinterpret_cast<const uint4*>(p.lanecnt + c * 32);
+    const uint4 a = lc4[0], b = lc4[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // bytes 4q .. 4q+3 = lanes; keep lanes < L
+        const int keep = min(max(L - 4 * q, 0), 4);
+        const uint32_t m = keep == 4 ? 0xffffffffu : ((1u << (8 * keep)) - 1u);
+        P += (int32_t)(((w[q] & m) * 0x01010101u) >> 24);  // byte sum (each byte <= 16)
+    }
+    if (j) P += __popc(lane_mask(mask_direct(p, c, L)).bits & ((1u << j) - 1u));
+    return P;
+}
+
 // ------------------------------------------------------------------ large driver
 __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& r,
                                    cg::grid_group& grid, int32_t* s_w, int32_t* s_pre) {
@@ -1045,7 +1077,6 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
 
     // phase 0: zero scratch; chunk -> first-trajectory table
     if (gtid == 0) p.meta[3] = 0;  // local count of trajectories with masked tokens (n_seq)
-    for (int64_t i = gtid; i < p.n_traj; i += gstride) p.n_g[i] = 0;
     for (int64_t i = gtid; i < p.n_groups; i += gstride) {
         p.grp_cnt[i] = 0;
         p.grp_fill[i] = 0;
@@ -1078,6 +1109,12 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
     grid.sync();
     phase_mark(2);
 
+    // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers)
+    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);
+    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
+        const int64_t a = p.off[g], e = p.off[g + 1];
+        p.n_g[g] = e > a ? masked_before(p, s_pre, G, e) - masked_before(p, s_pre, G, a) : 0;
+    }
     // phase B1: local exclusive scan of K_j over this block's groups; block total
     {
         const int64_t n = j_hi - j_lo;
@@ -1429,6 +1466,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.chunk_base = reinterpret_cast<int32_t*>(ws + w.wchunk_base);
     p.blk_grp = reinterpret_cast<int32_t*>(ws + w.blk_grp);
     p.blk_cnt = reinterpret_cast<int32_t*>(ws + w.blk_cnt);
+    p.lanecnt = ws + w.lanecnt;
     p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);
