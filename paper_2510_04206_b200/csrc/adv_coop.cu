@@ -324,32 +324,6 @@ struct Window {
     bool staged;
 };
 
-// unstaged window: global binary search per lane, global integer atomics on n_g
-__device__ __forceinline__ int32_t count_chunk_global(const AdvParams& p, const uint4& mk,
-                                                      int64_t t0) {
-    int32_t mine = 0;
-    if (t0 < p.T && p.n_traj > 0) {
-        int32_t g = coop_find_traj(p.off, p.n_traj, t0);
-        int64_t end = p.off[g + 1];
-        int32_t cnt = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int64_t t = t0 + i;
-            while (t >= end && g + 1 < p.n_traj) {
-                if (cnt) atomicAdd(&p.n_g[g], cnt);
-                cnt = 0;
-                ++g;
-                end = p.off[g + 1];
-            }
-            const int32_t bit = mbit(mk, i);
-            cnt += bit;
-            mine += bit;
-        }
-        if (cnt) atomicAdd(&p.n_g[g], cnt);
-    }
-    return mine;
-}
-
 // ------------------------------------------------------------------ phase C: apply
 // writes the 16 values of each lane through a swizzled transpose: lane L stores its q-th
 // float4 at word L*16 + 4*(q ^ ((L>>1)&3)) (conflict-free), then reads back the float4 of tokens
@@ -583,15 +557,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 const int32_t tot = __reduce_add_sync(0xffffffffu, pc);
                 if (lane == 0) p.chunk[c] = tot;
                 warp_total += tot;
-            } else if (PH == 0) {
+            } else if (PH == 0) {  // small driver: every window is staged
                 int32_t tot = 0;
-                if (any_traj && w.staged) {
-                    (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
-                } else {
-                    tot = any_traj ? count_chunk_global(p, mk, t0) : 0;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                }
+                if (any_traj) (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
                 if (lane == 0) p.chunk[c] = tot;
                 warp_total += tot;
             } else {
