@@ -155,7 +155,20 @@ typedef struct {
                                           grad_W hold the global sum, the other rows are
                                           scratch; needs V % world == 0 (else
                                           AGENTRL_ERR_SHAPE).  A callback communicator
-                                          without a reduce-scatter sums every row. */
+                                          without a reduce-scatter sums every row.
+                                          3 = vocabulary-parallel head (SURVEY 8(f) rank 4,
+                                          agentrl_policy_loss_fwd_bwd only, needs comm):
+                                          W_head holds rows [rank*V, (rank+1)*V) of a head
+                                          of V*world rows, every rank passes the SAME token
+                                          rows with global target ids in [0, V*world).  Per
+                                          row (max, sum-exp) over the shards and the owner's
+                                          target logit are all-gathered between the forward
+                                          GEMM and the merge; loss, logp and loss_stats come
+                                          out identical on every rank; grad_hidden is the
+                                          full gradient (fp32 partials summed over the group
+                                          inside the call); grad_W is this rank's complete
+                                          shard [V, d] (no collective).  Workspace:
+                                          agentrl_policy_loss_workspace_size_vp(). */
     int32_t reserved;
     /* ---- objective variants; all-zero = the base objective above ----
      * KL penalty (the "- beta D_KL" of P:1103 / P:1119; beta unstated in the paper, R11):
@@ -191,6 +204,10 @@ typedef struct {
 } agentrl_loss_out;
 
 size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V);
+/* workspace of grad_W_mode = 3 (V = the rank's shard rows, world = the group size): the base
+ * plan plus the all-gathered row statistics (8 * world * T B) and the fp32 grad_hidden
+ * partial (4 * T * d B) */
+size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int32_t d, int32_t V, int32_t world);
 int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
                                 size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                                 agentrl_stream stream);

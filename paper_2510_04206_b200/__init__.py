@@ -35,7 +35,8 @@ ST_GROUP_SPANS_TASKS, ST_GROUP_TOO_SMALL, ST_NO_TOKENS = 8, 16, 32
 
 EXPORTED = (
     "agentrl_task_adv_norm_workspace_size", "agentrl_task_adv_norm",
-    "agentrl_policy_loss_workspace_size", "agentrl_policy_loss_fwd_bwd",
+    "agentrl_policy_loss_workspace_size", "agentrl_policy_loss_workspace_size_vp",
+    "agentrl_policy_loss_fwd_bwd",
     "agentrl_grpo_step_workspace_size", "agentrl_grpo_step",
     "agentrl_comm_unique_id", "agentrl_comm_init", "agentrl_comm_destroy",
     "agentrl_status_string", "agentrl_version", "agentrl_last_launch_count",
@@ -80,6 +81,8 @@ _lib.agentrl_task_adv_norm_workspace_size.restype = _sz
 _lib.agentrl_task_adv_norm.argtypes = [C.POINTER(Batch), _f64, _P, _P, _P, _P, _sz, _P, _P, _P]
 _lib.agentrl_policy_loss_workspace_size.argtypes = [_i64, _i32, _i32]
 _lib.agentrl_policy_loss_workspace_size.restype = _sz
+_lib.agentrl_policy_loss_workspace_size_vp.argtypes = [_i64, _i32, _i32, _i32]
+_lib.agentrl_policy_loss_workspace_size_vp.restype = _sz
 _lib.agentrl_policy_loss_fwd_bwd.argtypes = [C.POINTER(LossArgs), C.POINTER(LossOut), _P, _sz,
                                              _P, _P, _P]
 _lib.agentrl_grpo_step_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i32, _i32]
@@ -160,6 +163,11 @@ def agentrl_task_adv_norm_workspace_size(T, n_traj, n_groups, n_tasks) -> int:
 
 def agentrl_policy_loss_workspace_size(T, d, V) -> int:
     return int(_lib.agentrl_policy_loss_workspace_size(T, d, V))
+
+
+def agentrl_policy_loss_workspace_size_vp(T, d, V, world) -> int:
+    """grad_W_mode = 3 (vocabulary-parallel head): V = this rank's shard rows"""
+    return int(_lib.agentrl_policy_loss_workspace_size_vp(T, d, V, world))
 
 
 def agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V) -> int:

@@ -8,6 +8,8 @@
 #include <mutex>
 #include <vector>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace agentrl {
@@ -174,6 +176,7 @@ int comm_reduce_scatter_f32(agentrl_comm c, float* b, size_t n, cudaStream_t s) 
                : AGENTRL_ERR_NCCL;
 }
 int comm_world(agentrl_comm c) { return c ? c->world : 1; }
+int comm_rank(agentrl_comm c) { return c ? c->rank : 0; }
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -203,7 +206,8 @@ static int check_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, boo
     if (!aligned(a->hidden, 16) || !aligned(a->W_head, 16) || !aligned(o->grad_hidden, 16) ||
         !aligned(o->grad_W, 16))
         return AGENTRL_ERR_SHAPE;
-    if (a->grad_W_mode < 0 || a->grad_W_mode > 2) return AGENTRL_ERR_INVALID_ARG;
+    if (a->grad_W_mode < 0 || a->grad_W_mode > 3) return AGENTRL_ERR_INVALID_ARG;
+    if (fused && a->grad_W_mode == 3) return AGENTRL_ERR_INVALID_ARG;  // standalone loss only
     // objective variants: beta >= 0 (ref log-probs needed when > 0); loss_agg 0/1, the
     // sequence mean only in the fused step (it needs the batch descriptor) unless the caller
     // supplies the weights
@@ -243,16 +247,21 @@ size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V) {
     return plan_loss(T, d, V).total;
 }
 
+size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int32_t d, int32_t V, int32_t world) {
+    return plan_loss(T, d, V, 0, std::max(world, 1)).total;
+}
+
 int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
                                 size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                                 agentrl_stream stream) {
     g_launches = 0;
     int rc = check_loss(a, o, false);
     if (!rc && a->grad_W_mode == 2 && comm && a->V % comm_world(comm) != 0) rc = AGENTRL_ERR_SHAPE;
+    if (!rc && a->grad_W_mode == 3 && !comm) rc = AGENTRL_ERR_INVALID_ARG;  // needs the group
     if (rc) return rc;
     if (!d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
     if ((rc = check_device())) return rc;
-    LossWs w = plan_loss(a->T, a->d, a->V);
+    LossWs w = plan_loss(a->T, a->d, a->V, 0, a->grad_W_mode == 3 ? comm_world(comm) : 0);
     if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
     return launch_policy_loss(a, o, static_cast<uint8_t*>(ws), w, nullptr, nullptr, nullptr,
                               nullptr, comm, d_status, reinterpret_cast<cudaStream_t>(stream));

@@ -74,12 +74,15 @@ struct LossWs {
     size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
     size_t fbnd;                            // int64 [MAX_FWD_CHUNKS + 1] forward row chunks
     size_t prog;                            // int64 [2 + MAX_FWD_CHUNKS][PROG_UNITS] GEMM progress
+    size_t vpstat;                          // vocab-parallel: float2 [world][rows_cap] (M_r, L'_r)
+    size_t vp_gh;                           // vocab-parallel: float [rows_cap, d] grad_h partial
+    int32_t vp_world;                       // 0 = not planned for the vocab-parallel head
     size_t total;
     int32_t n_tiles;
 };
 constexpr int MAX_FWD_CHUNKS = 8;
 constexpr int PROG_UNITS = 256;  // >= GEMM units (SMs, or SM pairs)
-LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0);
+LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0, int32_t vp_world = 0);
 
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:
 //   idx_dev  int32 [T] compacted token positions, rows_dev -> int64 number of rows (local T_eff),
@@ -112,6 +115,7 @@ int comm_allreduce_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
 int comm_allreduce_i64(agentrl_comm c, int64_t* buf, size_t n, cudaStream_t s);
 int comm_reduce_scatter_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s);
 int comm_world(agentrl_comm c);
+int comm_rank(agentrl_comm c);
 
 // launch counter for the bench's gpu_launches claim
 void count_launch(int n = 1);

@@ -231,7 +231,11 @@ __global__ void __launch_bounds__(256)
              const __nv_bfloat16* __restrict__ hidden, const int32_t* __restrict__ target,
              const float* __restrict__ old_logp, const int32_t* __restrict__ idx,
              __nv_bfloat16* __restrict__ H, int32_t* __restrict__ tgt_c,
-             float* __restrict__ old_c, int32_t* d_status) {
+             float* __restrict__ old_c, int32_t* d_status, int64_t v0 = 0,
+             int64_t V_total = -1) {
+    // vocab-parallel head: this rank holds columns [v0, v0 + V) of V_total; a target outside
+    // the shard gets tgt_c = -1 (never matches a column here)
+    if (V_total < 0) V_total = V;
     const int64_t rows = *rows_dev;
     const int64_t rows_pad = (rows + 63) / 64 * 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -244,12 +248,13 @@ __global__ void __launch_bounds__(256)
             const uint4* src = reinterpret_cast<const uint4*>(hidden + t * d);
             for (int c = lane; c < chunks; c += 32) dst[c] = __ldg(src + c);
             if (lane == 0) {
-                int32_t y = target[t];
-                if (y < 0 || y >= V) {
+                int64_t y = target[t];
+                if (y < 0 || y >= V_total) {
                     atomicOr(d_status, AGENTRL_ST_BAD_TARGET);
-                    y = 0;
+                    y = v0;
                 }
-                tgt_c[p] = y;
+                const int64_t yl = y - v0;
+                tgt_c[p] = (yl >= 0 && yl < V) ? (int32_t)yl : -1;
                 if (old_c) old_c[p] = old_logp[t];
             }
         } else {
@@ -278,11 +283,13 @@ __global__ void __launch_bounds__(MERGE_THREADS)
               float* __restrict__ row_rho, float* __restrict__ row_logp,
               int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
               float* __restrict__ logp_out,
-              const int64_t* __restrict__ rng /* optional row range [r0, r1) */) {
+              const int64_t* __restrict__ rng /* optional row range [r0, r1) */,
+              const float2* __restrict__ vpstat = nullptr /* [vp_R][vp_stride] (M_r, L'_r) */,
+              int32_t vp_R = 0, int64_t vp_stride = 0) {
     extern __shared__ float s_f[];  // [n_tiles] scale per tile
     __shared__ float s_red[MERGE_THREADS / 32];
     __shared__ int s_jm[MERGE_THREADS / 32];
-    __shared__ float s_bc[3];
+    __shared__ float s_bc[4];
     const int64_t rows = *rows_dev;
     const int64_t rows_pad = (rows + 63) / 64 * 64;
     const double Nd = (double)*nglob_dev;
@@ -340,11 +347,28 @@ __global__ void __launch_bounds__(MERGE_THREADS)
         if (threadIdx.x == 0) {
             float Lm1 = 0.f;
             for (int w = 0; w < MERGE_THREADS / 32; ++w) Lm1 += s_red[w];
+            float Mrow = M;  // the row max over every column of the head
+            if (vpstat) {
+                // vocab-parallel head: combine the ranks' (M_r, L'_r) like tiles -- the first
+                // rank holding the row max enters with L'_r, the others with
+                // (1 + L'_r) exp(M_r - M); this rank's own M, L' are those of slot rank
+                float Mg = -INFINITY;
+                for (int r = 0; r < vp_R; ++r) Mg = fmaxf(Mg, vpstat[r * vp_stride + p].x);
+                int rM = 0;
+                while (rM < vp_R - 1 && vpstat[rM * vp_stride + p].x != Mg) ++rM;
+                float L = 0.f;
+                for (int r = 0; r < vp_R; ++r) {
+                    const float2 st = vpstat[r * vp_stride + p];
+                    L += r == rM ? st.y : (1.f + st.y) * ex2_approx((st.x - Mg) * LOG2E);
+                }
+                Lm1 = L;
+                Mrow = Mg;
+            }
             // log p_y = (z_y - M) - log1p(L'), not z_y - lse: lse = M + log1p(L') rounds
             // log1p(L') to the ulp of M (~2e-6 at |z| ~ 24), which is the whole of 1 - p_y when
             // p_y -> 1 (the onehot-cancellation rows)
             const float l1 = log1pf(Lm1);
-            const float logp = (zy[p] - M) - l1;
+            const float logp = (zy[p] - Mrow) - l1;
             const float A = adv_c[p];
             const float rho = expf(logp - old_c[p]);
             const float lo = 1.f - eps_lo, hi = 1.f + eps_hi;
@@ -371,6 +395,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
             if (logp_out) logp_out[idx[p]] = logp;
             s_bc[0] = l1;
             s_bc[1] = c_t;
+            s_bc[3] = Mrow;
             // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
             s_bc[2] = c_t * expm1f(logp);
         }
@@ -378,9 +403,10 @@ __global__ void __launch_bounds__(MERGE_THREADS)
         const float l1 = s_bc[0];
         c_t = s_bc[1];
         const float g_y = s_bc[2];
+        const float Mrow = s_bc[3];
         // exp(m_j - lse) = exp((m_j - M) - log1p(L'))
         for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
-            s_f[j] = c_t * ex2_approx(((pr[j].x - M) - l1) * LOG2E);
+            s_f[j] = c_t * ex2_approx(((pr[j].x - Mrow) - l1) * LOG2E);
         __syncthreads();
         const int32_t y = tgt_c[p];
         // 16-byte vectors, MERGE_UNROLL loads in flight per thread before any store
@@ -484,7 +510,7 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ---------------------------------------------------------------------------- host
-LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
+LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base, int32_t vp_world) {
     WsPlan p;
     p.off = base;
     LossWs w;
@@ -513,8 +539,67 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base) {
     w.sched = p.take(sizeof(int) * 32);
     w.fbnd = p.take(sizeof(int64_t) * (MAX_FWD_CHUNKS + 1));
     w.prog = p.take(sizeof(int64_t) * (2 + MAX_FWD_CHUNKS) * PROG_UNITS);
+    w.vp_world = vp_world;
+    w.vpstat = w.vp_gh = 0;
+    if (vp_world > 0) {
+        w.vpstat = p.take(sizeof(float2) * (size_t)vp_world * rows_cap);
+        w.vp_gh = p.take(sizeof(float) * (size_t)rows_cap * d, 1024);
+    }
     w.total = p.off;
     return w;
+}
+
+// ---------------------------------------------------------------------------- vocab-parallel
+// (W_head sharded by vocabulary rows over the group, every rank holding the
+// same token rows).  Per row, this rank's statistics over its columns: M_r = max z,
+// L'_r = sum exp(z - M_r) - 1 (the first max left out, as in the tile merge) -> its slot of the
+// all-gather buffer (the other slots are zero; a sum all-reduce then fills every slot).
+__global__ void __launch_bounds__(256)
+    k_vp_row_stats(const int64_t* __restrict__ rows_dev, int32_t n_tiles,
+                   const float2* __restrict__ part, float2* __restrict__ slot) {
+    const int64_t rows = *rows_dev;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const float LOG2E = 1.4426950408889634f;
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < rows;
+         p += nw) {
+        const float2* pr = part + p * (int64_t)n_tiles;
+        float M = -INFINITY;
+        for (int j = lane; j < n_tiles; j += 32) M = fmaxf(M, pr[j].x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        int jm = 0x7fffffff;
+        for (int j = lane; j < n_tiles; j += 32)
+            if (pr[j].x == M) jm = min(jm, j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) jm = min(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+        float L = 0.f;
+        for (int j = lane; j < n_tiles; j += 32) {
+            const float2 ml = pr[j];
+            L += j == jm ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        if (lane == 0) slot[p] = make_float2(M, L);
+    }
+}
+
+// grad_hidden[idx[p]] = bf16(the all-reduced fp32 partial row p)
+__global__ void __launch_bounds__(256)
+    k_vp_scatter(const int64_t* __restrict__ rows_dev, int32_t d, const int32_t* __restrict__ idx,
+                 const float* __restrict__ gh32, __nv_bfloat16* __restrict__ gh) {
+    const int64_t rows = *rows_dev;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < rows;
+         p += nw) {
+        const float4* src = reinterpret_cast<const float4*>(gh32 + p * d);
+        uint2* dst = reinterpret_cast<uint2*>(gh + (int64_t)idx[p] * d);
+        for (int c = lane; c < d / 4; c += 32) {
+            const float4 v = src[c];
+            dst[c] = make_uint2(pack_bf162(v.x, v.y), pack_bf162(v.z, v.w));
+        }
+    }
 }
 
 // per-row aggregation weight w_t and reference log-prob (objective variants):
@@ -677,7 +762,13 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float* ref_c = reinterpret_cast<float*>(ws + w.ref_c);
     int* sched = reinterpret_cast<int*>(ws + w.sched);
     int64_t* fbnd = reinterpret_cast<int64_t*>(ws + w.fbnd);
-    const int n_fc = fwd_chunks();
+    // vocab-parallel head (grad_W_mode 3): W_head is this rank's vocabulary shard, every rank
+    // holds the same rows; the forward runs unchunked (the row statistics are all-gathered
+    // between the forward GEMM and the merge)
+    const bool vp = a->grad_W_mode == 3 && comm && w.vp_world > 0;
+    const int vp_R = vp ? comm_world(comm) : 0;
+    const int64_t vp_v0 = vp ? (int64_t)comm_rank(comm) * V : 0;
+    const int n_fc = vp ? 1 : fwd_chunks();
     int* ctr_fwd = gemm_dynamic() ? sched + 0 : nullptr;
     int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
     int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
@@ -720,7 +811,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         k_gather<<<grid, 256, 0, stream>>>(rows_dev, T, d, V,
                                            reinterpret_cast<const __nv_bfloat16*>(a->hidden),
                                            a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
-                                           d_status);
+                                           d_status, vp_v0, vp ? (int64_t)V * vp_R : V);
         k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
             rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
             fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
@@ -744,6 +835,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     // ---- K5 forward GEMM + softmax-statistics epilogue, K6 merge.  With n_fc > 1 row chunks
     // the forward runs chunk by chunk on a high-priority stream and the (HBM-bound) merge of
     // chunk c runs on a low-priority stream beside the (tensor-bound) forward of chunk c+1.
+    // vocab-parallel: z_y is written only by the rank whose shard holds y_t; the others keep 0
+    // for the sum all-reduce
+    if (vp) AG_CUDA(cudaMemsetAsync(zy, 0, sizeof(float) * (size_t)rows_cap, stream));
     ForkStreams* fs = n_fc > 1 ? &fork_streams() : nullptr;
     cudaStream_t s_fwd = stream, s_mrg = stream;
     if (fs) {
@@ -785,6 +879,18 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             AG_CUDA(cudaEventRecord(fs->ev[c], s_fwd));
             AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->ev[c], 0));
         }
+        float2* vpstat = vp ? reinterpret_cast<float2*>(ws + w.vpstat) : nullptr;
+        if (vp) {  // all-gather of (M_r, L'_r) per row and the owner's z_y (sum all-reduces)
+            AG_CUDA(cudaMemsetAsync(vpstat, 0, sizeof(float2) * (size_t)vp_R * rows_cap, stream));
+            k_vp_row_stats<<<num_sms() * 4, 256, 0, stream>>>(
+                rows_dev, w.n_tiles, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
+            count_launch();
+            AG_CUDA(cudaGetLastError());
+            if ((rc = comm_allreduce_f32(comm, reinterpret_cast<float*>(vpstat),
+                                         (size_t)2 * vp_R * rows_cap, stream)))
+                return rc;
+            if ((rc = comm_allreduce_f32(comm, zy, (size_t)rows_cap, stream))) return rc;
+        }
         // merge + loss terms + G (in place) of this chunk; chunks merged beside the next
         // forward chunk keep a small footprint (2 blocks per SM next to the GEMM CTA)
         size_t smem = sizeof(float) * (size_t)w.n_tiles;
@@ -794,7 +900,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
             a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
             a->kl_beta, PG, row_term, row_rho, row_logp, row_clip, row_kl, o->logp,
-            n_fc > 1 ? fbnd + c : nullptr);
+            n_fc > 1 ? fbnd + c : nullptr, vpstat, vp_R, rows_cap);
         count_launch();
         AG_CUDA(cudaGetLastError());
     }
@@ -810,7 +916,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     }
     count_launch();
     AG_CUDA(cudaGetLastError());
-    if (comm) {
+    if (comm && !vp) {  // (vocab-parallel: every rank already holds the whole loss)
         if ((rc = comm_allreduce_f64(comm, o->loss, 1, stream))) return rc;
     }
     // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff)
@@ -841,7 +947,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     }
     // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
     SideStream* ss = nullptr;
-    if (comm && a->grad_W_mode >= 1) {
+    if (comm && (a->grad_W_mode == 1 || a->grad_W_mode == 2)) {
         ss = &side_stream();
         AG_CUDA(cudaEventRecord(ss->e0, stream));
         AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
@@ -874,9 +980,26 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         // with C3 in flight on the side stream, leave SMs for the NCCL kernel so the
         // collective overlaps this GEMM instead of queueing behind its persistent CTAs
         const int rsv = ss && comm_world(comm) > 1 ? comm_reserve_sms() : 0;
-        rc = gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream, rsv)
-                           : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream, rsv);
-        if (rc) return rc;
+        if (vp) {
+            // this rank's vocabulary columns give a partial grad_h: fp32 rows (the EPI_GRADW
+            // epilogue, row = compacted row), summed over the group, then scattered as bf16
+            float* gh32 = reinterpret_cast<float*>(ws + w.vp_gh);
+            g.gw = gh32;
+            rc = gemm_wide_n()
+                     ? launch_gemm<EPI_GRADW, false, true, 2>(mG_K, mW_MN, g, tiles, stream, 0)
+                     : launch_gemm<EPI_GRADW, false, true, 1>(mG_K, mW_MN, g, tiles, stream, 0);
+            if (rc) return rc;
+            if ((rc = comm_allreduce_f32(comm, gh32, (size_t)rows_cap * d, stream))) return rc;
+            k_vp_scatter<<<num_sms() * 4, 256, 0, stream>>>(rows_dev, d, idx_dev, gh32,
+                                                           reinterpret_cast<__nv_bfloat16*>(o->grad_hidden));
+            count_launch();
+            AG_CUDA(cudaGetLastError());
+        } else {
+            rc = gemm_wide_n()
+                     ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream, rsv)
+                     : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream, rsv);
+            if (rc) return rc;
+        }
     }
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
     return AGENTRL_OK;

@@ -106,8 +106,8 @@ def test_missing_library_fails_loudly(tmp_path):
 
 def test_reduce_scatter_mode_contract(libpath):
     """grad_W_mode 2 (reduce-scatter row shards) needs V % world == 0: SHAPE before any device
-    work; mode 3 is INVALID_ARG.  Host-side checks only (fake, aligned, never-dereferenced
-    pointers; the call returns before touching the device)."""
+    work.  Host-side checks only (fake, aligned, never-dereferenced
+    pointers; the call returns before touching the device).  Mode 4 does not exist."""
     import paper_2510_04206_b200 as m
     comm = m.CallbackComm(3, 0, lambda *a: None)
     fake = 1 << 20
@@ -120,6 +120,13 @@ def test_reduce_scatter_mode_contract(libpath):
     assert call() == m.ERR_SHAPE          # 2000 % 3 != 0
     args.V = 2016                          # divisible: passes this check, fails later (no GPU)
     assert call() not in (m.ERR_SHAPE, m.ERR_INVALID_ARG, 0)
-    args.grad_W_mode = 3
+    args.grad_W_mode = 4
     assert call() == m.ERR_INVALID_ARG
+    # mode 3 (vocabulary-parallel head) needs a communicator and is not a fused-step mode
+    args.grad_W_mode = 3
+    assert m._lib.agentrl_policy_loss_fwd_bwd(ctypes.byref(args), ctypes.byref(out), fake,
+                                              1 << 30, None, fake, None) == m.ERR_INVALID_ARG
+    assert call() not in (m.ERR_SHAPE, m.ERR_INVALID_ARG, 0)  # passes the host checks
+    assert (m.agentrl_policy_loss_workspace_size_vp(1024, 64, 512, 4)
+            >= m.agentrl_policy_loss_workspace_size(1024, 64, 512) + 8 * 4 * 1024 + 4 * 1024 * 64)
     comm.destroy()
