@@ -64,7 +64,7 @@ struct LossWs {
     size_t chunk_cnt, chunk_base;           // int32 compaction scratch (standalone path)
     size_t tgt_c, old_c, adv_c;             // compacted per-row inputs
     size_t H;                               // bf16 [T_pad, d] gathered hidden rows
-    size_t P;                               // fp16/bf16 [T_pad, V]: P~ then G (in place)
+    size_t P;                               // bf16 [T_pad, V]: P~ then G (in place)
     size_t part;                            // float2 [T_pad, n_tiles]
     size_t zy;                              // float [T_pad]
     size_t row_term, row_rho, row_logp;     // double/float per row
