@@ -199,6 +199,15 @@ def run_native(args, cfg, world, rank, local_rank):
     # C3 as the FSDP-style reduce-scatter of grad_W rows (the paper's trainer shards the head,
     # P:1357) when V divides evenly, else the all-reduce of a replicated head
     gw_mode = (2 if V % world == 0 else 1) if comm is not None else 0
+    # C3 fused into the grad_W GEMM epilogue over peer memory (CUDA IPC windows; include/
+    # agentrl.h agentrl_comm_enable_peer_window), unless AGENTRL_C3_P2P=0 or the mapping fails
+    c3 = {0: "none", 1: "all-reduce (collective)", 2: "reduce-scatter (collective)"}[gw_mode]
+    if gw_mode == 2 and os.environ.get("AGENTRL_C3_P2P", "1") != "0":
+        try:
+            comm.enable_peer_window(V * d * 4)
+            c3 = "reduce-scatter fused into the grad_W GEMM epilogue (P2P stores)"
+        except RuntimeError as e:  # fall back to the collective
+            print(f"peer window unavailable ({e}); collective reduce-scatter", file=sys.stderr)
     step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm,
                    grad_W_mode=gw_mode)
     # behaviour log-probs: one untimed forward (old = 0), then old = logp + delta
@@ -347,7 +356,7 @@ def run_native(args, cfg, world, rank, local_rank):
         "config": {"workload": cfg.name, "T": T_global, "T_eff": T_eff_global, "d": d, "V": V,
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
-                   "grad_W_collective": {0: "none", 1: "all-reduce", 2: "reduce-scatter"}[gw_mode],
+                   "grad_W_collective": c3,
                    "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
         "masked_tokens_per_s": T_eff_global / (ms / 1e3),

@@ -61,6 +61,7 @@ extern "C" {
 #define AGENTRL_ST_GROUP_SPANS_TASKS 8   /* a group's members have different task_id */
 #define AGENTRL_ST_GROUP_TOO_SMALL 16    /* a group has one trajectory */
 #define AGENTRL_ST_NO_TOKENS 32          /* global masked-token count N == 0 */
+#define AGENTRL_ST_COMM_TIMEOUT 64       /* a peer never reached the fused reduce-scatter */
 
 typedef struct agentrl_comm_s* agentrl_comm;
 typedef struct CUstream_st* agentrl_stream; /* == cudaStream_t */
@@ -274,6 +275,20 @@ int agentrl_comm_init_callback(agentrl_comm* out, int world, int rank, agentrl_a
 typedef int (*agentrl_reduce_scatter_fn)(void* user, void* dev_buf, size_t recv_count, int dtype,
                                          agentrl_stream stream);
 int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn fn);
+/* Fused grad_W reduce-scatter over peer memory (grad_W_mode = 2).  Collective: every rank
+ * calls it with the same bytes_per_rank.  The communicator allocates a staging window of
+ * bytes_per_rank device bytes (and a few flags) on each rank and maps every other rank's window
+ * with CUDA IPC (NVLink / NVSwitch peer memory across GPUs; the same device across processes).
+ * The IPC handles travel through one sum all-reduce of the communicator.  From then on a call
+ * with grad_W_mode = 2 and a window of at least V*d*4 bytes makes the grad_W GEMM epilogue
+ * store each fp32 tile directly into the window of the rank that owns its rows (owner
+ * o = rows [o*V/world, (o+1)*V/world)), so the transfer overlaps the GEMM.  After a
+ * system-scope flag barrier the owner sums the world slots in rank order (deterministic) into
+ * its grad_W shard; the collective path is not used.  Every wait is bounded: a peer that never
+ * arrives sets AGENTRL_ST_COMM_TIMEOUT instead of hanging.  AGENTRL_C3_P2P=0 in the
+ * environment selects the collective path.  The window is freed by agentrl_comm_destroy (the
+ * one place the library allocates persistent device memory: it must be IPC-exportable). */
+int agentrl_comm_enable_peer_window(agentrl_comm comm, size_t bytes_per_rank);
 
 /* ---- misc -------------------------------------------------------------- */
 const char* agentrl_status_string(int code); /* text for a return code or status bit */

@@ -32,6 +32,7 @@ OK = 0
 ERR_INVALID_ARG, ERR_SHAPE, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = -1, -2, -3, -4, -5, -6
 ST_BAD_TARGET, ST_NONFINITE, ST_BAD_OFFSETS = 1, 2, 4
 ST_GROUP_SPANS_TASKS, ST_GROUP_TOO_SMALL, ST_NO_TOKENS = 8, 16, 32
+ST_COMM_TIMEOUT = 64
 
 EXPORTED = (
     "agentrl_task_adv_norm_workspace_size", "agentrl_task_adv_norm",
@@ -43,6 +44,7 @@ EXPORTED = (
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
     "agentrl_debug_adv_phase_ns", "agentrl_comm_init_callback",
     "agentrl_logprob_workspace_size", "agentrl_logprob_fwd", "agentrl_comm_set_reduce_scatter",
+    "agentrl_comm_enable_peer_window",
 )
 NUM_KERNEL_IDS = 12
 
@@ -93,6 +95,7 @@ _lib.agentrl_comm_unique_id.argtypes = [C.c_char_p]
 _lib.agentrl_comm_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_char_p]
 _lib.agentrl_comm_destroy.argtypes = [_P]
 _lib.agentrl_comm_set_reduce_scatter.argtypes = [_P, C.c_void_p]
+_lib.agentrl_comm_enable_peer_window.argtypes = [_P, _sz]
 _lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p,
                                             C.c_void_p]
 _lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i32, _i32]
@@ -272,6 +275,11 @@ class Comm:
                          device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
         dist.broadcast(t, src=0, group=group)
         return cls(world, rank, bytes(t.cpu().tolist()))
+
+    def enable_peer_window(self, nbytes: int):
+        """Fused grad_W reduce-scatter over peer memory (collective; include/agentrl.h)."""
+        _check(_lib.agentrl_comm_enable_peer_window(self.handle, int(nbytes)),
+               "agentrl_comm_enable_peer_window")
 
     def destroy(self):
         if self.handle:

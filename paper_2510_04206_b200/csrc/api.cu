@@ -126,6 +126,7 @@ struct agentrl_comm_s {
     agentrl_allreduce_fn fn;  // callback backend (non-null) instead of NCCL
     void* user;
     agentrl_reduce_scatter_fn rs;  // optional callback reduce-scatter
+    agentrl::PeerWindow* peer = nullptr;  // fused GEMM + reduce-scatter window (or none)
 };
 
 namespace agentrl {
@@ -177,6 +178,7 @@ int comm_reduce_scatter_f32(agentrl_comm c, float* b, size_t n, cudaStream_t s) 
 }
 int comm_world(agentrl_comm c) { return c ? c->world : 1; }
 int comm_rank(agentrl_comm c) { return c ? c->rank : 0; }
+PeerWindow* comm_peer(agentrl_comm c) { return c ? c->peer : nullptr; }
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -364,8 +366,21 @@ int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn
     return AGENTRL_OK;
 }
 
+int agentrl_comm_enable_peer_window(agentrl_comm comm, size_t bytes_per_rank) {
+    if (!comm || bytes_per_rank == 0) return AGENTRL_ERR_INVALID_ARG;
+    if (comm->peer) {
+        peer_window_destroy(comm->peer);
+        comm->peer = nullptr;
+    }
+    return peer_window_create(comm, bytes_per_rank, &comm->peer);
+}
+
 int agentrl_comm_destroy(agentrl_comm comm) {
     if (!comm) return AGENTRL_OK;
+    if (comm->peer) {
+        peer_window_destroy(comm->peer);
+        comm->peer = nullptr;
+    }
     if (comm->fn) {
         delete comm;
         return AGENTRL_OK;
@@ -392,6 +407,7 @@ const char* agentrl_status_string(int code) {
         case AGENTRL_ST_GROUP_SPANS_TASKS: return "a group spans tasks (or ids out of range)";
         case AGENTRL_ST_GROUP_TOO_SMALL: return "a group has fewer than 2 trajectories";
         case AGENTRL_ST_NO_TOKENS: return "no loss-masked tokens in the batch";
+        case AGENTRL_ST_COMM_TIMEOUT: return "a peer never reached the fused reduce-scatter";
         default: return "unknown";
     }
 }

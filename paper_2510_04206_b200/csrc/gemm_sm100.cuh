@@ -93,6 +93,11 @@ struct GemmArgs {
     // EPI_GRADW
     float* gw;  // [V, ldo]
     int64_t ldo;
+    // EPI_GRADW fused with the reduce-scatter (peer.cu): row r goes to owner o = r / peer_rows,
+    // into slot peer_rank of o's window: peer_out[o] + (peer_rank * peer_rows + r mod) * ldo
+    float* const* peer_out;
+    int64_t peer_rows;
+    int32_t peer_rank;
     // dynamic tile scheduler: zeroed int counter (tiles claimed in global order), or null for
     // the static persistent schedule (tile = unit + i * units)
     int* tile_counter;
@@ -527,7 +532,16 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     }
                 } else {  // EPI_GRADW
                     const float s = num_kb > 0 ? p.scale : 0.f;
-                    float* orow = p.gw + (row_ok ? row : 0) * p.ldo + col0;
+                    const int64_t rr = row_ok ? row : 0;
+                    float* orow;
+                    if (p.peer_out) {  // straight into the owner's window (NVLink peer memory)
+                        const int64_t o = rr / p.peer_rows;
+                        orow = p.peer_out[o] +
+                               ((int64_t)p.peer_rank * p.peer_rows + (rr - o * p.peer_rows)) * p.ldo +
+                               col0;
+                    } else {
+                        orow = p.gw + rr * p.ldo + col0;
+                    }
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
                         if (num_kb > 0) {
@@ -559,6 +573,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 else mbar_arrive(&tempty[acc]);
             }
             advance_acc<ACC_BUFS>(acc, acc_phase);
+        }
+        // peer stores visible system-wide before the kernel ends (the signal kernel follows)
+        if constexpr (EPI == EPI_GRADW) {
+            if (p.peer_out) __threadfence_system();
         }
     }
 

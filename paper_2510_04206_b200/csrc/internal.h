@@ -117,6 +117,28 @@ int comm_reduce_scatter_f32(agentrl_comm c, float* buf, size_t n, cudaStream_t s
 int comm_world(agentrl_comm c);
 int comm_rank(agentrl_comm c);
 
+// ---- peer window (peer.cu): the grad_W reduce-scatter fused into the grad_W GEMM epilogue
+struct PeerWindow {
+    static constexpr int MAX_RANKS = 64;
+    int world = 0, rank = 0;
+    size_t bytes = 0;              // staging bytes per rank (world slots of one grad_W shard)
+    float* staging = nullptr;      // this rank's window (cudaMalloc, comm-owned)
+    int64_t* flags = nullptr;      // [2][world]: ready[r], consumed[o] epochs
+    float** d_staging = nullptr;   // device [world]: every rank's window (IPC-mapped)
+    int64_t** d_flags = nullptr;   // device [world]: every rank's flags
+    int32_t* done_ctr = nullptr;   // reduce-kernel block counter
+    void* opened[MAX_RANKS] = {};
+    void* opened_flags[MAX_RANKS] = {};
+    long long epoch = 0;
+};
+int peer_window_create(agentrl_comm c, size_t bytes, PeerWindow** out);  // collective
+void peer_window_destroy(PeerWindow* pw);
+PeerWindow* comm_peer(agentrl_comm c);
+bool peer_window_fits(const PeerWindow* pw, int32_t V, int32_t d);
+int peer_guard(PeerWindow* pw, int32_t* d_status, cudaStream_t s);
+int peer_signal_reduce(PeerWindow* pw, float* grad_W, int32_t V, int32_t d, int32_t* d_status,
+                       cudaStream_t s);
+
 // launch counter for the bench's gpu_launches claim
 void count_launch(int n = 1);
 

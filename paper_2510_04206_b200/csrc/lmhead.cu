@@ -919,9 +919,18 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     if (comm && !vp) {  // (vocab-parallel: every rank already holds the whole loss)
         if ((rc = comm_allreduce_f64(comm, o->loss, 1, stream))) return rc;
     }
-    // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff)
+    // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff); with a peer window (grad_W_mode 2)
+    // the epilogue is also C3: each tile goes straight to its owner's window (peer.cu)
+    PeerWindow* pw = (comm && a->grad_W_mode == 2) ? comm_peer(comm) : nullptr;
+    if (pw && !peer_window_fits(pw, V, d)) pw = nullptr;
+    if (pw && (rc = peer_guard(pw, d_status, stream))) return rc;  // owners done with epoch-1
     {
         GemmArgs g{};
+        if (pw) {
+            g.peer_out = pw->d_staging;
+            g.peer_rows = V / pw->world;
+            g.peer_rank = pw->rank;
+        }
         g.M_static = V;
         g.N = d;
         g.k_dev = rows_dev;
@@ -951,7 +960,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         ss = &side_stream();
         AG_CUDA(cudaEventRecord(ss->e0, stream));
         AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
-        rc = a->grad_W_mode == 1
+        rc = pw ? peer_signal_reduce(pw, o->grad_W, V, d, d_status, ss->s)  // fused C3 tail
+             : a->grad_W_mode == 1
                  ? comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s)
                  : comm_reduce_scatter_f32(comm, o->grad_W, (size_t)V * d, ss->s);  // FSDP shard
         if (rc) return rc;

@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, out_dir, cfg_name, mode=1):
+def _rank(rank, world, port, out_dir, cfg_name, mode=1, p2p=False):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -51,13 +51,24 @@ def _rank(rank, world, port, out_dir, cfg_name, mode=1):
                                              minlength=gb["n_groups"]), world)
     lb = synth.shard_batch(gb, rog, rank)
     tok = lb["token_index"]
-    comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn(),
-                           rs_fn=ag.gloo_reduce_scatter_fn(world, rank) if mode == 2 else None)
+    def poison(*a):  # the fused path must not fall back to the collective reduce-scatter
+        raise RuntimeError("collective reduce-scatter called on the p2p path")
+    rs = (poison if p2p else ag.gloo_reduce_scatter_fn(world, rank)) if mode == 2 else None
+    comm = ag.CallbackComm(world, rank, ag.gloo_allreduce_fn(), rs_fn=rs)
+    if p2p:  # grad_W reduce-scatter fused into the GEMM epilogue over IPC peer memory
+        comm.enable_peer_window(cfg.V * cfg.d * 4)
     step = ag.Step(lb["T"], len(lb["task_id"]), lb["n_groups"], lb["n_tasks"], cfg.d, cfg.V,
                    comm=comm, grad_W_mode=mode)
-    step(batch_dev(lb), bf16_dev(hb[tok]), bf16_dev(Wb), t(y[tok], torch.int32),
-         t(old[tok], torch.float32))
+    inputs = (batch_dev(lb), bf16_dev(hb[tok]), bf16_dev(Wb), t(y[tok], torch.int32),
+              t(old[tok], torch.float32))
+    step(*inputs)
     torch.cuda.synchronize()
+    if p2p:  # a second epoch (exercises the consumed-slot guard): bitwise the same shard
+        sh = slice(rank * cfg.V // world, (rank + 1) * cfg.V // world)
+        first = step.grad_W[sh].clone()
+        step(*inputs)
+        torch.cuda.synchronize()
+        assert torch.equal(first, step.grad_W[sh])
     res = dict(loss=step.loss.item(), adv=step.adv_tok.cpu().numpy(),
                gh=step.grad_hidden.float().cpu().numpy(), gw=step.grad_W.cpu().numpy(),
                ts=step.task_stats.cpu().numpy(), st=int(step.status.item()), tok=tok)
@@ -101,10 +112,14 @@ def test_nccl_world1_matches_no_comm():
     comm.destroy()
 
 
-@pytest.mark.parametrize("cfg_name,mode", [("tiny", 1), ("ragged", 1), ("ragged", 2)])
-def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name, mode):
+@pytest.mark.parametrize("cfg_name,mode,p2p", [("tiny", 1, False), ("ragged", 1, False),
+                                               ("ragged", 2, False), ("ragged", 2, True),
+                                               ("tiny", 2, True)])
+def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name, mode, p2p):
     """mode 1: grad_W all-reduced (replicated head); mode 2: reduce-scattered (FSDP-style row
-    shard): each rank's rows [r V/2, (r+1) V/2) hold the global sum."""
+    shard): each rank's rows [r V/2, (r+1) V/2) hold the global sum.  p2p: the
+    reduce-scatter fused into the grad_W GEMM epilogue over CUDA-IPC peer memory (the two
+    processes map each other's windows on the one device)."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -114,7 +129,7 @@ def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name, mode):
     import synth
     from gpu_util import adv_close, f64, max_abs_rel
 
-    mp.spawn(_rank, args=(2, _port(), str(tmp_path), cfg_name, mode), nprocs=2, join=True)
+    mp.spawn(_rank, args=(2, _port(), str(tmp_path), cfg_name, mode, p2p), nprocs=2, join=True)
     cfg = synth.CONFIGS[cfg_name]
     gb = synth.make_structure(cfg)
     hb, Wb, y = synth.make_head(cfg, mask=gb["loss_mask"])
