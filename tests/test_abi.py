@@ -122,6 +122,9 @@ def test_reduce_scatter_mode_contract(libpath):
     assert call() not in (m.ERR_SHAPE, m.ERR_INVALID_ARG, 0)
     args.grad_W_mode = 4
     assert call() == m.ERR_INVALID_ARG
+    # the peer window needs a size (and, past the host checks, a device)
+    assert m._lib.agentrl_comm_enable_peer_window(comm.handle, 0) == m.ERR_INVALID_ARG
+    assert m._lib.agentrl_comm_enable_peer_window(None, 1 << 20) == m.ERR_INVALID_ARG
     # mode 3 (vocabulary-parallel head) needs a communicator and is not a fused-step mode
     args.grad_W_mode = 3
     assert m._lib.agentrl_policy_loss_fwd_bwd(ctypes.byref(args), ctypes.byref(out), fake,
