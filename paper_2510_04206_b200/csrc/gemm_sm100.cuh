@@ -59,7 +59,11 @@ struct GemmCfg {
     static constexpr int TILE_M = PAIR ? 2 * GEMM_BM : GEMM_BM;  // rows per tile
     static constexpr int TILE_N = GEMM_BN * NSPLIT;              // columns per tile
     static constexpr int ACC_BUFS = NSPLIT == 1 ? 2 : 1;
-    static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024;
+    // backward tiles: a 32 x 33 fp32 transpose slab per epilogue warp, so the peer-memory
+    // epilogue (grad_W fused with its reduce-scatter) writes 128 contiguous bytes per row and
+    // warp instruction instead of 16 B from each of 32 rows
+    static constexpr int EPI_STAGE = NSPLIT == 2 ? 4 * 32 * 33 * 4 : 0;
+    static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024 + EPI_STAGE;
     static constexpr int TX_BYTES = (A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
 
@@ -529,6 +533,45 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                 }
                             }
                         }
+                    }
+                } else if (Cfg::EPI_STAGE > 0 && p.peer_out) {
+                    // EPI_GRADW fused with the reduce-scatter: each 32 x 32 chunk goes through
+                    // the warp's smem slab; then row i of the warp's 32 rows is written by the
+                    // 32 lanes as 128 contiguous bytes straight into its owner's window
+                    const float s = num_kb > 0 ? p.scale : 0.f;
+                    float* slab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024) +
+                                  q * (32 * 33);
+                    const int64_t row0 = row - lane;
+                    const int64_t o0 = row0 / p.peer_rows;  // owner of the warp's first row
+#pragma unroll 1
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
+                        if (num_kb > 0) {
+                            tmem_ld_32x32b_x32(taddr + c * 32, r);
+                            tmem_ld_wait();
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) r[j] = 0u;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) slab[lane * 33 + j] = s * __uint_as_float(r[j]);
+                        __syncwarp();
+                        const bool col_ok = c * 32 + lane < ncol;
+#pragma unroll 4
+                        for (int i = 0; i < 32; ++i) {
+                            const int64_t ri = row0 + i;
+                            if (ri < M && col_ok) {
+                                int64_t o = o0, lr = ri - o0 * p.peer_rows;
+                                if (lr >= p.peer_rows) {  // the 32 rows cross an owner boundary
+                                    o = ri / p.peer_rows;
+                                    lr = ri - o * p.peer_rows;
+                                }
+                                float* dst = p.peer_out[o] +
+                                             ((int64_t)p.peer_rank * p.peer_rows + lr) * p.ldo + col0 +
+                                             c * 32 + lane;
+                                *dst = slab[i * 33 + lane];
+                            }
+                        }
+                        __syncwarp();
                     }
                 } else {  // EPI_GRADW
                     const float s = num_kb > 0 ? p.scale : 0.f;
