@@ -62,8 +62,12 @@ struct GemmCfg {
     // backward tiles: a 32 x 33 fp32 transpose slab per epilogue warp, so the peer-memory
     // epilogue (grad_W fused with its reduce-scatter) writes 128 contiguous bytes per row and
     // warp instruction instead of 16 B from each of 32 rows
-    static constexpr int EPI_STAGE = NSPLIT == 2 ? 4 * 32 * 33 * 4 : 0;
-    static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024 + EPI_STAGE;
+#ifndef AGENTRL_EPI_SLAB
+#define AGENTRL_EPI_SLAB 1
+#endif
+    static constexpr int EPI_STAGE = (NSPLIT == 2 && AGENTRL_EPI_SLAB) ? 4 * 32 * 33 * 4 : 0;
+    // (EPI_STAGE is added by the launcher for the grad_W GEMM only)
+    static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024;
     static constexpr int TX_BYTES = (A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
 
@@ -534,7 +538,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             }
                         }
                     }
-                } else if (Cfg::EPI_STAGE > 0 && p.peer_out) {
+                } else if (EPI == EPI_GRADW && Cfg::EPI_STAGE > 0 && p.peer_out) {
                     // EPI_GRADW fused with the reduce-scatter: each 32 x 32 chunk goes through
                     // the warp's smem slab; then row i of the warp's 32 rows is written by the
                     // 32 lanes as 128 contiguous bytes straight into its owner's window

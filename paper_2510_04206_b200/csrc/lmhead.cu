@@ -132,7 +132,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     // max_tiles is counted in 128 x 256 tiles (an upper bound of the CTAs worth launching)
     if (gemm_use_pair()) {
         auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB>;
-        constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM;
+        constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM +
+                             (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0);
         static bool attr_done = false;  // per instantiation
         if (!attr_done) {
             AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
