@@ -354,6 +354,12 @@ __device__ __forceinline__ void store_transposed(const AdvParams& p, float* os, 
     __syncwarp();
 }
 
+// Eq.1 from smem copies of A^ and the task ids (identical arithmetic to adv_tilde)
+__device__ __forceinline__ float adv_tilde_s(const AdvParams& p, const double2* s_task,
+                                             const double* ah, const int32_t* tid, int32_t g) {
+    const int32_t ti = tid[g];
+    return (ti >= 0 && ti < p.n_tasks) ? (float)((ah[g] - s_task[ti].x) / s_task[ti].y) : 0.f;
+}
 // Eq.1 for trajectory g with the block's per-task (mu, max(sigma, eps))
 __device__ __forceinline__ float adv_tilde(const AdvParams& p, const double2* s_task, int32_t g) {
     const int32_t ti = p.task_id[g];
@@ -453,10 +459,12 @@ struct NoPre {
     __device__ void operator()() const {}
 };
 // pre(): work run after the ring's first copies are issued (overlaps their latency)
+// ah_s / tid_s (PH 1, small driver): A^ and task ids of every trajectory already in smem
 template <int PH, typename Pre = NoPre>
 __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int64_t c_lo,
                              int64_t c_hi, bool small, const int64_t* s_offall, int32_t blk_base,
-                             int32_t& warp_total, bool resident = false, Pre pre = Pre()) {
+                             int32_t& warp_total, bool resident = false, Pre pre = Pre(),
+                             const double* ah_s = nullptr, const int32_t* tid_s = nullptr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t B = blockIdx.x;
     int32_t* s_rel = reinterpret_cast<int32_t*>(smem + p.lay.srel);
@@ -520,7 +528,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                     const int64_t o = (small ? s_offall[f + k] : p.off[f + k]) - w.base;
                     s_rel[k] = (int32_t)min(max(o, (int64_t)0), (int64_t)INT_MAX);
                     if (k < w.nbt)
-                        s_aux[k] = PH == 0 ? 0 : __float_as_int(adv_tilde(p, s_task, f + k));
+                        s_aux[k] = PH == 0 ? 0
+                                   : (ah_s ? __float_as_int(adv_tilde_s(p, s_task, ah_s, tid_s, f + k))
+                                           : __float_as_int(adv_tilde(p, s_task, f + k)));
                 }
             }
         }
@@ -870,36 +880,48 @@ __device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w)
 // phase A.  publish (block 0): n_g, task_stats, N, n_seq and the local masked-row count;
 // stats_only (second launch follows the all-reduce): block 0 writes the raw per-task sums.
 __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
-                            bool publish, bool stats_only) {
+                            bool publish, bool stats_only, int32_t* s_pre = nullptr) {
     const SmallArrays a = small_arrays(p, smem);
     const bool blk0 = blockIdx.x == 0;
     const int64_t GS = G - 1;  // streaming blocks 1..G-1
-    if (!blk0) {
-        for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
-            a.gcnt[j] = p.grp_cnt[j];
-            a.gstart[j] = p.grp_start[j];
-            a.gtask[j] = p.grp_task[j];
-        }
-        for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
-            a.mem[g] = p.members[g];
-            a.ah[g] = p.adv_hat[g];
-        }
-    }
     int32_t rows = 0;  // local masked rows = sum of the streaming blocks' totals
     if (blk0 && publish)
         for (int64_t b = 1 + threadIdx.x; b < G; b += COOP_THREADS) rows += p.blk_chunk[b];
-    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
-        const int64_t s0 = a.off[g], e = a.off[g + 1];
-        int32_t n = 0;
-        if (e > s0 && s0 >= 0 && GS > 0) {
-            const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
-            const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
-            for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+    // one pass, all loads independent: the group table and members / A^ / task ids block 0
+    // published (streaming blocks), the per-block counts of every trajectory (-> n_g), and the
+    // per-block masked totals for the compaction bases (s_pre, streaming blocks)
+    const int64_t nloop = max(max((int64_t)p.n_traj, (int64_t)p.n_groups), s_pre ? G : 0);
+    for (int64_t i = threadIdx.x; i < nloop; i += COOP_THREADS) {
+        if (!blk0 && i < p.n_groups) {
+            a.gcnt[i] = p.grp_cnt[i];
+            a.gstart[i] = p.grp_start[i];
+            a.gtask[i] = p.grp_task[i];
         }
-        a.ng[g] = n;
-        if (blk0) p.n_g[g] = n;
+        if (s_pre && i < G) s_pre[i] = p.blk_chunk[i];
+        if (i < p.n_traj) {
+            const int32_t g = (int32_t)i;
+            if (!blk0) {
+                a.mem[g] = p.members[g];
+                a.ah[g] = p.adv_hat[g];
+                a.tid[g] = p.task_id[g];
+            }
+            const int64_t s0 = a.off[g], e = a.off[g + 1];
+            int32_t n = 0;
+            if (e > s0 && s0 >= 0 && GS > 0) {
+                const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
+                const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
+                for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+            }
+            a.ng[g] = n;
+            if (blk0) p.n_g[g] = n;
+        }
     }
     __syncthreads();
+    if (s_pre) {  // exclusive prefix of the block totals (compaction base of every block)
+        const int32_t total = coop_block_scan_array(s_pre, G, s_w);
+        if (threadIdx.x == 0) s_pre[G] = total;
+        __syncthreads();
+    }
     unsigned long long nz = 0;
     for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
         const int32_t K = a.gcnt[j];
@@ -1005,10 +1027,11 @@ __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, W
     int64_t c_lo, c_hi;
     small_range(p, c_lo, c_hi);
     const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-    if (fused) block_prefix_smem(p.blk_chunk, gridDim.x, s_pre, s_w);
-    else load_task_params(p, smem, s_pre, s_w);
+    if (!fused) load_task_params(p, smem, s_pre, s_w);  // fused: s_pre, s_task from small_stats
+    const SmallArrays a = small_arrays(p, smem);
     int32_t dummy = 0;
-    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused);
+    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused, NoPre(),
+                    fused ? a.ah : nullptr, fused ? a.tid : nullptr);
 }
 
 // masked tokens before position t (large driver, after phase A): block prefix + the chunk's
@@ -1342,7 +1365,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvPara
     }
     grid.sync();
     phase_mark(1);
-    small_stats(p, smem, gridDim.x, ss.s_w, true, false);
+    small_stats(p, smem, gridDim.x, ss.s_w, true, false, blockIdx.x != 0 ? ss.s_pre : nullptr);
     if (blockIdx.x != 0) small_apply(p, smem, r, ss.s_pre, ss.s_w, true);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
