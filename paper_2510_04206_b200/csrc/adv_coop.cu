@@ -1141,6 +1141,11 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
     // order.  Groups of <= REG_K members: ids sorted by a register sorting network and their
     // reward / task / count loads issued together (no dependent global round trips).
     unsigned long long nz = 0;
+    // at most one group per thread (the usual case): its (task, N, S, Q) stay in registers for
+    // the per-task partials below instead of being re-read from global per task
+    const bool one_per_thread = j_hi - j_lo <= COOP_THREADS;
+    int32_t my_task = -1;
+    double my_N = 0.0, my_S = 0.0, my_Q = 0.0;
     for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
         const int32_t K = p.grp_cnt[j];
         int32_t* mbg = p.members + s_pre[B] + p.grp_start[j];
@@ -1234,6 +1239,10 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
         p.grp_nsq[3 * j + 0] = N;
         p.grp_nsq[3 * j + 1] = S;
         p.grp_nsq[3 * j + 2] = Q;
+        my_task = task0;
+        my_N = N;
+        my_S = S;
+        my_Q = Q;
     }
     {  // one atomic per block (same-address atomics from every thread serialise at L2)
         int32_t nzt = 0;
@@ -1250,12 +1259,20 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
             const int32_t nb = min(TASK_BATCH, p.n_tasks - i0);
             for (int32_t ii = 0; ii < nb; ++ii) {
                 double N = 0.0, S = 0.0, Q = 0.0;
-                for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS)
-                    if (p.grp_task[j] == i0 + ii) {
-                        N += p.grp_nsq[3 * j];
-                        S += p.grp_nsq[3 * j + 1];
-                        Q += p.grp_nsq[3 * j + 2];
+                if (one_per_thread) {
+                    if (my_task == i0 + ii) {
+                        N = my_N;
+                        S = my_S;
+                        Q = my_Q;
                     }
+                } else {
+                    for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS)
+                        if (p.grp_task[j] == i0 + ii) {
+                            N += p.grp_nsq[3 * j];
+                            S += p.grp_nsq[3 * j + 1];
+                            Q += p.grp_nsq[3 * j + 2];
+                        }
+                }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     N += __shfl_down_sync(0xffffffffu, N, o);
