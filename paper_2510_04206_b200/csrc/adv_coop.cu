@@ -1127,12 +1127,34 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
 
     // phase B2: global group starts = block prefix + local; scatter member lists
     block_prefix_smem(p.blk_grp, G, s_pre, s_w);
-    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
-        const int32_t j = p.group_id[g], i = p.task_id[g];
-        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) continue;
-        const int64_t owner = part_owner(p.n_groups, j, G);
-        const int32_t slot = atomicAdd(&p.grp_fill[j], 1);
-        p.members[s_pre[owner] + p.grp_start[j] + slot] = (int32_t)g;
+    {
+        // BATCH trajectories per thread at a time: their loads, then their slot atomics are
+        // issued together (one dependent round trip per batch instead of per trajectory)
+        constexpr int BATCH = 4;
+        for (int64_t g0 = gtid; g0 < p.n_traj; g0 += BATCH * gstride) {
+            int32_t jj[BATCH], sl[BATCH], gs[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int64_t g = g0 + u * gstride;
+                jj[u] = -1;
+                if (g < p.n_traj) {
+                    const int32_t j = p.group_id[g], i = p.task_id[g];
+                    if (j >= 0 && j < p.n_groups && i >= 0 && i < p.n_tasks) jj[u] = j;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                if (jj[u] >= 0) {
+                    sl[u] = atomicAdd(&p.grp_fill[jj[u]], 1);
+                    gs[u] = p.grp_start[jj[u]];
+                }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                if (jj[u] >= 0) {
+                    const int64_t owner = part_owner(p.n_groups, jj[u], G);
+                    p.members[s_pre[owner] + gs[u] + sl[u]] = (int32_t)(g0 + u * gstride);
+                }
+        }
     }
     grid.sync();
     phase_mark(4);
