@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--all-masked", action="store_true",
+                    help="every token a loss token (SURVEY 8(d): the compute upper bound)")
     return ap.parse_args()
 
 
@@ -112,9 +114,11 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- inputs
-def build_inputs(cfg, rank, world):
+def build_inputs(cfg, rank, world, all_masked=False):
     """Global batch structure; this rank's shard (whole groups, LPT on masked tokens)."""
     b = synth.make_structure(cfg)
+    if all_masked:
+        b["loss_mask"] = np.ones_like(b["loss_mask"])
     if world > 1:
         ng = np.zeros(len(b["task_id"]), np.int64)
         off = b["traj_offsets"]
@@ -169,7 +173,7 @@ def run_native(args, cfg, world, rank, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
-    gb, lb = build_inputs(cfg, rank, world)
+    gb, lb = build_inputs(cfg, rank, world, args.all_masked)
     T = int(lb["T"])
     d, V = cfg.d, cfg.V
     n_traj = len(lb["task_id"])
@@ -357,6 +361,7 @@ def run_native(args, cfg, world, rank, local_rank):
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
                    "grad_W_collective": c3,
+                   "mask": "all tokens (--all-masked)" if args.all_masked else "synthetic multi-turn (~40% assistant)",
                    "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
         "masked_tokens_per_s": T_eff_global / (ms / 1e3),
