@@ -447,8 +447,8 @@ def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
     out = {"latency_us": ms * 1e3, "graph_latency_us": None if gms is None else gms * 1e3,
            "alg_bytes": by, "GBps": by / (ms / 1e3) / 1e9,
            "frac_hbm": by / (ms / 1e3) / 1e9 / hbm_gbs, "cold_l2": True,
-           "note": "launch-latency bound at this size (empty cooperative launch + 2 grid "
-                   "barriers ~8 us); bandwidth_point is the HBM-bound regime"}
+           "note": "launch-latency bound at this size (an empty cooperative launch is ~5 us, "
+                   "a grid barrier ~1.5 us); bandwidth_point is the HBM-bound regime"}
     try:
         sb = synth.make_sweep_structure(1 << 27)
         sbd = {k: (torch.from_numpy(np.ascontiguousarray(v)).to(dev) if isinstance(v, np.ndarray)
