@@ -700,10 +700,13 @@ static int comm_reserve_sms() {
     return std::min(v, num_sms() / 2);
 }
 
-// forward row chunks (AGENTRL_FWD_CHUNKS, default 4, 1 = no overlap of the merge)
+// forward row chunks (AGENTRL_FWD_CHUNKS; default 1 = the merge runs after the whole forward).
+// With 4 chunks the merge of chunk c overlaps the forward of chunk c+1, but the co-resident
+// merge blocks slow the forward GEMM about as much as they hide (live forward 51 vs 47.7 ms at
+// glm9b), and the last merge stays exposed: 1 chunk measured 0.7 ms/step faster (3 A/B pairs)
 static int fwd_chunks() {
     static int v = -1;
-    if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 4), MAX_FWD_CHUNKS);
+    if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 1), MAX_FWD_CHUNKS);
     return v;
 }
 // size ratio of consecutive forward row chunks (AGENTRL_FWD_RATIO, default 1 = equal; 0.5 and

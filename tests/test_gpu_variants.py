@@ -7,7 +7,7 @@ reads the AGENTRL_* switches once):
   AGENTRL_ADV_COOP=0        3-kernel adv-norm path
   AGENTRL_GROUP_M / _BWD    raster group sizes
   AGENTRL_FWD_KSUB=1        one 64-wide K atom per forward stage
-  AGENTRL_FWD_CHUNKS=n      forward row chunks (merge overlap)
+  AGENTRL_FWD_CHUNKS=n      forward row chunks (merge overlap; default 1)
   AGENTRL_THROTTLE_LEAD=n   backward progress throttle (0 = off; 1 with EVERY=1: lockstep)
 Schedule-only switches must not change a bit of the result (test_schedule_variants_bitwise).
 """
@@ -37,7 +37,7 @@ VARIANTS = [
 SCHEDULE_ONLY = [
     {"AGENTRL_THROTTLE_LEAD": "0"},
     {"AGENTRL_THROTTLE_LEAD": "1", "AGENTRL_THROTTLE_EVERY": "1"},
-    {"AGENTRL_FWD_CHUNKS": "1"},
+    {"AGENTRL_FWD_CHUNKS": "4"},
     {"AGENTRL_FWD_CHUNKS": "8"},
     {"AGENTRL_FWD_KSUB": "1"},
     {"AGENTRL_GEMM_SCHED": "static"},
