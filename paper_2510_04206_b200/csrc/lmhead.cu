@@ -667,14 +667,15 @@ static SideStream& side_stream() {
 }
 
 // backward-GEMM progress throttle: max lead in k-blocks over the slowest pair
-// (AGENTRL_THROTTLE_LEAD, default 192, 0 = off) checked every AGENTRL_THROTTLE_EVERY k-blocks.
-// glm9b: grad GEMM HBM reads 144/151 -> 67/64 GB, +3% cycles, step 157 -> 150 ms on the
-// power-capped part (profiles/r01_throttle.txt)
+// (AGENTRL_THROTTLE_LEAD, default 96, 0 = off) checked every AGENTRL_THROTTLE_EVERY k-blocks.
+// glm9b: grad GEMM HBM reads 144/151 -> 67/64 GB at lead 192, +3% cycles, step 157 -> 150 ms on
+// the power-capped part (profiles/r01_throttle.txt); lead 96 then measured 0.6 ms/step faster
+// than 192 (less DRAM, higher clock; 2 x 3 interleaved A/B rounds, profiles/r01_ab_lead.txt)
 static int throttle_lead() {
     static int v = -2;
     if (v == -2) {
         const char* e = getenv("AGENTRL_THROTTLE_LEAD");
-        v = e ? atoi(e) : 192;
+        v = e ? atoi(e) : 96;
     }
     return gemm_dynamic() ? v : 0;
 }
