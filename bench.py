@@ -174,6 +174,13 @@ def run_native(args, cfg, world, rank, local_rank):
         return float(tt.item())
 
     gb, lb = build_inputs(cfg, rank, world, args.all_masked)
+    # analysis mode: one GPU runs rank 0's LPT shard of an n-GPU run, no communication (the
+    # per-rank compute of the scaling configuration); the line then describes that shard
+    shard_of = int(os.environ.get("AGENTRL_BENCH_SHARD", "0"))
+    if world == 1 and shard_of > 1:
+        _, lb = build_inputs(cfg, 0, shard_of, args.all_masked)
+        lb = {k: v for k, v in lb.items() if k != "token_index"}
+        gb = lb
     T = int(lb["T"])
     d, V = cfg.d, cfg.V
     n_traj = len(lb["task_id"])
@@ -361,6 +368,8 @@ def run_native(args, cfg, world, rank, local_rank):
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
                    "grad_W_collective": c3,
+                   **({"shard": f"rank 0 of {shard_of} (LPT), no communication"}
+                      if world == 1 and shard_of > 1 else {}),
                    "mask": "all tokens (--all-masked)" if args.all_masked else "synthetic multi-turn (~40% assistant)",
                    "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
