@@ -710,6 +710,17 @@ static int fwd_chunks() {
     if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 1), MAX_FWD_CHUNKS);
     return v;
 }
+// one GPU: grad_hidden and grad_W on two prioritised streams so their tails overlap
+// (AGENTRL_BWD_OVERLAP=1; off: measured neutral, 155.75 vs 155.46 ms full size and 20.50 vs
+// 20.43 ms at the 1/8 shard, interleaved A/B)
+static bool bwd_overlap() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("AGENTRL_BWD_OVERLAP");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 // size ratio of consecutive forward row chunks (AGENTRL_FWD_RATIO, default 1 = equal; 0.5 and
 // 0.35 shorten the last, un-overlapped merge but slow the forward as much: same step time)
 static float fwd_ratio() {
@@ -929,7 +940,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     PeerWindow* pw = (comm && a->grad_W_mode == 2) ? comm_peer(comm) : nullptr;
     if (pw && !peer_window_fits(pw, V, d)) pw = nullptr;
     if (pw && (rc = peer_guard(pw, d_status, stream))) return rc;  // owners done with epoch-1
-    {
+    auto launch_grad_W = [&](cudaStream_t s) -> int {
         GemmArgs g{};
         if (pw) {
             g.peer_out = pw->d_staging;
@@ -955,25 +966,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.gw = o->grad_W;
         g.ldo = d;
         const int64_t tiles = ceil_div(V, GEMM_BM) * ceil_div(d, GEMM_BN);
-        rc = gemm_wide_n() ? launch_gemm<EPI_GRADW, true, true, 2>(mG_MN, mH_MN, g, tiles, stream)
-                           : launch_gemm<EPI_GRADW, true, true, 1>(mG_MN, mH_MN, g, tiles, stream);
-        if (rc) return rc;
-    }
-    // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
-    SideStream* ss = nullptr;
-    if (comm && (a->grad_W_mode == 1 || a->grad_W_mode == 2)) {
-        ss = &side_stream();
-        AG_CUDA(cudaEventRecord(ss->e0, stream));
-        AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
-        rc = pw ? peer_signal_reduce(pw, o->grad_W, V, d, d_status, ss->s)  // fused C3 tail
-             : a->grad_W_mode == 1
-                 ? comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s)
-                 : comm_reduce_scatter_f32(comm, o->grad_W, (size_t)V * d, ss->s);  // FSDP shard
-        if (rc) return rc;
-        AG_CUDA(cudaEventRecord(ss->e1, ss->s));
-    }
+        return gemm_wide_n() ? launch_gemm<EPI_GRADW, true, true, 2>(mG_MN, mH_MN, g, tiles, s)
+                             : launch_gemm<EPI_GRADW, true, true, 1>(mG_MN, mH_MN, g, tiles, s);
+    };
     // ---- K8 grad_hidden = s G W   (M = T_eff, N = d, K = V), scattered to idx rows
-    {
+    auto launch_grad_hidden = [&](cudaStream_t s, int rsv) -> int {
         GemmArgs g{};
         g.m_dev = rows_dev;
         g.N = d;
@@ -992,30 +989,59 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
         g.ldo = d;
         const int64_t tiles = max_m_tiles * ceil_div(d, GEMM_BN);
-        // with C3 in flight on the side stream, leave SMs for the NCCL kernel so the
-        // collective overlaps this GEMM instead of queueing behind its persistent CTAs
-        const int rsv = ss && comm_world(comm) > 1 ? comm_reserve_sms() : 0;
+        int r;
         if (vp) {
             // this rank's vocabulary columns give a partial grad_h: fp32 rows (the EPI_GRADW
             // epilogue, row = compacted row), summed over the group, then scattered as bf16
             float* gh32 = reinterpret_cast<float*>(ws + w.vp_gh);
             g.gw = gh32;
-            rc = gemm_wide_n()
-                     ? launch_gemm<EPI_GRADW, false, true, 2>(mG_K, mW_MN, g, tiles, stream, 0)
-                     : launch_gemm<EPI_GRADW, false, true, 1>(mG_K, mW_MN, g, tiles, stream, 0);
-            if (rc) return rc;
-            if ((rc = comm_allreduce_f32(comm, gh32, (size_t)rows_cap * d, stream))) return rc;
-            k_vp_scatter<<<num_sms() * 4, 256, 0, stream>>>(rows_dev, d, idx_dev, gh32,
-                                                           reinterpret_cast<__nv_bfloat16*>(o->grad_hidden));
+            r = gemm_wide_n() ? launch_gemm<EPI_GRADW, false, true, 2>(mG_K, mW_MN, g, tiles, s, 0)
+                              : launch_gemm<EPI_GRADW, false, true, 1>(mG_K, mW_MN, g, tiles, s, 0);
+            if (r) return r;
+            if ((r = comm_allreduce_f32(comm, gh32, (size_t)rows_cap * d, s))) return r;
+            k_vp_scatter<<<num_sms() * 4, 256, 0, s>>>(rows_dev, d, idx_dev, gh32,
+                                                       reinterpret_cast<__nv_bfloat16*>(o->grad_hidden));
             count_launch();
             AG_CUDA(cudaGetLastError());
-        } else {
-            rc = gemm_wide_n()
-                     ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, stream, rsv)
-                     : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, stream, rsv);
-            if (rc) return rc;
+            return AGENTRL_OK;
         }
+        return gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, s, rsv)
+                             : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, s, rsv);
+    };
+    SideStream* ss = nullptr;
+    if (!comm && bwd_overlap()) {
+        // one GPU: grad_hidden (fewer, longer tiles) on the high-priority stream takes every SM
+        // first; grad_W on the low-priority stream starts on the SMs grad_hidden's last wave
+        // leaves idle, so the two GEMMs' tails overlap
+        ForkStreams& f = fork_streams();
+        AG_CUDA(cudaEventRecord(f.fork, stream));
+        AG_CUDA(cudaStreamWaitEvent(f.hi, f.fork, 0));
+        AG_CUDA(cudaStreamWaitEvent(f.lo, f.fork, 0));
+        if ((rc = launch_grad_hidden(f.hi, 0))) return rc;
+        if ((rc = launch_grad_W(f.lo))) return rc;
+        AG_CUDA(cudaEventRecord(f.ev[0], f.hi));
+        AG_CUDA(cudaEventRecord(f.ev[1], f.lo));
+        AG_CUDA(cudaStreamWaitEvent(stream, f.ev[0], 0));
+        AG_CUDA(cudaStreamWaitEvent(stream, f.ev[1], 0));
+        return AGENTRL_OK;
     }
+    if ((rc = launch_grad_W(stream))) return rc;
+    // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
+    if (comm && (a->grad_W_mode == 1 || a->grad_W_mode == 2)) {
+        ss = &side_stream();
+        AG_CUDA(cudaEventRecord(ss->e0, stream));
+        AG_CUDA(cudaStreamWaitEvent(ss->s, ss->e0, 0));
+        rc = pw ? peer_signal_reduce(pw, o->grad_W, V, d, d_status, ss->s)  // fused C3 tail
+             : a->grad_W_mode == 1
+                 ? comm_allreduce_f32(comm, o->grad_W, (size_t)V * d, ss->s)
+                 : comm_reduce_scatter_f32(comm, o->grad_W, (size_t)V * d, ss->s);  // FSDP shard
+        if (rc) return rc;
+        AG_CUDA(cudaEventRecord(ss->e1, ss->s));
+    }
+    // with C3 in flight on the side stream, leave SMs for the NCCL kernel so the collective
+    // overlaps this GEMM instead of queueing behind its persistent CTAs
+    if ((rc = launch_grad_hidden(stream, ss && comm_world(comm) > 1 ? comm_reserve_sms() : 0)))
+        return rc;
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
     return AGENTRL_OK;
 }

@@ -39,6 +39,7 @@ SCHEDULE_ONLY = [
     {"AGENTRL_THROTTLE_LEAD": "1", "AGENTRL_THROTTLE_EVERY": "1"},
     {"AGENTRL_FWD_CHUNKS": "4"},
     {"AGENTRL_FWD_CHUNKS": "8"},
+    {"AGENTRL_BWD_OVERLAP": "1"},
     {"AGENTRL_FWD_KSUB": "1"},
     {"AGENTRL_GEMM_SCHED": "static"},
     {"AGENTRL_GEMM_FULLGRID": "1"},
