@@ -61,7 +61,7 @@ __global__ void k_peer_signal(int64_t* const* peer_flags, int world, int rank, l
 // every writer its slot may be rewritten (flags[1][owner] on the writer)
 __global__ void __launch_bounds__(256)
     k_peer_reduce(const int64_t* my_flags, int64_t* const* peer_flags, int world, int rank,
-                  long long epoch, const float* __restrict__ staging, float* __restrict__ out,
+                  long long epoch, const float* staging, float* __restrict__ out,
                   int64_t n, int32_t* done_ctr, int32_t* d_status) {
     __shared__ int ok;
     if (threadIdx.x == 0) {
@@ -75,9 +75,11 @@ __global__ void __launch_bounds__(256)
         float4* o4 = reinterpret_cast<float4*>(out);
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
              i += (int64_t)gridDim.x * blockDim.x) {
-            float4 acc = s4[i];
+            // L2 loads (ld.global.cg): the slots are written by peers while this kernel waits,
+            // so the non-coherent read-only path is not allowed here
+            float4 acc = __ldcg(s4 + i);
             for (int r = 1; r < world; ++r) {
-                const float4 v = s4[(int64_t)r * n4 + i];
+                const float4 v = __ldcg(s4 + (int64_t)r * n4 + i);
                 acc.x += v.x;
                 acc.y += v.y;
                 acc.z += v.z;
