@@ -127,9 +127,10 @@ struct PeerWindow {
     float** d_staging = nullptr;   // device [world]: every rank's window (IPC-mapped)
     int64_t** d_flags = nullptr;   // device [world]: every rank's flags
     int32_t* done_ctr = nullptr;   // reduce-kernel block counter
+    int64_t* d_epoch = nullptr;    // device [1]: the current epoch (advanced by the guard
+                                   // kernel, so a captured step replays with fresh epochs)
     void* opened[MAX_RANKS] = {};
     void* opened_flags[MAX_RANKS] = {};
-    long long epoch = 0;
 };
 int peer_window_create(agentrl_comm c, size_t bytes, PeerWindow** out);  // collective
 void peer_window_destroy(PeerWindow* pw);

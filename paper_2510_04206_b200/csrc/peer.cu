@@ -13,6 +13,8 @@
 //           writer's consumed[o];
 //   guard   before the next GEMM writes into owner o's window, rank r waits until consumed[o]
 //           >= e - 1 (o has finished reading the previous epoch's slots).
+// The epoch lives in device memory: the guard kernel advances it and the signal and reduce
+// kernels read it (stream-ordered after the guard), so a captured step can be replayed.
 // No cycle exists (writers never wait for anything but the previous epoch's readers), and
 // every wait is bounded: on timeout the kernel sets AGENTRL_ST_COMM_TIMEOUT and returns instead
 // of hanging the GPU.
@@ -50,8 +52,10 @@ __device__ bool wait_flags(const int64_t* flags, int n, long long want) {
 }
 
 // rank r -> every owner o: "my tiles of epoch e are in your window"  (flags[0][r])
-__global__ void k_peer_signal(int64_t* const* peer_flags, int world, int rank, long long epoch) {
+__global__ void k_peer_signal(int64_t* const* peer_flags, int world, int rank,
+                              const int64_t* d_epoch) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const long long epoch = *d_epoch;
         __threadfence_system();
         for (int o = 0; o < world; ++o) st_release_sys(peer_flags[o] + rank, epoch);
     }
@@ -61,10 +65,12 @@ __global__ void k_peer_signal(int64_t* const* peer_flags, int world, int rank, l
 // every writer its slot may be rewritten (flags[1][owner] on the writer)
 __global__ void __launch_bounds__(256)
     k_peer_reduce(const int64_t* my_flags, int64_t* const* peer_flags, int world, int rank,
-                  long long epoch, const float* staging, float* __restrict__ out,
+                  const int64_t* d_epoch, const float* staging, float* __restrict__ out,
                   int64_t n, int32_t* done_ctr, int32_t* d_status) {
     __shared__ int ok;
+    __shared__ long long epoch;
     if (threadIdx.x == 0) {
+        epoch = *d_epoch;
         ok = wait_flags(my_flags, world, epoch);
         if (!ok) atomicOr(d_status, AGENTRL_ST_COMM_TIMEOUT);
     }
@@ -102,10 +108,13 @@ __global__ void __launch_bounds__(256)
 
 // writer: before writing into the owners' windows for epoch e, every owner must have consumed
 // epoch e - 1 (flags[1][o] on this rank)
-__global__ void k_peer_guard(const int64_t* my_flags, int world, long long prev,
+__global__ void k_peer_guard(const int64_t* my_flags, int world, int64_t* d_epoch,
                              int32_t* d_status) {
-    if (threadIdx.x == 0 && blockIdx.x == 0 && prev > 0) {
-        if (!wait_flags(my_flags + world, world, prev)) atomicOr(d_status, AGENTRL_ST_COMM_TIMEOUT);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const long long prev = *d_epoch;
+        *d_epoch = prev + 1;  // this call's epoch (every rank makes the same sequence of calls)
+        if (prev > 0 && !wait_flags(my_flags + world, world, prev))
+            atomicOr(d_status, AGENTRL_ST_COMM_TIMEOUT);
     }
 }
 
@@ -185,7 +194,9 @@ int peer_window_create(agentrl_comm c, size_t bytes, PeerWindow** out) {
         cudaMemcpy(pw->d_flags, fl.data(), sizeof(int64_t*) * R, cudaMemcpyHostToDevice) !=
             cudaSuccess ||
         cudaMalloc(&pw->done_ctr, sizeof(int32_t)) != cudaSuccess ||
-        cudaMemset(pw->done_ctr, 0, sizeof(int32_t)) != cudaSuccess)
+        cudaMemset(pw->done_ctr, 0, sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&pw->d_epoch, sizeof(int64_t)) != cudaSuccess ||
+        cudaMemset(pw->d_epoch, 0, sizeof(int64_t)) != cudaSuccess)
         return fail(AGENTRL_ERR_CUDA);
     if (xch) cudaFree(xch);
     if (s) cudaStreamDestroy(s);
@@ -205,6 +216,7 @@ void peer_window_destroy(PeerWindow* pw) {
     if (pw->d_staging) cudaFree(pw->d_staging);
     if (pw->d_flags) cudaFree(pw->d_flags);
     if (pw->done_ctr) cudaFree(pw->done_ctr);
+    if (pw->d_epoch) cudaFree(pw->d_epoch);
     delete pw;
 }
 
@@ -215,8 +227,7 @@ bool peer_window_fits(const PeerWindow* pw, int32_t V, int32_t d) {
 }
 
 int peer_guard(PeerWindow* pw, int32_t* d_status, cudaStream_t s) {
-    ++pw->epoch;  // this call's epoch (every rank makes the same sequence of calls)
-    k_peer_guard<<<1, 32, 0, s>>>(pw->flags, pw->world, pw->epoch - 1, d_status);
+    k_peer_guard<<<1, 32, 0, s>>>(pw->flags, pw->world, pw->d_epoch, d_status);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? AGENTRL_OK : AGENTRL_ERR_CUDA;
 }
@@ -225,10 +236,10 @@ int peer_signal_reduce(PeerWindow* pw, float* grad_W, int32_t V, int32_t d, int3
                        cudaStream_t s) {
     const int R = pw->world;
     const int64_t rows = V / R, n = rows * (int64_t)d;
-    k_peer_signal<<<1, 32, 0, s>>>(pw->d_flags, R, pw->rank, pw->epoch);
+    k_peer_signal<<<1, 32, 0, s>>>(pw->d_flags, R, pw->rank, pw->d_epoch);
     count_launch();
     const int grid = std::max(1, std::min<int>(num_sms() / 4, (int)((n / 4 + 255) / 256)));
-    k_peer_reduce<<<grid, 256, 0, s>>>(pw->flags, pw->d_flags, R, pw->rank, pw->epoch, pw->staging,
+    k_peer_reduce<<<grid, 256, 0, s>>>(pw->flags, pw->d_flags, R, pw->rank, pw->d_epoch, pw->staging,
                                        grad_W + (int64_t)pw->rank * n, n, pw->done_ctr, d_status);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? AGENTRL_OK : AGENTRL_ERR_CUDA;
