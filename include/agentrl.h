@@ -286,7 +286,10 @@ int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn
  * system-scope flag barrier the owner sums the world slots in rank order (deterministic) into
  * its grad_W shard; the collective path is not used.  Every wait is bounded: a peer that never
  * arrives sets AGENTRL_ST_COMM_TIMEOUT instead of hanging.  AGENTRL_C3_P2P=0 in the
- * environment selects the collective path.  The window is freed by agentrl_comm_destroy (the
+ * environment selects the collective path.  Every rank must make the same sequence of
+ * grad_W_mode = 2 calls on the communicator: each call is one epoch of the flag protocol, and
+ * the epoch counter is kept in device memory (advanced by the call's first kernel), so the call
+ * may be captured in a CUDA graph and replayed.  The window is freed by agentrl_comm_destroy (the
  * one place the library allocates persistent device memory: it must be IPC-exportable). */
 int agentrl_comm_enable_peer_window(agentrl_comm comm, size_t bytes_per_rank);
 
