@@ -910,7 +910,16 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         // merge + loss terms + G (in place) of this chunk; chunks merged beside the next
         // forward chunk keep a small footprint (2 blocks per SM next to the GEMM CTA)
         size_t smem = sizeof(float) * (size_t)w.n_tiles;
-        int grid = num_sms() * (c + 1 < n_fc ? 2 : 8);
+        // one wave: every block resident, so the grid-stride row split has no second-wave tail
+        // (8 blocks per SM at 40 registers left a quarter of the blocks for a second wave)
+        static int merge_occ = 0;
+        if (merge_occ <= 0 &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&merge_occ, k_merge_g, MERGE_THREADS,
+                                                          sizeof(float) * 4096) != cudaSuccess)
+            merge_occ = 4;
+        static const int merge_bps = env_int("AGENTRL_MERGE_BPS", 0);  // A/B override
+        if (merge_bps > 0) merge_occ = merge_bps;
+        int grid = num_sms() * (c + 1 < n_fc ? 2 : std::max(1, merge_occ));
         ProfScope ps(KID_MERGE, s_mrg);
         k_merge_g<<<grid, MERGE_THREADS, smem, s_mrg>>>(
             rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,

@@ -8,6 +8,7 @@ reads the AGENTRL_* switches once):
   AGENTRL_GROUP_M / _BWD    raster group sizes
   AGENTRL_FWD_KSUB=1        one 64-wide K atom per forward stage
   AGENTRL_FWD_CHUNKS=n      forward row chunks (merge overlap; default 1)
+  AGENTRL_MERGE_BPS=n       merge blocks per SM (default: the occupancy limit, one wave)
   AGENTRL_THROTTLE_LEAD=n   backward progress throttle (0 = off; 1 with EVERY=1: lockstep)
 Schedule-only switches must not change a bit of the result (test_schedule_variants_bitwise).
 """
@@ -40,6 +41,8 @@ SCHEDULE_ONLY = [
     {"AGENTRL_FWD_CHUNKS": "4"},
     {"AGENTRL_FWD_CHUNKS": "8"},
     {"AGENTRL_BWD_OVERLAP": "1"},
+    {"AGENTRL_MERGE_BPS": "1"},
+    {"AGENTRL_MERGE_BPS": "8"},
     {"AGENTRL_FWD_KSUB": "1"},
     {"AGENTRL_GEMM_SCHED": "static"},
     {"AGENTRL_GEMM_FULLGRID": "1"},
