@@ -270,8 +270,16 @@ __global__ void __launch_bounds__(256)
 
 // ---------------------------------------------------------------------------- K6 merge + G
 constexpr int MERGE_THREADS = 256;
+#ifndef MERGE_MINB
+#define MERGE_MINB 0  // 0: no residency hint
+#endif
+#if MERGE_MINB > 0
+#define MERGE_BOUNDS __launch_bounds__(MERGE_THREADS, MERGE_MINB)
+#else
+#define MERGE_BOUNDS __launch_bounds__(MERGE_THREADS)
+#endif
 
-__global__ void __launch_bounds__(MERGE_THREADS)
+__global__ void MERGE_BOUNDS
     k_merge_g(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
               int32_t V, int32_t n_tiles, const float2* __restrict__ part,
               const float* __restrict__ zy, const int32_t* __restrict__ tgt_c,
