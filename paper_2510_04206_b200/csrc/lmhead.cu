@@ -465,10 +465,10 @@ __global__ void __launch_bounds__(1024)
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
     double a = 0.0, b = 0.0, c = 0.0, e = 0.0, k = 0.0;
-    // contiguous per-thread segments, fixed order
-    const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
-    const int64_t lo = min(rows, (int64_t)threadIdx.x * per), hi = min(rows, lo + per);
-    for (int64_t p = lo; p < hi; ++p) {
+    // thread t sums rows t, t + 1024, ... in order (coalesced loads; a fixed order, so the
+    // result is deterministic), then a fixed shuffle tree and a fixed warp order
+#pragma unroll 4
+    for (int64_t p = threadIdx.x; p < rows; p += blockDim.x) {
         a += row_term[p];  // w_t (-term_t + beta KL_t)
         b += (double)row_rho[p];
         c += (double)row_logp[p];
