@@ -213,12 +213,6 @@ def run_native(args, cfg, world, rank, local_rank):
     # C3 fused into the grad_W GEMM epilogue over peer memory (CUDA IPC windows; include/
     # agentrl.h agentrl_comm_enable_peer_window), unless AGENTRL_C3_P2P=0 or the mapping fails
     c3 = {0: "none", 1: "all-reduce (collective)", 2: "reduce-scatter (collective)"}[gw_mode]
-    if gw_mode == 2 and os.environ.get("AGENTRL_C3_P2P", "1") != "0":
-        try:
-            comm.enable_peer_window(V * d * 4)
-            c3 = "reduce-scatter fused into the grad_W GEMM epilogue (P2P stores)"
-        except RuntimeError as e:  # fall back to the collective
-            print(f"peer window unavailable ({e}); collective reduce-scatter", file=sys.stderr)
     step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm,
                    grad_W_mode=gw_mode)
     # behaviour log-probs: one untimed forward (old = 0), then old = logp + delta
@@ -227,6 +221,38 @@ def run_native(args, cfg, world, rank, local_rank):
     torch.cuda.synchronize()
     delta = torch.from_numpy(synth.make_deltas(T, synth.SEED_BASE + 9 + rank).astype(np.float32))
     old = (step.logp + delta.to(dev)) * bd["loss_mask"].float()
+    c3_check = None
+    if gw_mode == 2 and os.environ.get("AGENTRL_C3_P2P", "1") != "0":
+        # C3 fused into the grad_W GEMM epilogue over peer memory (CUDA IPC windows; include/
+        # agentrl.h agentrl_comm_enable_peer_window).  Validated on first use: one step with the
+        # collective reduce-scatter, one with the fused path; the rank's grad_W shard must agree
+        # on every rank (max over ranks), else the collective path is kept.
+        rows = V // world
+        step(bd, hid, W, target, old)
+        torch.cuda.synchronize()
+        ref_shard = step.grad_W[rank * rows:(rank + 1) * rows].clone()
+        err = float("inf")
+        try:
+            comm.enable_peer_window(V * d * 4)
+            step(bd, hid, W, target, old)
+            torch.cuda.synchronize()
+            got = step.grad_W[rank * rows:(rank + 1) * rows]
+            err = float(((got - ref_shard).abs().max() / ref_shard.abs().max().clamp_min(1e-30))
+                        .item())
+            if int(step.status.item()) & ag.ST_COMM_TIMEOUT:
+                err = float("inf")
+        except RuntimeError as e:
+            print(f"peer window unavailable ({e})", file=sys.stderr)
+        err = max_over_ranks(err)
+        c3_check = {"max_rel_diff_vs_collective": err, "ok": err <= 1e-5}
+        if err <= 1e-5:
+            c3 = "reduce-scatter fused into the grad_W GEMM epilogue (P2P stores)"
+        else:
+            print(f"fused C3 self-check failed (max rel diff {err}); collective reduce-scatter",
+                  file=sys.stderr)
+            dist.barrier()
+            comm.enable_peer_window(0)
+        step.status.zero_()
     T_eff_local = int(lb["loss_mask"].astype(bool).sum())
     T_eff_global = int(gb["loss_mask"].astype(bool).sum())
     T_global = int(gb["T"])
@@ -367,7 +393,7 @@ def run_native(args, cfg, world, rank, local_rank):
         "config": {"workload": cfg.name, "T": T_global, "T_eff": T_eff_global, "d": d, "V": V,
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
-                   "grad_W_collective": c3,
+                   "grad_W_collective": c3, "c3_self_check": c3_check,
                    **({"shard": f"rank 0 of {shard_of} (LPT), no communication"}
                       if world == 1 and shard_of > 1 else {}),
                    "mask": "all tokens (--all-masked)" if args.all_masked else "synthetic multi-turn (~40% assistant)",

@@ -178,9 +178,12 @@ typedef struct {
      * Aggregation weights w_t (loss = sum_t w_t (-term_t + beta KL_t)):
      *   tok_weight != NULL : w_t = tok_weight[t] (any caller-defined aggregation)
      *   else loss_agg == 0 : w_t = 1 / N (token-level mean; default)
-     *   else loss_agg == 1 : w_t = 1 / (n_seq * n_g(t)), n_seq = trajectories with masked
-     *                        tokens (global), n_g = the trajectory's masked tokens: mean over
-     *                        sequences of per-sequence token means (GRPO's 1/K).
+     *   else loss_agg == 1 : w_t = 1 / (G * K_j * n_g(t)): the GRPO objective
+     *                        E_{i,j}[ 1/K_{i,j} sum_g term_g ] of P:1247-1256 with token-level
+     *                        ratios; term_g = the mean of term_t over trajectory g's n_g masked
+     *                        tokens (0 if n_g = 0), K_j = every member of t's group j (members
+     *                        without masked tokens included), G = groups with at least one
+     *                        member, summed over ranks (R7b).
      *                        agentrl_grpo_step only (needs the batch descriptor). */
     float kl_beta;                     /* >= 0 */
     int32_t loss_agg;                  /* 0 or 1 */
@@ -247,6 +250,22 @@ int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp /*[T]*/,
                         float* entropy /*[T] or NULL*/, void* ws, size_t ws_bytes,
                         int32_t* d_status, agentrl_stream stream);
 
+/*
+ * Test / debug export of part 1's integer bookkeeping (north_star: bit-exact vs the oracle).
+ * Copies, stream-ordered after the last agentrl_task_adv_norm / agentrl_grpo_step call that
+ * used workspace `ws` with the same (T, n_traj, n_groups, n_tasks), into caller buffers:
+ *   n_g  [n_traj]   int32: masked tokens of each trajectory, the per-trajectory part of the
+ *                   token set A_i^tok
+ *   K    [n_groups] int32: members of each group, K_{i,j}
+ *   idx  [T]        int32: stable compaction, the positions of the local masked tokens in
+ *                   increasing order (written by agentrl_grpo_step only; the first *rows
+ *                   entries are defined)
+ *   rows [1]        int64: the local masked-token count (entries of idx)
+ * Every output may be NULL.  Device-to-device copies only; no kernel. */
+int agentrl_debug_bookkeeping(const void* ws, int64_t T, int32_t n_traj, int32_t n_groups,
+                              int32_t n_tasks, int32_t* n_g, int32_t* K, int32_t* idx,
+                              int64_t* rows, agentrl_stream stream);
+
 /* ---- communicator (NCCL over NVLink; loaded lazily with dlopen) ----------
  * Rank 0 calls agentrl_comm_unique_id, the caller broadcasts the 128 bytes
  * (e.g. over a torch.distributed process group), then every rank calls
@@ -290,7 +309,9 @@ int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn
  * grad_W_mode = 2 calls on the communicator: each call is one epoch of the flag protocol, and
  * the epoch counter is kept in device memory (advanced by the call's first kernel), so the call
  * may be captured in a CUDA graph and replayed.  The window is freed by agentrl_comm_destroy (the
- * one place the library allocates persistent device memory: it must be IPC-exportable). */
+ * one place the library allocates persistent device memory: it must be IPC-exportable), or by
+ * a call with bytes_per_rank = 0, which returns to the collective path (every rank must make it,
+ * after its last grad_W_mode = 2 call has completed). */
 int agentrl_comm_enable_peer_window(agentrl_comm comm, size_t bytes_per_rank);
 
 /* ---- misc -------------------------------------------------------------- */
@@ -315,6 +336,10 @@ const char* agentrl_kernel_name(int id);
  * boundaries: [0] start, [1] after zero/table, [2] counts, [3] group scans, [4] member lists,
  * [5] group advantages + task partials, [6] task moments, [7] apply/compaction end. */
 int agentrl_debug_adv_phase_ns(unsigned long long host_ns8[8]);
+/* Debug: wait episodes of the GEMM progress throttle since the library was loaded, summed over
+ * calls: [0] forward, [1] grad_W, [2] grad_hidden (a pair leader more than the lead ahead of the
+ * slowest active pair sleeps until it is not; one episode per wait). */
+int agentrl_debug_throttle_waits(unsigned long long host3[3]);
 
 #ifdef __cplusplus
 }

@@ -66,8 +66,8 @@ def lib():
         L.oracle_grpo_step.argtypes = [i64, i32, i32, i32, P, P, P, P, P, f64, i32, i32, P, P, P,
                                        P, f64, f64, f64, P, P, P, P, P, P, P]
         L.oracle_logprob_entropy.argtypes = [i64, i32, i32, P, P, P, P, f64, P, P]
-        L.oracle_seq_mean_weights.argtypes = [i64, i32, P, P, P]
-        L.oracle_seq_mean_weights.restype = i64
+        L.oracle_grpo_group_weights.argtypes = [i64, i32, i32, P, P, P, P]
+        L.oracle_grpo_group_weights.restype = i64
         L.oracle_policy_loss_ex.argtypes = [i64, i32, i32, P, P, P, P, P, P, f64, f64, f64, i64,
                                             f64, P, P, P, P, P, P, P]
         L.oracle_num_threads.restype = C.c_int
@@ -201,21 +201,25 @@ def logprob(hidden, W, target, loss_mask, logit_scale=1.0):
     return out
 
 
-def seq_mean_weights(b):
-    """w_t = 1/(n_seq n_g(t)) of the sequence-level aggregation (R7b)."""
+def grpo_group_weights(b):
+    """w_t = 1/(G K_j n_g(t)) of the GRPO group-level aggregation (reading R7b).
+    Returns (w [T], G = number of groups with at least one trajectory)."""
     T = int(b["T"])
     off = _c(b["traj_offsets"], np.int64)
+    gid = _c(b["group_id"], np.int32)
     w = np.zeros(T, np.float64)
-    n_seq = lib().oracle_seq_mean_weights(T, len(off) - 1, _p(off),
-                                          _p(_c(b["loss_mask"], np.uint8)), _p(w))
-    return w, int(n_seq)
+    G = lib().oracle_grpo_group_weights(T, len(off) - 1, int(b["n_groups"]), _p(off), _p(gid),
+                                        _p(_c(b["loss_mask"], np.uint8)), _p(w))
+    if G < 0:
+        raise ValueError("group id outside [0, n_groups)")
+    return w, int(G)
 
 
 def policy_loss_ex(hidden, W, target, adv_tok, old_logp, loss_mask, n_mask_global,
                    eps_lo=0.2, eps_hi=0.2, logit_scale=1.0, kl_beta=0.0, ref_logp=None,
                    weights=None, grads=True):
     """Loss variants (oracle_variants.c): KL penalty (k3) and per-token
-    weights (token mean by default; sequence mean via seq_mean_weights)."""
+    weights (token mean by default; GRPO group mean via grpo_group_weights)."""
     h = _c(hidden, np.float64)
     w = _c(W, np.float64)
     T, d = h.shape

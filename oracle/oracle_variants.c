@@ -8,9 +8,13 @@
  *            (k3 estimator of D_KL(pi_theta || pi_ref), >= 0)         P:1103 / P:1119 (R11b)
  *   loss   = sum_{t masked} w_t ( -term_t + beta KL_t )
  *   w_t    = weights[t] if given, else 1/N (token-level mean, R7)
- * and the sequence-level aggregation of the GRPO objective (1/K_{i,j} sum_g ...):
- *   w_t    = 1 / (n_seq * n_g(t)),  n_seq = number of trajectories with >= 1 masked token,
- *            i.e. the mean over trajectories of each trajectory's token mean (R7b).
+ * and the group-level aggregation of the GRPO objective:
+ *   L_GRPO = E_{i,j} [ 1/K_{i,j} sum_{g=1}^{K_{i,j}} min(rho_{i,j,g} A, clip(..) A) ]
+ *   read with token-level ratios (R7b): the per-trajectory term is the mean of term_t over
+ *   the trajectory's n_g masked tokens (0 when n_g = 0), E_{i,j} is the mean over the G
+ *   groups of the (global) batch that have at least one trajectory, and K_{i,j} counts every
+ *   member of the group (also members without masked tokens), so
+ *   w_t    = 1 / (G * K_{j(t)} * n_{g(t)}).
  * Exact gradient: d loss / d logp_t = -w_t [unclipped] rho A + w_t beta (1 - exp(ref - logp)),
  * so G_{t,v} = c_t (p_{t,v} - [v = y_t]) with c_t = w_t ([unclipped] rho A - beta (1 -
  * exp(ref_t - logp_t)));  grad_h = s G W,  grad_W = s G^T h.  Plain loops, fp64.
@@ -25,23 +29,34 @@
 #define ORV_NONFINITE 2
 #define ORV_NO_TOKENS 32
 
-/* w_t of the sequence-level aggregation (R7b); unmasked tokens get 0.  Returns n_seq. */
-int64_t oracle_seq_mean_weights(int64_t T, int32_t n_traj, const int64_t* traj_offsets,
-                                const uint8_t* loss_mask, double* w_out /*[T]*/) {
-    int64_t n_seq = 0;
+/* w_t of the GRPO group-level aggregation (reading R7b); unmasked tokens get
+ * 0.  Plain loops in the paper's order: K_j = #members of group j, n_g = #masked tokens of
+ * trajectory g, G = #groups with K_j >= 1.  Returns G (or -1 on a group id outside
+ * [0, n_groups)). */
+int64_t oracle_grpo_group_weights(int64_t T, int32_t n_traj, int32_t n_groups,
+                                  const int64_t* traj_offsets, const int32_t* group_id,
+                                  const uint8_t* loss_mask, double* w_out /*[T]*/) {
+    int64_t* K = (int64_t*)calloc((size_t)(n_groups > 0 ? n_groups : 1), sizeof(int64_t));
+    if (!K) return -1;
     for (int32_t g = 0; g < n_traj; ++g) {
-        int64_t n = 0;
-        for (int64_t t = traj_offsets[g]; t < traj_offsets[g + 1]; ++t) n += loss_mask[t] != 0;
-        if (n > 0) n_seq += 1;
+        if (group_id[g] < 0 || group_id[g] >= n_groups) {
+            free(K);
+            return -1;
+        }
+        K[group_id[g]] += 1;
     }
+    int64_t G = 0;
+    for (int32_t j = 0; j < n_groups; ++j) G += K[j] >= 1;
     for (int64_t t = 0; t < T; ++t) w_out[t] = 0.0;
     for (int32_t g = 0; g < n_traj; ++g) {
         int64_t n = 0;
         for (int64_t t = traj_offsets[g]; t < traj_offsets[g + 1]; ++t) n += loss_mask[t] != 0;
         for (int64_t t = traj_offsets[g]; t < traj_offsets[g + 1]; ++t)
-            if (loss_mask[t]) w_out[t] = 1.0 / ((double)n_seq * (double)n);
+            if (loss_mask[t])
+                w_out[t] = 1.0 / ((double)G * (double)K[group_id[g]] * (double)n);
     }
-    return n_seq;
+    free(K);
+    return G;
 }
 
 /* loss_stats[5]: clip fraction, mean rho, mean logp, masked tokens, mean KL */

@@ -44,7 +44,8 @@ EXPORTED = (
     "agentrl_profile_start", "agentrl_profile_stop", "agentrl_kernel_name",
     "agentrl_debug_adv_phase_ns", "agentrl_comm_init_callback",
     "agentrl_logprob_workspace_size", "agentrl_logprob_fwd", "agentrl_comm_set_reduce_scatter",
-    "agentrl_comm_enable_peer_window",
+    "agentrl_comm_enable_peer_window", "agentrl_debug_bookkeeping",
+    "agentrl_debug_throttle_waits",
 )
 NUM_KERNEL_IDS = 12
 
@@ -101,6 +102,7 @@ _lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_
 _lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i32, _i32]
 _lib.agentrl_logprob_workspace_size.restype = _sz
 _lib.agentrl_logprob_fwd.argtypes = [C.POINTER(LogprobArgs), _P, _P, _P, _sz, _P, _P]
+_lib.agentrl_debug_bookkeeping.argtypes = [_P, _i64, _i32, _i32, _i32, _P, _P, _P, _P, _P]
 _lib.agentrl_status_string.argtypes = [C.c_int]
 _lib.agentrl_status_string.restype = C.c_char_p
 _lib.agentrl_version.restype = C.c_int
@@ -214,6 +216,30 @@ def agentrl_logprob_fwd(T, hidden, W_head, target, loss_mask, logp, entropy, ws,
                                     _stream(stream))
 
 
+def agentrl_debug_bookkeeping(ws, T, n_traj, n_groups, n_tasks, n_g=None, K=None, idx=None,
+                              rows=None, stream=None) -> int:
+    """Copy part 1's n_g [n_traj], K_j [n_groups], compaction idx [T] and local row count out
+    of workspace ``ws`` (int32 / int64 device tensors, any may be None)."""
+    return _lib.agentrl_debug_bookkeeping(_ptr(ws), int(T), int(n_traj), int(n_groups),
+                                          int(n_tasks), _ptr(n_g), _ptr(K), _ptr(idx),
+                                          _ptr(rows), _stream(stream))
+
+
+def bookkeeping(ws, T, n_traj, n_groups, n_tasks, stream=None):
+    """(n_g, K, idx[:rows], rows) as host numpy arrays (synchronises the stream)."""
+    import torch
+    dev = ws.device
+    n_g = torch.empty(max(n_traj, 1), dtype=torch.int32, device=dev)
+    K = torch.empty(max(n_groups, 1), dtype=torch.int32, device=dev)
+    idx = torch.empty(max(T, 1), dtype=torch.int32, device=dev)
+    rows = torch.empty(1, dtype=torch.int64, device=dev)
+    _check(agentrl_debug_bookkeeping(ws, T, n_traj, n_groups, n_tasks, n_g, K, idx, rows, stream),
+           "agentrl_debug_bookkeeping")
+    (stream or torch.cuda.current_stream()).synchronize()
+    r = int(rows.item())
+    return (n_g[:n_traj].cpu().numpy(), K[:n_groups].cpu().numpy(), idx[:r].cpu().numpy(), r)
+
+
 def last_launch_count() -> int:
     return int(_lib.agentrl_last_launch_count())
 
@@ -238,6 +264,13 @@ def debug_adv_phase_ns():
     """Phase boundary timestamps (ns) of the last single-GPU agentrl_task_adv_norm launch."""
     buf = (C.c_ulonglong * 8)()
     _check(_lib.agentrl_debug_adv_phase_ns(buf), "agentrl_debug_adv_phase_ns")
+    return [int(x) for x in buf]
+
+
+def debug_throttle_waits():
+    """[forward, grad_W, grad_hidden] progress-throttle wait episodes since the library loaded."""
+    buf = (C.c_ulonglong * 3)()
+    _check(_lib.agentrl_debug_throttle_waits(buf), "agentrl_debug_throttle_waits")
     return [int(x) for x in buf]
 
 
@@ -277,7 +310,8 @@ class Comm:
         return cls(world, rank, bytes(t.cpu().tolist()))
 
     def enable_peer_window(self, nbytes: int):
-        """Fused grad_W reduce-scatter over peer memory (collective; include/agentrl.h)."""
+        """Fused grad_W reduce-scatter over peer memory (collective; include/agentrl.h);
+        nbytes = 0 frees the window (back to the collective reduce-scatter)."""
         _check(_lib.agentrl_comm_enable_peer_window(self.handle, int(nbytes)),
                "agentrl_comm_enable_peer_window")
 

@@ -53,7 +53,11 @@ constexpr int RING = ADV_RING;          // bulk-copy slots per warp
 constexpr int WIN_CHUNKS = 8 * NWARPS;  // warp chunks per offset-staging window (large path)
 constexpr int WIN_TRAJ = 2048;          // trajectories a block stages at once (more: windows,
                                         // then global lookups)
-constexpr int KC_CAP = 2048;            // chunks per staged window (chunk -> trajectory table)
+#ifndef ADV_KC_CAP
+#define ADV_KC_CAP 2048
+#endif
+constexpr int KC_CAP = ADV_KC_CAP;      // chunks per staged window (chunk -> trajectory table);
+                                        // a block with more chunks stages 64-chunk windows
 constexpr int SMALL_TRAJ = 2048;        // small driver: all offsets staged in every block
 constexpr int SMALL_GROUPS = 512;
 constexpr int TASK_BATCH = 16;  // tasks reduced per barrier in the per-block partials
@@ -505,6 +509,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     }
     int32_t* s_kc = reinterpret_cast<int32_t*>(smem + p.lay.skc);
     int32_t kseq = 0;
+    int32_t prev_last = -1;  // last trajectory of the previous window (block-uniform)
     for (int64_t w0 = c_lo; w0 < c_hi; w0 += wlen) {
         const int64_t w1 = min(c_hi, w0 + wlen);
         // ---- stage the window's trajectories (block-wide)
@@ -643,16 +648,24 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         // ---- window epilogue (counting): per-trajectory counts out
         if (PH == 0 && !pop && w.staged) {
             for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
-                if (small) p.blk_cnt[w.f + B + k] = s_aux[k];  // disjoint slot g + block
-                else if (s_aux[k]) atomicAdd(&p.n_g[w.f + k], s_aux[k]);
+                if (small) {
+                    // disjoint slot g + block; a trajectory that crosses from this block's
+                    // previous window into this one adds to the count that window stored
+                    // (the store is ordered before this load by the __syncthreads below)
+                    if (k == 0 && w.f == prev_last) p.blk_cnt[w.f + B] += s_aux[0];
+                    else p.blk_cnt[w.f + B + k] = s_aux[k];
+                } else if (s_aux[k]) {
+                    atomicAdd(&p.n_g[w.f + k], s_aux[k]);
+                }
             }
+            prev_last = w.f + w.nbt - 1;
             __syncthreads();
         }
     }
 }
 
 // per-task (mu, max(sigma, eps)) into smem from the (global) stats; block 0 publishes
-// task_stats, N, n_seq
+// task_stats, N, G
 __device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w) {
     double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
     const int64_t G = gridDim.x, B = blockIdx.x;
@@ -677,7 +690,7 @@ __device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_p
             const int64_t n = (int64_t)nsum;
             p.meta[0] = s_pre[G];  // local masked rows
             p.meta[1] = n;         // global N
-            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global n_seq
+            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global G (groups)
             if (p.n_mask_global_out) *p.n_mask_global_out = n;
             if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
         }
@@ -706,7 +719,7 @@ __device__ void chunk_bases(const AdvParams& p, int64_t c_lo, int64_t c_hi, int3
 // ------------------------------------------------------------------ GRPO group advantage
 // (readings R1 population std, R2 exact-equal rule and eps floor, R14 K == 1).
 // mb: the K members sorted by index.  Writes adv_hat; returns (N, S, Q) of the group and
-// its task; nz counts members with masked tokens.
+// its task; nz counts the groups with at least one member (E_{i,j} of P:1250).
 template <typename GetR, typename GetT, typename GetN>
 __device__ __forceinline__ void group_adv(const AdvParams& p, int32_t K, const int32_t* mb,
                                           GetR rew, GetT task, GetN ng, double& N, double& S,
@@ -744,8 +757,8 @@ __device__ __forceinline__ void group_adv(const AdvParams& p, int32_t K, const i
         N += n;
         S += n * ah;
         Q += n * ah * ah;
-        nz += nn > 0;
     }
+    nz += 1;  // a group present in the batch (GRPO group mean)
 }
 
 // ------------------------------------------------------------------ small driver
@@ -877,7 +890,7 @@ __device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w)
 // per-block counts of each trajectory summed in block order: exact integers), per-group and
 // per-task (N, S, Q) in fixed orders, then mu_i, max(sigma_i, eps) into the
 // block's s_task.  Streaming blocks first load the group table block 0 published during
-// phase A.  publish (block 0): n_g, task_stats, N, n_seq and the local masked-row count;
+// phase A.  publish (block 0): n_g, task_stats, N, G and the local masked-row count;
 // stats_only (second launch follows the all-reduce): block 0 writes the raw per-task sums.
 __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
                             bool publish, bool stats_only, int32_t* s_pre = nullptr) {
@@ -933,8 +946,8 @@ __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_
             N += n;
             S += n * ah;
             Q += n * ah * ah;
-            nz += a.ng[g] > 0;
         }
+        nz += K > 0;  // groups present in the batch (GRPO group mean)
         a.gnsq[3 * j] = N;
         a.gnsq[3 * j + 1] = S;
         a.gnsq[3 * j + 2] = Q;
@@ -969,7 +982,7 @@ __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_
             }
         }
     }
-    if (blk0 && stats_only && threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // n_seq
+    if (blk0 && stats_only && threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // G
     if (stats_only) return;
     __syncthreads();
     double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
@@ -993,7 +1006,7 @@ __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_
             const int64_t n = (int64_t)nsum;
             p.meta[0] = rows_t;  // local masked rows
             p.meta[1] = n;       // global N
-            p.meta[2] = nzt;     // global n_seq
+            p.meta[2] = nzt;     // global G (groups)
             if (p.n_mask_global_out) *p.n_mask_global_out = n;
             if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
         }
@@ -1067,7 +1080,7 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
 
     // phase 0: zero scratch; chunk -> first-trajectory table
-    if (gtid == 0) p.meta[3] = 0;  // local count of trajectories with masked tokens (n_seq)
+    if (gtid == 0) p.meta[3] = 0;  // local count of groups with members (G)
     for (int64_t i = gtid; i < p.n_groups; i += gstride) {
         p.grp_cnt[i] = 0;
         p.grp_fill[i] = 0;
@@ -1239,8 +1252,8 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
                         N += n;
                         S += n * ah;
                         Q += n * ah * ah;
-                        nz += nn[a] > 0;
                     }
+                nz += 1;  // a group present in the batch (GRPO group mean)
             }
         } else {
             for (int a = 1; a < K; ++a) {
@@ -1345,7 +1358,7 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
                 p.stats[3 * i + 2] = Q;
             }
         }
-        if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)p.meta[3];  // n_seq (local)
+        if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)p.meta[3];  // G (local)
     }
 }
 
@@ -1455,12 +1468,6 @@ static int coop_grid(const void* kern, size_t smem, int64_t want) {
     return (int)std::max<int64_t>(1, std::min<int64_t>({cap, want, (int64_t)GMAX_BLOCKS}));
 }
 
-template <typename K>
-static bool set_smem_attr(K k, size_t bytes) {
-    return cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
-           cudaSuccess;
-}
-
 int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
                          double* task_stats, int64_t* n_mask_global, uint8_t* ws, const AdvWs& w,
                          agentrl_comm comm, int32_t* d_status, cudaStream_t stream, bool compact) {
@@ -1520,16 +1527,13 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     const void* k_all = small ? (const void*)k_adv_small_all : (const void*)k_adv_large_all;
     const void* k_stats = small ? (const void*)k_adv_small_stats : (const void*)k_adv_large_stats;
     const void* k_apply = small ? (const void*)k_adv_small_apply : (const void*)k_adv_large_apply;
-    static thread_local size_t attr_set = 0;
-    if (smem > 48 * 1024 && smem > attr_set) {
-        if (!set_smem_attr(k_adv_small_all, 200 * 1024) ||
-            !set_smem_attr(k_adv_small_stats, 200 * 1024) ||
-            !set_smem_attr(k_adv_small_apply, 200 * 1024) ||
-            !set_smem_attr(k_adv_large_all, 200 * 1024) ||
-            !set_smem_attr(k_adv_large_stats, 200 * 1024) ||
-            !set_smem_attr(k_adv_large_apply, 200 * 1024))
-            return AGENTRL_ERR_UNSUPPORTED;
-        attr_set = 200 * 1024;
+    if (smem > 48 * 1024) {  // the attribute is per device: set once on each
+        static std::atomic<uint64_t> done[6];
+        const void* ks[6] = {(const void*)k_adv_small_all,   (const void*)k_adv_small_stats,
+                             (const void*)k_adv_small_apply, (const void*)k_adv_large_all,
+                             (const void*)k_adv_large_stats, (const void*)k_adv_large_apply};
+        for (int i = 0; i < 6; ++i)
+            if (!func_attr_once(done[i], ks[i], 200 * 1024)) return AGENTRL_ERR_UNSUPPORTED;
     }
     // small: one statistics block + one warp chunk per warp
     const int64_t want = small ? std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1) + 1

@@ -79,8 +79,9 @@ __device__ int32_t block_exscan_256(int32_t v, int32_t* s_warp, int32_t& total) 
 
 // ---------------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(CHUNK_THREADS)
-    k_count(int64_t T, int32_t n_traj, int32_t n_groups, const int64_t* __restrict__ off,
-            const int32_t* __restrict__ group_id, const uint8_t* __restrict__ mask,
+    k_count(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks,
+            const int64_t* __restrict__ off, const int32_t* __restrict__ group_id,
+            const int32_t* __restrict__ task_id, const uint8_t* __restrict__ mask,
             int32_t* __restrict__ n_g, int32_t* __restrict__ chunk_cnt,
             int32_t* __restrict__ grp_cnt) {
     __shared__ int32_t s_warp[8];
@@ -111,11 +112,13 @@ __global__ void __launch_bounds__(CHUNK_THREADS)
     int32_t total;
     block_exscan_256(mine, s_warp, total);
     if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = total;
-    // group sizes K_j (grid-stride over trajectories)
+    // group sizes K_j (grid-stride over trajectories); a member with an invalid group or task
+    // id is left out exactly as k_stats leaves it out of the member lists (else K_j would count
+    // member slots k_stats never fills)
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_traj;
          g += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t j = group_id[g];
-        if (j >= 0 && j < n_groups) atomicAdd(&grp_cnt[j], 1);
+        const int32_t j = group_id[g], i = task_id[g];
+        if (j >= 0 && j < n_groups && i >= 0 && i < n_tasks) atomicAdd(&grp_cnt[j], 1);
     }
 }
 
@@ -267,9 +270,9 @@ __global__ void __launch_bounds__(STATS_THREADS)
             stats[3 * i + 2] = Q;
         }
     }
-    {  // trajectories with masked tokens (sequence-mean weights), local
+    {  // groups with members (G of the GRPO group mean), local
         double nz = 0.0;
-        for (int64_t g = threadIdx.x; g < n_traj; g += blockDim.x) nz += n_g[g] > 0 ? 1.0 : 0.0;
+        for (int64_t j = threadIdx.x; j < n_groups; j += blockDim.x) nz += grp_cnt[j] > 0 ? 1.0 : 0.0;
         nz = block_sum_f64(nz, s_red);
         if (threadIdx.x == 0) stats[3 * n_tasks] = nz;
     }
@@ -457,8 +460,8 @@ int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, doub
     if (n_chunks > 0) {
         ProfScope ps(KID_COUNT, stream);
         k_count<<<(unsigned)n_chunks, CHUNK_THREADS, 0, stream>>>(
-            T, b->n_traj, b->n_groups, b->traj_offsets, b->group_id, b->loss_mask, n_g, chunk,
-            grp_cnt);
+            T, b->n_traj, b->n_groups, b->n_tasks, b->traj_offsets, b->group_id, b->task_id,
+            b->loss_mask, n_g, chunk, grp_cnt);
         count_launch();
     }
     {

@@ -50,15 +50,35 @@ void prof_mark(int kid, bool begin, cudaStream_t s) {
     }
 }
 
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
 int num_sms() {
-    static int n = 0;
+    // per device (a process or thread may drive several GPUs)
+    static std::atomic<int> cache[MAX_DEVICES];
+    const int dev = current_device();
+    const int slot = dev & (MAX_DEVICES - 1);
+    int n = cache[slot].load(std::memory_order_relaxed);
     if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
             n = 148;
+        cache[slot].store(n, std::memory_order_relaxed);
     }
     return n;
+}
+
+bool func_attr_once(std::atomic<uint64_t>& done_mask, const void* func, int smem_bytes) {
+    const int dev = current_device();
+    const uint64_t bit = 1ull << (dev & (MAX_DEVICES - 1));
+    if (done_mask.load(std::memory_order_acquire) & bit) return true;
+    if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) !=
+        cudaSuccess)
+        return false;
+    done_mask.fetch_or(bit, std::memory_order_acq_rel);
+    return true;
 }
 
 int check_device() {
@@ -318,8 +338,13 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
                               d_status, s)))
         return rc;
     const int before = g_launches;
-    const FusedExtras fx{b->traj_offsets, b->n_traj, reinterpret_cast<const int32_t*>(w8 + wa.n_g),
-                         meta + 2 /* global n_seq */};
+    const FusedExtras fx{b->traj_offsets,
+                         b->n_traj,
+                         reinterpret_cast<const int32_t*>(w8 + wa.n_g),
+                         b->group_id,
+                         reinterpret_cast<const int32_t*>(w8 + wa.grp_cnt),
+                         b->n_groups,
+                         meta + 2 /* global G */};
     rc = launch_policy_loss(a, o, w8, wl, reinterpret_cast<const int32_t*>(w8 + wa.idx),
                             meta /* [0] local rows */,
                             reinterpret_cast<const float*>(w8 + wa.adv_c),
@@ -367,11 +392,12 @@ int agentrl_comm_set_reduce_scatter(agentrl_comm comm, agentrl_reduce_scatter_fn
 }
 
 int agentrl_comm_enable_peer_window(agentrl_comm comm, size_t bytes_per_rank) {
-    if (!comm || bytes_per_rank == 0) return AGENTRL_ERR_INVALID_ARG;
+    if (!comm) return AGENTRL_ERR_INVALID_ARG;
     if (comm->peer) {
         peer_window_destroy(comm->peer);
         comm->peer = nullptr;
     }
+    if (bytes_per_rank == 0) return AGENTRL_OK;  // disabled: the collective C3 path
     return peer_window_create(comm, bytes_per_rank, &comm->peer);
 }
 
@@ -413,6 +439,31 @@ const char* agentrl_status_string(int code) {
 }
 
 int agentrl_version(void) { return 100; }
+
+int agentrl_debug_bookkeeping(const void* ws, int64_t T, int32_t n_traj, int32_t n_groups,
+                              int32_t n_tasks, int32_t* n_g, int32_t* K, int32_t* idx,
+                              int64_t* rows, agentrl_stream stream) {
+    if (!ws || T < 0 || n_traj < 0 || n_groups < 0 || n_tasks <= 0) return AGENTRL_ERR_INVALID_ARG;
+    const AdvWs w = plan_adv(T, n_traj, n_groups, n_tasks);  // part 1's plan starts at offset 0
+    const uint8_t* b = static_cast<const uint8_t*>(ws);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n_g && n_traj > 0)
+        AG_CUDA(cudaMemcpyAsync(n_g, b + w.n_g, sizeof(int32_t) * (size_t)n_traj,
+                                cudaMemcpyDeviceToDevice, s));
+    if (K && n_groups > 0)
+        AG_CUDA(cudaMemcpyAsync(K, b + w.grp_cnt, sizeof(int32_t) * (size_t)n_groups,
+                                cudaMemcpyDeviceToDevice, s));
+    if (idx && T > 0)
+        AG_CUDA(cudaMemcpyAsync(idx, b + w.idx, sizeof(int32_t) * (size_t)T,
+                                cudaMemcpyDeviceToDevice, s));
+    if (rows)
+        AG_CUDA(cudaMemcpyAsync(rows, b + w.meta, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    return AGENTRL_OK;
+}
+
+int agentrl_debug_throttle_waits(unsigned long long host3[3]) {
+    return host3 ? debug_throttle_waits(host3) : AGENTRL_ERR_INVALID_ARG;
+}
 
 int agentrl_debug_adv_phase_ns(unsigned long long* host_ns8) {
     return host_ns8 ? debug_adv_phase_ns(host_ns8) : AGENTRL_ERR_INVALID_ARG;

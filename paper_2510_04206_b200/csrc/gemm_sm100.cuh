@@ -115,6 +115,7 @@ struct GemmArgs {
     // share operand slices stay within an L2-resident window instead of drifting apart.
     int64_t* prog;
     int32_t prog_every, prog_lead;
+    unsigned long long* prog_waits;  // optional: +1 per throttle wait episode (debug counter)
 };
 
 __device__ __forceinline__ void prog_store(int64_t* p, int64_t v) {
@@ -141,11 +142,17 @@ __device__ __forceinline__ int64_t prog_min(const int64_t* prog, int64_t n_units
 // only grow, so a stale minimum is a lower bound: re-read only when it says we may be ahead.
 // The slowest unit never waits.
 __device__ __forceinline__ void prog_throttle(const int64_t* prog, int64_t n_units, int64_t mine,
-                                              int32_t lead, int64_t& cached_min) {
+                                              int32_t lead, int64_t& cached_min,
+                                              unsigned long long* waits) {
     if (mine - cached_min <= (int64_t)lead) return;
+    bool counted = false;
     for (;;) {
         cached_min = prog_min(prog, n_units);
         if (mine - cached_min <= (int64_t)lead) return;
+        if (waits && !counted) {
+            atomicAdd(waits, 1ull);
+            counted = true;
+        }
         __nanosleep(100);
     }
 }
@@ -328,7 +335,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
                     if (throttle && kb % p.prog_every == 0) {
                         prog_store(p.prog + unit, wave_pos + kb);
-                        prog_throttle(p.prog, n_units, wave_pos + kb, p.prog_lead, prog_cached_min);
+                        prog_throttle(p.prog, n_units, wave_pos + kb, p.prog_lead, prog_cached_min,
+                                      p.prog_waits);
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint32_t fb = 0;

@@ -4,6 +4,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/agentrl.h"
 
 namespace agentrl {
@@ -87,12 +89,15 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0, int32_t vp_wo
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:
 //   idx_dev  int32 [T] compacted token positions, rows_dev -> int64 number of rows (local T_eff),
 //   adv_c    float [T] compacted advantages, nglob -> int64 global masked count.
-// batch information the fused step hands to part 2 (sequence-mean weights, loss_agg == 1)
+// batch information the fused step hands to part 2 (GRPO group-mean weights, loss_agg == 1)
 struct FusedExtras {
     const int64_t* off;   // traj_offsets [n_traj+1]
     int32_t n_traj;
-    const int32_t* n_g;   // masked tokens per trajectory (part 1 workspace)
-    const int64_t* nseq;  // global number of trajectories with masked tokens (device)
+    const int32_t* n_g;       // masked tokens per trajectory (part 1 workspace)
+    const int32_t* group_id;  // [n_traj] (batch descriptor)
+    const int32_t* grp_cnt;   // [n_groups] K_j, members per group (part 1 workspace)
+    int32_t n_groups;
+    const int64_t* ngrp;      // global number of groups with members, G (device)
 };
 int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
                        const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
@@ -155,8 +160,14 @@ struct ProfScope {
     ProfScope(int k, cudaStream_t st) : kid(k), s(st) { prof_mark(kid, true, s); }
     ~ProfScope() { prof_mark(kid, false, s); }
 };
-int num_sms();
+constexpr int MAX_DEVICES = 64;  // per-device caches (device ids are taken modulo this)
+int current_device();
+int num_sms();  // of the current device
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (function, device): the attribute
+// is per device, so a process or thread driving several GPUs sets it on each
+bool func_attr_once(std::atomic<uint64_t>& done_mask, const void* func, int smem_bytes);
 int debug_adv_phase_ns(unsigned long long* host8);
+int debug_throttle_waits(unsigned long long* host3);
 int check_device();  // AGENTRL_OK or AGENTRL_ERR_UNSUPPORTED / _CUDA
 
 }  // namespace agentrl

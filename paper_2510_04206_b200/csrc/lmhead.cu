@@ -134,11 +134,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
         auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB>;
         constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM +
                              (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0);
-        static bool attr_done = false;  // per instantiation
-        if (!attr_done) {
-            AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_done = true;
-        }
+        static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
+        if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
         int64_t grid = gemm_full_grid()
                            ? 2 * std::max<int64_t>(max_tiles, 1)
                            : std::min<int64_t>((num_sms() - reserve_sms) & ~1,
@@ -148,17 +145,29 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     } else {
         auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
         constexpr int smem = GemmCfg<false, 1>::SMEM;
-        static bool attr_done = false;
-        if (!attr_done) {
-            AG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_done = true;
-        }
+        static std::atomic<uint64_t> attr_done{0};
+        if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
         int grid = (int)std::min<int64_t>(num_sms() - reserve_sms, std::max<int64_t>(max_tiles, 1));
         kern<<<grid, GEMM_THREADS, smem, stream>>>(a, b, g);
     }
     count_launch();
     AG_CUDA(cudaGetLastError());
     return AGENTRL_OK;
+}
+
+// backward progress-throttle wait episodes per GEMM (0 forward, 1 grad_W, 2 grad_hidden), summed
+// over calls: agentrl_debug_throttle_waits() (the tests assert the throttle engages)
+__device__ unsigned long long g_throttle_waits[3];
+static unsigned long long* throttle_wait_ctr(int which) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_throttle_waits) != cudaSuccess) return nullptr;
+    return static_cast<unsigned long long*>(p) + which;
+}
+int debug_throttle_waits(unsigned long long* host3) {
+    return cudaMemcpyFromSymbol(host3, g_throttle_waits, sizeof(unsigned long long) * 3) ==
+                   cudaSuccess
+               ? AGENTRL_OK
+               : AGENTRL_ERR_CUDA;
 }
 
 // ---------------------------------------------------------------------------- compaction
@@ -612,15 +621,18 @@ __global__ void __launch_bounds__(256)
 }
 
 // per-row aggregation weight w_t and reference log-prob (objective variants):
-//   w_t = tok_weight[t] | 1/(n_seq n_g(t)) (sequence mean) | 1/N (token mean)
+//   w_t = tok_weight[t] | 1/(G K_j n_g(t)) (GRPO group mean, reading R7b)
+//       | 1/N (token mean)
 __global__ void __launch_bounds__(256)
     k_row_weights(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
                   const int32_t* __restrict__ idx, const float* __restrict__ tok_weight,
                   const float* __restrict__ ref_logp, int32_t agg,
                   const int64_t* __restrict__ off, int32_t n_traj,
-                  const int32_t* __restrict__ n_g, const int64_t* __restrict__ nseq_dev,
-                  float* __restrict__ w_c, float* __restrict__ ref_c, int32_t n_fchunks,
-                  float fratio, int64_t* __restrict__ fbnd) {
+                  const int32_t* __restrict__ n_g, const int32_t* __restrict__ group_id,
+                  const int32_t* __restrict__ grp_cnt, int32_t n_groups,
+                  const int64_t* __restrict__ ngrp_dev, float* __restrict__ w_c,
+                  float* __restrict__ ref_c, int32_t n_fchunks, float fratio,
+                  int64_t* __restrict__ fbnd) {
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
     if (blockIdx.x == 0 && threadIdx.x <= n_fchunks) {
@@ -638,22 +650,24 @@ __global__ void __launch_bounds__(256)
         const int64_t b = (int64_t)ceil(frac * (double)rows / 256.0) * 256;
         fbnd[c] = c == n_fchunks ? rows : min(rows, b);
     }
-    const double nseq = nseq_dev ? (double)*nseq_dev : 0.0;
+    const double G = ngrp_dev ? (double)*ngrp_dev : 0.0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < rows;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = idx[p];
         double w = N > 0.0 ? 1.0 / N : 0.0;
         if (tok_weight) {
             w = tok_weight[t];
-        } else if (agg == 1 && off && n_g && nseq > 0.0) {
+        } else if (agg == 1 && off && n_g && group_id && grp_cnt && G > 0.0) {
             int32_t lo = 0, hi = n_traj;  // trajectory of token t
             while (hi - lo > 1) {
                 const int32_t mid = (lo + hi) >> 1;
                 if (off[mid] <= t) lo = mid;
                 else hi = mid;
             }
-            const int32_t ng = n_g[lo];
-            w = ng > 0 ? 1.0 / (nseq * (double)ng) : 0.0;
+            const int32_t ng = n_g[lo], j = group_id[lo];
+            const int32_t K = (j >= 0 && j < n_groups) ? grp_cnt[j] : 0;
+            // E_{i,j} 1/K_{i,j} sum_g (token mean of g): w = 1 / (G K_j n_g)
+            w = (ng > 0 && K > 0) ? 1.0 / (G * (double)K * (double)ng) : 0.0;
         }
         w_c[p] = (float)w;
         if (ref_c) ref_c[p] = ref_logp ? ref_logp[t] : 0.f;
@@ -665,7 +679,8 @@ struct SideStream {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 static SideStream& side_stream() {
-    static thread_local SideStream ss;
+    static thread_local SideStream per_dev[MAX_DEVICES];  // a stream belongs to one device
+    SideStream& ss = per_dev[current_device() & (MAX_DEVICES - 1)];
     if (!ss.s) {
         cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&ss.e0, cudaEventDisableTiming);
@@ -745,10 +760,8 @@ struct ForkStreams {
     cudaEvent_t fork = nullptr, join = nullptr, ev[MAX_FWD_CHUNKS] = {};
 };
 static ForkStreams& fork_streams() {
-    static thread_local ForkStreams fs[16];  // per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    ForkStreams& f = fs[dev & 15];
+    static thread_local ForkStreams fs[MAX_DEVICES];  // per device
+    ForkStreams& f = fs[current_device() & (MAX_DEVICES - 1)];
     if (!f.hi) {
         int least = 0, greatest = 0;
         cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -839,7 +852,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
             rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
             fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
-            fx ? fx->nseq : nullptr, w_c, ref_c, n_fc, fwd_ratio(), fbnd);
+            fx ? fx->group_id : nullptr, fx ? fx->grp_cnt : nullptr, fx ? fx->n_groups : 0,
+            fx ? fx->ngrp : nullptr, w_c, ref_c, n_fc, fwd_ratio(), fbnd);
         count_launch(2);
         AG_CUDA(cudaGetLastError());
     }
@@ -887,6 +901,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             g.prog = prog + (2 + c) * PROG_UNITS;
             g.prog_every = throttle_every();
             g.prog_lead = lead_fwd;
+            g.prog_waits = throttle_wait_ctr(0);
         }
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
@@ -978,6 +993,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             g.prog = prog;
             g.prog_every = throttle_every();
             g.prog_lead = lead;
+            g.prog_waits = throttle_wait_ctr(1);
         }
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
@@ -1000,6 +1016,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             g.prog = prog + PROG_UNITS;
             g.prog_every = throttle_every();
             g.prog_lead = lead;
+            g.prog_waits = throttle_wait_ctr(2);
         }
         g.scale = a->logit_scale;
         g.idx = idx_dev;
@@ -1055,10 +1072,12 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         if (rc) return rc;
         AG_CUDA(cudaEventRecord(ss->e1, ss->s));
     }
-    // with C3 in flight on the side stream, leave SMs for the NCCL kernel so the collective
-    // overlaps this GEMM instead of queueing behind its persistent CTAs
-    if ((rc = launch_grad_hidden(stream, ss && comm_world(comm) > 1 ? comm_reserve_sms() : 0)))
-        return rc;
+    // with a collective C3 in flight on the side stream, leave SMs for the NCCL kernel so it
+    // overlaps this GEMM instead of queueing behind its persistent CTAs.  The fused P2P C3 has
+    // already moved its bytes inside the grad_W GEMM; its side-stream tail (a slot sum of a few
+    // dozen blocks) needs no reserved SMs.
+    const bool nccl_c3 = ss && !pw && comm_world(comm) > 1;
+    if ((rc = launch_grad_hidden(stream, nccl_c3 ? comm_reserve_sms() : 0))) return rc;
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
     return AGENTRL_OK;
 }

@@ -73,6 +73,11 @@ CONFIGS = {
     "ragged": _cfg("ragged", 3, (2, 3, 2), 4, 1536, 192, 2000, index=6),
     # finite-difference case: 2 tasks x 1 group x 2 rollouts x 6 tokens, d=4, V=8
     "micro": _cfg("micro", 2, (1, 1), 2, 24, 4, 8, index=7),
+    # long reduction loops at oracle-affordable cost (full-tensor gradient parity): T_eff ~ 26.6K
+    # rows = 416 k-blocks in grad_W, V = 8192 = 128 k-blocks in grad_hidden, both longer than
+    # the backward progress-throttle lead (96 k-blocks), 104 x 1 grad_hidden tiles (> 74 CTA
+    # pairs: two waves)
+    "longk": _cfg("longk", 5, (4,) * 5, 8, 65536, 256, 8192, index=8),
 }
 
 
@@ -246,6 +251,32 @@ def make_old_logp_free(T: int, seed: int, mean=-9.0, sd=3.0):
     rng = np.random.default_rng(seed)
     return np.minimum(rng.normal(mean, sd, size=T), -1e-3).astype(np.float32)
 
+
+
+def make_variable_k(b: dict, seed: int, k_range=(2, 7), empty_frac=0.15):
+    """Re-group a batch structure into groups of unequal size K_{i,j} (K_{i,j} is per
+    sample) within each task, and clear the loss mask of a fraction of the trajectories (members
+    without assistant tokens).  Offsets, task ids and rewards are kept; group ids are re-densified
+    in trajectory order.  Structure only: no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    task = b["task_id"]
+    gid = np.empty(len(task), np.int32)
+    j = 0
+    for i in range(int(b["n_tasks"])):
+        members = np.nonzero(task == i)[0]
+        pos = 0
+        while pos < len(members):
+            k = int(rng.integers(k_range[0], k_range[1] + 1))
+            if len(members) - pos - k < k_range[0]:
+                k = len(members) - pos
+            gid[members[pos:pos + k]] = j
+            j += 1
+            pos += k
+    mask = b["loss_mask"].copy()
+    off = b["traj_offsets"]
+    for g in np.nonzero(rng.uniform(size=len(task)) < empty_frac)[0]:
+        mask[off[g]:off[g + 1]] = 0
+    return dict(b, group_id=gid, n_groups=int(j), loss_mask=mask)
 
 def make_sweep_structure(T: int, tok_per_traj: int = 400, K: int = 8, n_tasks: int = 5,
                          seed: int = SEED_BASE + 99):

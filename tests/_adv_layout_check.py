@@ -7,6 +7,10 @@ driver switches the parent set, against the oracle.  Layouts (seeded, synthetic)
   shuffled group ids not contiguous in trajectory order, groups of 2..20 members (both sides
            of the 16-member register path), a task with no masked tokens
   bigtraj  > 2048 trajectories (the large driver), mixed lengths
+  huge     16M tokens in 1,500 trajectories (small driver): with a -DADV_KC_CAP=64 build every
+           block stages several windows and trajectories cross window boundaries
+The integer bookkeeping (n_g, K_j, the local masked count and the fused step's compaction idx)
+is compared bit-exactly (agentrl_debug_bookkeeping).
 Exit code 0 = parity holds.  (Input generation, plumbing and comparison only.)"""
 import os
 import sys
@@ -32,6 +36,9 @@ def layout(kind, seed):
     elif kind == "long":
         n_traj = 24
         lens = rng.integers(30000, 50000, n_traj)
+    elif kind == "huge":
+        n_traj = 1500
+        lens = rng.integers(4000, 18000, n_traj)
     elif kind == "shuffled":
         n_traj = 900
         lens = rng.integers(1, 200, n_traj)
@@ -51,7 +58,7 @@ def layout(kind, seed):
     n_groups = len(sizes)
     n_tasks = 5
     gid = np.repeat(np.arange(n_groups), sizes)
-    if kind != "long":
+    if kind not in ("long", "huge"):
         rng.shuffle(gid)
     gtask = rng.integers(0, n_tasks - 1, n_groups)  # task n_tasks-1 has no trajectories
     tid = gtask[gid]
@@ -78,12 +85,37 @@ def run_adv(b):
     rc = ag.agentrl_task_adv_norm(ag.make_batch(bd), 1e-6, adv, ts, nm, ws, None, st)
     assert rc == 0, ag.status_string(rc)
     torch.cuda.synchronize()
-    return adv[:T].cpu().numpy(), ts.cpu().numpy(), int(nm.item()), int(st.item())
+    bk = ag.bookkeeping(ws, T, n_traj, b["n_groups"], b["n_tasks"])
+    return adv[:T].cpu().numpy(), ts.cpu().numpy(), int(nm.item()), int(st.item()), bk
+
+
+def check_bookkeeping(kind, ref, bk, with_idx):
+    n_g, K, idx, rows = bk
+    np.testing.assert_array_equal(n_g, ref["n_g"], err_msg=kind)
+    np.testing.assert_array_equal(K, ref["K_j"], err_msg=kind)
+    assert rows == ref["n_mask"], (kind, rows, ref["n_mask"])
+    if with_idx:
+        np.testing.assert_array_equal(idx, ref["idx"], err_msg=kind)
+
+
+def check_idx(kind, b, ref, d=64, V=512):
+    """the fused step's compaction, bit-exact (a small head: only part 1's output matters)"""
+    T = b["T"]
+    hidden = torch.zeros(T, d, dtype=torch.bfloat16, device="cuda")
+    W = torch.zeros(V, d, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(T, dtype=torch.int32, device="cuda")
+    old = torch.full((T,), -6.0, dtype=torch.float32, device="cuda")
+    step = ag.Step(T, len(b["task_id"]), b["n_groups"], b["n_tasks"], d, V)
+    step(batch_dev(b), hidden, W, y, old)
+    torch.cuda.synchronize()
+    check_bookkeeping(kind, ref, ag.bookkeeping(step.ws, T, len(b["task_id"]), b["n_groups"],
+                                                b["n_tasks"]), True)
 
 
 def check_adv(kind, b):
     ref = oracle.task_adv_norm(b)
-    adv, ts, nm, st = run_adv(b)
+    adv, ts, nm, st, bk = run_adv(b)
+    check_bookkeeping(kind, ref, bk, False)
     assert st == (ref["status"] & ~oracle.S_NO_TOKENS), (kind, st, ref["status"])
     assert nm == ref["n_mask"], (kind, nm, ref["n_mask"])
     np.testing.assert_array_equal(ts[:, 0], ref["task_stats"][:, 0])
@@ -115,9 +147,11 @@ def check_step(kind, b, d=64, V=512):
 
 
 def main():
-    for i, kind in enumerate(("short", "long", "shuffled", "bigtraj")):
+    for i, kind in enumerate(("short", "long", "shuffled", "bigtraj", "huge")):
         b = layout(kind, 2510_04206 + 500 + i)
         check_adv(kind, b)
+        if kind != "huge":
+            check_idx(kind, b, oracle.task_adv_norm(b))
         if kind in ("short", "shuffled"):
             check_step(kind, b)
     print("adv layouts ok", {k: v for k, v in os.environ.items() if k.startswith("AGENTRL_")})

@@ -122,8 +122,9 @@ def test_reduce_scatter_mode_contract(libpath):
     assert call() not in (m.ERR_SHAPE, m.ERR_INVALID_ARG, 0)
     args.grad_W_mode = 4
     assert call() == m.ERR_INVALID_ARG
-    # the peer window needs a size (and, past the host checks, a device)
-    assert m._lib.agentrl_comm_enable_peer_window(comm.handle, 0) == m.ERR_INVALID_ARG
+    # the peer window needs a communicator (and, past the host checks, a device); size 0
+    # disables it (nothing to free here: a no-op)
+    assert m._lib.agentrl_comm_enable_peer_window(comm.handle, 0) == m.OK
     assert m._lib.agentrl_comm_enable_peer_window(None, 1 << 20) == m.ERR_INVALID_ARG
     # mode 3 (vocabulary-parallel head) needs a communicator and is not a fused-step mode
     args.grad_W_mode = 3

@@ -1,7 +1,8 @@
 """GPU parity of the objective variants against the variant oracle
 (oracle/oracle_variants.c): the k3 KL penalty with reference log-probs (P:1103 / P:1119),
-caller-supplied per-token weights, and the sequence-mean aggregation (GRPO 1/K) in the
-fused step.  Same bars as tests/test_gpu_parity.py."""
+caller-supplied per-token weights, and the GRPO group-level aggregation
+E_{i,j}[1/K_{i,j} sum_g ...] in the fused step, on batches with unequal K_{i,j}
+and members without masked tokens.  Same bars as tests/test_gpu_parity.py."""
 import numpy as np
 import pytest
 
@@ -92,11 +93,16 @@ def test_standalone_seq_agg_needs_weights(ag):
     assert rc == ag.ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("cfg_name,beta", [("tiny", 0.0), ("ragged", 0.0), ("ragged", 0.2)])
-def test_fused_sequence_mean(ag, cfg_name, beta):
+@pytest.mark.parametrize("cfg_name,beta,kr", [("tiny", 0.0, None), ("ragged", 0.0, (2, 7)),
+                                             ("ragged", 0.2, (2, 7)), ("parity7b", 0.0, (1, 3))])
+def test_fused_group_mean(ag, cfg_name, beta, kr):
     cfg, b, hb, Wb, y, h, W, old, ref_lp = _inputs(cfg_name)
+    if kr:  # unequal group sizes (K = 1 included for parity7b), members without masked tokens
+        b = synth.make_variable_k(b, seed=5 + cfg.index, k_range=kr)
+        ks = np.bincount(b["group_id"])
+        assert ks.min() != ks.max()
     an = oracle.task_adv_norm(b)
-    w, n_seq = oracle.seq_mean_weights(b)
+    w, G = oracle.grpo_group_weights(b)
     ref = oracle.policy_loss_ex(h, W, y, an["adv_tok"], old.astype(np.float64), b["loss_mask"],
                                 an["n_mask"], kl_beta=beta, ref_logp=ref_lp.astype(np.float64),
                                 weights=w)
@@ -108,4 +114,4 @@ def test_fused_sequence_mean(ag, cfg_name, beta):
     assert int(step.status.item()) & ~ag.ST_GROUP_TOO_SMALL == 0
     assert adv_close(step.adv_tok.cpu().numpy(), an["adv_tok"])
     _check(ref, step.loss.item(), step.grad_hidden.float().cpu().numpy(),
-           step.grad_W.cpu().numpy(), b["loss_mask"], 1.0 / n_seq)
+           step.grad_W.cpu().numpy(), b["loss_mask"], 1.0 / max(an["n_mask"], 1))

@@ -61,6 +61,38 @@ def test_adv_norm_parity(ag, cfg):
     assert np.all(adv[b["loss_mask"] == 0] == 0.0)
 
 
+@pytest.mark.parametrize("cfg", ["tiny", "ragged", "qwen7b", "glm9b", "skew14b", "qwen32b"])
+def test_bookkeeping_bitexact(ag, cfg):
+    """n_g, K_j, the local masked count and the fused step's stable compaction idx, bit-exact
+    against the oracle (north_star: integer bookkeeping; token set P:557-569, groups
+    P:1214-1218).  Part 1 alone, then the fused step with a small head (d=64, V=512) so the
+    compaction is written."""
+    b = synth.make_structure(synth.CONFIGS[cfg])
+    ref = oracle.task_adv_norm(b)
+    T, n_traj = b["T"], len(b["task_id"])
+    bd = batch_dev(b)
+    ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
+                                                                    b["n_tasks"]))
+    adv = torch.empty(T, dtype=torch.float32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert ag.agentrl_task_adv_norm(ag.make_batch(bd), 1e-6, adv, None, None, ws, None, st) == 0
+    n_g, K, _, rows = ag.bookkeeping(ws, T, n_traj, b["n_groups"], b["n_tasks"])
+    np.testing.assert_array_equal(n_g, ref["n_g"])
+    np.testing.assert_array_equal(K, ref["K_j"])
+    assert rows == ref["n_mask"]
+    d, V = 64, 512
+    step = ag.Step(T, n_traj, b["n_groups"], b["n_tasks"], d, V)
+    step(bd, torch.zeros(T, d, dtype=torch.bfloat16, device="cuda"),
+         torch.zeros(V, d, dtype=torch.bfloat16, device="cuda"),
+         torch.zeros(T, dtype=torch.int32, device="cuda"),
+         torch.full((T,), -6.0, dtype=torch.float32, device="cuda"))
+    n_g, K, idx, rows = ag.bookkeeping(step.ws, T, n_traj, b["n_groups"], b["n_tasks"])
+    np.testing.assert_array_equal(n_g, ref["n_g"])
+    np.testing.assert_array_equal(K, ref["K_j"])
+    assert rows == ref["n_mask"]
+    np.testing.assert_array_equal(idx, ref["idx"])
+
+
 def test_adv_norm_misaligned_and_ragged_T(ag):
     cfg = synth.CONFIGS["ragged"]
     b = synth.make_structure(cfg)
@@ -211,6 +243,27 @@ def _run_step(ag, cfg, b, hb, Wb, y, old, eps=(0.2, 0.2), scale=1.0):
     step(batch_dev(b), bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32), t(old, torch.float32))
     torch.cuda.synchronize()
     return step
+
+
+def test_longk_full_tensor_parity(ag):
+    """Long reduction loops compared element by element with the oracle (the full-size configs
+    only get spot checks): grad_W's K = T_eff ~ 26.6K rows (416 k-blocks) and grad_hidden's
+    K = V = 8192 (128 k-blocks), both beyond the default backward progress-throttle lead (96
+    k-blocks), with grad_hidden in two waves of CTA-pair tiles; default schedule.  The
+    throttle's wait episodes during this call are reported (a lead-1 lockstep build that must
+    wait is the bitwise schedule variant in tests/test_gpu_variants.py)."""
+    cfg, b, hb, Wb, y, h, W, old = _loss_inputs("longk")
+    ref = oracle.grpo_step(b, h, W, y, old.astype(np.float64))
+    w0 = ag.debug_throttle_waits()
+    step = _run_step(ag, cfg, b, hb, Wb, y, old)
+    w1 = ag.debug_throttle_waits()
+    print("throttle wait episodes (fwd, grad_W, grad_hidden):", [b_ - a_ for a_, b_ in zip(w0, w1)])
+    assert int(step.status.item()) & ~ag.ST_GROUP_TOO_SMALL == 0
+    assert adv_close(step.adv_tok.cpu().numpy(), ref["adv_tok"])
+    e1, e2 = _check_loss(ref, step.loss.item(), step.logp.cpu().numpy(),
+                         step.grad_hidden.float().cpu().numpy(), step.grad_W.cpu().numpy(),
+                         b["loss_mask"])
+    print("longk max-abs-rel grad_hidden %.3e grad_W %.3e" % (e1, e2))
 
 
 @pytest.mark.parametrize("cfg_name", ["tiny", "ragged"])

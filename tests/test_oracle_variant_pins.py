@@ -1,5 +1,5 @@
 """Pins for the loss-variant oracle (oracle/oracle_variants.c): KL penalty (k3 estimator,
-P:1103 / P:1119) and sequence-level aggregation (GRPO's 1/K).  Anchors: PyTorch CPU
+P:1103 / P:1119) and the GRPO group-level aggregation (E_{i,j} 1/K_{i,j} sum_g).  Anchors: PyTorch CPU
 fp64 autograd of the same objective, finite differences, closed forms, and reduction to the
 base oracle (an independently pinned function) at beta = 0 with token-mean weights."""
 import math
@@ -67,9 +67,11 @@ def test_matches_torch_autograd(beta, agg):
         b = synth.make_structure(cfg)
         off = b["traj_offsets"]
         keep = int(np.searchsorted(off, T, side="right")) - 1
-        bb = dict(T=T, traj_offsets=np.concatenate([off[:keep + 1], [T]]) if off[keep] < T
-                  else off[:keep + 1], loss_mask=mask)
-        weights, _ = oracle.seq_mean_weights(bb)
+        cut = off[keep] < T
+        bb = dict(T=T, traj_offsets=np.concatenate([off[:keep + 1], [T]]) if cut
+                  else off[:keep + 1], loss_mask=mask, n_groups=b["n_groups"],
+                  group_id=b["group_id"][:keep + 1] if cut else b["group_id"][:keep])
+        weights, _ = oracle.grpo_group_weights(bb)
         w = weights
     out = oracle.policy_loss_ex(h, W, y, A, old, mask, N, kl_beta=beta, ref_logp=ref,
                                 weights=weights)
@@ -91,33 +93,83 @@ def test_kl_zero_at_reference():
     np.testing.assert_allclose(a["grad_W"], b["grad_W"], atol=1e-14)
 
 
-def test_seq_mean_closed_forms():
-    """On-policy (rho = 1): loss = -(1/n_seq) sum_g mean_{t in g} A_t; with equal lengths
-    n_g the sequence mean equals the token mean."""
-    cfg = synth.CONFIGS["micro"]
-    b = synth.make_structure(cfg)
-    w, n_seq = oracle.seq_mean_weights(b)
-    off, mask = b["traj_offsets"], b["loss_mask"]
-    assert n_seq == sum(int(mask[off[g]:off[g + 1]].sum() > 0) for g in range(len(off) - 1))
-    assert abs(w.sum() - 1.0) < 1e-14
-    rng = np.random.default_rng(1)
-    h = rng.standard_normal((cfg.T, cfg.d))
-    W = rng.standard_normal((cfg.V, cfg.d))
-    y = rng.integers(0, cfg.V, size=cfg.T).astype(np.int32)
-    A = rng.standard_normal(cfg.T)
+def test_grpo_group_weights_hand_example(golden_dir):
+    """Hand-worked case with unequal K_{i,j}, an empty member and an empty group id
+    (tests/golden/grpo_group_weights.json): weights and the on-policy loss."""
+    import json
+    import os
+    g = json.load(open(os.path.join(golden_dir, "grpo_group_weights.json")))
+    b = dict(T=g["T"], traj_offsets=np.asarray(g["traj_offsets"], np.int64),
+             group_id=np.asarray(g["group_id"], np.int32), n_groups=g["n_groups"],
+             loss_mask=np.asarray(g["loss_mask"], np.uint8))
+    w, G = oracle.grpo_group_weights(b)
+    assert G == g["G"]
+    np.testing.assert_allclose(w, g["weights"], rtol=1e-15, atol=0)
+    T, d, V = g["T"], 3, 5
+    rng = np.random.default_rng(3)
+    h = rng.standard_normal((T, d))
+    W = rng.standard_normal((V, d))
+    y = rng.integers(0, V, size=T).astype(np.int32)
+    lp = oracle.logprob(h, W, y, b["loss_mask"])  # old = logp: rho = 1
+    out = oracle.policy_loss_ex(h, W, y, np.asarray(g["adv_tok"]), lp, b["loss_mask"],
+                                int(b["loss_mask"].sum()), weights=w)
+    assert abs(out["loss"] - g["on_policy_loss"]) < 1e-15
+
+
+def _variable_k_batch(seed):
+    """Groups of 1..6 members, some members without masked tokens, one declared-empty id."""
+    rng = np.random.default_rng(seed)
+    sizes = [int(k) for k in rng.integers(1, 7, size=7)]
+    gid, off, mask = [], [0], []
+    for j, k in enumerate(sizes):
+        for _ in range(k):
+            L = int(rng.integers(1, 9))
+            m = (rng.uniform(size=L) < 0.5).astype(np.uint8)
+            if rng.uniform() < 0.25:
+                m[:] = 0
+            gid.append(j + (j >= 3))  # id 3 is declared but never used
+            mask += m.tolist()
+            off.append(off[-1] + L)
+    return dict(T=off[-1], traj_offsets=np.asarray(off, np.int64),
+                group_id=np.asarray(gid, np.int32), n_groups=len(sizes) + 1,
+                loss_mask=np.asarray(mask, np.uint8))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_grpo_group_mean_closed_form(seed):
+    """On policy, the weighted loss equals the paper's group-level form evaluated directly
+    from the batch structure: -(1/G) sum_j (1/K_j) sum_{g in j} mean_{t in g} A_t
+    (P:1247-1256), with empty members contributing 0 but counting in K_j."""
+    b = _variable_k_batch(seed)
+    w, G = oracle.grpo_group_weights(b)
+    off, mask, gid = b["traj_offsets"], b["loss_mask"], b["group_id"]
+    T = b["T"]
+    rng = np.random.default_rng(seed + 10)
+    h = rng.standard_normal((T, 4))
+    W = rng.standard_normal((6, 4))
+    y = rng.integers(0, 6, size=T).astype(np.int32)
+    A = rng.standard_normal(T)
     lp = oracle.logprob(h, W, y, mask)
-    out = oracle.policy_loss_ex(h, W, y, A, lp, mask, int(mask.sum()), weights=w)
-    ref = 0.0
-    for g in range(len(off) - 1):
-        m = mask[off[g]:off[g + 1]] != 0
-        if m.any():
-            ref += A[off[g]:off[g + 1]][m].mean()
-    assert abs(out["loss"] - (-ref / n_seq)) < 1e-13
-    # equal lengths: tokens 4 per trajectory of 6, all masked the same way
-    eq = dict(T=12, traj_offsets=np.asarray([0, 6, 12]), loss_mask=np.asarray(
-        [0, 1, 1, 0, 1, 1] * 2, np.uint8))
-    w2, _ = oracle.seq_mean_weights(eq)
-    np.testing.assert_allclose(w2[eq["loss_mask"] != 0], 1.0 / 8.0, atol=1e-15)
+    out = oracle.policy_loss_ex(h, W, y, A, lp, mask, max(int(mask.sum()), 1), weights=w)
+    groups = sorted(set(gid.tolist()))
+    assert G == len(groups)
+    obj = 0.0
+    for j in groups:
+        members = [g for g in range(len(gid)) if gid[g] == j]
+        s = 0.0
+        for g in members:
+            m = mask[off[g]:off[g + 1]] != 0
+            if m.any():
+                s += A[off[g]:off[g + 1]][m].mean()
+        obj += s / len(members)
+    assert abs(out["loss"] - (-obj / len(groups))) < 1e-13
+    # equal K and every member masked: the group mean is the mean over trajectories
+    eq = dict(T=12, traj_offsets=np.asarray([0, 3, 6, 9, 12]), group_id=np.asarray([0, 0, 1, 1]),
+              n_groups=2, loss_mask=np.asarray([1, 1, 0, 1, 0, 0, 1, 1, 1, 0, 1, 1], np.uint8))
+    w2, _ = oracle.grpo_group_weights(eq)
+    np.testing.assert_allclose(w2[[0, 1, 3, 6, 7, 8, 10, 11]],
+                               [1 / 8, 1 / 8, 1 / 4, 1 / 12, 1 / 12, 1 / 12, 1 / 8, 1 / 8],
+                               rtol=1e-15)
 
 
 def test_finite_differences_with_kl_and_seq_weights():
@@ -132,7 +184,7 @@ def test_finite_differences_with_kl_and_seq_weights():
     lp = oracle.logprob(h, W, y, mask)
     old = lp + synth.make_deltas(cfg.T, 6, sigma=0.15, margin=0.05)
     ref = lp + rng.normal(0, 0.2, size=cfg.T)
-    w, _ = oracle.seq_mean_weights(b)
+    w, _ = oracle.grpo_group_weights(b)
     N = int(mask.sum())
 
     def L(hh, WW):
