@@ -213,8 +213,11 @@ def run_native(args, cfg, world, rank, local_rank):
     # C3 fused into the grad_W GEMM epilogue over peer memory (CUDA IPC windows; include/
     # agentrl.h agentrl_comm_enable_peer_window), unless AGENTRL_C3_P2P=0 or the mapping fails
     c3 = {0: "none", 1: "all-reduce (collective)", 2: "reduce-scatter (collective)"}[gw_mode]
+    # the host built the mask, so it knows this rank's masked-token count: the workspace's
+    # T_eff x V intermediate is sized by it (max_rows), not by T
+    T_eff_local = int(lb["loss_mask"].astype(bool).sum())
     step = ag.Step(T, n_traj, lb["n_groups"], lb["n_tasks"], d, V, device=dev, comm=comm,
-                   grad_W_mode=gw_mode)
+                   grad_W_mode=gw_mode, max_rows=T_eff_local)
     # behaviour log-probs: one untimed forward (old = 0), then old = logp + delta
     old = torch.zeros(T, dtype=torch.float32, device=dev)
     step(bd, hid, W, target, old)
@@ -253,7 +256,6 @@ def run_native(args, cfg, world, rank, local_rank):
             dist.barrier()
             comm.enable_peer_window(0)
         step.status.zero_()
-    T_eff_local = int(lb["loss_mask"].astype(bool).sum())
     T_eff_global = int(gb["loss_mask"].astype(bool).sum())
     T_global = int(gb["T"])
 
@@ -394,10 +396,11 @@ def run_native(args, cfg, world, rank, local_rank):
                    "n_tasks": cfg.n_tasks, "groups": int(gb["n_groups"]),
                    "rollouts": cfg.rollouts, "parallelism": f"dp{world}",
                    "grad_W_collective": c3, "c3_self_check": c3_check,
+                   "workspace_gb": round(step.ws.numel() / 1e9, 2),
                    **({"shard": f"rank 0 of {shard_of} (LPT), no communication"}
                       if world == 1 and shard_of > 1 else {}),
                    "mask": "all tokens (--all-masked)" if args.all_masked else "synthetic multi-turn (~40% assistant)",
-                   "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P/G %.1f GB)" % (
+                   "l2": "inputs larger than L2 (hidden %.2f GB, W %.2f GB, P~ %.1f GB)" % (
                        T * d * 2 / 1e9, V * d * 2 / 1e9, T_eff_local * V * 2 / 1e9)},
         "masked_tokens_per_s": T_eff_global / (ms / 1e3),
         "rank_imbalance_masked_rows": imbalance,

@@ -62,6 +62,9 @@ extern "C" {
 #define AGENTRL_ST_GROUP_TOO_SMALL 16    /* a group has one trajectory */
 #define AGENTRL_ST_NO_TOKENS 32          /* global masked-token count N == 0 */
 #define AGENTRL_ST_COMM_TIMEOUT 64       /* a peer never reached the fused reduce-scatter */
+#define AGENTRL_ST_ROWS_OVERFLOW 128     /* more local masked tokens than the max_rows the
+                                            workspace was sized for: only the first max_rows
+                                            (in token order) entered part 2 */
 
 typedef struct agentrl_comm_s* agentrl_comm;
 typedef struct CUstream_st* agentrl_stream; /* == cudaStream_t */
@@ -170,7 +173,10 @@ typedef struct {
                                           inside the call); grad_W is this rank's complete
                                           shard [V, d] (no collective).  Workspace:
                                           agentrl_policy_loss_workspace_size_vp(). */
-    int32_t reserved;
+    int32_t max_rows;                  /* upper bound on this rank's masked tokens T_eff that
+                                          the workspace was sized for (the same value passed to
+                                          the *_workspace_size() query); <= 0 means T.  The
+                                          T_eff x V intermediate scales with it, not with T */
     /* ---- objective variants; all-zero = the base objective above ----
      * KL penalty (the "- beta D_KL" of P:1103 / P:1119; beta unstated in the paper, R11):
      *   loss += sum_t w_t * beta * KL_t,  KL_t = exp(ref_t - logp_t) - (ref_t - logp_t) - 1
@@ -207,11 +213,15 @@ typedef struct {
     double* loss_stats;
 } agentrl_loss_out;
 
-size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V);
+/* Workspace: about (2 V + 8 ceil(V/256) + 2 d + 64) bytes per row of max_rows (<= 0: T) plus
+ * ~8 bytes per token of T -- the bf16 P~ = exp(z - m_tile) [max_rows, V] dominates (16.1 GB at
+ * T_eff = 53K, V = 152K).  The host knows the mask, so it knows T_eff (or a bound). */
+size_t agentrl_policy_loss_workspace_size(int64_t T, int64_t max_rows, int32_t d, int32_t V);
 /* workspace of grad_W_mode = 3 (V = the rank's shard rows, world = the group size): the base
- * plan plus the all-gathered row statistics (8 * world * T B) and the fp32 grad_hidden
- * partial (4 * T * d B) */
-size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int32_t d, int32_t V, int32_t world);
+ * plan plus the all-gathered row statistics (8 * world * rows B) and the fp32 grad_hidden
+ * partial (4 * rows * d B) */
+size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int64_t max_rows, int32_t d, int32_t V,
+                                             int32_t world);
 int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
                                 size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                                 agentrl_stream stream);
@@ -219,7 +229,7 @@ int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_o
 /* Fused: part 1 then part 2 (a->adv_tok and a->n_mask_global are ignored; the
  * step uses its own).  adv_tok_out [T] float required; task_stats optional. */
 size_t agentrl_grpo_step_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
-                                        int32_t n_tasks, int32_t d, int32_t V);
+                                        int32_t n_tasks, int64_t max_rows, int32_t d, int32_t V);
 int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss_args* a,
                       const agentrl_loss_out* o, float* adv_tok_out, double* task_stats,
                       void* ws, size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
@@ -242,10 +252,10 @@ typedef struct {
     const int32_t* target;
     const uint8_t* loss_mask;
     float logit_scale;
-    int32_t reserved;
+    int32_t max_rows; /* bound on the masked tokens (<= 0: T), as in agentrl_loss_args */
 } agentrl_logprob_args;
 
-size_t agentrl_logprob_workspace_size(int64_t T, int32_t d, int32_t V);
+size_t agentrl_logprob_workspace_size(int64_t T, int64_t max_rows, int32_t d, int32_t V);
 int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp /*[T]*/,
                         float* entropy /*[T] or NULL*/, void* ws, size_t ws_bytes,
                         int32_t* d_status, agentrl_stream stream);

@@ -33,6 +33,7 @@ ERR_INVALID_ARG, ERR_SHAPE, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED =
 ST_BAD_TARGET, ST_NONFINITE, ST_BAD_OFFSETS = 1, 2, 4
 ST_GROUP_SPANS_TASKS, ST_GROUP_TOO_SMALL, ST_NO_TOKENS = 8, 16, 32
 ST_COMM_TIMEOUT = 64
+ST_ROWS_OVERFLOW = 128
 
 EXPORTED = (
     "agentrl_task_adv_norm_workspace_size", "agentrl_task_adv_norm",
@@ -53,7 +54,7 @@ NUM_KERNEL_IDS = 12
 class LogprobArgs(C.Structure):
     _fields_ = [("T", C.c_int64), ("d", C.c_int32), ("V", C.c_int32), ("hidden", C.c_void_p),
                 ("W_head", C.c_void_p), ("target", C.c_void_p), ("loss_mask", C.c_void_p),
-                ("logit_scale", C.c_float), ("reserved", C.c_int32)]
+                ("logit_scale", C.c_float), ("max_rows", C.c_int32)]
 
 
 class Batch(C.Structure):
@@ -68,7 +69,7 @@ class LossArgs(C.Structure):
                 ("old_logp", C.c_void_p), ("loss_mask", C.c_void_p),
                 ("clip_eps_low", C.c_float), ("clip_eps_high", C.c_float),
                 ("logit_scale", C.c_float), ("n_mask_global", C.c_void_p),
-                ("grad_W_mode", C.c_int32), ("reserved", C.c_int32),
+                ("grad_W_mode", C.c_int32), ("max_rows", C.c_int32),
                 ("kl_beta", C.c_float), ("loss_agg", C.c_int32), ("ref_logp", C.c_void_p),
                 ("tok_weight", C.c_void_p)]
 
@@ -82,13 +83,13 @@ _P, _i64, _i32, _f64, _sz = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_si
 _lib.agentrl_task_adv_norm_workspace_size.argtypes = [_i64, _i32, _i32, _i32]
 _lib.agentrl_task_adv_norm_workspace_size.restype = _sz
 _lib.agentrl_task_adv_norm.argtypes = [C.POINTER(Batch), _f64, _P, _P, _P, _P, _sz, _P, _P, _P]
-_lib.agentrl_policy_loss_workspace_size.argtypes = [_i64, _i32, _i32]
+_lib.agentrl_policy_loss_workspace_size.argtypes = [_i64, _i64, _i32, _i32]
 _lib.agentrl_policy_loss_workspace_size.restype = _sz
-_lib.agentrl_policy_loss_workspace_size_vp.argtypes = [_i64, _i32, _i32, _i32]
+_lib.agentrl_policy_loss_workspace_size_vp.argtypes = [_i64, _i64, _i32, _i32, _i32]
 _lib.agentrl_policy_loss_workspace_size_vp.restype = _sz
 _lib.agentrl_policy_loss_fwd_bwd.argtypes = [C.POINTER(LossArgs), C.POINTER(LossOut), _P, _sz,
                                              _P, _P, _P]
-_lib.agentrl_grpo_step_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i32, _i32]
+_lib.agentrl_grpo_step_workspace_size.argtypes = [_i64, _i32, _i32, _i32, _i64, _i32, _i32]
 _lib.agentrl_grpo_step_workspace_size.restype = _sz
 _lib.agentrl_grpo_step.argtypes = [C.POINTER(Batch), _f64, C.POINTER(LossArgs),
                                    C.POINTER(LossOut), _P, _P, _P, _sz, _P, _P, _P]
@@ -99,7 +100,7 @@ _lib.agentrl_comm_set_reduce_scatter.argtypes = [_P, C.c_void_p]
 _lib.agentrl_comm_enable_peer_window.argtypes = [_P, _sz]
 _lib.agentrl_comm_init_callback.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p,
                                             C.c_void_p]
-_lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i32, _i32]
+_lib.agentrl_logprob_workspace_size.argtypes = [_i64, _i64, _i32, _i32]
 _lib.agentrl_logprob_workspace_size.restype = _sz
 _lib.agentrl_logprob_fwd.argtypes = [C.POINTER(LogprobArgs), _P, _P, _P, _sz, _P, _P]
 _lib.agentrl_debug_bookkeeping.argtypes = [_P, _i64, _i32, _i32, _i32, _P, _P, _P, _P, _P]
@@ -149,12 +150,12 @@ def make_batch(b) -> Batch:
 def make_loss_args(T, hidden, W_head, target, old_logp, loss_mask, adv_tok=None,
                    n_mask_global=None, eps_low=0.2, eps_high=0.2, logit_scale=1.0,
                    grad_W_mode=0, kl_beta=0.0, loss_agg=0, ref_logp=None,
-                   tok_weight=None) -> LossArgs:
+                   tok_weight=None, max_rows=0) -> LossArgs:
     d = int(hidden.shape[1])
     V = int(W_head.shape[0])
     return LossArgs(int(T), d, V, _ptr(hidden), _ptr(W_head), _ptr(target), _ptr(adv_tok),
                     _ptr(old_logp), _ptr(loss_mask), float(eps_low), float(eps_high),
-                    float(logit_scale), _ptr(n_mask_global), int(grad_W_mode), 0,
+                    float(logit_scale), _ptr(n_mask_global), int(grad_W_mode), int(max_rows),
                     float(kl_beta), int(loss_agg), _ptr(ref_logp), _ptr(tok_weight))
 
 
@@ -166,17 +167,19 @@ def agentrl_task_adv_norm_workspace_size(T, n_traj, n_groups, n_tasks) -> int:
     return int(_lib.agentrl_task_adv_norm_workspace_size(T, n_traj, n_groups, n_tasks))
 
 
-def agentrl_policy_loss_workspace_size(T, d, V) -> int:
-    return int(_lib.agentrl_policy_loss_workspace_size(T, d, V))
+def agentrl_policy_loss_workspace_size(T, d, V, max_rows=0) -> int:
+    """max_rows: bound on the masked tokens (<= 0: T); pass the same value in the args"""
+    return int(_lib.agentrl_policy_loss_workspace_size(T, max_rows, d, V))
 
 
-def agentrl_policy_loss_workspace_size_vp(T, d, V, world) -> int:
+def agentrl_policy_loss_workspace_size_vp(T, d, V, world, max_rows=0) -> int:
     """grad_W_mode = 3 (vocabulary-parallel head): V = this rank's shard rows"""
-    return int(_lib.agentrl_policy_loss_workspace_size_vp(T, d, V, world))
+    return int(_lib.agentrl_policy_loss_workspace_size_vp(T, max_rows, d, V, world))
 
 
-def agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V) -> int:
-    return int(_lib.agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V))
+def agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, d, V, max_rows=0) -> int:
+    return int(_lib.agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks, max_rows, d,
+                                                     V))
 
 
 def agentrl_task_adv_norm(batch: Batch, eps_std, adv_tok, task_stats, n_mask_global, ws,
@@ -202,15 +205,16 @@ def agentrl_grpo_step(batch: Batch, eps_std, args: LossArgs, out: LossOut, adv_t
                                   _stream(stream))
 
 
-def agentrl_logprob_workspace_size(T, d, V) -> int:
-    return int(_lib.agentrl_logprob_workspace_size(T, d, V))
+def agentrl_logprob_workspace_size(T, d, V, max_rows=0) -> int:
+    return int(_lib.agentrl_logprob_workspace_size(T, max_rows, d, V))
 
 
 def agentrl_logprob_fwd(T, hidden, W_head, target, loss_mask, logp, entropy, ws, d_status,
-                        logit_scale=1.0, stream=None) -> int:
+                        logit_scale=1.0, stream=None, max_rows=0) -> int:
     """Forward-only log-probs (and entropies if ``entropy`` is a tensor) of the masked tokens."""
     a = LogprobArgs(int(T), int(hidden.shape[1]), int(W_head.shape[0]), _ptr(hidden),
-                    _ptr(W_head), _ptr(target), _ptr(loss_mask), float(logit_scale), 0)
+                    _ptr(W_head), _ptr(target), _ptr(loss_mask), float(logit_scale),
+                    int(max_rows))
     return _lib.agentrl_logprob_fwd(C.byref(a), _ptr(logp), _ptr(entropy), _ptr(ws),
                                     ws.numel() * ws.element_size(), _ptr(d_status),
                                     _stream(stream))
@@ -431,15 +435,17 @@ class Step:
 
     def __init__(self, T, n_traj, n_groups, n_tasks, d, V, device="cuda", eps_std=1e-6,
                  eps_low=0.2, eps_high=0.2, logit_scale=1.0, comm: Comm | None = None,
-                 grad_W_mode=None, kl_beta=0.0, loss_agg=0):
+                 grad_W_mode=None, kl_beta=0.0, loss_agg=0, max_rows=0):
         import torch
         self.T, self.d, self.V = int(T), int(d), int(V)
         self.eps_std, self.eps_low, self.eps_high, self.scale = eps_std, eps_low, eps_high, logit_scale
         self.kl_beta, self.loss_agg = float(kl_beta), int(loss_agg)
         self.comm = comm
         self.grad_W_mode = (1 if comm is not None else 0) if grad_W_mode is None else grad_W_mode
+        # max_rows: bound on the local masked tokens (<= 0: T); the P~ intermediate is sized by it
+        self.max_rows = int(max_rows)
         self.ws = alloc_workspace(agentrl_grpo_step_workspace_size(T, n_traj, n_groups, n_tasks,
-                                                                   d, V), device)
+                                                                   d, V, self.max_rows), device)
         self.n_tasks = n_tasks
         self.adv_tok = torch.empty(T, dtype=torch.float32, device=device)
         self.task_stats = torch.empty(n_tasks, 3, dtype=torch.float64, device=device)
@@ -459,7 +465,7 @@ class Step:
                            eps_low=self.eps_low, eps_high=self.eps_high,
                            logit_scale=self.scale, grad_W_mode=self.grad_W_mode,
                            kl_beta=self.kl_beta, loss_agg=self.loss_agg, ref_logp=ref_logp,
-                           tok_weight=tok_weight)
+                           tok_weight=tok_weight, max_rows=self.max_rows)
         o = make_loss_out(self.loss, self.grad_hidden, self.grad_W, self.logp, self.loss_stats)
         rc = agentrl_grpo_step(b, self.eps_std, a, o, self.adv_tok, self.task_stats, self.ws,
                                self.comm.handle if self.comm else None, self.status, stream)

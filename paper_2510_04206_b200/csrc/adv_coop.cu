@@ -46,6 +46,9 @@ constexpr int WCHUNK = 512;        // tokens per warp chunk (32 lanes x 16 token
 #ifndef ADV_LDGSTS
 #define ADV_LDGSTS 1  // ring filled by per-lane cp.async (1) or one cp.async.bulk per chunk (0)
 #endif
+#ifndef AGENTRL_ADV_SMALL
+#define AGENTRL_ADV_SMALL 1  // 0: the large driver for every batch
+#endif
 #ifndef ADV_LARGE_MINB
 #define ADV_LARGE_MINB 2  // resident blocks per SM the large driver's register budget is cut for
 #endif
@@ -1516,11 +1519,9 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.task_stats_out = task_stats;
     p.n_mask_global_out = n_mask_global;
     p.compact = compact ? 1 : 0;
-    bool small = b->n_traj <= SMALL_TRAJ && b->n_groups <= SMALL_GROUPS && b->n_tasks <= 64;
-    {
-        const char* e = getenv("AGENTRL_ADV_SMALL");  // A/B: force the large driver
-        if (e && e[0] == '0') small = false;
-    }
+    // AGENTRL_ADV_SMALL=0 (build): always the large driver (A/B and layout tests)
+    const bool small = AGENTRL_ADV_SMALL && b->n_traj <= SMALL_TRAJ &&
+                       b->n_groups <= SMALL_GROUPS && b->n_tasks <= 64;
     p.lay = make_lay(b->n_tasks, compact, small, b->n_traj, b->n_groups);
     const size_t smem = p.lay.total;
     if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;

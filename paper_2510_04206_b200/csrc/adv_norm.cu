@@ -23,6 +23,12 @@
 
 #include "internal.h"
 
+// the cooperative kernels (adv_coop.cu) unless built with -DAGENTRL_ADV_COOP=0; the 3-kernel path
+// below also serves devices without cooperative launch
+#ifndef AGENTRL_ADV_COOP
+#define AGENTRL_ADV_COOP 1
+#endif
+
 namespace agentrl {
 
 __device__ __forceinline__ int32_t find_traj(const int64_t* __restrict__ off, int32_t n_traj,
@@ -432,13 +438,10 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
 int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, double* task_stats,
                     int64_t* n_mask_global, uint8_t* ws, const AdvWs& w, agentrl_comm comm,
                     int32_t* d_status, cudaStream_t stream, bool compact) {
-    {
-        const char* e = getenv("AGENTRL_ADV_COOP");
-        if (!(e && e[0] == '0')) {
-            int rc = launch_adv_norm_coop(b, eps_std, adv_tok, task_stats, n_mask_global, ws, w,
-                                          comm, d_status, stream, compact);
-            if (rc != AGENTRL_ERR_UNSUPPORTED) return rc;
-        }
+    if (AGENTRL_ADV_COOP) {  // build switch; 0: always the 3-kernel path below
+        int rc = launch_adv_norm_coop(b, eps_std, adv_tok, task_stats, n_mask_global, ws, w, comm,
+                                      d_status, stream, compact);
+        if (rc != AGENTRL_ERR_UNSUPPORTED) return rc;
     }
     const int64_t T = b->T;
     const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);

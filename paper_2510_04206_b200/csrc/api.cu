@@ -265,12 +265,13 @@ int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok
                            reinterpret_cast<cudaStream_t>(stream), /*compact=*/false);
 }
 
-size_t agentrl_policy_loss_workspace_size(int64_t T, int32_t d, int32_t V) {
-    return plan_loss(T, d, V).total;
+size_t agentrl_policy_loss_workspace_size(int64_t T, int64_t max_rows, int32_t d, int32_t V) {
+    return plan_loss(T, max_rows, d, V).total;
 }
 
-size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int32_t d, int32_t V, int32_t world) {
-    return plan_loss(T, d, V, 0, std::max(world, 1)).total;
+size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int64_t max_rows, int32_t d, int32_t V,
+                                             int32_t world) {
+    return plan_loss(T, max_rows, d, V, 0, std::max(world, 1)).total;
 }
 
 int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
@@ -283,14 +284,15 @@ int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_o
     if (rc) return rc;
     if (!d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
     if ((rc = check_device())) return rc;
-    LossWs w = plan_loss(a->T, a->d, a->V, 0, a->grad_W_mode == 3 ? comm_world(comm) : 0);
+    LossWs w = plan_loss(a->T, a->max_rows, a->d, a->V, 0,
+                         a->grad_W_mode == 3 ? comm_world(comm) : 0);
     if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
     return launch_policy_loss(a, o, static_cast<uint8_t*>(ws), w, nullptr, nullptr, nullptr,
                               nullptr, comm, d_status, reinterpret_cast<cudaStream_t>(stream));
 }
 
-size_t agentrl_logprob_workspace_size(int64_t T, int32_t d, int32_t V) {
-    return plan_logp(T, d, V).total;
+size_t agentrl_logprob_workspace_size(int64_t T, int64_t max_rows, int32_t d, int32_t V) {
+    return plan_logp(T, max_rows, d, V).total;
 }
 
 int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp, float* entropy, void* ws,
@@ -304,16 +306,16 @@ int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp, float* entro
         return AGENTRL_ERR_SHAPE;
     int rc = check_device();
     if (rc) return rc;
-    LogpWs w = plan_logp(a->T, a->d, a->V);
+    LogpWs w = plan_logp(a->T, a->max_rows, a->d, a->V);
     if (ws_bytes < w.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
     return launch_logprob(a, logp, entropy, static_cast<uint8_t*>(ws), w, d_status,
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t agentrl_grpo_step_workspace_size(int64_t T, int32_t n_traj, int32_t n_groups,
-                                        int32_t n_tasks, int32_t d, int32_t V) {
+                                        int32_t n_tasks, int64_t max_rows, int32_t d, int32_t V) {
     AdvWs wa = plan_adv(T, n_traj, n_groups, n_tasks);
-    return plan_loss(T, d, V, align_up(wa.total, 1024)).total;
+    return plan_loss(T, max_rows, d, V, align_up(wa.total, 1024)).total;
 }
 
 int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss_args* a,
@@ -329,7 +331,7 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
     if ((b->T > 0 && !adv_tok_out) || !d_status || !ws) return AGENTRL_ERR_INVALID_ARG;
     if ((rc = check_device())) return rc;
     AdvWs wa = plan_adv(b->T, b->n_traj, b->n_groups, b->n_tasks);
-    LossWs wl = plan_loss(a->T, a->d, a->V, align_up(wa.total, 1024));
+    LossWs wl = plan_loss(a->T, a->max_rows, a->d, a->V, align_up(wa.total, 1024));
     if (ws_bytes < wl.total || !aligned(ws, 1024)) return AGENTRL_ERR_WORKSPACE;
     uint8_t* w8 = static_cast<uint8_t*>(ws);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -434,6 +436,7 @@ const char* agentrl_status_string(int code) {
         case AGENTRL_ST_GROUP_TOO_SMALL: return "a group has fewer than 2 trajectories";
         case AGENTRL_ST_NO_TOKENS: return "no loss-masked tokens in the batch";
         case AGENTRL_ST_COMM_TIMEOUT: return "a peer never reached the fused reduce-scatter";
+        case AGENTRL_ST_ROWS_OVERFLOW: return "more masked tokens than the workspace's max_rows";
         default: return "unknown";
     }
 }
@@ -513,7 +516,7 @@ int agentrl_profile_stop(double* ms_sum, int* counts, int n_ids) {
 
 const char* agentrl_kernel_name(int id) {
     static const char* names[KID_N] = {"k_count", "k_stats", "k_apply", "k_compact",
-                                       "k_gather", "gemm_fwd", "k_merge_g", "k_loss_reduce",
+                                       "k_gather", "gemm_fwd", "k_row_stats", "k_loss_reduce",
                                        "gemm_grad_W", "gemm_grad_hidden", "gemm_logp",
                                        "k_logp_merge"};
     return (id >= 0 && id < KID_N) ? names[id] : "unknown";

@@ -31,6 +31,15 @@
 //             in the tile.  The T x V logits never reach HBM in fp32 (P~ is 2 B/entry).
 //   EPI_GRADH grad_hidden[idx[r], :] = bf16(s * acc)   (scatter to the original token row)
 //   EPI_GRADW grad_W[r, :] = s * acc (fp32); zeros if the (dynamic) K extent is 0.
+//
+// XF = true (the two backward GEMMs): operand A is the forward's bf16 P~ = exp(z - m_tile), and
+// 4 transform warps (warps 6..9) rewrite each staged A tile in shared memory as the softmax
+// gradient G = bf16(f * P~) with f = c_t exp((m_tile - M_t) - log1p(L'_t)) per (row, 256-column
+// vocabulary tile) and the target column replaced by c_t expm1(log p_t),
+// before the MMA may read it.  Every 128-byte line of a SWIZZLE_128B tile belongs to one token
+// and one vocabulary tile, so one scale covers a line.  Each CTA's TMA then completes on its own
+// full barrier; the transform warps of both CTAs arrive on the leader's `ready` barrier, which
+// the MMA issuer waits on instead.  No G tensor exists in HBM.
 #pragma once
 #include "ptx.cuh"
 
@@ -39,7 +48,9 @@ namespace agentrl {
 constexpr int GEMM_BM = 128;  // rows per CTA
 constexpr int GEMM_BN = 256;  // columns per MMA (and per FWD statistics tile)
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_THREADS = 192;     // producer, MMA, 4 epilogue warps
+constexpr int GEMM_THREADS_XF = 320;  // + 4 transform warps (XF)
+constexpr int XF_WARP0 = 6;
 
 // KSUB: 64-wide K atoms per pipeline stage (K-major operands only).  KSUB = 2 stages 128 K
 // per k-block: 8 MMAs per barrier round trip instead of 4, for the short-K forward GEMM whose
@@ -116,6 +127,13 @@ struct GemmArgs {
     int64_t* prog;
     int32_t prog_every, prog_lead;
     unsigned long long* prog_waits;  // optional: +1 per throttle wait episode (debug counter)
+    // XF: operand A is P~ (bf16 [rows, V]); G = bf16(xf_scale[row * xf_ntiles + tile] * P~),
+    // target column (xf_row[row].x, -1 = none) = __int_as_float(xf_row[row].y); rows at or past
+    // *xf_rows (the dynamic T_eff) are zero
+    const float* xf_scale;
+    const int2* xf_row;
+    const int64_t* xf_rows;
+    int32_t xf_ntiles;
 };
 
 __device__ __forceinline__ void prog_store(int64_t* p, int64_t v) {
@@ -186,7 +204,9 @@ __device__ __forceinline__ void advance_acc(int& acc, uint32_t& acc_phase) {
 }
 
 // TMA loads of one k-block: A (128 rows of this CTA) and B (per MMA half: B_ROWS rows)
-template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB>
+// LOCAL_BAR (XF): every CTA's bytes complete on its own full barrier (its transform warps
+// wait on it), else a pair's bytes complete on the leader's
+template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB, bool LOCAL_BAR>
 __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                            uint64_t* full_bar, uint32_t full_bar_leader,
                                            uint8_t* a_dst, uint8_t* b_dst, int32_t m0,
@@ -195,7 +215,7 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
     using Cfg = GemmCfg<PAIR, NSPLIT, KSUB>;
     static_assert(KSUB == 1 || (!A_MN && !B_MN), "K atoms are stacked for K-major operands");
     auto ld = [&](const CUtensorMap& m, uint8_t* dst, int32_t x, int32_t y, uint64_t pol) {
-        if constexpr (PAIR) tma_load_2d_pair(&m, full_bar_leader, dst, x, y, pol);
+        if constexpr (PAIR && !LOCAL_BAR) tma_load_2d_pair(&m, full_bar_leader, dst, x, y, pol);
         else tma_load_2d(&m, full_bar, dst, x, y, pol);
     };
     if constexpr (!A_MN) {
@@ -219,10 +239,44 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
     }
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB>
+// XF: one 128-byte line of a SWIZZLE_128B tile (64 bf16 of one token and one vocabulary tile;
+// logical 16-byte chunk c sits at physical chunk c ^ (line & 7)) rewritten in place as
+// G = bf16(f * P~), element ycol (0..63, else none) = gy; zero: the whole line is 0
+__device__ __forceinline__ void xf_line(uint8_t* line, int l, float f, int ycol, float gy,
+                                        bool zero) {
+    uint4* L = reinterpret_cast<uint4*>(line);
+    const int sw = l & 7;
+    uint4 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = L[c ^ sw];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[c]);
+        float g[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 x = __bfloat1622float2(h2[k]);
+            g[2 * k] = f * x.x;
+            g[2 * k + 1] = f * x.y;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (c * 8 + k == ycol) g[k] = gy;
+        uint4 o;
+        o.x = pack_bf162(g[0], g[1]);
+        o.y = pack_bf162(g[2], g[3]);
+        o.z = pack_bf162(g[4], g[5]);
+        o.w = pack_bf162(g[6], g[7]);
+        if (zero) o = make_uint4(0u, 0u, 0u, 0u);
+        L[c ^ sw] = o;
+    }
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB, bool XF = false>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                           const GemmArgs& p) {
     using Cfg = GemmCfg<PAIR, NSPLIT, KSUB>;
+    static_assert(!XF || KSUB == 1, "the transform handles one 64-wide K atom per stage");
     static_assert((EPI != EPI_FWD && EPI != EPI_LOGP) || NSPLIT == 1,
                   "forward statistics are per 256-column tile");
     constexpr int STAGES = Cfg::STAGES;
@@ -239,7 +293,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     uint64_t* tempty = tfull + 2;
     uint64_t* tq_full = tempty + 2;   // tile queue (dynamic scheduler): QD slots
     uint64_t* tq_empty = tq_full + QD;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + QD);
+    uint64_t* ready = tq_empty + QD;  // XF: stage transformed (leader's is the one used)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + STAGES);
     volatile int32_t* tile_q = reinterpret_cast<volatile int32_t*>(tmem_slot + 4);
     const bool dyn = p.tile_counter != nullptr;
 
@@ -269,10 +324,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         }
         for (int q = 0; q < QD; ++q) {
             mbar_init(&tq_full[q], 1);
-            // consumers of a queue slot: leader MMA + 4 epilogue warps (+ peer producer and its
-            // 4 epilogue warps); only the leader's tq_empty is used
-            mbar_init(&tq_empty[q], PAIR ? 10 : 5);
+            // consumers of a queue slot: leader MMA + 4 epilogue warps (+ 4 transform warps)
+            // (+ peer producer and its 4 epilogue (+ 4 transform) warps); only the leader's
+            // tq_empty is used
+            constexpr int per_cta = XF ? 8 : 4;
+            mbar_init(&tq_empty[q], PAIR ? 2 + 2 * per_cta : 1 + per_cta);
         }
+        if constexpr (XF)
+            for (int s = 0; s < STAGES; ++s) mbar_init(&ready[s], PAIR ? 8 : 4);
         fence_mbar_init();
         fence_proxy_async_smem();
     }
@@ -340,15 +399,17 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint32_t fb = 0;
-                    if constexpr (PAIR) {
+                    if constexpr (PAIR && !XF) {
                         fb = mapa_shared(smem_u32(&full[stage]), 0);
                         // leader: arm its own full barrier for both CTAs' bytes (CTA scope; the
                         // peer's TMA completes its bytes on it directly)
                         if (leader) mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
                     } else {
-                        mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
+                        // XF: each CTA's own bytes on its own barrier (its transform warps)
+                        mbar_arrive_expect_tx(&full[stage], XF && PAIR ? Cfg::TX_BYTES / 2
+                                                                       : Cfg::TX_BYTES);
                     }
-                    load_stage<A_MN, B_MN, PAIR, NSPLIT, KSUB>(
+                    load_stage<A_MN, B_MN, PAIR, NSPLIT, KSUB, XF>(
                         tmA, tmB, &full[stage], fb, sA + stage * Cfg::A_STAGE,
                         sB + stage * Cfg::B_STAGE, m0, n0, (int32_t)(kb * Cfg::BK), pol_a, pol_b);
                     if (++stage == STAGES) {
@@ -382,7 +443,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_BN);
                 for (int64_t kb = 0; kb < num_kb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    mbar_wait(XF ? &ready[stage] : &full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sA + stage * Cfg::A_STAGE);
                     const uint32_t b_base = smem_u32(sB + stage * Cfg::B_STAGE);
@@ -419,6 +480,98 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             }
         }
         __syncwarp();
+    } else if (XF && warp >= XF_WARP0) {
+        // ------------------------------------------------------------ transform (XF)
+        if constexpr (XF) {
+            const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127: the line this thread owns
+            const int64_t rows = *p.xf_rows;
+            const uint32_t ready_leader = PAIR ? mapa_shared(smem_u32(&ready[0]), 0) : 0u;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t it = 0;; ++it) {
+                int64_t tile;
+                if (!dyn) {
+                    tile = unit + it * n_units;
+                } else {
+                    const int slot = (int)(it & (QD - 1));
+                    mbar_wait(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                    tile = tile_q[slot];
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (leader) mbar_arrive(&tq_empty[slot]);
+                        else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
+                    }
+                }
+                if (tile >= num_tiles) break;
+                int64_t m_blk, n_blk;
+                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                const int64_t m0 = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM;
+                // A_MN = false (grad_hidden): line t = token row m0 + t, K = vocabulary.
+                // A_MN = true (grad_W): line t = token k0 + (t & 63) of the vocabulary atom
+                // m0 + 64 (t >> 6), K = tokens.
+                int64_t tok = 0, vcol0 = 0;  // fixed per tile: the row (grad_h) / vocab atom (grad_W)
+                int2 yr = make_int2(-1, 0);
+                if constexpr (!A_MN) {
+                    tok = m0 + t;
+                    if (tok < rows) yr = p.xf_row[tok];
+                } else {
+                    vcol0 = m0 + 64 * (t >> 6);
+                }
+                const bool vcol_ok = !A_MN || vcol0 < M;
+                auto inputs = [&](int64_t kb, float& f, int& ycol, float& gy, bool& zero) {
+                    const int64_t k0 = kb * GEMM_BK;
+                    if constexpr (!A_MN) {
+                        zero = tok >= rows;
+                        f = zero ? 0.f : __ldg(p.xf_scale + tok * p.xf_ntiles + (k0 >> 8));
+                        const int64_t yl = (int64_t)yr.x - k0;
+                        ycol = (yr.x >= 0 && yl >= 0 && yl < GEMM_BK) ? (int)yl : -1;
+                        gy = __int_as_float(yr.y);
+                    } else {
+                        const int64_t tk = k0 + (t & 63);
+                        zero = tk >= rows || !vcol_ok;
+                        int2 y2 = make_int2(-1, 0);
+                        f = 0.f;
+                        if (!zero) {
+                            f = __ldg(p.xf_scale + tk * p.xf_ntiles + (vcol0 >> 8));
+                            y2 = __ldg(p.xf_row + tk);
+                        }
+                        const int64_t yl = (int64_t)y2.x - vcol0;
+                        ycol = (y2.x >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
+                        gy = __int_as_float(y2.y);
+                    }
+                };
+                float f, gy;
+                int ycol;
+                bool zero;
+                inputs(0, f, ycol, gy, zero);
+                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    // the next k-block's scale / target loads are issued before this one's
+                    // wait, so their latency hides behind the TMA and the transform
+                    float f2 = 0.f, gy2 = 0.f;
+                    int ycol2 = -1;
+                    bool zero2 = true;
+                    if (kb + 1 < num_kb) inputs(kb + 1, f2, ycol2, gy2, zero2);
+                    mbar_wait(&full[stage], phase);
+                    uint8_t* a = sA + stage * Cfg::A_STAGE;
+                    const int line = A_MN ? (t & 63) : t;
+                    xf_line(a + (A_MN ? (t >> 6) * 8192 : 0) + line * 128, line, f, ycol, gy, zero);
+                    fence_proxy_async_smem();  // generic smem writes -> visible to the MMA
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (PAIR) mbar_arrive_cluster(ready_leader + stage * 8);
+                        else mbar_arrive(&ready[stage]);
+                    }
+                    f = f2;
+                    gy = gy2;
+                    ycol = ycol2;
+                    zero = zero2;
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
     } else {
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -645,18 +798,18 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     }
 }
 
-template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB, bool XF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? GEMM_THREADS_XF : GEMM_THREADS, 1)
     gemm_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, true, NSPLIT, KSUB>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, true, NSPLIT, KSUB, XF>(tmA, tmB, p);
 }
 
-template <int EPI, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+template <int EPI, bool A_MN, bool B_MN, bool XF>
+__global__ void __launch_bounds__(XF ? GEMM_THREADS_XF : GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
-    gemm_body<EPI, A_MN, B_MN, false, 1, 1>(tmA, tmB, p);
+    gemm_body<EPI, A_MN, B_MN, false, 1, 1, XF>(tmA, tmB, p);
 }
 
 }  // namespace agentrl

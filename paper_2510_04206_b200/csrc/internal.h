@@ -64,27 +64,31 @@ int launch_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok, doub
 struct LossWs {
     size_t idx, meta;                       // int32 [T] (standalone path), int64 [4]
     size_t chunk_cnt, chunk_base;           // int32 compaction scratch (standalone path)
-    size_t tgt_c, old_c, adv_c;             // compacted per-row inputs
-    size_t H;                               // bf16 [T_pad, d] gathered hidden rows
-    size_t P;                               // bf16 [T_pad, V]: P~ then G (in place)
-    size_t part;                            // float2 [T_pad, n_tiles]
-    size_t zy;                              // float [T_pad]
+    size_t tgt_c, old_c;                    // compacted per-row inputs [rows_cap]
+    size_t adv_c;                           // float [T] compacted advantages (standalone path)
+    size_t H;                               // bf16 [rows_cap, d] gathered hidden rows
+    size_t P;                               // bf16 [rows_cap, V]: P~ = exp(z - m_tile)
+    size_t part;                            // float2 [rows_cap, n_tiles] (m_tile, l'_tile)
+    size_t fscale;                          // float [rows_cap, n_tiles] gradient scale f
+    size_t xrow;                            // int2 [rows_cap] (target column, G value bits)
+    size_t zy;                              // float [rows_cap]
     size_t row_term, row_rho, row_logp;     // double/float per row
     size_t row_clip;                        // int32 per row
     size_t row_kl, w_c, ref_c;              // float per row: KL_t, weight w_t, ref log-prob
-    size_t red;                             // double [8] loss reduction output
+    size_t rows_eff;                        // int64 [2]: min(T_eff, rows_cap)
     size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
-    size_t fbnd;                            // int64 [MAX_FWD_CHUNKS + 1] forward row chunks
-    size_t prog;                            // int64 [2 + MAX_FWD_CHUNKS][PROG_UNITS] GEMM progress
+    size_t prog;                            // int64 [3][PROG_UNITS] GEMM progress
     size_t vpstat;                          // vocab-parallel: float2 [world][rows_cap] (M_r, L'_r)
     size_t vp_gh;                           // vocab-parallel: float [rows_cap, d] grad_h partial
     int32_t vp_world;                       // 0 = not planned for the vocab-parallel head
+    int64_t rows_cap;                       // row capacity (max_rows rounded up to 128)
     size_t total;
     int32_t n_tiles;
 };
-constexpr int MAX_FWD_CHUNKS = 8;
 constexpr int PROG_UNITS = 256;  // >= GEMM units (SMs, or SM pairs)
-LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base = 0, int32_t vp_world = 0);
+int64_t loss_rows_cap(int64_t T, int64_t max_rows);
+LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base = 0,
+                 int32_t vp_world = 0);
 
 // Enqueue part 2.  If `idx_dev` / `rows_dev` are given (fused step) the compaction is reused:
 //   idx_dev  int32 [T] compacted token positions, rows_dev -> int64 number of rows (local T_eff),
@@ -108,9 +112,10 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
 // ---- forward-only log-prob / entropy (lmhead.cu) ----
 struct LogpWs {
     size_t idx, meta, chunk, tgt_c, H, part4, zy, sched, total;
+    int64_t rows_cap;
     int32_t n_tiles;
 };
-LogpWs plan_logp(int64_t T, int32_t d, int32_t V, size_t base = 0);
+LogpWs plan_logp(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base = 0);
 int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, uint8_t* ws,
                    const LogpWs& w, int32_t* d_status, cudaStream_t stream);
 

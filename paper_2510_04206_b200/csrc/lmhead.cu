@@ -2,20 +2,26 @@
 // exact backward (PAPER.md P:1182-1190 token factorisation, P:1230-1241 PPO-clip,
 // P:1132-1141 token-level mean / decoupled eps).
 //
-//   K4 k_gather       compacted rows: H[p] = hidden[idx[p]], target/old/adv per row; rows
-//                     [T_eff, pad64) zeroed (they are inside GEMM3's K range)
+//   K4 k_gather       compacted rows: H[p] = hidden[idx[p]], target/old per row; rows
+//                     [T_eff, pad64) zeroed (they are inside grad_W's K range)
 //   K5 gemm<FWD>      z = s * H W^T on tcgen05; epilogue: per (row, 256-col tile) max m and
-//                     l = sum exp(z - m), P~ = exp(z - m) -> bf16 [rows, V], z_y gathered
-//   K6 k_merge_g      per row: lse = logsumexp over tiles, logp, rho, PPO-clip term,
-//                     c = unclipped ? rho*A/N : 0; rewrites the row in place as
-//                     G = bf16(c * (P~ * exp(m_tile - lse) - [v == y]))
+//                     l' = sum exp(z - m) - 1, P~ = exp(z - m) -> bf16 [rows, V], z_y gathered
+//   K6 k_row_stats    per row: lse over tiles, logp, rho, PPO-clip term, c = unclipped ? w rho A
+//                     : 0; the per-(row, tile) gradient scale f = c exp((m_tile - M) - log1p(L'))
+//                     and the target column's G value c expm1(logp)
 //   K7 k_loss_reduce  fixed-order fp64 reduction of the per-row terms -> loss, stats
-//   K9 gemm<GRADW>    grad_W = s * G^T H      (A = G MN-major, B = H MN-major, K = T_eff)
-//   C3                NCCL all-reduce of grad_W on a side stream, overlapped with K8
-//   K8 gemm<GRADH>    grad_hidden[idx] = s * G W  (A = G K-major, B = W MN-major, K = V)
+//   K9 gemm<GRADW,XF> grad_W = s * G^T H   (A = P~ MN-major, B = H MN-major, K = T_eff)
+//   C3                grad_W all-reduce / reduce-scatter on a side stream, overlapped with K8, or
+//                     fused into K9's epilogue as peer stores (peer.cu)
+//   K8 gemm<GRADH,XF> grad_hidden[idx] = s * G W  (A = P~ K-major, B = W MN-major, K = V)
+// In K8 and K9 (XF) transform warps rewrite each staged P~ tile in shared memory as
+// G = bf16(f * P~) (target column replaced) before the MMA reads it: G never exists in HBM.
 //
 // Executed tensor work is 6 * T_eff * V * d FLOP (three GEMMs; no recompute: the bf16 P~
 // written by the forward epilogue replaces the second logits GEMM).  See DESIGN.md.
+//
+// Schedule and staging choices are compile-time constants (measured defaults; A/B builds pass
+// -D overrides through build.py, tests/test_gpu_variants.py keeps them parity-green).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -66,89 +72,107 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS ? AGENTRL_OK : AGENTRL_ERR_CUDA;
 }
 
-// CTA-pair (cta_group::2) GEMMs unless AGENTRL_GEMM_PAIR=0 (1-CTA variant, for A/B runs)
-static bool gemm_use_pair() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("AGENTRL_GEMM_PAIR");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
+// ---------------------------------------------------------------------------- build knobs
+// CTA-pair (cta_group::2) GEMMs; 0: the 1-CTA cta_group::1 variant (128 x 256 tiles)
+#ifndef AGENTRL_GEMM_PAIR
+#define AGENTRL_GEMM_PAIR 1
+#endif
+// dynamic tile scheduler (atomic counter, tiles claimed in global order); 0: static persistent
+// striding (tile = unit + i * units: pairs drift apart over long runs)
+#ifndef AGENTRL_GEMM_DYNAMIC
+#define AGENTRL_GEMM_DYNAMIC 1
+#endif
+// 1: one CTA (pair) per tile instead of one per SM
+#ifndef AGENTRL_GEMM_FULLGRID
+#define AGENTRL_GEMM_FULLGRID 0
+#endif
+// 512-column tiles for the long-K backward GEMMs (CTA pairs only); 0: 256-column tiles
+#ifndef AGENTRL_GEMM_WIDE_N
+#define AGENTRL_GEMM_WIDE_N 1
+#endif
+// forward / log-prob GEMMs stage two 64-wide K atoms per k-block (8 MMAs per barrier round
+// trip: 94% vs 89% tensor-pipe active, profiles/r01_fwd_ksub.txt); 1: one atom
+#ifndef AGENTRL_FWD_KSUB
+#define AGENTRL_FWD_KSUB 2
+#endif
+// raster: tiles grouped by GROUP_M row blocks, columns fastest inside (forward / backward)
+#ifndef AGENTRL_GROUP_M
+#define AGENTRL_GROUP_M 16
+#endif
+#ifndef AGENTRL_GROUP_M_BWD
+#define AGENTRL_GROUP_M_BWD 8
+#endif
+// L2 eviction policy per operand (0 normal, 1 evict_first, 2 evict_last): forward H evict_last
+// (reused by every column block of its row group), W evict_first (streamed); backward all
+// normal (evict_first on G made the pairs sharing a row block re-read it from HBM,
+// profiles/r01_l2pol_dyn.txt)
+#ifndef AGENTRL_L2POL_FWD_A
+#define AGENTRL_L2POL_FWD_A 2
+#endif
+#ifndef AGENTRL_L2POL_FWD_B
+#define AGENTRL_L2POL_FWD_B 1
+#endif
+#ifndef AGENTRL_L2POL_BWD
+#define AGENTRL_L2POL_BWD 0
+#endif
+// backward-GEMM progress throttle: max lead in k-blocks over the slowest pair (0 = off),
+// checked every THROTTLE_EVERY k-blocks.  glm9b: grad GEMM HBM reads 144/151 -> 67/64 GB at
+// lead 192, +3% cycles, step 157 -> 150 ms on the power-capped part (profiles/r01_throttle.txt);
+// lead 96 then measured 0.6 ms/step faster than 192 (profiles/r01_ab_lead.txt)
+#ifndef AGENTRL_THROTTLE_LEAD
+#define AGENTRL_THROTTLE_LEAD 96
+#endif
+#ifndef AGENTRL_THROTTLE_EVERY
+#define AGENTRL_THROTTLE_EVERY 8
+#endif
+// forward GEMM throttle (k-blocks of 128 K; 0 = off)
+#ifndef AGENTRL_THROTTLE_LEAD_FWD
+#define AGENTRL_THROTTLE_LEAD_FWD 0
+#endif
+// SMs left free for an NCCL C3 kernel while grad_hidden overlaps it (multi-rank only)
+#ifndef AGENTRL_COMM_SMS
+#define AGENTRL_COMM_SMS 16
+#endif
 
-// L2 eviction policy per GEMM operand (0 normal, 1 evict_first, 2 evict_last); the defaults
-// can be overridden for experiments with AGENTRL_L2POL="fa fb wa wb ha hb" (six digits).
-static int l2_policy(int which, int dflt) {
-    const char* e = getenv("AGENTRL_L2POL");
-    if (!e || (int)strlen(e) < 6) return dflt;
-    const int v = e[which] - '0';
-    return (v >= 0 && v <= 2) ? v : dflt;
-}
-static int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : dflt;
-}
-static int gemm_group_m() { return env_int("AGENTRL_GROUP_M", 16); }
-static int gemm_group_m_bwd() { return env_int("AGENTRL_GROUP_M_BWD", 8); }
-// dynamic tile scheduler (atomic counter, tiles claimed in global order) unless
-// AGENTRL_GEMM_SCHED=static (tile = unit + i * units: pairs drift apart over long runs)
-static bool gemm_dynamic() {
-    const char* e = getenv("AGENTRL_GEMM_SCHED");
-    return !(e && strcmp(e, "static") == 0);
-}
-// persistent grid (one CTA per SM) unless AGENTRL_GEMM_FULLGRID=1 (one CTA per tile)
-static bool gemm_full_grid() { return env_int("AGENTRL_GEMM_FULLGRID", 0) == 1; }
+constexpr bool kPair = AGENTRL_GEMM_PAIR != 0;
+constexpr bool kDynamic = AGENTRL_GEMM_DYNAMIC != 0;
+constexpr bool kWideN = AGENTRL_GEMM_WIDE_N != 0 && kPair;
+constexpr int kFwdKsub = AGENTRL_FWD_KSUB == 1 ? 1 : 2;
+constexpr int kThrottleLead = kDynamic ? AGENTRL_THROTTLE_LEAD : 0;
+constexpr int kThrottleLeadFwd = kDynamic ? AGENTRL_THROTTLE_LEAD_FWD : 0;
 
-// 512-column tiles for the long-K backward GEMMs (CTA pairs only) unless
-// AGENTRL_GEMM_NSPLIT=1
-static bool gemm_wide_n() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("AGENTRL_GEMM_NSPLIT");
-        v = (e && e[0] == '1') ? 0 : 1;
-    }
-    return v == 1 && gemm_use_pair();
-}
-
-// forward/log-prob GEMMs stage two 64-wide K atoms per k-block unless AGENTRL_FWD_KSUB=1
-static bool gemm_fwd_ksub2() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("AGENTRL_FWD_KSUB");
-        v = (e && e[0] == '1') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB = 1>
+template <int EPI, bool A_MN, bool B_MN, int NSPLIT, int KSUB = 1, bool XF = false>
 static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g,
                        int64_t max_tiles, cudaStream_t stream, int reserve_sms = 0) {
     ProfScope ps(EPI == EPI_FWD    ? KID_FWD
-                 : EPI == EPI_GRADW ? KID_GRADW
+                 : EPI == EPI_GRADW ? (A_MN ? KID_GRADW : KID_GRADH)
                  : EPI == EPI_LOGP  ? KID_LOGP_GEMM
                                     : KID_GRADH,
                  stream);
+    constexpr int threads = XF ? GEMM_THREADS_XF : GEMM_THREADS;
     // max_tiles is counted in 128 x 256 tiles (an upper bound of the CTAs worth launching)
-    if (gemm_use_pair()) {
-        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB>;
+    if constexpr (kPair) {
+        auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB, XF>;
         constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM +
                              (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0);
         static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
-        int64_t grid = gemm_full_grid()
+        int64_t grid = AGENTRL_GEMM_FULLGRID
                            ? 2 * std::max<int64_t>(max_tiles, 1)
                            : std::min<int64_t>((num_sms() - reserve_sms) & ~1,
                                                std::max<int64_t>(max_tiles, 2));
         grid &= ~int64_t(1);
-        kern<<<(unsigned)grid, GEMM_THREADS, smem, stream>>>(a, b, g);
+        kern<<<(unsigned)grid, threads, smem, stream>>>(a, b, g);
     } else {
-        auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN>;
+        auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN, XF>;
         constexpr int smem = GemmCfg<false, 1>::SMEM;
         static std::atomic<uint64_t> attr_done{0};
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
-        int grid = (int)std::min<int64_t>(num_sms() - reserve_sms, std::max<int64_t>(max_tiles, 1));
-        kern<<<grid, GEMM_THREADS, smem, stream>>>(a, b, g);
+        int grid = AGENTRL_GEMM_FULLGRID
+                       ? (int)std::max<int64_t>(max_tiles, 1)
+                       : (int)std::min<int64_t>(num_sms() - reserve_sms,
+                                                std::max<int64_t>(max_tiles, 1));
+        kern<<<grid, threads, smem, stream>>>(a, b, g);
     }
     count_launch();
     AG_CUDA(cudaGetLastError());
@@ -236,17 +260,25 @@ __global__ void __launch_bounds__(CHUNK_THREADS)
 }
 
 // ---------------------------------------------------------------------------- K4 gather
+// rows_eff: the masked rows part 2 processes, min(T_eff, rows_cap) (the workspace holds
+// rows_cap rows; more masked tokens than that set AGENTRL_ST_ROWS_OVERFLOW and only the first
+// rows_cap are processed).  Written here by block 0 for every later kernel of the call.
 __global__ void __launch_bounds__(256)
-    k_gather(const int64_t* __restrict__ rows_dev, int64_t T, int32_t d, int32_t V,
-             const __nv_bfloat16* __restrict__ hidden, const int32_t* __restrict__ target,
-             const float* __restrict__ old_logp, const int32_t* __restrict__ idx,
-             __nv_bfloat16* __restrict__ H, int32_t* __restrict__ tgt_c,
-             float* __restrict__ old_c, int32_t* d_status, int64_t v0 = 0,
-             int64_t V_total = -1) {
+    k_gather(const int64_t* __restrict__ rows_dev, int64_t rows_cap, int64_t* rows_eff, int64_t T,
+             int32_t d, int32_t V, const __nv_bfloat16* __restrict__ hidden,
+             const int32_t* __restrict__ target, const float* __restrict__ old_logp,
+             const int32_t* __restrict__ idx, __nv_bfloat16* __restrict__ H,
+             int32_t* __restrict__ tgt_c, float* __restrict__ old_c, int32_t* d_status,
+             int64_t v0 = 0, int64_t V_total = -1) {
     // vocab-parallel head: this rank holds columns [v0, v0 + V) of V_total; a target outside
     // the shard gets tgt_c = -1 (never matches a column here)
     if (V_total < 0) V_total = V;
-    const int64_t rows = *rows_dev;
+    const int64_t rows_all = *rows_dev;
+    const int64_t rows = rows_all < rows_cap ? rows_all : rows_cap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *rows_eff = rows;
+        if (rows_all > rows_cap) atomicOr(d_status, AGENTRL_ST_ROWS_OVERFLOW);
+    }
     const int64_t rows_pad = (rows + 63) / 64 * 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * 8;
@@ -277,72 +309,56 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// ---------------------------------------------------------------------------- K6 merge + G
-constexpr int MERGE_THREADS = 256;
-#ifndef MERGE_MINB
-#define MERGE_MINB 0  // 0: no residency hint
-#endif
-#if MERGE_MINB > 0
-#define MERGE_BOUNDS __launch_bounds__(MERGE_THREADS, MERGE_MINB)
-#else
-#define MERGE_BOUNDS __launch_bounds__(MERGE_THREADS)
-#endif
+// ---------------------------------------------------------------------------- K6 row stats
+// One block per row (grid-stride).  Same reductions, in the same order, as the former in-place
+// merge, so G = bf16(f * P~) (formed later inside the backward GEMMs) is bit-identical to the G
+// that merge wrote.
+constexpr int STATS_THREADS_ROW = 256;
 
-__global__ void MERGE_BOUNDS
-    k_merge_g(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
-              int32_t V, int32_t n_tiles, const float2* __restrict__ part,
-              const float* __restrict__ zy, const int32_t* __restrict__ tgt_c,
-              const float* __restrict__ old_c, const float* __restrict__ adv_c,
-              const int32_t* __restrict__ idx, float eps_lo, float eps_hi,
-              const float* __restrict__ w_c /* per-row weight w_t */,
-              const float* __restrict__ ref_c /* per-row ref log-prob or null */,
-              float kl_beta, uint16_t* __restrict__ PG /* bf16 P~ in, bf16 G out, [rows, V] */,
-              double* __restrict__ row_term /* w (-term + beta KL) */,
-              float* __restrict__ row_rho, float* __restrict__ row_logp,
-              int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
-              float* __restrict__ logp_out,
-              const int64_t* __restrict__ rng /* optional row range [r0, r1) */,
-              const float2* __restrict__ vpstat = nullptr /* [vp_R][vp_stride] (M_r, L'_r) */,
-              int32_t vp_R = 0, int64_t vp_stride = 0) {
-    extern __shared__ float s_f[];  // [n_tiles] scale per tile
-    __shared__ float s_red[MERGE_THREADS / 32];
-    __shared__ int s_jm[MERGE_THREADS / 32];
+__global__ void __launch_bounds__(STATS_THREADS_ROW)
+    k_row_stats(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
+                int32_t n_tiles, const float2* __restrict__ part, const float* __restrict__ zy,
+                const int32_t* __restrict__ tgt_c, const float* __restrict__ old_c,
+                const float* __restrict__ adv_c, const int32_t* __restrict__ idx, float eps_lo,
+                float eps_hi, const float* __restrict__ w_c /* per-row weight w_t */,
+                const float* __restrict__ ref_c /* per-row ref log-prob or null */,
+                float kl_beta, float* __restrict__ fscale /* [rows, n_tiles] */,
+                int2* __restrict__ xrow /* [rows] (target column, G value bits) */,
+                double* __restrict__ row_term /* w (-term + beta KL) */,
+                float* __restrict__ row_rho, float* __restrict__ row_logp,
+                int32_t* __restrict__ row_clip, float* __restrict__ row_kl,
+                float* __restrict__ logp_out,
+                const float2* __restrict__ vpstat = nullptr /* [vp_R][vp_stride] (M_r, L'_r) */,
+                int32_t vp_R = 0, int64_t vp_stride = 0) {
+    constexpr int NT = STATS_THREADS_ROW;
+    __shared__ float s_red[NT / 32];
+    __shared__ int s_jm[NT / 32];
     __shared__ float s_bc[4];
     const int64_t rows = *rows_dev;
-    const int64_t rows_pad = (rows + 63) / 64 * 64;
     const double Nd = (double)*nglob_dev;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float LOG2E = 1.4426950408889634f;
-    // row range of this launch; the one ending at rows also zeroes the padding rows
-    const int64_t p_lo = rng ? rng[0] : 0;
-    const int64_t p_hi = rng ? (rng[1] >= rows ? rows_pad : rng[1]) : rows_pad;
 
-    for (int64_t p = p_lo + blockIdx.x; p < p_hi; p += gridDim.x) {
-        uint4* row4 = reinterpret_cast<uint4*>(PG + p * (int64_t)V);
-        const int nvec = V / 8;
-        if (p >= rows) {  // padding rows inside GEMM3's K range: zero
-            for (int c = threadIdx.x; c < nvec; c += MERGE_THREADS) row4[c] = make_uint4(0, 0, 0, 0);
-            continue;
-        }
+    for (int64_t p = blockIdx.x; p < rows; p += gridDim.x) {
         const float2* pr = part + p * (int64_t)n_tiles;
         // lse over tiles: M = max m_j, L = sum l_j exp(m_j - M)   (fixed order per thread +
         // fixed tree -> deterministic)
         float mloc = -INFINITY;
-        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS) mloc = fmaxf(mloc, pr[j].x);
+        for (int j = threadIdx.x; j < n_tiles; j += NT) mloc = fmaxf(mloc, pr[j].x);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
         if (lane == 0) s_red[wid] = mloc;
         __syncthreads();
         if (threadIdx.x == 0) {
             float m = s_red[0];
-            for (int w = 1; w < MERGE_THREADS / 32; ++w) m = fmaxf(m, s_red[w]);
+            for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, s_red[w]);
             s_bc[0] = m;
         }
         __syncthreads();
         const float M = s_bc[0];
         // first tile holding the row max (its l' enters without the leading 1)
         int jloc = 0x7fffffff;
-        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
+        for (int j = threadIdx.x; j < n_tiles; j += NT)
             if (pr[j].x == M) jloc = min(jloc, j);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) jloc = min(jloc, __shfl_xor_sync(0xffffffffu, jloc, o));
@@ -350,10 +366,10 @@ __global__ void MERGE_BOUNDS
         if (lane == 0) s_jm[wid] = jloc;
         __syncthreads();
         int jM = s_jm[0];
-        for (int w = 1; w < MERGE_THREADS / 32; ++w) jM = min(jM, s_jm[w]);
+        for (int w = 1; w < NT / 32; ++w) jM = min(jM, s_jm[w]);
         // L' = sum_v exp(z_v - M) - 1 = l'_{jM} + sum_{j != jM} (1 + l'_j) exp(m_j - M)
         float lloc = 0.f;
-        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS) {
+        for (int j = threadIdx.x; j < n_tiles; j += NT) {
             const float2 ml = pr[j];
             lloc += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
         }
@@ -361,10 +377,9 @@ __global__ void MERGE_BOUNDS
         for (int o = 16; o > 0; o >>= 1) lloc += __shfl_xor_sync(0xffffffffu, lloc, o);
         if (lane == 0) s_red[wid] = lloc;
         __syncthreads();
-        float c_t = 0.f;
         if (threadIdx.x == 0) {
             float Lm1 = 0.f;
-            for (int w = 0; w < MERGE_THREADS / 32; ++w) Lm1 += s_red[w];
+            for (int w = 0; w < NT / 32; ++w) Lm1 += s_red[w];
             float Mrow = M;  // the row max over every column of the head
             if (vpstat) {
                 // vocab-parallel head: combine the ranks' (M_r, L'_r) like tiles -- the first
@@ -404,61 +419,29 @@ __global__ void MERGE_BOUNDS
                 kl = er - r - 1.0;
                 dkl = 1.0 - er;
             }
-            c_t = (float)(w * ((clipped ? 0.0 : (double)rho * (double)A) - (double)kl_beta * dkl));
+            const float c_t =
+                (float)(w * ((clipped ? 0.0 : (double)rho * (double)A) - (double)kl_beta * dkl));
             row_term[p] = w * (-term + (double)kl_beta * kl);
             row_rho[p] = rho;
             row_logp[p] = logp;
             row_clip[p] = clipped ? 1 : 0;
             row_kl[p] = (float)kl;
             if (logp_out) logp_out[idx[p]] = logp;
+            // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
+            xrow[p] = make_int2(tgt_c[p], __float_as_int(c_t * expm1f(logp)));
             s_bc[0] = l1;
             s_bc[1] = c_t;
             s_bc[3] = Mrow;
-            // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
-            s_bc[2] = c_t * expm1f(logp);
         }
         __syncthreads();
         const float l1 = s_bc[0];
-        c_t = s_bc[1];
-        const float g_y = s_bc[2];
+        const float c_t = s_bc[1];
         const float Mrow = s_bc[3];
-        // exp(m_j - lse) = exp((m_j - M) - log1p(L'))
-        for (int j = threadIdx.x; j < n_tiles; j += MERGE_THREADS)
-            s_f[j] = c_t * ex2_approx(((pr[j].x - Mrow) - l1) * LOG2E);
-        __syncthreads();
-        const int32_t y = tgt_c[p];
-        // 16-byte vectors, MERGE_UNROLL loads in flight per thread before any store
-        auto conv = [&](const uint4& in, int v0) -> uint4 {
-            const float f = s_f[v0 >> 8];  // 256-column tiles
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&in);
-            float g[8];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 x = __bfloat1622float2(h2[k]);
-                g[2 * k] = f * x.x;
-                g[2 * k + 1] = f * x.y;
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (v0 + k == y) g[k] = g_y;
-            uint4 out;
-            out.x = pack_bf162(g[0], g[1]);
-            out.y = pack_bf162(g[2], g[3]);
-            out.z = pack_bf162(g[4], g[5]);
-            out.w = pack_bf162(g[6], g[7]);
-            return out;
-        };
-        constexpr int MERGE_UNROLL = 4;
-        int c = threadIdx.x;
-        for (; c + (MERGE_UNROLL - 1) * MERGE_THREADS < nvec; c += MERGE_UNROLL * MERGE_THREADS) {
-            uint4 in[MERGE_UNROLL];
-#pragma unroll
-            for (int u = 0; u < MERGE_UNROLL; ++u) in[u] = row4[c + u * MERGE_THREADS];
-#pragma unroll
-            for (int u = 0; u < MERGE_UNROLL; ++u)
-                row4[c + u * MERGE_THREADS] = conv(in[u], (c + u * MERGE_THREADS) * 8);
-        }
-        for (; c < nvec; c += MERGE_THREADS) row4[c] = conv(row4[c], c * 8);
+        // G = bf16(f_j * P~) per 256-column tile j, f_j = c exp(m_j - lse) = c exp((m_j - M) -
+        // log1p(L')) (formed by the backward GEMMs' transform warps)
+        float* fr = fscale + p * (int64_t)n_tiles;
+        for (int j = threadIdx.x; j < n_tiles; j += NT)
+            fr[j] = c_t * ex2_approx(((pr[j].x - Mrow) - l1) * LOG2E);
         __syncthreads();
     }
 }
@@ -528,12 +511,20 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ---------------------------------------------------------------------------- host
-LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base, int32_t vp_world) {
+// rows_cap: the row capacity of the per-row buffers, max_rows (<= 0: T) rounded up to GEMM_BM
+int64_t loss_rows_cap(int64_t T, int64_t max_rows) {
+    const int64_t r = (max_rows > 0 && max_rows < T) ? max_rows : T;
+    return ceil_div(std::max<int64_t>(r, 1), GEMM_BM) * GEMM_BM;
+}
+
+LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
+                 int32_t vp_world) {
     WsPlan p;
     p.off = base;
     LossWs w;
-    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t rows_cap = loss_rows_cap(T, max_rows);
     const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    w.rows_cap = rows_cap;
     w.n_tiles = (int32_t)ceil_div(V, GEMM_BN);
     w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
     w.meta = p.take(sizeof(int64_t) * 4);
@@ -541,10 +532,12 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base, int32_t vp_world)
     w.chunk_base = w.chunk_cnt;
     w.tgt_c = p.take(sizeof(int32_t) * (size_t)rows_cap);
     w.old_c = p.take(sizeof(float) * (size_t)rows_cap);
-    w.adv_c = p.take(sizeof(float) * (size_t)rows_cap);
+    w.adv_c = p.take(sizeof(float) * (size_t)std::max<int64_t>(T, 1));  // standalone compaction
     w.H = p.take((size_t)rows_cap * d * 2, 1024);
     w.P = p.take((size_t)rows_cap * V * 2, 1024);
     w.part = p.take(sizeof(float2) * (size_t)rows_cap * w.n_tiles);
+    w.fscale = p.take(sizeof(float) * (size_t)rows_cap * w.n_tiles);
+    w.xrow = p.take(sizeof(int2) * (size_t)rows_cap);
     w.zy = p.take(sizeof(float) * (size_t)rows_cap);
     w.row_term = p.take(sizeof(double) * (size_t)rows_cap);
     w.row_rho = p.take(sizeof(float) * (size_t)rows_cap);
@@ -553,10 +546,9 @@ LossWs plan_loss(int64_t T, int32_t d, int32_t V, size_t base, int32_t vp_world)
     w.row_kl = p.take(sizeof(float) * (size_t)rows_cap);
     w.w_c = p.take(sizeof(float) * (size_t)rows_cap);
     w.ref_c = p.take(sizeof(float) * (size_t)rows_cap);
-    w.red = p.take(sizeof(double) * 8);
+    w.rows_eff = p.take(sizeof(int64_t) * 2);
     w.sched = p.take(sizeof(int) * 32);
-    w.fbnd = p.take(sizeof(int64_t) * (MAX_FWD_CHUNKS + 1));
-    w.prog = p.take(sizeof(int64_t) * (2 + MAX_FWD_CHUNKS) * PROG_UNITS);
+    w.prog = p.take(sizeof(int64_t) * 3 * PROG_UNITS);
     w.vp_world = vp_world;
     w.vpstat = w.vp_gh = 0;
     if (vp_world > 0) {
@@ -631,25 +623,9 @@ __global__ void __launch_bounds__(256)
                   const int32_t* __restrict__ n_g, const int32_t* __restrict__ group_id,
                   const int32_t* __restrict__ grp_cnt, int32_t n_groups,
                   const int64_t* __restrict__ ngrp_dev, float* __restrict__ w_c,
-                  float* __restrict__ ref_c, int32_t n_fchunks, float fratio,
-                  int64_t* __restrict__ fbnd) {
+                  float* __restrict__ ref_c) {
     const int64_t rows = *rows_dev;
     const double N = (double)*nglob_dev;
-    if (blockIdx.x == 0 && threadIdx.x <= n_fchunks) {
-        // forward row chunks [fbnd[c], fbnd[c+1]): 256-row aligned, the last ends at rows;
-        // geometric sizes (chunk c+1 = fratio x chunk c) keep the merge of the last chunk,
-        // the one that cannot overlap a forward chunk, short
-        const int c = threadIdx.x;
-        double frac;
-        if (fratio == 1.f) {
-            frac = (double)c / n_fchunks;
-        } else {
-            const double r = fratio;
-            frac = (1.0 - pow(r, (double)c)) / (1.0 - pow(r, (double)n_fchunks));
-        }
-        const int64_t b = (int64_t)ceil(frac * (double)rows / 256.0) * 256;
-        fbnd[c] = c == n_fchunks ? rows : min(rows, b);
-    }
     const double G = ngrp_dev ? (double)*ngrp_dev : 0.0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < rows;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -689,106 +665,23 @@ static SideStream& side_stream() {
     return ss;
 }
 
-// backward-GEMM progress throttle: max lead in k-blocks over the slowest pair
-// (AGENTRL_THROTTLE_LEAD, default 96, 0 = off) checked every AGENTRL_THROTTLE_EVERY k-blocks.
-// glm9b: grad GEMM HBM reads 144/151 -> 67/64 GB at lead 192, +3% cycles, step 157 -> 150 ms on
-// the power-capped part (profiles/r01_throttle.txt); lead 96 then measured 0.6 ms/step faster
-// than 192 (less DRAM, higher clock; 2 x 3 interleaved A/B rounds, profiles/r01_ab_lead.txt)
-static int throttle_lead() {
-    static int v = -2;
-    if (v == -2) {
-        const char* e = getenv("AGENTRL_THROTTLE_LEAD");
-        v = e ? atoi(e) : 96;
-    }
-    return gemm_dynamic() ? v : 0;
-}
-static int throttle_every() { return env_int("AGENTRL_THROTTLE_EVERY", 8); }
-// forward GEMM throttle (AGENTRL_THROTTLE_LEAD_FWD, k-blocks of 128 K; 0 = off)
-static int throttle_lead_fwd() {
-    static int v = -2;
-    if (v == -2) {
-        const char* e = getenv("AGENTRL_THROTTLE_LEAD_FWD");
-        v = e ? atoi(e) : 0;
-    }
-    return gemm_dynamic() ? v : 0;
-}
-
-// SMs left free for NCCL while grad_hidden overlaps C3 (AGENTRL_COMM_SMS, default 16), only
-// when the communicator spans more than one rank
-static int comm_reserve_sms() {
-    static int v = -2;
-    if (v == -2) {
-        const char* e = getenv("AGENTRL_COMM_SMS");
-        v = e ? std::max(0, atoi(e)) : 16;
-    }
-    return std::min(v, num_sms() / 2);
-}
-
-// forward row chunks (AGENTRL_FWD_CHUNKS; default 1 = the merge runs after the whole forward).
-// With 4 chunks the merge of chunk c overlaps the forward of chunk c+1, but the co-resident
-// merge blocks slow the forward GEMM about as much as they hide (live forward 51 vs 47.7 ms at
-// glm9b), and the last merge stays exposed: 1 chunk measured 0.7 ms/step faster (3 A/B pairs)
-static int fwd_chunks() {
-    static int v = -1;
-    if (v < 0) v = std::min(env_int("AGENTRL_FWD_CHUNKS", 1), MAX_FWD_CHUNKS);
-    return v;
-}
-// one GPU: grad_hidden and grad_W on two prioritised streams so their tails overlap
-// (AGENTRL_BWD_OVERLAP=1; off: measured neutral, 155.75 vs 155.46 ms full size and 20.50 vs
-// 20.43 ms at the 1/8 shard, interleaved A/B)
-static bool bwd_overlap() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("AGENTRL_BWD_OVERLAP");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-// size ratio of consecutive forward row chunks (AGENTRL_FWD_RATIO, default 1 = equal; 0.5 and
-// 0.35 shorten the last, un-overlapped merge but slow the forward as much: same step time)
-static float fwd_ratio() {
-    static float v = -1.f;
-    if (v < 0.f) {
-        const char* e = getenv("AGENTRL_FWD_RATIO");
-        const float x = e ? (float)atof(e) : 0.f;
-        v = (x > 0.f && x <= 1.f) ? x : 1.f;
-    }
-    return v;
-}
-struct ForkStreams {
-    cudaStream_t hi = nullptr, lo = nullptr;  // forward chunks / merges
-    cudaEvent_t fork = nullptr, join = nullptr, ev[MAX_FWD_CHUNKS] = {};
-};
-static ForkStreams& fork_streams() {
-    static thread_local ForkStreams fs[MAX_DEVICES];  // per device
-    ForkStreams& f = fs[current_device() & (MAX_DEVICES - 1)];
-    if (!f.hi) {
-        int least = 0, greatest = 0;
-        cudaDeviceGetStreamPriorityRange(&least, &greatest);
-        cudaStreamCreateWithPriority(&f.hi, cudaStreamNonBlocking, greatest);
-        cudaStreamCreateWithPriority(&f.lo, cudaStreamNonBlocking, least);
-        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
-        for (auto& e : f.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    }
-    return f;
-}
-
 int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, uint8_t* ws,
                        const LossWs& w, const int32_t* idx_dev, const int64_t* rows_dev,
                        const float* adv_c_dev, const int64_t* nglob_dev, agentrl_comm comm,
                        int32_t* d_status, cudaStream_t stream, const FusedExtras* fx) {
     const int64_t T = a->T;
     const int32_t d = a->d, V = a->V;
-    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t rows_cap = w.rows_cap;
     int64_t* meta = reinterpret_cast<int64_t*>(ws + w.meta);
     int32_t* idx = reinterpret_cast<int32_t*>(ws + w.idx);
     float* adv_c = reinterpret_cast<float*>(ws + w.adv_c);
     int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + w.tgt_c);
     float* old_c = reinterpret_cast<float*>(ws + w.old_c);
     __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(ws + w.H);
-    uint16_t* PG = reinterpret_cast<uint16_t*>(ws + w.P);
+    __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(ws + w.P);
     float2* part = reinterpret_cast<float2*>(ws + w.part);
+    float* fscale = reinterpret_cast<float*>(ws + w.fscale);
+    int2* xrow = reinterpret_cast<int2*>(ws + w.xrow);
     float* zy = reinterpret_cast<float*>(ws + w.zy);
     double* row_term = reinterpret_cast<double*>(ws + w.row_term);
     float* row_rho = reinterpret_cast<float*>(ws + w.row_rho);
@@ -797,25 +690,22 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float* row_kl = reinterpret_cast<float*>(ws + w.row_kl);
     float* w_c = reinterpret_cast<float*>(ws + w.w_c);
     float* ref_c = reinterpret_cast<float*>(ws + w.ref_c);
+    int64_t* rows_eff = reinterpret_cast<int64_t*>(ws + w.rows_eff);
     int* sched = reinterpret_cast<int*>(ws + w.sched);
-    int64_t* fbnd = reinterpret_cast<int64_t*>(ws + w.fbnd);
     // vocab-parallel head (grad_W_mode 3): W_head is this rank's vocabulary shard, every rank
-    // holds the same rows; the forward runs unchunked (the row statistics are all-gathered
-    // between the forward GEMM and the merge)
+    // holds the same rows (the row statistics are all-gathered between the forward GEMM and the
+    // row statistics kernel)
     const bool vp = a->grad_W_mode == 3 && comm && w.vp_world > 0;
     const int vp_R = vp ? comm_world(comm) : 0;
     const int64_t vp_v0 = vp ? (int64_t)comm_rank(comm) * V : 0;
-    const int n_fc = vp ? 1 : fwd_chunks();
-    int* ctr_fwd = gemm_dynamic() ? sched + 0 : nullptr;
-    int* ctr_gw = gemm_dynamic() ? sched + 4 : nullptr;
-    int* ctr_gh = gemm_dynamic() ? sched + 8 : nullptr;
+    int* ctr_fwd = kDynamic ? sched + 0 : nullptr;
+    int* ctr_gw = kDynamic ? sched + 4 : nullptr;
+    int* ctr_gh = kDynamic ? sched + 8 : nullptr;
     AG_CUDA(cudaMemsetAsync(sched, 0, 32 * sizeof(int), stream));
-    // progress arrays: [0] grad_W, [1] grad_hidden, [2 + c] forward chunk c
+    // progress arrays: [0] grad_W, [1] grad_hidden, [2] forward
     int64_t* prog = reinterpret_cast<int64_t*>(ws + w.prog);
-    const int lead = throttle_lead(), lead_fwd = throttle_lead_fwd();
-    if (lead > 0 || lead_fwd > 0)
-        AG_CUDA(cudaMemsetAsync(prog, 0xff, (2 + MAX_FWD_CHUNKS) * PROG_UNITS * sizeof(int64_t),
-                                stream));
+    if (kThrottleLead > 0 || kThrottleLeadFwd > 0)
+        AG_CUDA(cudaMemsetAsync(prog, 0xff, 3 * PROG_UNITS * sizeof(int64_t), stream));
 
     // ---- compaction (standalone) or reuse of part 1's
     if (!idx_dev) {
@@ -836,125 +726,92 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         nglob_dev = a->n_mask_global;
     }
 
-    // ---- outputs that are defined everywhere (grad_hidden's zero rows: below, beside the
-    // forward when the merge stream exists -- only the grad_hidden GEMM reads it back)
-    if (n_fc <= 1 && T > 0) AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, stream));
+    // ---- outputs that are defined everywhere (grad_hidden's zero rows; only the grad_hidden
+    // GEMM writes it back)
+    if (T > 0) AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, stream));
     if (o->logp) AG_CUDA(cudaMemsetAsync(o->logp, 0, (size_t)T * sizeof(float), stream));
 
-    // ---- K4 gather
+    // ---- K4 gather (+ the row count clamped to the workspace's rows_cap -> rows_eff)
     {
         int grid = num_sms() * 4;
         ProfScope ps(KID_GATHER, stream);
-        k_gather<<<grid, 256, 0, stream>>>(rows_dev, T, d, V,
+        k_gather<<<grid, 256, 0, stream>>>(rows_dev, rows_cap, rows_eff, T, d, V,
                                            reinterpret_cast<const __nv_bfloat16*>(a->hidden),
                                            a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
                                            d_status, vp_v0, vp ? (int64_t)V * vp_R : V);
         k_row_weights<<<num_sms() * 2, 256, 0, stream>>>(
-            rows_dev, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
+            rows_eff, nglob_dev, idx_dev, a->tok_weight, a->ref_logp, a->loss_agg,
             fx ? fx->off : nullptr, fx ? fx->n_traj : 0, fx ? fx->n_g : nullptr,
             fx ? fx->group_id : nullptr, fx ? fx->grp_cnt : nullptr, fx ? fx->n_groups : 0,
-            fx ? fx->ngrp : nullptr, w_c, ref_c, n_fc, fwd_ratio(), fbnd);
+            fx ? fx->ngrp : nullptr, w_c, ref_c);
         count_launch(2);
         AG_CUDA(cudaGetLastError());
     }
+    rows_dev = rows_eff;
 
     // ---- tensor maps
-    CUtensorMap mH_K, mH_MN, mW_K, mW_MN, mG_K, mG_MN;
+    CUtensorMap mH_K, mH_MN, mW_K, mW_MN, mP_K, mP_MN;
     int rc;
     if ((rc = make_map(&mH_K, H, d, rows_cap, d, 64, 128))) return rc;
     if ((rc = make_map(&mH_MN, H, d, rows_cap, d, 64, 64))) return rc;
     // K-major B box = the B rows one CTA stages (128 in a CTA pair, 256 alone)
-    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, gemm_use_pair() ? 128 : 256))) return rc;
+    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, kPair ? 128 : 256))) return rc;
     if ((rc = make_map(&mW_MN, a->W_head, d, V, d, 64, 64))) return rc;
-    if ((rc = make_map(&mG_K, PG, V, rows_cap, V, 64, 128))) return rc;
-    if ((rc = make_map(&mG_MN, PG, V, rows_cap, V, 64, 64))) return rc;
+    if ((rc = make_map(&mP_K, P, V, rows_cap, V, 64, 128))) return rc;
+    if ((rc = make_map(&mP_MN, P, V, rows_cap, V, 64, 64))) return rc;
 
     const int64_t max_m_tiles = rows_cap / GEMM_BM;
-    // ---- K5 forward GEMM + softmax-statistics epilogue, K6 merge.  With n_fc > 1 row chunks
-    // the forward runs chunk by chunk on a high-priority stream and the (HBM-bound) merge of
-    // chunk c runs on a low-priority stream beside the (tensor-bound) forward of chunk c+1.
-    // vocab-parallel: z_y is written only by the rank whose shard holds y_t; the others keep 0
-    // for the sum all-reduce
+    // ---- K5 forward GEMM + softmax-statistics epilogue.  vocab-parallel: z_y is written only
+    // by the rank whose shard holds y_t; the others keep 0 for the sum all-reduce
     if (vp) AG_CUDA(cudaMemsetAsync(zy, 0, sizeof(float) * (size_t)rows_cap, stream));
-    ForkStreams* fs = n_fc > 1 ? &fork_streams() : nullptr;
-    cudaStream_t s_fwd = stream, s_mrg = stream;
-    if (fs) {
-        s_fwd = fs->hi;
-        s_mrg = fs->lo;
-        AG_CUDA(cudaEventRecord(fs->fork, stream));
-        AG_CUDA(cudaStreamWaitEvent(s_fwd, fs->fork, 0));
-        AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->fork, 0));
-        // 2 T d bytes of zeros on the low-priority stream, overlapped with the forward GEMM
-        if (T > 0) AG_CUDA(cudaMemsetAsync(o->grad_hidden, 0, (size_t)T * d * 2, s_mrg));
-    }
-    for (int c = 0; c < n_fc; ++c) {
+    {
         GemmArgs g{};
-        g.m_range = n_fc > 1 ? fbnd + c : nullptr;
         g.m_dev = rows_dev;
         g.N = V;
         g.K_static = d;
-        g.group_m = gemm_group_m();
-        g.pol_a = l2_policy(0, 2);  // H rows of the current row group: reused by every column
-        g.pol_b = l2_policy(1, 1);  // W: streamed, shared only by the concurrent row tiles
-        g.tile_counter = ctr_fwd ? ctr_fwd + 16 * (c > 0) + c : nullptr;
-        if (lead_fwd > 0) {
-            g.prog = prog + (2 + c) * PROG_UNITS;
-            g.prog_every = throttle_every();
-            g.prog_lead = lead_fwd;
+        g.group_m = AGENTRL_GROUP_M;
+        g.pol_a = AGENTRL_L2POL_FWD_A;  // H rows of the current row group: reused by every column
+        g.pol_b = AGENTRL_L2POL_FWD_B;  // W: streamed, shared only by the concurrent row tiles
+        g.tile_counter = ctr_fwd;
+        if (kThrottleLeadFwd > 0) {
+            g.prog = prog + 2 * PROG_UNITS;
+            g.prog_every = AGENTRL_THROTTLE_EVERY;
+            g.prog_lead = kThrottleLeadFwd;
             g.prog_waits = throttle_wait_ctr(0);
         }
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
-        g.P = reinterpret_cast<__nv_bfloat16*>(PG);
+        g.P = P;
         g.ldP = V;
         g.part = part;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
-        rc = gemm_fwd_ksub2()
-                 ? launch_gemm<EPI_FWD, false, false, 1, 2>(mH_K, mW_K, g, max_m_tiles * w.n_tiles, s_fwd)
-                 : launch_gemm<EPI_FWD, false, false, 1, 1>(mH_K, mW_K, g, max_m_tiles * w.n_tiles, s_fwd);
+        rc = launch_gemm<EPI_FWD, false, false, 1, kFwdKsub>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
+                                                             stream);
         if (rc) return rc;
-        if (fs) {
-            AG_CUDA(cudaEventRecord(fs->ev[c], s_fwd));
-            AG_CUDA(cudaStreamWaitEvent(s_mrg, fs->ev[c], 0));
-        }
-        float2* vpstat = vp ? reinterpret_cast<float2*>(ws + w.vpstat) : nullptr;
-        if (vp) {  // all-gather of (M_r, L'_r) per row and the owner's z_y (sum all-reduces)
-            AG_CUDA(cudaMemsetAsync(vpstat, 0, sizeof(float2) * (size_t)vp_R * rows_cap, stream));
-            k_vp_row_stats<<<num_sms() * 4, 256, 0, stream>>>(
-                rows_dev, w.n_tiles, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
-            count_launch();
-            AG_CUDA(cudaGetLastError());
-            if ((rc = comm_allreduce_f32(comm, reinterpret_cast<float*>(vpstat),
-                                         (size_t)2 * vp_R * rows_cap, stream)))
-                return rc;
-            if ((rc = comm_allreduce_f32(comm, zy, (size_t)rows_cap, stream))) return rc;
-        }
-        // merge + loss terms + G (in place) of this chunk; chunks merged beside the next
-        // forward chunk keep a small footprint (2 blocks per SM next to the GEMM CTA)
-        size_t smem = sizeof(float) * (size_t)w.n_tiles;
-        // one wave: every block resident, so the grid-stride row split has no second-wave tail
-        // (8 blocks per SM at 40 registers left a quarter of the blocks for a second wave)
-        static int merge_occ = 0;
-        if (merge_occ <= 0 &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&merge_occ, k_merge_g, MERGE_THREADS,
-                                                          sizeof(float) * 4096) != cudaSuccess)
-            merge_occ = 4;
-        static const int merge_bps = env_int("AGENTRL_MERGE_BPS", 0);  // A/B override
-        if (merge_bps > 0) merge_occ = merge_bps;
-        int grid = num_sms() * (c + 1 < n_fc ? 2 : std::max(1, merge_occ));
-        ProfScope ps(KID_MERGE, s_mrg);
-        k_merge_g<<<grid, MERGE_THREADS, smem, s_mrg>>>(
-            rows_dev, nglob_dev, V, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
-            a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
-            a->kl_beta, PG, row_term, row_rho, row_logp, row_clip, row_kl, o->logp,
-            n_fc > 1 ? fbnd + c : nullptr, vpstat, vp_R, rows_cap);
+    }
+    float2* vpstat = vp ? reinterpret_cast<float2*>(ws + w.vpstat) : nullptr;
+    if (vp) {  // all-gather of (M_r, L'_r) per row and the owner's z_y (sum all-reduces)
+        AG_CUDA(cudaMemsetAsync(vpstat, 0, sizeof(float2) * (size_t)vp_R * rows_cap, stream));
+        k_vp_row_stats<<<num_sms() * 4, 256, 0, stream>>>(
+            rows_dev, w.n_tiles, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
         count_launch();
         AG_CUDA(cudaGetLastError());
+        if ((rc = comm_allreduce_f32(comm, reinterpret_cast<float*>(vpstat),
+                                     (size_t)2 * vp_R * rows_cap, stream)))
+            return rc;
+        if ((rc = comm_allreduce_f32(comm, zy, (size_t)rows_cap, stream))) return rc;
     }
-    if (fs) {  // join: the last merge waited on the last forward chunk
-        AG_CUDA(cudaEventRecord(fs->join, s_mrg));
-        AG_CUDA(cudaStreamWaitEvent(stream, fs->join, 0));
+    // ---- K6 row statistics: loss terms, gradient scales and target columns
+    {
+        ProfScope ps(KID_MERGE, stream);
+        k_row_stats<<<num_sms() * 8, STATS_THREADS_ROW, 0, stream>>>(
+            rows_dev, nglob_dev, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
+            a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
+            a->kl_beta, fscale, xrow, row_term, row_rho, row_logp, row_clip, row_kl, o->logp,
+            vpstat, vp_R, rows_cap);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
     }
     // ---- K7 loss reduction (+ C2)
     {
@@ -967,6 +824,12 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     if (comm && !vp) {  // (vocab-parallel: every rank already holds the whole loss)
         if ((rc = comm_allreduce_f64(comm, o->loss, 1, stream))) return rc;
     }
+    auto xf_args = [&](GemmArgs& g) {
+        g.xf_scale = fscale;
+        g.xf_row = xrow;
+        g.xf_rows = rows_dev;
+        g.xf_ntiles = w.n_tiles;
+    };
     // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff); with a peer window (grad_W_mode 2)
     // the epilogue is also C3: each tile goes straight to its owner's window (peer.cu)
     PeerWindow* pw = (comm && a->grad_W_mode == 2) ? comm_peer(comm) : nullptr;
@@ -982,25 +845,22 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.M_static = V;
         g.N = d;
         g.k_dev = rows_dev;
-        g.group_m = gemm_group_m_bwd();
-        // G^T column blocks are shared by the d/512 pairs of one row block, which drift apart
-        // over the K = T_eff loop: evict_first made the laggards re-read G from HBM (DRAM
-        // 160 -> 131 GB at glm9b with evict_normal, profiles/r01_l2pol_dyn.txt)
-        g.pol_a = l2_policy(2, 0);
-        g.pol_b = l2_policy(3, 0);  // H: re-read by every wave
+        g.group_m = AGENTRL_GROUP_M_BWD;
+        g.pol_a = AGENTRL_L2POL_BWD;  // P~ column blocks, shared by the d/512 pairs of a row block
+        g.pol_b = AGENTRL_L2POL_BWD;  // H: re-read by every wave
         g.tile_counter = ctr_gw;
-        if (lead > 0) {
+        if (kThrottleLead > 0) {
             g.prog = prog;
-            g.prog_every = throttle_every();
-            g.prog_lead = lead;
+            g.prog_every = AGENTRL_THROTTLE_EVERY;
+            g.prog_lead = kThrottleLead;
             g.prog_waits = throttle_wait_ctr(1);
         }
         g.scale = a->logit_scale;
         g.gw = o->grad_W;
         g.ldo = d;
+        xf_args(g);
         const int64_t tiles = ceil_div(V, GEMM_BM) * ceil_div(d, GEMM_BN);
-        return gemm_wide_n() ? launch_gemm<EPI_GRADW, true, true, 2>(mG_MN, mH_MN, g, tiles, s)
-                             : launch_gemm<EPI_GRADW, true, true, 1>(mG_MN, mH_MN, g, tiles, s);
+        return launch_gemm<EPI_GRADW, true, true, kWideN ? 2 : 1, 1, true>(mP_MN, mH_MN, g, tiles, s);
     };
     // ---- K8 grad_hidden = s G W   (M = T_eff, N = d, K = V), scattered to idx rows
     auto launch_grad_hidden = [&](cudaStream_t s, int rsv) -> int {
@@ -1008,20 +868,21 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.m_dev = rows_dev;
         g.N = d;
         g.K_static = V;
-        g.group_m = gemm_group_m_bwd();
-        g.pol_a = l2_policy(4, 0);  // G rows: shared by the pairs of one row block (as above)
-        g.pol_b = l2_policy(5, 0);  // W: re-read by every wave
+        g.group_m = AGENTRL_GROUP_M_BWD;
+        g.pol_a = AGENTRL_L2POL_BWD;  // P~ rows: shared by the pairs of one row block
+        g.pol_b = AGENTRL_L2POL_BWD;  // W: re-read by every wave
         g.tile_counter = ctr_gh;
-        if (lead > 0) {
+        if (kThrottleLead > 0) {
             g.prog = prog + PROG_UNITS;
-            g.prog_every = throttle_every();
-            g.prog_lead = lead;
+            g.prog_every = AGENTRL_THROTTLE_EVERY;
+            g.prog_lead = kThrottleLead;
             g.prog_waits = throttle_wait_ctr(2);
         }
         g.scale = a->logit_scale;
         g.idx = idx_dev;
         g.gh = reinterpret_cast<__nv_bfloat16*>(o->grad_hidden);
         g.ldo = d;
+        xf_args(g);
         const int64_t tiles = max_m_tiles * ceil_div(d, GEMM_BN);
         int r;
         if (vp) {
@@ -1029,8 +890,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             // epilogue, row = compacted row), summed over the group, then scattered as bf16
             float* gh32 = reinterpret_cast<float*>(ws + w.vp_gh);
             g.gw = gh32;
-            r = gemm_wide_n() ? launch_gemm<EPI_GRADW, false, true, 2>(mG_K, mW_MN, g, tiles, s, 0)
-                              : launch_gemm<EPI_GRADW, false, true, 1>(mG_K, mW_MN, g, tiles, s, 0);
+            r = launch_gemm<EPI_GRADW, false, true, kWideN ? 2 : 1, 1, true>(mP_K, mW_MN, g, tiles, s, 0);
             if (r) return r;
             if ((r = comm_allreduce_f32(comm, gh32, (size_t)rows_cap * d, s))) return r;
             k_vp_scatter<<<num_sms() * 4, 256, 0, s>>>(rows_dev, d, idx_dev, gh32,
@@ -1039,28 +899,11 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             AG_CUDA(cudaGetLastError());
             return AGENTRL_OK;
         }
-        return gemm_wide_n() ? launch_gemm<EPI_GRADH, false, true, 2>(mG_K, mW_MN, g, tiles, s, rsv)
-                             : launch_gemm<EPI_GRADH, false, true, 1>(mG_K, mW_MN, g, tiles, s, rsv);
+        return launch_gemm<EPI_GRADH, false, true, kWideN ? 2 : 1, 1, true>(mP_K, mW_MN, g, tiles, s, rsv);
     };
-    SideStream* ss = nullptr;
-    if (!comm && bwd_overlap()) {
-        // one GPU: grad_hidden (fewer, longer tiles) on the high-priority stream takes every SM
-        // first; grad_W on the low-priority stream starts on the SMs grad_hidden's last wave
-        // leaves idle, so the two GEMMs' tails overlap
-        ForkStreams& f = fork_streams();
-        AG_CUDA(cudaEventRecord(f.fork, stream));
-        AG_CUDA(cudaStreamWaitEvent(f.hi, f.fork, 0));
-        AG_CUDA(cudaStreamWaitEvent(f.lo, f.fork, 0));
-        if ((rc = launch_grad_hidden(f.hi, 0))) return rc;
-        if ((rc = launch_grad_W(f.lo))) return rc;
-        AG_CUDA(cudaEventRecord(f.ev[0], f.hi));
-        AG_CUDA(cudaEventRecord(f.ev[1], f.lo));
-        AG_CUDA(cudaStreamWaitEvent(stream, f.ev[0], 0));
-        AG_CUDA(cudaStreamWaitEvent(stream, f.ev[1], 0));
-        return AGENTRL_OK;
-    }
     if ((rc = launch_grad_W(stream))) return rc;
-    // ---- C3 grad_W all-reduce on a side stream, overlapped with K8
+    // ---- C3 grad_W all-reduce / reduce-scatter on a side stream, overlapped with K8
+    SideStream* ss = nullptr;
     if (comm && (a->grad_W_mode == 1 || a->grad_W_mode == 2)) {
         ss = &side_stream();
         AG_CUDA(cudaEventRecord(ss->e0, stream));
@@ -1077,7 +920,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     // already moved its bytes inside the grad_W GEMM; its side-stream tail (a slot sum of a few
     // dozen blocks) needs no reserved SMs.
     const bool nccl_c3 = ss && !pw && comm_world(comm) > 1;
-    if ((rc = launch_grad_hidden(stream, nccl_c3 ? comm_reserve_sms() : 0))) return rc;
+    const int rsv = nccl_c3 ? std::min(AGENTRL_COMM_SMS, num_sms() / 2) : 0;
+    if ((rc = launch_grad_hidden(stream, rsv))) return rc;
     if (ss) AG_CUDA(cudaStreamWaitEvent(stream, ss->e1, 0));
     return AGENTRL_OK;
 }
@@ -1131,7 +975,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) Hs += __shfl_xor_sync(0xffffffffu, Hs, o);
         if (lane == 0) {
-            const float logp = (zy[p] - M) - l1;  // see k_merge_g
+            const float logp = (zy[p] - M) - l1;  // see k_row_stats
             const int64_t t = idx[p];
             logp_out[t] = logp;
             if (ent_out) ent_out[t] = l1 + Hs;
@@ -1140,12 +984,13 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-LogpWs plan_logp(int64_t T, int32_t d, int32_t V, size_t base) {
+LogpWs plan_logp(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base) {
     WsPlan p;
     p.off = base;
     LogpWs w;
-    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t rows_cap = loss_rows_cap(T, max_rows);
     const int64_t n_chunks = ceil_div(T, CHUNK_TOKENS);
+    w.rows_cap = rows_cap;
     w.n_tiles = (int32_t)ceil_div(V, GEMM_BN);
     w.idx = p.take(sizeof(int32_t) * (size_t)(T + 1));
     w.meta = p.take(sizeof(int64_t) * 4);
@@ -1163,7 +1008,7 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
                    const LogpWs& w, int32_t* d_status, cudaStream_t stream) {
     const int64_t T = a->T;
     const int32_t d = a->d, V = a->V;
-    const int64_t rows_cap = ceil_div(std::max<int64_t>(T, 1), GEMM_BM) * GEMM_BM;
+    const int64_t rows_cap = w.rows_cap;
     int64_t* meta = reinterpret_cast<int64_t*>(ws + w.meta);
     int32_t* idx = reinterpret_cast<int32_t*>(ws + w.idx);
     int32_t* chunk = reinterpret_cast<int32_t*>(ws + w.chunk);
@@ -1172,6 +1017,7 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
     float4* part4 = reinterpret_cast<float4*>(ws + w.part4);
     float* zy = reinterpret_cast<float*>(ws + w.zy);
     int* sched = reinterpret_cast<int*>(ws + w.sched);
+    int64_t* rows_eff = meta + 2;  // min(T_eff, rows_cap), written by k_gather
     AG_CUDA(cudaMemsetAsync(meta, 0, 4 * sizeof(int64_t), stream));
     AG_CUDA(cudaMemsetAsync(sched, 0, 16 * sizeof(int), stream));
     AG_CUDA(cudaMemsetAsync(logp, 0, (size_t)T * sizeof(float), stream));
@@ -1188,37 +1034,36 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
     {
         ProfScope ps(KID_GATHER, stream);
         k_gather<<<num_sms() * 4, 256, 0, stream>>>(
-            meta, T, d, V, reinterpret_cast<const __nv_bfloat16*>(a->hidden), a->target, nullptr,
-            idx, H, tgt_c, nullptr, d_status);
+            meta, rows_cap, rows_eff, T, d, V, reinterpret_cast<const __nv_bfloat16*>(a->hidden),
+            a->target, nullptr, idx, H, tgt_c, nullptr, d_status);
         count_launch();
         AG_CUDA(cudaGetLastError());
     }
     CUtensorMap mH_K, mW_K;
     int rc;
     if ((rc = make_map(&mH_K, H, d, rows_cap, d, 64, 128))) return rc;
-    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, gemm_use_pair() ? 128 : 256))) return rc;
+    if ((rc = make_map(&mW_K, a->W_head, d, V, d, 64, kPair ? 128 : 256))) return rc;
     {
         GemmArgs g{};
-        g.m_dev = meta;
+        g.m_dev = rows_eff;
         g.N = V;
         g.K_static = d;
-        g.group_m = gemm_group_m();
-        g.pol_a = l2_policy(0, 2);
-        g.pol_b = l2_policy(1, 1);
-        g.tile_counter = gemm_dynamic() ? sched : nullptr;
+        g.group_m = AGENTRL_GROUP_M;
+        g.pol_a = AGENTRL_L2POL_FWD_A;
+        g.pol_b = AGENTRL_L2POL_FWD_B;
+        g.tile_counter = kDynamic ? sched : nullptr;
         g.scale = a->logit_scale;
         g.tgt = tgt_c;
         g.part4 = part4;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
         const int64_t mt = (rows_cap / GEMM_BM) * w.n_tiles;
-        rc = gemm_fwd_ksub2() ? launch_gemm<EPI_LOGP, false, false, 1, 2>(mH_K, mW_K, g, mt, stream)
-                              : launch_gemm<EPI_LOGP, false, false, 1, 1>(mH_K, mW_K, g, mt, stream);
+        rc = launch_gemm<EPI_LOGP, false, false, 1, kFwdKsub>(mH_K, mW_K, g, mt, stream);
         if (rc) return rc;
     }
     {
         ProfScope ps(KID_LOGP_MERGE, stream);
-        k_logp_merge<<<num_sms() * 8, 256, 0, stream>>>(meta, w.n_tiles, part4, zy, idx, logp,
+        k_logp_merge<<<num_sms() * 8, 256, 0, stream>>>(rows_eff, w.n_tiles, part4, zy, idx, logp,
                                                         entropy, d_status);
         count_launch();
         AG_CUDA(cudaGetLastError());

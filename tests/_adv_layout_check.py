@@ -1,6 +1,6 @@
 """Subprocess body for tests/test_gpu_adv_layouts.py: part 1 (and the fused step's compaction,
-through the loss and gradients) on adversarial batch layouts, under whatever AGENTRL_ADV_*
-driver switches the parent set, against the oracle.  Layouts (seeded, synthetic):
+through the loss and gradients) on adversarial batch layouts, with the library AGENTRL_LIB
+names (the default build or an adv-norm driver variant), against the oracle.  Layouts (seeded, synthetic):
   short    trajectories of 0..5 tokens (empty ones included): > 32 trajectory starts per
            512-token chunk, many per lane
   long     few trajectories of ~40K tokens: every trajectory spans many chunks and blocks
@@ -154,7 +154,7 @@ def main():
             check_idx(kind, b, oracle.task_adv_norm(b))
         if kind in ("short", "shuffled"):
             check_step(kind, b)
-    print("adv layouts ok", {k: v for k, v in os.environ.items() if k.startswith("AGENTRL_")})
+    print("adv layouts ok", ag.LIB_PATH)
 
 
 if __name__ == "__main__":

@@ -1,5 +1,5 @@
-"""Subprocess body for tests/test_gpu_variants.py: one fused step on `ragged` and `tiny`
-under whatever AGENTRL_* variant environment the parent set, checked against the oracle.
+"""Subprocess body for tests/test_gpu_variants.py: one fused step on `ragged` and `tiny` with
+the library AGENTRL_LIB names (a build variant), checked against the oracle.
 Exit code 0 = parity holds.  (Argument plumbing + comparison only.)"""
 import os
 import sys
@@ -35,7 +35,7 @@ def main():
         e1 = max_abs_rel(step.grad_hidden.float().cpu().numpy(), ref["grad_hidden"])
         e2 = max_abs_rel(step.grad_W.cpu().numpy(), ref["grad_W"])
         assert e1 <= 2e-2 and e2 <= 2e-2, (name, e1, e2)
-    print("variant ok", {k: v for k, v in os.environ.items() if k.startswith("AGENTRL_")})
+    print("variant ok", ag.LIB_PATH)
 
 
 if __name__ == "__main__":

@@ -1,7 +1,7 @@
 """Subprocess body for tests/test_gpu_variants.py::test_schedule_variants_bitwise: one fused
-step on `ragged` and `parity7b` under the parent's AGENTRL_* environment; the outputs are
-saved to the .npz named by argv[1] for a bitwise comparison against the default schedule.
-(Argument plumbing only.)"""
+step on `ragged`, `parity7b` and `longk` with the library AGENTRL_LIB names (a build variant,
+or the default build); the outputs and the throttle's wait counts are saved to the .npz named by
+argv[1] for a bitwise comparison against the default build.  (Argument plumbing only.)"""
 import os
 import sys
 
@@ -19,7 +19,8 @@ from gpu_util import batch_dev, bf16_dev, t  # noqa: E402
 
 def main(path):
     out = {}
-    for name in ("ragged", "parity7b"):
+    w0 = ag.debug_throttle_waits()
+    for name in ("ragged", "parity7b", "longk"):
         cfg = synth.CONFIGS[name]
         b = synth.make_structure(cfg)
         hb, Wb, y = synth.make_head(cfg, mask=b["loss_mask"])
@@ -32,6 +33,7 @@ def main(path):
         out[name + "_adv"] = step.adv_tok.cpu().numpy()
         out[name + "_gh"] = step.grad_hidden.view(torch.int16).cpu().numpy()
         out[name + "_gw"] = step.grad_W.cpu().numpy()
+    out["throttle_waits"] = np.asarray(ag.debug_throttle_waits()) - np.asarray(w0)
     np.savez(path, **out)
 
 

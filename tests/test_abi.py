@@ -60,9 +60,14 @@ def test_host_calls_without_gpu(libpath):
     assert ag.status_string(ag.ERR_WORKSPACE).startswith("workspace")
     assert ag.status_string(ag.ST_NO_TOKENS).startswith("no loss-masked")
     ws = ag.agentrl_grpo_step_workspace_size(131072, 640, 80, 5, 4096, 151552)
-    # P~/G buffer dominates: rows_cap * V * 2 bytes
+    # the bf16 P~ buffer dominates: rows_cap * V * 2 bytes, rows_cap = T without a bound
     assert ws >= 131072 * 151552 * 2
     assert ws < 131072 * 151552 * 2 * 1.1
+    # sized by the caller's bound on the masked rows instead (glm9b: T_eff = 53,039 -> 16.1 GB)
+    ws_b = ag.agentrl_grpo_step_workspace_size(131072, 640, 80, 5, 4096, 151552, max_rows=53039)
+    rows_cap = (53039 + 127) // 128 * 128
+    assert rows_cap * 151552 * 2 <= ws_b < rows_cap * 151552 * 2 * 1.1
+    assert ag.agentrl_policy_loss_workspace_size(131072, 4096, 151552, max_rows=53039) < ws_b
     assert ag.agentrl_task_adv_norm_workspace_size(0, 0, 0, 1) > 0
 
 
@@ -134,3 +139,13 @@ def test_reduce_scatter_mode_contract(libpath):
     assert (m.agentrl_policy_loss_workspace_size_vp(1024, 64, 512, 4)
             >= m.agentrl_policy_loss_workspace_size(1024, 64, 512) + 8 * 4 * 1024 + 4 * 1024 * 64)
     comm.destroy()
+
+
+def test_product_library_reads_one_runtime_switch():
+    """Schedule and staging choices are compile-time constants (build.py VARIANTS); the only
+    environment switch the library reads is the documented AGENTRL_C3_P2P."""
+    hits = []
+    for f in sorted(os.listdir(os.path.join(PKG, "csrc"))):
+        src = open(os.path.join(PKG, "csrc", f)).read()
+        hits += re.findall(r'getenv\("([A-Z_0-9]+)"\)', src)
+    assert hits == ["AGENTRL_C3_P2P"], hits
