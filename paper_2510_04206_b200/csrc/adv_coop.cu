@@ -69,8 +69,8 @@ constexpr int REG_K = 16;       // groups up to this size are handled in registe
 // phase timestamps of the last cooperative launch (block 0, after each grid barrier), read by
 // agentrl_debug_adv_phase_ns(); 8 x %globaltimer ns
 __device__ unsigned long long g_adv_phase_ns[8];
-__device__ __forceinline__ void phase_mark(int i) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+__device__ __forceinline__ void phase_mark(int i, unsigned blk = 0) {
+    if (blockIdx.x == blk && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_adv_phase_ns[i] = t;
@@ -149,8 +149,10 @@ struct AdvParams {
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
     int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
     int32_t* blk_cnt;              // small driver: per-block trajectory counts at [g + block]
-    uint8_t* lanecnt;              // large driver: masked tokens of each lane (16 tokens) of
-                                   // each chunk, [n_chunks * 32]
+    uint16_t* lanebits;            // large driver: the 16-token mask bits of each lane of each
+                                   // chunk, [n_chunks * 32] (phase A writes them; phase C and
+                                   // the trajectory-bound prefix counts read them instead of
+                                   // the mask: 1 bit per token instead of 1 byte)
     double* blk_part;              // per-block per-task (N, S, Q) partials
     double *adv_hat, *grp_nsq, *stats;
     int64_t* meta;
@@ -183,11 +185,6 @@ __device__ __forceinline__ int32_t smem_find_in(const int64_t* s, int32_t lo, in
         else hi = mid;
     }
     return lo;
-}
-// mask byte i (compile-time after unrolling) of a 16-byte vector, as 0/1
-__device__ __forceinline__ int32_t mbit(const uint4& v, int i) {
-    const uint32_t w = i < 4 ? v.x : (i < 8 ? v.y : (i < 12 ? v.z : v.w));
-    return ((w >> (8 * (i & 3))) & 0xffu) != 0u;
 }
 __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
     const int lane = threadIdx.x & 31;
@@ -399,6 +396,19 @@ __device__ __forceinline__ LaneMask lane_mask(const uint4& mk) {
     return m;
 }
 
+// the LaneMask of 16 stored mask bits (phase C of the large driver)
+__device__ __forceinline__ LaneMask lane_mask_bits(uint32_t bits) {
+    LaneMask m;
+    m.bits = bits & 0xffffu;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t x = (bits >> (4 * q)) & 0xfu;
+        const uint32_t y = (x | (x << 7) | (x << 14) | (x << 21)) & 0x01010101u;
+        m.byte[q] = y * 0xFFu;
+    }
+    return m;
+}
+
 // phase A, staged window: per-trajectory masked counts of chunk c (window-relative start tc,
 // first trajectory kc).  With E the exclusive prefix of the lanes' popcounts, the count below
 // a boundary x is P(x) = E[x/16] + popc(bits[x/16] & low(x%16)); lane j handles the segment
@@ -486,7 +496,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     // chunk indices fit in 32 bits (T < 2^31): keep the per-chunk bookkeeping 32-bit
     const int32_t n_full = (int32_t)(p.T / WCHUNK);  // chunks with all 512 tokens < T
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
-    const bool res = resident && n_mine <= RING;  // warp-uniform
+    // large driver, phase C: the lane bits phase A stored replace the mask (no ring)
+    const bool from_bits = PH == 1 && !small;
+    const bool res = (resident && n_mine <= RING) || from_bits;  // warp-uniform
     if (ADV_LDGSTS && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
             const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
@@ -555,9 +567,12 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         // ---- this warp's chunks of the window
         for (int32_t c = (int32_t)w0 + warp; c < w1; c += NWARPS, ++kseq) {
             const int slot = kseq & (RING - 1);
-            uint4 mk;
+            uint4 mk = make_uint4(0u, 0u, 0u, 0u);
+            uint32_t sbits = 0u;
             if (ADV_LDGSTS && r.on && !res) lane_wait_oldest();  // this chunk's group
-            if (r.on && c < n_full) {
+            if (from_bits) {
+                sbits = p.lanebits[(int64_t)c * 32 + lane];
+            } else if (r.on && c < n_full) {
                 if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
                     r.par ^= 1u << slot;
@@ -570,8 +585,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             const int32_t tc = (int32_t)((int64_t)c * WCHUNK - w.base);  // window-relative
             const int32_t kc = (any_traj && w.staged) ? s_kc[c - (int32_t)w0] : 0;
             if (pop) {
-                const int32_t pc = any_traj ? __popc(lane_mask(mk).bits) : 0;
-                p.lanecnt[(int64_t)c * 32 + lane] = (uint8_t)pc;  // 32 contiguous bytes
+                const uint32_t lb = any_traj ? lane_mask(mk).bits : 0u;
+                const int32_t pc = __popc(lb);
+                p.lanebits[(int64_t)c * 32 + lane] = (uint16_t)lb;  // 64 B per chunk
                 const int32_t tot = __reduce_add_sync(0xffffffffu, pc);
                 if (lane == 0) p.chunk[c] = tot;
                 warp_total += tot;
@@ -581,7 +597,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 if (lane == 0) p.chunk[c] = tot;
                 warp_total += tot;
             } else {
-                const LaneMask lm = lane_mask(mk);
+                const LaneMask lm = from_bits ? lane_mask_bits(sbits) : lane_mask(mk);
                 const int32_t mine = any_traj ? __popc(lm.bits) : 0;
                 int32_t wtotal = 0, pos = 0;
                 if (p.compact) {  // positions of the lane's masked tokens in the chunk
@@ -618,7 +634,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                             end = p.off[g + 1];
                             at = adv_tilde(p, s_task, g);
                         }
-                        const bool on = mbit(mk, i);
+                        const bool on = (lm.bits >> i) & 1u;
                         outv[i] = on ? at : 0.f;
                         if (p.compact && on) {
                             s_cidx[pos] = (int32_t)t;
@@ -1051,23 +1067,26 @@ __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, W
 }
 
 // masked tokens before position t (large driver, after phase A): block prefix + the chunk's
-// local base + the lane counts below t's lane + the masked bytes below t in its lane
+// local base + the popcount of the chunk's lane bits below t
 __device__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64_t G, int64_t t) {
     if (t <= 0) return 0;
     if (t >= p.T) return s_pre[G];
     const int64_t c = t / WCHUNK;
-    const int r = (int)(t - c * WCHUNK), L = r >> 4, j = r & 15;
+    const int r = (int)(t - c * WCHUNK);  // bits below r of the chunk's 512-bit mask
     int32_t P = s_pre[part_owner(p.n_chunks, c, G)] + p.chunk_base[c];
-    const uint4* lc4 = reinterpret_cast<const uint4*>(p.lanecnt + c * 32);
-    const uint4 a = lc4[0], b = lc4[1];
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint4* b4 = reinterpret_cast<const uint4*>(p.lanebits + c * 32);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {  // bytes 4q .. 4q+3 = lanes; keep lanes < L
-        const int keep = min(max(L - 4 * q, 0), 4);
-        const uint32_t m = keep == 4 ? 0xffffffffu : ((1u << (8 * keep)) - 1u);
-        P += (int32_t)(((w[q] & m) * 0x01010101u) >> 24);  // byte sum (each byte <= 16)
+    for (int q = 0; q < 4; ++q) {  // 128 bits (8 lanes) per vector
+        const uint4 v = b4[q];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int b0 = (q * 4 + k) * 32;  // first token of this word
+            const int keep = min(max(r - b0, 0), 32);
+            const uint32_t m = keep == 32 ? 0xffffffffu : ((1u << keep) - 1u);
+            P += __popc(w[k] & m);
+        }
     }
-    if (j) P += __popc(lane_mask(mask_direct(p, c, L)).bits & ((1u << j) - 1u));
     return P;
 }
 
@@ -1406,22 +1425,29 @@ __global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_appl
     large_apply(p, smem, r, ss.s_pre, ss.s_w);
 }
 
+// phase stamps (agentrl_debug_adv_phase_ns), small driver: [0] start and [1] counts done in
+// streaming block 1, [2] block 0's group work done, [3] after the grid barrier, [4] moments
+// reduced, [5] apply done (block 1)
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    phase_mark(0);
+    phase_mark(0, 1);
     WarpRing r{};
     if (blockIdx.x == 0) {
         small_group_pre(p, smem, ss.s_w);  // stages the offsets itself
+        phase_mark(2, 0);
     } else {
         r = ring_setup(p, smem);
         small_count(p, smem, r, ss.s_w);
+        phase_mark(1, 1);
     }
     grid.sync();
-    phase_mark(1);
+    phase_mark(3, 1);
     small_stats(p, smem, gridDim.x, ss.s_w, true, false, blockIdx.x != 0 ? ss.s_pre : nullptr);
+    phase_mark(4, 1);
     if (blockIdx.x != 0) small_apply(p, smem, r, ss.s_pre, ss.s_w, true);
+    phase_mark(5, 1);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1506,7 +1532,7 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.chunk_base = reinterpret_cast<int32_t*>(ws + w.wchunk_base);
     p.blk_grp = reinterpret_cast<int32_t*>(ws + w.blk_grp);
     p.blk_cnt = reinterpret_cast<int32_t*>(ws + w.blk_cnt);
-    p.lanecnt = ws + w.lanecnt;
+    p.lanebits = reinterpret_cast<uint16_t*>(ws + w.lanebits);
     p.blk_part = reinterpret_cast<double*>(ws + w.blk_part);
     p.adv_hat = reinterpret_cast<double*>(ws + w.adv_hat);
     p.grp_nsq = reinterpret_cast<double*>(ws + w.grp_nsq);

@@ -423,7 +423,7 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.chunk_first = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.wchunk_base = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.blk_cnt = p.take(sizeof(int32_t) * ((size_t)n_traj + 2049));
-    w.lanecnt = p.take((size_t)n_chunks * 32 + 32);
+    w.lanebits = p.take(sizeof(uint16_t) * ((size_t)n_chunks * 32 + 32));
     w.blk_chunk = p.take(sizeof(int32_t) * 2048);
     w.blk_grp = p.take(sizeof(int32_t) * 2048);
     w.blk_part = p.take(sizeof(double) * 3 * 2048 * (size_t)std::max(n_tasks, 1));

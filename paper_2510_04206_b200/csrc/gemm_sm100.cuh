@@ -102,7 +102,8 @@ struct GemmArgs {
     __nv_bfloat16* P;    // [rows, ldP] exp(z - m), bf16: fp32's exponent range, so entries far
                          // below the tile max survive (p_y -> 1 rows)
     int64_t ldP;
-    float2* part;   // [rows, n_tiles] (m, l')             (EPI_FWD)
+    float2* part;   // [n_tiles][ldpart] (m, l'), tile-major  (EPI_FWD)
+    int64_t ldpart;
     float4* part4;  // [rows, n_tiles] (m, l', u, 0)       (EPI_LOGP)
     int32_t n_tiles;
     float* zy;  // [rows]
@@ -127,13 +128,13 @@ struct GemmArgs {
     int64_t* prog;
     int32_t prog_every, prog_lead;
     unsigned long long* prog_waits;  // optional: +1 per throttle wait episode (debug counter)
-    // XF: operand A is P~ (bf16 [rows, V]); G = bf16(xf_scale[row * xf_ntiles + tile] * P~),
-    // target column (xf_row[row].x, -1 = none) = __int_as_float(xf_row[row].y); rows at or past
-    // *xf_rows (the dynamic T_eff) are zero
+    // XF: operand A is P~ (bf16 [rows, V]); G = bf16(xf_scale[tile * xf_ld + row] * P~)
+    // (tile-major: consecutive rows are contiguous), target column (xf_row[row].x, -1 = none)
+    // = __int_as_float(xf_row[row].y); rows at or past *xf_rows (the dynamic T_eff) are zero
     const float* xf_scale;
     const int2* xf_row;
     const int64_t* xf_rows;
-    int32_t xf_ntiles;
+    int64_t xf_ld;
 };
 
 __device__ __forceinline__ void prog_store(int64_t* p, int64_t v) {
@@ -518,57 +519,68 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     vcol0 = m0 + 64 * (t >> 6);
                 }
                 const bool vcol_ok = !A_MN || vcol0 < M;
-                auto inputs = [&](int64_t kb, float& f, int& ycol, float& gy, bool& zero) {
+                // per k-block inputs: scale f, target column in the line (or -1), its G value,
+                // zero line.  grad_hidden: f changes once per 256-column tile (4 k-blocks),
+                // the target is the row's; grad_W: each k-block holds 64 new tokens.  Loads of
+                // k-block group g+1 (4 k-blocks, tile-major scales: coalesced) are issued before
+                // group g is transformed, so their latency hides behind 4 k-blocks of MMAs.
+                constexpr int XD = 4;
+                struct XIn {
+                    float f, gy;
+                    int ycol;
+                    bool zero;
+                };
+                auto inputs = [&](int64_t kb) -> XIn {
+                    XIn x{0.f, 0.f, -1, true};
+                    if (kb >= num_kb) return x;
                     const int64_t k0 = kb * GEMM_BK;
                     if constexpr (!A_MN) {
-                        zero = tok >= rows;
-                        f = zero ? 0.f : __ldg(p.xf_scale + tok * p.xf_ntiles + (k0 >> 8));
+                        x.zero = tok >= rows;
+                        if (!x.zero) x.f = __ldg(p.xf_scale + (k0 >> 8) * p.xf_ld + tok);
                         const int64_t yl = (int64_t)yr.x - k0;
-                        ycol = (yr.x >= 0 && yl >= 0 && yl < GEMM_BK) ? (int)yl : -1;
-                        gy = __int_as_float(yr.y);
+                        x.ycol = (yr.x >= 0 && yl >= 0 && yl < GEMM_BK) ? (int)yl : -1;
+                        x.gy = __int_as_float(yr.y);
                     } else {
                         const int64_t tk = k0 + (t & 63);
-                        zero = tk >= rows || !vcol_ok;
-                        int2 y2 = make_int2(-1, 0);
-                        f = 0.f;
-                        if (!zero) {
-                            f = __ldg(p.xf_scale + tk * p.xf_ntiles + (vcol0 >> 8));
-                            y2 = __ldg(p.xf_row + tk);
+                        x.zero = tk >= rows || !vcol_ok;
+                        if (!x.zero) {
+                            x.f = __ldg(p.xf_scale + (vcol0 >> 8) * p.xf_ld + tk);
+                            const int2 y2 = __ldg(p.xf_row + tk);
+                            const int64_t yl = (int64_t)y2.x - vcol0;
+                            x.ycol = (y2.x >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
+                            x.gy = __int_as_float(y2.y);
                         }
-                        const int64_t yl = (int64_t)y2.x - vcol0;
-                        ycol = (y2.x >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
-                        gy = __int_as_float(y2.y);
                     }
+                    return x;
                 };
-                float f, gy;
-                int ycol;
-                bool zero;
-                inputs(0, f, ycol, gy, zero);
-                for (int64_t kb = 0; kb < num_kb; ++kb) {
-                    // the next k-block's scale / target loads are issued before this one's
-                    // wait, so their latency hides behind the TMA and the transform
-                    float f2 = 0.f, gy2 = 0.f;
-                    int ycol2 = -1;
-                    bool zero2 = true;
-                    if (kb + 1 < num_kb) inputs(kb + 1, f2, ycol2, gy2, zero2);
-                    mbar_wait(&full[stage], phase);
-                    uint8_t* a = sA + stage * Cfg::A_STAGE;
-                    const int line = A_MN ? (t & 63) : t;
-                    xf_line(a + (A_MN ? (t >> 6) * 8192 : 0) + line * 128, line, f, ycol, gy, zero);
-                    fence_proxy_async_smem();  // generic smem writes -> visible to the MMA
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (PAIR) mbar_arrive_cluster(ready_leader + stage * 8);
-                        else mbar_arrive(&ready[stage]);
+                XIn cur[XD], nxt[XD];
+#pragma unroll
+                for (int u = 0; u < XD; ++u) cur[u] = inputs(u);
+                const int line = A_MN ? (t & 63) : t;
+                uint8_t* line_off = sA + (A_MN ? (t >> 6) * 8192 : 0) + line * 128;
+                for (int64_t kg = 0; kg < num_kb; kg += XD) {
+#pragma unroll
+                    for (int u = 0; u < XD; ++u) nxt[u] = inputs(kg + XD + u);
+#pragma unroll
+                    for (int u = 0; u < XD; ++u) {
+                        if (kg + u < num_kb) {
+                            mbar_wait(&full[stage], phase);
+                            xf_line(line_off + stage * Cfg::A_STAGE, line, cur[u].f, cur[u].ycol,
+                                    cur[u].gy, cur[u].zero);
+                            fence_proxy_async_smem();  // generic smem writes -> the MMA's proxy
+                            __syncwarp();
+                            if (lane == 0) {
+                                if constexpr (PAIR) mbar_arrive_cluster(ready_leader + stage * 8);
+                                else mbar_arrive(&ready[stage]);
+                            }
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
                     }
-                    f = f2;
-                    gy = gy2;
-                    ycol = ycol2;
-                    zero = zero2;
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+#pragma unroll
+                    for (int u = 0; u < XD; ++u) cur[u] = nxt[u];
                 }
             }
         }
@@ -670,7 +682,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         }
                     }
                     if (row_ok) {
-                        if constexpr (kStoreP) p.part[row * p.n_tiles + n_blk] = make_float2(m, l);
+                        // tile-major [n_tiles][ldpart]: the 32 lanes (rows) of a warp store 256
+                        // contiguous bytes
+                        if constexpr (kStoreP) p.part[n_blk * p.ldpart + row] = make_float2(m, l);
                         else p.part4[row * p.n_tiles + n_blk] = make_float4(m, l, u, 0.f);
                     }
                 } else if constexpr (EPI == EPI_GRADH) {

@@ -38,7 +38,7 @@ struct AdvWs {
     size_t blk_chunk, blk_grp, blk_part;  // per cooperative block: int32, int32, double[3*n_tasks]
     size_t wchunk_base;                   // int32 [n_chunks] local compaction base per chunk
     size_t blk_cnt;  // int32 [n_traj + 2049] per-block trajectory counts (small coop driver)
-    size_t lanecnt;  // uint8 [n_chunks * 32] per-lane masked counts (large coop driver)
+    size_t lanebits;  // uint16 [n_chunks * 32] per-lane mask bits (large coop driver)
     size_t stats;     // double [3*n_tasks]: N_i, S_i, Q_i (local, then global)
     size_t meta;      // int64 [4]: n_mask_local, n_mask_global, pad
     size_t idx;       // int32 [T] compacted token positions

@@ -310,19 +310,24 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K6 row stats
-// One block per row (grid-stride).  Same reductions, in the same order, as the former in-place
-// merge, so G = bf16(f * P~) (formed later inside the backward GEMMs) is bit-identical to the G
-// that merge wrote.
-constexpr int STATS_THREADS_ROW = 256;
+// A block owns RS_ROWS consecutive rows (lane = row, so every access to the tile-major part /
+// fscale arrays is 32 consecutive rows); warp w takes the 256-column tiles j = w, w + 8, ...
+// Per row, in a fixed order (deterministic): M = max_j m_j and the first tile jM holding it;
+// L' = sum_v exp(z_v - M) - 1 = l'_{jM} + sum_{j != jM} (1 + l'_j) exp(m_j - M) (warp partials
+// added in warp order); then the loss terms and the gradient scale of every tile,
+// f_j = c exp(m_j - lse) = c exp((m_j - M) - log1p(L')).
+constexpr int RS_ROWS = 32;
+constexpr int RS_WARPS = 8;
 
-__global__ void __launch_bounds__(STATS_THREADS_ROW)
+__global__ void __launch_bounds__(RS_ROWS * RS_WARPS)
     k_row_stats(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
-                int32_t n_tiles, const float2* __restrict__ part, const float* __restrict__ zy,
-                const int32_t* __restrict__ tgt_c, const float* __restrict__ old_c,
-                const float* __restrict__ adv_c, const int32_t* __restrict__ idx, float eps_lo,
-                float eps_hi, const float* __restrict__ w_c /* per-row weight w_t */,
+                int32_t n_tiles, int64_t ld, const float2* __restrict__ part /* [n_tiles][ld] */,
+                const float* __restrict__ zy, const int32_t* __restrict__ tgt_c,
+                const float* __restrict__ old_c, const float* __restrict__ adv_c,
+                const int32_t* __restrict__ idx, float eps_lo, float eps_hi,
+                const float* __restrict__ w_c /* per-row weight w_t */,
                 const float* __restrict__ ref_c /* per-row ref log-prob or null */,
-                float kl_beta, float* __restrict__ fscale /* [rows, n_tiles] */,
+                float kl_beta, float* __restrict__ fscale /* [n_tiles][ld] */,
                 int2* __restrict__ xrow /* [rows] (target column, G value bits) */,
                 double* __restrict__ row_term /* w (-term + beta KL) */,
                 float* __restrict__ row_rho, float* __restrict__ row_logp,
@@ -330,118 +335,123 @@ __global__ void __launch_bounds__(STATS_THREADS_ROW)
                 float* __restrict__ logp_out,
                 const float2* __restrict__ vpstat = nullptr /* [vp_R][vp_stride] (M_r, L'_r) */,
                 int32_t vp_R = 0, int64_t vp_stride = 0) {
-    constexpr int NT = STATS_THREADS_ROW;
-    __shared__ float s_red[NT / 32];
-    __shared__ int s_jm[NT / 32];
-    __shared__ float s_bc[4];
+    __shared__ float s_m[RS_WARPS][RS_ROWS];
+    __shared__ int s_j[RS_WARPS][RS_ROWS];
+    __shared__ float s_l[RS_WARPS][RS_ROWS];
+    __shared__ float s_c[RS_ROWS], s_sub[RS_ROWS];
     const int64_t rows = *rows_dev;
     const double Nd = (double)*nglob_dev;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const float LOG2E = 1.4426950408889634f;
 
-    for (int64_t p = blockIdx.x; p < rows; p += gridDim.x) {
-        const float2* pr = part + p * (int64_t)n_tiles;
-        // lse over tiles: M = max m_j, L = sum l_j exp(m_j - M)   (fixed order per thread +
-        // fixed tree -> deterministic)
-        float mloc = -INFINITY;
-        for (int j = threadIdx.x; j < n_tiles; j += NT) mloc = fmaxf(mloc, pr[j].x);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
-        if (lane == 0) s_red[wid] = mloc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float m = s_red[0];
-            for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, s_red[w]);
-            s_bc[0] = m;
-        }
-        __syncthreads();
-        const float M = s_bc[0];
-        // first tile holding the row max (its l' enters without the leading 1)
-        int jloc = 0x7fffffff;
-        for (int j = threadIdx.x; j < n_tiles; j += NT)
-            if (pr[j].x == M) jloc = min(jloc, j);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) jloc = min(jloc, __shfl_xor_sync(0xffffffffu, jloc, o));
-        __syncthreads();
-        if (lane == 0) s_jm[wid] = jloc;
-        __syncthreads();
-        int jM = s_jm[0];
-        for (int w = 1; w < NT / 32; ++w) jM = min(jM, s_jm[w]);
-        // L' = sum_v exp(z_v - M) - 1 = l'_{jM} + sum_{j != jM} (1 + l'_j) exp(m_j - M)
-        float lloc = 0.f;
-        for (int j = threadIdx.x; j < n_tiles; j += NT) {
-            const float2 ml = pr[j];
-            lloc += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) lloc += __shfl_xor_sync(0xffffffffu, lloc, o);
-        if (lane == 0) s_red[wid] = lloc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float Lm1 = 0.f;
-            for (int w = 0; w < NT / 32; ++w) Lm1 += s_red[w];
-            float Mrow = M;  // the row max over every column of the head
-            if (vpstat) {
-                // vocab-parallel head: combine the ranks' (M_r, L'_r) like tiles -- the first
-                // rank holding the row max enters with L'_r, the others with
-                // (1 + L'_r) exp(M_r - M); this rank's own M, L' are those of slot rank
-                float Mg = -INFINITY;
-                for (int r = 0; r < vp_R; ++r) Mg = fmaxf(Mg, vpstat[r * vp_stride + p].x);
-                int rM = 0;
-                while (rM < vp_R - 1 && vpstat[rM * vp_stride + p].x != Mg) ++rM;
-                float L = 0.f;
-                for (int r = 0; r < vp_R; ++r) {
-                    const float2 st = vpstat[r * vp_stride + p];
-                    L += r == rM ? st.y : (1.f + st.y) * ex2_approx((st.x - Mg) * LOG2E);
+    for (int64_t p0 = (int64_t)blockIdx.x * RS_ROWS; p0 < rows; p0 += (int64_t)gridDim.x * RS_ROWS) {
+        const int64_t p = p0 + lane;
+        const bool ok = p < rows;
+        // ---- row max and the first tile holding it (tiles in increasing order per warp)
+        float m = -INFINITY;
+        int jm = 0x7fffffff;
+        if (ok)
+#pragma unroll 4
+            for (int j = w; j < n_tiles; j += RS_WARPS) {
+                const float x = part[(int64_t)j * ld + p].x;
+                if (x > m) {
+                    m = x;
+                    jm = j;
                 }
-                Lm1 = L;
-                Mrow = Mg;
             }
-            // log p_y = (z_y - M) - log1p(L'), not z_y - lse: lse = M + log1p(L') rounds
-            // log1p(L') to the ulp of M (~2e-6 at |z| ~ 24), which is the whole of 1 - p_y when
-            // p_y -> 1 (the onehot-cancellation rows)
-            const float l1 = log1pf(Lm1);
-            const float logp = (zy[p] - Mrow) - l1;
-            const float A = adv_c[p];
-            const float rho = expf(logp - old_c[p]);
-            const float lo = 1.f - eps_lo, hi = 1.f + eps_hi;
-            const float rc = fminf(fmaxf(rho, lo), hi);
-            const double u = (double)rho * (double)A, cl = (double)rc * (double)A;
-            const double term = u < cl ? u : cl;
-            const bool clipped = (A > 0.f && rho > hi) || (A < 0.f && rho < lo);
-            // weight w_t (1/N token mean by default) and the k3 KL penalty (8(f) variants):
-            //   loss_t = w (-term + beta KL),  c_t = w ([unclipped] rho A - beta (1 - e^r))
-            const double w = w_c ? (double)w_c[p] : 1.0 / Nd;
-            double kl = 0.0, dkl = 0.0;
-            if (kl_beta > 0.f && ref_c) {
-                const double r = (double)ref_c[p] - (double)logp;
-                const double er = exp(r);
-                kl = er - r - 1.0;
-                dkl = 1.0 - er;
+        s_m[w][lane] = m;
+        s_j[w][lane] = jm;
+        __syncthreads();
+        float M = s_m[0][lane];
+        int jM = s_j[0][lane];
+#pragma unroll
+        for (int q = 1; q < RS_WARPS; ++q) {
+            const float x = s_m[q][lane];
+            const int jq = s_j[q][lane];
+            if (x > M || (x == M && jq < jM)) {
+                M = x;
+                jM = jq;
             }
-            const float c_t =
-                (float)(w * ((clipped ? 0.0 : (double)rho * (double)A) - (double)kl_beta * dkl));
-            row_term[p] = w * (-term + (double)kl_beta * kl);
-            row_rho[p] = rho;
-            row_logp[p] = logp;
-            row_clip[p] = clipped ? 1 : 0;
-            row_kl[p] = (float)kl;
-            if (logp_out) logp_out[idx[p]] = logp;
-            // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
-            xrow[p] = make_int2(tgt_c[p], __float_as_int(c_t * expm1f(logp)));
-            s_bc[0] = l1;
-            s_bc[1] = c_t;
-            s_bc[3] = Mrow;
+        }
+        // ---- L' partials
+        float L = 0.f;
+        if (ok)
+#pragma unroll 4
+            for (int j = w; j < n_tiles; j += RS_WARPS) {
+                const float2 ml = part[(int64_t)j * ld + p];
+                L += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
+            }
+        s_l[w][lane] = L;
+        __syncthreads();
+        if (w == 0) {
+            float Lm1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < RS_WARPS; ++q) Lm1 += s_l[q][lane];
+            float c_t = 0.f;
+            if (ok) {
+                float Mrow = M;  // the row max over every column of the head
+                if (vpstat) {
+                    // vocab-parallel head: combine the ranks' (M_r, L'_r) like tiles -- the first
+                    // rank holding the row max enters with L'_r, the others with
+                    // (1 + L'_r) exp(M_r - M); this rank's own M, L' are those of slot rank
+                    float Mg = -INFINITY;
+                    for (int r = 0; r < vp_R; ++r) Mg = fmaxf(Mg, vpstat[r * vp_stride + p].x);
+                    int rM = 0;
+                    while (rM < vp_R - 1 && vpstat[rM * vp_stride + p].x != Mg) ++rM;
+                    float Lg = 0.f;
+                    for (int r = 0; r < vp_R; ++r) {
+                        const float2 st = vpstat[r * vp_stride + p];
+                        Lg += r == rM ? st.y : (1.f + st.y) * ex2_approx((st.x - Mg) * LOG2E);
+                    }
+                    Lm1 = Lg;
+                    Mrow = Mg;
+                }
+                // log p_y = (z_y - M) - log1p(L'), not z_y - lse: lse = M + log1p(L') rounds
+                // log1p(L') to the ulp of M (~2e-6 at |z| ~ 24), which is the whole of 1 - p_y
+                // when p_y -> 1 (the onehot-cancellation rows)
+                const float l1 = log1pf(Lm1);
+                const float logp = (zy[p] - Mrow) - l1;
+                const float A = adv_c[p];
+                const float rho = expf(logp - old_c[p]);
+                const float lo = 1.f - eps_lo, hi = 1.f + eps_hi;
+                const float rc = fminf(fmaxf(rho, lo), hi);
+                const double u = (double)rho * (double)A, cl = (double)rc * (double)A;
+                const double term = u < cl ? u : cl;
+                const bool clipped = (A > 0.f && rho > hi) || (A < 0.f && rho < lo);
+                // weight w_t (1/N token mean by default) and the k3 KL penalty (8(f)):
+                //   loss_t = w (-term + beta KL),  c_t = w ([unclipped] rho A - beta (1 - e^r))
+                const double wt = w_c ? (double)w_c[p] : 1.0 / Nd;
+                double kl = 0.0, dkl = 0.0;
+                if (kl_beta > 0.f && ref_c) {
+                    const double r = (double)ref_c[p] - (double)logp;
+                    const double er = exp(r);
+                    kl = er - r - 1.0;
+                    dkl = 1.0 - er;
+                }
+                c_t = (float)(wt * ((clipped ? 0.0 : (double)rho * (double)A) -
+                                    (double)kl_beta * dkl));
+                row_term[p] = wt * (-term + (double)kl_beta * kl);
+                row_rho[p] = rho;
+                row_logp[p] = logp;
+                row_clip[p] = clipped ? 1 : 0;
+                row_kl[p] = (float)kl;
+                if (logp_out) logp_out[idx[p]] = logp;
+                // target column: c (p_y - 1) = c expm1(z_y - lse), exact where p_y -> 1
+                xrow[p] = make_int2(tgt_c[p], __float_as_int(c_t * expm1f(logp)));
+                s_sub[lane] = l1;  // f_j = c exp((m_j - M) - l1)
+                s_m[0][lane] = Mrow;
+            }
+            s_c[lane] = c_t;
         }
         __syncthreads();
-        const float l1 = s_bc[0];
-        const float c_t = s_bc[1];
-        const float Mrow = s_bc[3];
-        // G = bf16(f_j * P~) per 256-column tile j, f_j = c exp(m_j - lse) = c exp((m_j - M) -
-        // log1p(L')) (formed by the backward GEMMs' transform warps)
-        float* fr = fscale + p * (int64_t)n_tiles;
-        for (int j = threadIdx.x; j < n_tiles; j += NT)
-            fr[j] = c_t * ex2_approx(((pr[j].x - Mrow) - l1) * LOG2E);
+        // ---- gradient scale of every tile (the backward GEMMs form G = bf16(f * P~))
+        if (ok) {
+            const float c_t = s_c[lane], l1 = s_sub[lane], Mrow = s_m[0][lane];
+#pragma unroll 4
+            for (int j = w; j < n_tiles; j += RS_WARPS)
+                fscale[(int64_t)j * ld + p] =
+                    c_t * ex2_approx(((part[(int64_t)j * ld + p].x - Mrow) - l1) * LOG2E);
+        }
         __syncthreads();
     }
 }
@@ -565,27 +575,28 @@ LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
 // L'_r = sum exp(z - M_r) - 1 (the first max left out, as in the tile merge) -> its slot of the
 // all-gather buffer (the other slots are zero; a sum all-reduce then fills every slot).
 __global__ void __launch_bounds__(256)
-    k_vp_row_stats(const int64_t* __restrict__ rows_dev, int32_t n_tiles,
-                   const float2* __restrict__ part, float2* __restrict__ slot) {
+    k_vp_row_stats(const int64_t* __restrict__ rows_dev, int32_t n_tiles, int64_t ld,
+                   const float2* __restrict__ part /* [n_tiles][ld] */,
+                   float2* __restrict__ slot) {
     const int64_t rows = *rows_dev;
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const float LOG2E = 1.4426950408889634f;
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < rows;
          p += nw) {
-        const float2* pr = part + p * (int64_t)n_tiles;
+        const float2* pr = part + p;
         float M = -INFINITY;
-        for (int j = lane; j < n_tiles; j += 32) M = fmaxf(M, pr[j].x);
+        for (int j = lane; j < n_tiles; j += 32) M = fmaxf(M, pr[j * ld].x);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         int jm = 0x7fffffff;
         for (int j = lane; j < n_tiles; j += 32)
-            if (pr[j].x == M) jm = min(jm, j);
+            if (pr[j * ld].x == M) jm = min(jm, j);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) jm = min(jm, __shfl_xor_sync(0xffffffffu, jm, o));
         float L = 0.f;
         for (int j = lane; j < n_tiles; j += 32) {
-            const float2 ml = pr[j];
+            const float2 ml = pr[j * ld];
             L += j == jm ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
         }
 #pragma unroll
@@ -784,6 +795,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.P = P;
         g.ldP = V;
         g.part = part;
+        g.ldpart = rows_cap;
         g.n_tiles = w.n_tiles;
         g.zy = zy;
         rc = launch_gemm<EPI_FWD, false, false, 1, kFwdKsub>(mH_K, mW_K, g, max_m_tiles * w.n_tiles,
@@ -794,7 +806,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     if (vp) {  // all-gather of (M_r, L'_r) per row and the owner's z_y (sum all-reduces)
         AG_CUDA(cudaMemsetAsync(vpstat, 0, sizeof(float2) * (size_t)vp_R * rows_cap, stream));
         k_vp_row_stats<<<num_sms() * 4, 256, 0, stream>>>(
-            rows_dev, w.n_tiles, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
+            rows_dev, w.n_tiles, rows_cap, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
         count_launch();
         AG_CUDA(cudaGetLastError());
         if ((rc = comm_allreduce_f32(comm, reinterpret_cast<float*>(vpstat),
@@ -805,8 +817,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     // ---- K6 row statistics: loss terms, gradient scales and target columns
     {
         ProfScope ps(KID_MERGE, stream);
-        k_row_stats<<<num_sms() * 8, STATS_THREADS_ROW, 0, stream>>>(
-            rows_dev, nglob_dev, w.n_tiles, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
+        k_row_stats<<<(unsigned)std::max<int64_t>(ceil_div(rows_cap, RS_ROWS), 1),
+                      RS_ROWS * RS_WARPS, 0, stream>>>(
+            rows_dev, nglob_dev, w.n_tiles, rows_cap, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
             a->clip_eps_low, a->clip_eps_high, w_c, a->kl_beta > 0.f ? ref_c : nullptr,
             a->kl_beta, fscale, xrow, row_term, row_rho, row_logp, row_clip, row_kl, o->logp,
             vpstat, vp_R, rows_cap);
@@ -828,7 +841,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         g.xf_scale = fscale;
         g.xf_row = xrow;
         g.xf_rows = rows_dev;
-        g.xf_ntiles = w.n_tiles;
+        g.xf_ld = rows_cap;
     };
     // ---- K9 grad_W = s G^T H   (M = V, N = d, K = T_eff); with a peer window (grad_W_mode 2)
     // the epilogue is also C3: each tile goes straight to its owner's window (peer.cu)

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running (full-size shapes)")
+    config.addinivalue_line("markers", "gpu2: needs two CUDA devices (skips otherwise)")
 
 
 @pytest.fixture(scope="session")

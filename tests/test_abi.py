@@ -145,7 +145,7 @@ def test_product_library_reads_one_runtime_switch():
     """Schedule and staging choices are compile-time constants (build.py VARIANTS); the only
     environment switch the library reads is the documented AGENTRL_C3_P2P."""
     hits = []
-    for f in sorted(os.listdir(os.path.join(PKG, "csrc"))):
+    for f in sorted(x for x in os.listdir(os.path.join(PKG, "csrc")) if x.endswith((".cu", ".cuh", ".h"))):
         src = open(os.path.join(PKG, "csrc", f)).read()
         hits += re.findall(r'getenv\("([A-Z_0-9]+)"\)', src)
     assert hits == ["AGENTRL_C3_P2P"], hits

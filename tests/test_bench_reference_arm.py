@@ -29,6 +29,8 @@ def test_reference_line_contract():
     assert d["config"]["workload"] == "tiny"
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["one_thread"]["cores"] == 1 and 0 < cb["one_thread"]["value"]
+    assert d["ms_per_step_extrapolated"] is True and d["sample_wall_s_per_step"] > 0
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
 

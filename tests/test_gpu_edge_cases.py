@@ -6,7 +6,9 @@ outputs; host-checkable problems return error codes before any launch.
   - no loss-masked token at all                 -> ST_NO_TOKENS, loss 0, zero grads (R16)
   - an empty batch (T = 0)                      -> ST_NO_TOKENS, loss 0, zero grad_W
   - d % 64 != 0, clip eps outside [0, 1), a workspace one byte short -> SHAPE / INVALID_ARG /
-    WORKSPACE return codes."""
+    WORKSPACE return codes
+  - a workspace sized by max_rows: = T_eff gives the T-sized result bit for bit; below T_eff
+    -> ST_ROWS_OVERFLOW, only the first max_rows masked tokens are processed, no fault."""
 import numpy as np
 import pytest
 
@@ -40,7 +42,7 @@ def _inputs(T=512, d=64, V=512, seed=3):
 def _loss(ag, hb, Wb, y, old, adv, mask, ws_bytes=None, **kw):
     T, d = hb.shape
     V = Wb.shape[0]
-    need = ag.agentrl_policy_loss_workspace_size(T, d, V)
+    need = ag.agentrl_policy_loss_workspace_size(T, d, V, kw.get("max_rows", 0))
     ws = ag.alloc_workspace(need if ws_bytes is None else ws_bytes)
     loss = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda")
     gh = torch.full((max(T, 1), d), float("nan"), dtype=torch.bfloat16, device="cuda")
@@ -134,3 +136,38 @@ def test_host_checked_errors(ag):
     need = ag.agentrl_policy_loss_workspace_size(hb.shape[0], hb.shape[1], Wb.shape[0])
     rc = _loss(ag, hb, Wb, y, old, adv, mask, ws_bytes=need - 1)[0]
     assert rc == ag.ERR_WORKSPACE
+
+
+def test_max_rows_workspace(ag):
+    """max_rows = T_eff: the same bits as the T-sized workspace with a far smaller buffer;
+    max_rows < T_eff: ST_ROWS_OVERFLOW and the first max_rows rows only (defined outputs)."""
+    hb, Wb, y, old, adv, mask = _inputs(T=1500, d=128, V=1000, seed=8)
+    T, d = hb.shape
+    V = Wb.shape[0]
+    n = int(mask.sum())
+    assert ag.agentrl_policy_loss_workspace_size(T, d, V, n) < \
+        ag.agentrl_policy_loss_workspace_size(T, d, V) * 0.75
+    rc0, l0, gh0, gw0, st0 = _loss(ag, hb, Wb, y, old, adv, mask)
+    rc1, l1, gh1, gw1, st1 = _loss(ag, hb, Wb, y, old, adv, mask, max_rows=n)
+    assert rc0 == rc1 == 0 and st0 == st1 == 0
+    assert l0 == l1 and np.array_equal(gh0, gh1) and np.array_equal(gw0, gw1)
+    cut = n - 200  # the first `cut` masked tokens (token order) are processed
+    rc2, l2, gh2, gw2, st2 = _loss(ag, hb, Wb, y, old, adv, mask, max_rows=cut)
+    assert rc2 == 0 and st2 & ag.ST_ROWS_OVERFLOW
+    keep = np.zeros(T, np.uint8)
+    keep[np.nonzero(mask)[0][:cut]] = 1
+    # same as a batch whose mask holds only those tokens, with the full N in the mean
+    args_n = n
+    ws = ag.alloc_workspace(ag.agentrl_policy_loss_workspace_size(T, d, V))
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    gh = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    gw = torch.empty(V, d, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    a = ag.make_loss_args(T, bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32), t(old, torch.float32),
+                          t(keep, torch.uint8), adv_tok=t(adv, torch.float32),
+                          n_mask_global=torch.tensor([args_n], dtype=torch.int64, device="cuda"))
+    assert ag.agentrl_policy_loss_fwd_bwd(a, ag.make_loss_out(loss, gh, gw), ws, None, st) == 0
+    torch.cuda.synchronize()
+    assert abs(loss.item() - l2) <= 1e-12 * max(abs(l2), 1e-30)
+    assert np.array_equal(gh.float().cpu().numpy(), gh2)
+    assert np.array_equal(gw.cpu().numpy(), gw2)

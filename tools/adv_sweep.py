@@ -70,8 +70,10 @@ def time_adv(b, iters=20, graph=False):
     times.sort()
     ms = times[len(times) // 2]
     ph = ag.debug_adv_phase_ns()
-    phases = [round((ph[i + 1] - ph[i]) / 1e3, 1) if 0 <= ph[i + 1] - ph[i] < 1e9 else None
-              for i in range(7)]
+    # stamps relative to stamp 0 (small driver: [1] counts done, [2] block 0's group work,
+    # [3] after the grid barrier, [4] moments, [5] apply done; large driver: one per phase)
+    phases = [round((ph[i] - ph[0]) / 1e3, 1) if 0 <= ph[i] - ph[0] < 1e9 else None
+              for i in range(1, 8)]
     return ms, int(nm.item()), phases
 
 
