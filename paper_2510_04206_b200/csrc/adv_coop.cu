@@ -313,6 +313,18 @@ __device__ __forceinline__ void lane_issue(const AdvParams& p, WarpRing& r, int 
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// bits variant (phase C of the large driver): lanes 0..3 copy the chunk's 64 bytes of stored
+// lane bits (one commit group per chunk on every lane, as above)
+__device__ __forceinline__ void lane_issue_bits(const AdvParams& p, WarpRing& r, int slot,
+                                                int64_t c, bool valid) {
+    const int lane = threadIdx.x & 31;
+    if (valid && lane < 4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         smem_u32(r.buf + slot * WCHUNK + lane * 16)),
+                     "l"(reinterpret_cast<const uint8_t*>(p.lanebits) + c * 64 + lane * 16)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void lane_wait_oldest() {
     asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
 }
@@ -496,10 +508,16 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     // chunk indices fit in 32 bits (T < 2^31): keep the per-chunk bookkeeping 32-bit
     const int32_t n_full = (int32_t)(p.T / WCHUNK);  // chunks with all 512 tokens < T
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
-    // large driver, phase C: the lane bits phase A stored replace the mask (no ring)
-    const bool from_bits = PH == 1 && !small;
-    const bool res = (resident && n_mine <= RING) || from_bits;  // warp-uniform
-    if (ADV_LDGSTS && r.on && !res) {
+    // large driver, phase C: the lane bits phase A stored replace the mask (64 B per chunk
+    // through the same ring instead of 512 B)
+    const bool from_bits = ADV_LDGSTS && PH == 1 && !small;
+    const bool res = resident && n_mine <= RING && !from_bits;  // warp-uniform
+    if (from_bits) {
+        for (int s = 0; s < RING; ++s) {
+            const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
+            lane_issue_bits(p, r, s, c, c < c_hi);
+        }
+    } else if (ADV_LDGSTS && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
             const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
             lane_issue(p, r, s, c, c < c_hi && c < n_full);
@@ -569,9 +587,10 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             const int slot = kseq & (RING - 1);
             uint4 mk = make_uint4(0u, 0u, 0u, 0u);
             uint32_t sbits = 0u;
-            if (ADV_LDGSTS && r.on && !res) lane_wait_oldest();  // this chunk's group
+            if (from_bits || (ADV_LDGSTS && r.on && !res)) lane_wait_oldest();  // this chunk's group
             if (from_bits) {
-                sbits = p.lanebits[(int64_t)c * 32 + lane];
+                __syncwarp();  // lanes 0..3 copied the slot: their completed copies -> every lane
+                sbits = reinterpret_cast<const uint16_t*>(r.buf + slot * WCHUNK)[lane];
             } else if (r.on && c < n_full) {
                 if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
@@ -655,7 +674,10 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 }
             }
             __syncwarp();
-            if (ADV_LDGSTS && r.on && !res) {
+            if (from_bits) {
+                const int32_t c2 = c + RING * NWARPS;
+                lane_issue_bits(p, r, slot, c2, c2 < c_hi);
+            } else if (ADV_LDGSTS && r.on && !res) {
                 const int32_t c2 = c + RING * NWARPS;
                 lane_issue(p, r, slot, c2, c2 < c_hi && c2 < n_full);
             } else if (lane == 0 && r.on && !res) {

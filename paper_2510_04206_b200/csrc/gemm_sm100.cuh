@@ -241,35 +241,37 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
 }
 
 // XF: one 128-byte line of a SWIZZLE_128B tile (64 bf16 of one token and one vocabulary tile;
-// logical 16-byte chunk c sits at physical chunk c ^ (line & 7)) rewritten in place as
-// G = bf16(f * P~), element ycol (0..63, else none) = gy; zero: the whole line is 0
-__device__ __forceinline__ void xf_line(uint8_t* line, int l, float f, int ycol, float gy,
+// logical 16-byte chunk c sits at physical chunk c ^ (line & 7)), at shared address `line`,
+// rewritten in place as G = bf16(f * P~) (each product rounded once in fp32, then to bf16);
+// element ycol (0..63, else none) = gy; zero: the whole line is 0
+__device__ __forceinline__ void xf_line(uint32_t line, int l, float f, int ycol, float gy,
                                         bool zero) {
-    uint4* L = reinterpret_cast<uint4*>(line);
     const int sw = l & 7;
+    if (zero) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sts128(line + ((c ^ sw) << 4), make_uint4(0u, 0u, 0u, 0u));
+        return;
+    }
     uint4 v[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = L[c ^ sw];
+    for (int c = 0; c < 8; ++c) v[c] = lds128(line + ((c ^ sw) << 4));
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[c]);
-        float g[8];
+        const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+        uint32_t o[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const float2 x = __bfloat1622float2(h2[k]);
-            g[2 * k] = f * x.x;
-            g[2 * k + 1] = f * x.y;
+            // bf16 pair -> fp32 pair {lo, hi}: the bf16 bits are the fp32's high half
+            const uint64_t x = ((uint64_t)(w[k] & 0xffff0000u) << 32) | (uint64_t)(w[k] << 16);
+            const uint64_t g = fmul2(x, f);
+            o[k] = pack_bf162(__uint_as_float((uint32_t)g), __uint_as_float((uint32_t)(g >> 32)));
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (c * 8 + k == ycol) g[k] = gy;
-        uint4 o;
-        o.x = pack_bf162(g[0], g[1]);
-        o.y = pack_bf162(g[2], g[3]);
-        o.z = pack_bf162(g[4], g[5]);
-        o.w = pack_bf162(g[6], g[7]);
-        if (zero) o = make_uint4(0u, 0u, 0u, 0u);
-        L[c ^ sw] = o;
+        sts128(line + ((c ^ sw) << 4), make_uint4(o[0], o[1], o[2], o[3]));
+    }
+    if (ycol >= 0) {  // the target column: c (p_y - 1), stored over this thread's own product
+        const __nv_bfloat16 b = __float2bfloat16_rn(gy);
+        sts16(line + ((((ycol >> 3) ^ sw) << 4) | ((ycol & 7) << 1)),
+              *reinterpret_cast<const uint16_t*>(&b));
     }
 }
 
@@ -495,7 +497,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     tile = unit + it * n_units;
                 } else {
                     const int slot = (int)(it & (QD - 1));
-                    mbar_wait(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                    mbar_wait_sleep(&tq_full[slot], (uint32_t)(it / QD) & 1u);
                     tile = tile_q[slot];
                     __syncwarp();
                     if (lane == 0) {
@@ -530,6 +532,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     int ycol;
                     bool zero;
                 };
+                // loads only here (f, and for grad_W the row's (target, G value)); the
+                // target column is derived when the k-block is transformed, so nothing waits on
+                // these loads before the group that needs them
                 auto inputs = [&](int64_t kb) -> XIn {
                     XIn x{0.f, 0.f, -1, true};
                     if (kb >= num_kb) return x;
@@ -537,36 +542,41 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     if constexpr (!A_MN) {
                         x.zero = tok >= rows;
                         if (!x.zero) x.f = __ldg(p.xf_scale + (k0 >> 8) * p.xf_ld + tok);
-                        const int64_t yl = (int64_t)yr.x - k0;
-                        x.ycol = (yr.x >= 0 && yl >= 0 && yl < GEMM_BK) ? (int)yl : -1;
-                        x.gy = __int_as_float(yr.y);
                     } else {
                         const int64_t tk = k0 + (t & 63);
                         x.zero = tk >= rows || !vcol_ok;
                         if (!x.zero) {
                             x.f = __ldg(p.xf_scale + (vcol0 >> 8) * p.xf_ld + tk);
                             const int2 y2 = __ldg(p.xf_row + tk);
-                            const int64_t yl = (int64_t)y2.x - vcol0;
-                            x.ycol = (y2.x >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
+                            x.ycol = y2.x;  // the global target column (resolved at use)
                             x.gy = __int_as_float(y2.y);
                         }
                     }
                     return x;
                 };
+                // target column of k-block kb inside this thread's line, or -1
+                auto ycol_of = [&](const XIn& x, int64_t kb) -> int {
+                    int64_t yl;
+                    if constexpr (!A_MN) yl = (int64_t)yr.x - kb * GEMM_BK;
+                    else yl = (int64_t)x.ycol - vcol0;
+                    const int y = A_MN ? x.ycol : yr.x;
+                    return (y >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
+                };
                 XIn cur[XD], nxt[XD];
 #pragma unroll
                 for (int u = 0; u < XD; ++u) cur[u] = inputs(u);
                 const int line = A_MN ? (t & 63) : t;
-                uint8_t* line_off = sA + (A_MN ? (t >> 6) * 8192 : 0) + line * 128;
+                const uint32_t line_off = smem_u32(sA) + (A_MN ? (t >> 6) * 8192 : 0) + line * 128;
                 for (int64_t kg = 0; kg < num_kb; kg += XD) {
 #pragma unroll
                     for (int u = 0; u < XD; ++u) nxt[u] = inputs(kg + XD + u);
 #pragma unroll
                     for (int u = 0; u < XD; ++u) {
                         if (kg + u < num_kb) {
-                            mbar_wait(&full[stage], phase);
-                            xf_line(line_off + stage * Cfg::A_STAGE, line, cur[u].f, cur[u].ycol,
-                                    cur[u].gy, cur[u].zero);
+                            mbar_wait_sleep(&full[stage], phase);
+                            xf_line(line_off + stage * Cfg::A_STAGE, line, cur[u].f,
+                                    ycol_of(cur[u], kg + u), A_MN ? cur[u].gy : __int_as_float(yr.y),
+                                    cur[u].zero);
                             fence_proxy_async_smem();  // generic smem writes -> the MMA's proxy
                             __syncwarp();
                             if (lane == 0) {
@@ -601,7 +611,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 tile = unit + it * n_units;
             } else {
                 const int slot = (int)(it & (QD - 1));
-                mbar_wait(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                mbar_wait_sleep(&tq_full[slot], (uint32_t)(it / QD) & 1u);
                 tile = tile_q[slot];
                 __syncwarp();
                 if (lane == 0) {
@@ -614,7 +624,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
             const int64_t row = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
             const bool row_ok = row < M;
-            mbar_wait(&tfull[acc], acc_phase);
+            mbar_wait_sleep(&tfull[acc], acc_phase);
             tc_fence_after();
             uint32_t r[32];
 #pragma unroll 1

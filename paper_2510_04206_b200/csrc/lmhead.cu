@@ -260,11 +260,11 @@ __global__ void __launch_bounds__(CHUNK_THREADS)
 }
 
 // ---------------------------------------------------------------------------- K4 gather
-// rows_eff: the masked rows part 2 processes, min(T_eff, rows_cap) (the workspace holds
-// rows_cap rows; more masked tokens than that set AGENTRL_ST_ROWS_OVERFLOW and only the first
-// rows_cap are processed).  Written here by block 0 for every later kernel of the call.
+// rows_eff: the masked rows part 2 processes, min(T_eff, row_limit) (the caller's max_rows;
+// more masked tokens than that set AGENTRL_ST_ROWS_OVERFLOW and only the first row_limit are
+// processed).  Written here by block 0 for every later kernel of the call.
 __global__ void __launch_bounds__(256)
-    k_gather(const int64_t* __restrict__ rows_dev, int64_t rows_cap, int64_t* rows_eff, int64_t T,
+    k_gather(const int64_t* __restrict__ rows_dev, int64_t row_limit, int64_t* rows_eff, int64_t T,
              int32_t d, int32_t V, const __nv_bfloat16* __restrict__ hidden,
              const int32_t* __restrict__ target, const float* __restrict__ old_logp,
              const int32_t* __restrict__ idx, __nv_bfloat16* __restrict__ H,
@@ -274,10 +274,10 @@ __global__ void __launch_bounds__(256)
     // the shard gets tgt_c = -1 (never matches a column here)
     if (V_total < 0) V_total = V;
     const int64_t rows_all = *rows_dev;
-    const int64_t rows = rows_all < rows_cap ? rows_all : rows_cap;
+    const int64_t rows = rows_all < row_limit ? rows_all : row_limit;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *rows_eff = rows;
-        if (rows_all > rows_cap) atomicOr(d_status, AGENTRL_ST_ROWS_OVERFLOW);
+        if (rows_all > row_limit) atomicOr(d_status, AGENTRL_ST_ROWS_OVERFLOW);
     }
     const int64_t rows_pad = (rows + 63) / 64 * 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -746,7 +746,9 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     {
         int grid = num_sms() * 4;
         ProfScope ps(KID_GATHER, stream);
-        k_gather<<<grid, 256, 0, stream>>>(rows_dev, rows_cap, rows_eff, T, d, V,
+        // the caller's bound exactly (rows_cap is it rounded up to GEMM_BM)
+        const int64_t row_limit = (a->max_rows > 0 && a->max_rows < T) ? a->max_rows : T;
+        k_gather<<<grid, 256, 0, stream>>>(rows_dev, row_limit, rows_eff, T, d, V,
                                            reinterpret_cast<const __nv_bfloat16*>(a->hidden),
                                            a->target, a->old_logp, idx_dev, H, tgt_c, old_c,
                                            d_status, vp_v0, vp ? (int64_t)V * vp_R : V);
@@ -1046,8 +1048,9 @@ int launch_logprob(const agentrl_logprob_args* a, float* logp, float* entropy, u
     }
     {
         ProfScope ps(KID_GATHER, stream);
+        const int64_t row_limit = (a->max_rows > 0 && a->max_rows < T) ? a->max_rows : T;
         k_gather<<<num_sms() * 4, 256, 0, stream>>>(
-            meta, rows_cap, rows_eff, T, d, V, reinterpret_cast<const __nv_bfloat16*>(a->hidden),
+            meta, row_limit, rows_eff, T, d, V, reinterpret_cast<const __nv_bfloat16*>(a->hidden),
             a->target, nullptr, idx, H, tgt_c, nullptr, d_status);
         count_launch();
         AG_CUDA(cudaGetLastError());

@@ -48,6 +48,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(a, parity)) {
     }
 }
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit (NANOSLEEP.SYNCS)
+// until the phase completes instead of spinning, so waiting warps do not take issue slots
+// from the warps that share their scheduler (the MMA issuer, the transform warps)
+__device__ __forceinline__ uint32_t mbar_try_wait_sleep(uint32_t bar_addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar_addr), "r"(parity), "r"(0x989680)
+        : "memory");
+    return ok;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait_sleep(a, parity)) {
+    }
+}
 
 // ---------------------------------------------------------------- TMA
 // 1-D bulk copy global -> this CTA's shared memory (16 B aligned, bytes % 16 == 0); completes
@@ -251,7 +270,32 @@ __device__ __forceinline__ void st_async_remote_u32(uint32_t cluster_addr, uint3
         : "memory");
 }
 
+// ---------------------------------------------------------------- shared memory (explicit)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint16_t v) {
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+
 // ---------------------------------------------------------------- numerics
+// two fp32 products in one instruction (FMUL2): {lo, hi} * f, each rounded to nearest
+__device__ __forceinline__ uint64_t fmul2(uint64_t lohi, float f) {
+    uint64_t d;
+    const uint64_t ff = ((uint64_t)__float_as_uint(f) << 32) | __float_as_uint(f);
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(lohi), "l"(ff));
+    return d;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
