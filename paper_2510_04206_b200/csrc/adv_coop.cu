@@ -1055,6 +1055,164 @@ __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_
     __syncthreads();  // s_task visible to the staging
 }
 
+// Small driver, single launch, after the first grid barrier (every block, distributed):
+// block B takes trajectories [part_lo(n_traj, B), part_lo(n_traj, B+1)): n_g = the sum of the
+// per-block counts of the trajectory in block order (exact integers; published), and the
+// block's per-task partial (N, S, Q) = sum n_g (1, A^, A^^2) in a fixed order (thread strides,
+// shuffle tree, warp order) -> blk_part[B]; groups [part_lo(n_groups, B), ...) with members
+// -> blk_grp[B].  Also the exclusive prefix of the streaming blocks' masked totals (s_pre, the
+// compaction bases).  P:557-578 (Eq.1's token-set moments).
+__device__ void small_partials(const AdvParams& p, int64_t G, int32_t* s_w, int32_t* s_pre) {
+    const int64_t B = blockIdx.x;
+    const int64_t GS = G - 1;
+    const int64_t g_lo = part_lo(p.n_traj, B, G), g_hi = part_lo(p.n_traj, B + 1, G);
+    const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
+    for (int64_t b = threadIdx.x; b < G; b += COOP_THREADS) s_pre[b] = p.blk_chunk[b];
+    // at most one trajectory per thread in every BASELINE config (n_traj <= 2048, G >= 2)
+    __shared__ double s_wp[NWARPS][TASK_BATCH][3];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // per-thread: its trajectories in stride order, (task, n, A^) kept for the task loop below;
+    // a trajectory with an invalid group or task id is in no group (as in the member lists)
+    constexpr int MAXT = 2;  // trajectories per thread held in registers (else re-read)
+    int32_t tt[MAXT] = {-1, -1};
+    double nn[MAXT] = {0.0, 0.0}, aa[MAXT] = {0.0, 0.0};
+    int q = 0;
+    for (int64_t g = g_lo + threadIdx.x; g < g_hi; g += COOP_THREADS, ++q) {
+        const int64_t s0 = p.off[g], e = p.off[g + 1];
+        int32_t n = 0;
+        if (e > s0 && s0 >= 0 && GS > 0) {
+            const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
+            const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
+            for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+        }
+        p.n_g[g] = n;
+        const int32_t ti = p.task_id[g], j = p.group_id[g];
+        if (q < MAXT) {
+            tt[q] = (ti >= 0 && ti < p.n_tasks && j >= 0 && j < p.n_groups) ? ti : -1;
+            nn[q] = (double)n;
+            aa[q] = p.adv_hat[g];
+        }
+    }
+    const bool in_regs = (g_hi - g_lo) <= (int64_t)MAXT * COOP_THREADS;
+    __syncthreads();  // n_g of this block's trajectories published (re-read below if needed)
+    for (int32_t i0 = 0; i0 < p.n_tasks; i0 += TASK_BATCH) {
+        const int32_t nb = min(TASK_BATCH, p.n_tasks - i0);
+        for (int32_t ii = 0; ii < nb; ++ii) {
+            double N = 0.0, S = 0.0, Q = 0.0;
+            if (in_regs) {
+#pragma unroll
+                for (int k = 0; k < MAXT; ++k)
+                    if (tt[k] == i0 + ii) {
+                        N += nn[k];
+                        S += nn[k] * aa[k];
+                        Q += nn[k] * aa[k] * aa[k];
+                    }
+            } else {
+                for (int64_t g = g_lo + threadIdx.x; g < g_hi; g += COOP_THREADS)
+                    if (p.task_id[g] == i0 + ii && p.group_id[g] >= 0 &&
+                        p.group_id[g] < p.n_groups) {
+                        const double n = (double)p.n_g[g], ah = p.adv_hat[g];
+                        N += n;
+                        S += n * ah;
+                        Q += n * ah * ah;
+                    }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                N += __shfl_down_sync(0xffffffffu, N, o);
+                S += __shfl_down_sync(0xffffffffu, S, o);
+                Q += __shfl_down_sync(0xffffffffu, Q, o);
+            }
+            if (lane == 0) {
+                s_wp[wid][ii][0] = N;
+                s_wp[wid][ii][1] = S;
+                s_wp[wid][ii][2] = Q;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 3 * nb) {
+            const int ii = threadIdx.x / 3, k = threadIdx.x % 3;
+            double v = 0.0;
+            for (int w = 0; w < NWARPS; ++w) v += s_wp[w][ii][k];
+            p.blk_part[3 * (B * p.n_tasks + i0 + ii) + k] = v;
+        }
+        __syncthreads();
+    }
+    // groups with members (G of the GRPO group mean) and the compaction bases
+    int32_t ng = 0;
+    for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) ng += p.grp_cnt[j] > 0;
+    int32_t ngt = 0;
+    (void)coop_block_exscan(ng, s_w, ngt);
+    if (threadIdx.x == 0) p.blk_grp[B] = ngt;
+    const int32_t total = coop_block_scan_array(s_pre, G, s_w);
+    if (threadIdx.x == 0) s_pre[G] = total;
+    __syncthreads();
+}
+
+// after the second grid barrier (every block, identical order -> identical results): per-task
+// moments = the block partials summed in block order (warp w: tasks w, w+8, ...; lanes stride
+// the blocks, then a fixed shuffle tree), mu_i and max(sigma_i, eps) into s_task; block 0
+// publishes task_stats, N, G and the local masked-row count (s_pre[G]).
+__device__ void small_moments(const AdvParams& p, uint8_t* smem, int64_t G, const int32_t* s_pre) {
+    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
+    __shared__ double s_nsum[NWARPS];
+    __shared__ int32_t s_ngrp;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool blk0 = blockIdx.x == 0;
+    double nsum = 0.0;
+    for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
+        double N = 0.0, S = 0.0, Q = 0.0;
+        for (int64_t b = lane; b < G; b += 32) {
+            const double* bp = p.blk_part + 3 * (b * p.n_tasks + i);
+            N += bp[0];
+            S += bp[1];
+            Q += bp[2];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            N += __shfl_down_sync(0xffffffffu, N, o);
+            S += __shfl_down_sync(0xffffffffu, S, o);
+            Q += __shfl_down_sync(0xffffffffu, Q, o);
+        }
+        if (lane == 0) {
+            const double mu = N > 0.0 ? S / N : 0.0;
+            const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
+            s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
+            if (blk0 && p.task_stats_out) {
+                p.task_stats_out[3 * i] = N;
+                p.task_stats_out[3 * i + 1] = mu;
+                p.task_stats_out[3 * i + 2] = sd;
+            }
+            if (blk0) p.stats[3 * i] = N;
+            nsum += N;
+        }
+    }
+    if (blk0) {
+        if (lane == 0) s_nsum[wid] = nsum;
+        if (wid == 0) {
+            int32_t c = 0;
+            for (int64_t b = lane; b < G; b += 32) c += p.blk_grp[b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+            if (lane == 0) s_ngrp = c;
+        }
+    }
+    __syncthreads();
+    if (blk0 && threadIdx.x == 0) {
+        double n = 0.0;
+        // tasks were summed warp by warp: add the warp totals in task order (task i in warp
+        // i % NWARPS) -- any fixed order gives an exact integer here
+        for (int w = 0; w < NWARPS; ++w) n += s_nsum[w];
+        const int64_t nn = (int64_t)n;
+        p.meta[0] = s_pre[G];  // local masked rows
+        p.meta[1] = nn;        // global N
+        p.meta[2] = s_ngrp;    // global G (groups)
+        if (p.n_mask_global_out) *p.n_mask_global_out = nn;
+        if (nn == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void small_range(const AdvParams& p, int64_t& c_lo, int64_t& c_hi) {
     const int64_t GS = gridDim.x - 1, B = (int64_t)blockIdx.x - 1;
     c_lo = B < 0 ? 0 : part_lo(p.n_chunks, B, GS);
@@ -1448,8 +1606,8 @@ __global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_appl
 }
 
 // phase stamps (agentrl_debug_adv_phase_ns), small driver: [0] start and [1] counts done in
-// streaming block 1, [2] block 0's group work done, [3] after the grid barrier, [4] moments
-// reduced, [5] apply done (block 1)
+// streaming block 1, [2] block 0's group work done, [3] after the first grid barrier, [4] after
+// the second (partials done everywhere), [5] apply done (block 1)
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
@@ -1466,9 +1624,18 @@ __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvPara
     }
     grid.sync();
     phase_mark(3, 1);
-    small_stats(p, smem, gridDim.x, ss.s_w, true, false, blockIdx.x != 0 ? ss.s_pre : nullptr);
+    small_partials(p, gridDim.x, ss.s_w, ss.s_pre);  // n_g and per-block task partials
+    grid.sync();
     phase_mark(4, 1);
-    if (blockIdx.x != 0) small_apply(p, smem, r, ss.s_pre, ss.s_w, true);
+    small_moments(p, smem, gridDim.x, ss.s_pre);  // every block: mu_i, sigma_i
+    if (blockIdx.x != 0) {
+        int64_t c_lo, c_hi;
+        small_range(p, c_lo, c_hi);
+        const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+        int32_t dummy = 0;
+        // the mask is still in the ring from phase A; A^ and task ids come from global
+        stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, ss.s_pre[blockIdx.x], dummy, true);
+    }
     phase_mark(5, 1);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
