@@ -15,10 +15,10 @@
 //            512 B contiguous per warp instruction; optional stable compaction idx[] / adv_c[].
 //
 // Two drivers:
-//   small  (n_traj <= 2048, n_groups <= 1024; every BASELINE config): all offsets staged per
-//          block; A -> grid barrier -> block 0 does the group/task statistics in shared memory
-//          -> grid barrier -> C.  Per-block trajectory counts are written to disjoint slots
-//          (index g + block) and summed in block order: no zeroing pass, exact integers.
+//   small  (n_traj <= 2048, n_groups <= 512; every BASELINE config): every block streams and
+//          holds the whole trajectory table in smem; A + the A^ of its groups + its partial
+//          moments -> ONE grid barrier -> moments (identical in every block) -> C.  Per-block
+//          trajectory counts go to disjoint slots (index g + block): no zeroing pass.
 //   large  phase 0 (zero, chunk -> first-trajectory table) | A | B1 K_j scans | B2 member lists
 //          | B3 group advantages (members of groups of <= 16 sorted in registers) | B4 task
 //          moments | C.
@@ -80,7 +80,7 @@ __device__ __forceinline__ void phase_mark(int i, unsigned blk = 0) {
 // dynamic shared memory layout (byte offsets), identical on host and device
 struct Lay {
     uint32_t ring, bars, ostage, soff, srel, saux, skc, stask, cidx, cadv;
-    uint32_t sng, sgid, stid, srew, smem, sah, gcnt, gstart, gfill, gtask, gnsq;  // small: block 0
+    uint32_t sgid, stid, srew, sah, gflag, gtask, glist;  // small driver: trajectory table
     uint32_t total;
 };
 __host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
@@ -106,32 +106,18 @@ __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, i
     L.saux = lay_take(o, 4u * (uint32_t)(nst + 1));
     L.skc = lay_take(o, 4u * KC_CAP);
     L.stask = lay_take(o, 16u * (uint32_t)(n_tasks > 0 ? n_tasks : 1));
-    const uint32_t fixed_end = o;
-    // small driver: group arrays after the fixed arrays (every block reduces the moments
-    // itself while its mask stays resident in the ring)
-    uint32_t b = stream_begin;
+    // small driver: the whole trajectory table and per-group scratch (every block streams)
     const uint32_t nt = small ? (uint32_t)n_traj : 0u, ng = small ? (uint32_t)n_groups + 1 : 0u;
-    L.sng = lay_take(b, 4u * nt);
-    L.sgid = lay_take(b, 4u * nt);
-    L.stid = lay_take(b, 4u * nt);
-    L.srew = lay_take(b, 4u * nt);
-    L.smem = lay_take(b, 4u * nt);
-    L.sah = lay_take(b, 8u * nt);
-    L.gcnt = lay_take(b, 4u * ng);
-    L.gstart = lay_take(b, 4u * ng);
-    L.gfill = lay_take(b, 4u * ng);
-    L.gtask = lay_take(b, 4u * ng);
-    L.gnsq = lay_take(b, 24u * ng);
+    L.sgid = lay_take(o, 4u * nt);
+    L.stid = lay_take(o, 4u * nt);
+    L.srew = lay_take(o, 4u * nt);
+    L.sah = lay_take(o, 8u * nt);
+    L.gflag = lay_take(o, 4u * ng);
+    L.gtask = lay_take(o, 4u * ng);
+    L.glist = lay_take(o, 4u * ng);
+    (void)stream_begin;
     (void)stream_end;
-    if (!small) {
-        L.total = fixed_end;
-    } else {
-        const uint32_t shift = ((fixed_end + 127u) & ~127u) - stream_begin;
-        uint32_t* f[] = {&L.sng, &L.sgid, &L.stid, &L.srew, &L.smem, &L.sah,
-                         &L.gcnt, &L.gstart, &L.gfill, &L.gtask, &L.gnsq};
-        for (uint32_t* x : f) *x += shift;
-        L.total = b + shift;
-    }
+    L.total = o;
     return L;
 }
 
@@ -803,30 +789,34 @@ __device__ __forceinline__ void group_adv(const AdvParams& p, int32_t K, const i
 }
 
 // ------------------------------------------------------------------ small driver
-// Block 0 is the statistics block: while blocks 1..G-1 count tokens (phase A) it loads the
-// trajectory table, builds the group member lists and computes every A^_g (none of which
-// depends on the counts); after the grid barrier it only adds the per-block counts and
-// reduces the moments.  Blocks 1..G-1 own contiguous chunk ranges.
-struct SmallArrays {
-    const int64_t* off;
-    int32_t *ng, *gid, *tid, *mem, *gcnt, *gstart, *gfill, *gtask;
+// Every block streams a contiguous chunk range (warp w: chunks w, w+8, ...) and also owns a
+// contiguous slice of the trajectories and of the groups (part_lo).  One grid barrier:
+//   before it, each block
+//     - loads the whole trajectory table (offsets, group / task ids, rewards) into shared
+//       memory while its first mask copies are in flight;
+//     - counts its chunks (phase A): c_{g,B} = masked tokens of trajectory g in block B;
+//     - computes A^ of every group with a trajectory in its token range, and of the groups it
+//       owns (one warp per group: ballot scans of the staged ids in index order);
+//     - writes its per-task partial moments sum_g c_{g,B} (1, A^_g, A^_g^2).  Eq.1's moments
+//       are linear in the counts, so the partials of the blocks sharing a trajectory add up to
+//       n_g (1, A^_g, A^_g^2); N_i stays an exact integer;
+//   after it, every block sums the G partials in block order (the same code and order in
+//   every block, so every block holds identical mu_i, sigma_i) and applies Eq.1 to its chunks,
+//   which are still resident in its ring; then it publishes n_g of the trajectories it owns.
+struct SmallT {
+    int32_t *gid, *tid, *gflag, *gtask, *glist;
     float* rew;
-    double *ah, *gnsq;
+    double* ah;
 };
-__device__ __forceinline__ SmallArrays small_arrays(const AdvParams& p, uint8_t* smem) {
-    SmallArrays a;
-    a.off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-    a.ng = reinterpret_cast<int32_t*>(smem + p.lay.sng);
+__device__ __forceinline__ SmallT small_t(const AdvParams& p, uint8_t* smem) {
+    SmallT a;
     a.gid = reinterpret_cast<int32_t*>(smem + p.lay.sgid);
     a.tid = reinterpret_cast<int32_t*>(smem + p.lay.stid);
     a.rew = reinterpret_cast<float*>(smem + p.lay.srew);
-    a.mem = reinterpret_cast<int32_t*>(smem + p.lay.smem);
     a.ah = reinterpret_cast<double*>(smem + p.lay.sah);
-    a.gcnt = reinterpret_cast<int32_t*>(smem + p.lay.gcnt);
-    a.gstart = reinterpret_cast<int32_t*>(smem + p.lay.gstart);
-    a.gfill = reinterpret_cast<int32_t*>(smem + p.lay.gfill);
+    a.gflag = reinterpret_cast<int32_t*>(smem + p.lay.gflag);
     a.gtask = reinterpret_cast<int32_t*>(smem + p.lay.gtask);
-    a.gnsq = reinterpret_cast<double*>(smem + p.lay.gnsq);
+    a.glist = reinterpret_cast<int32_t*>(smem + p.lay.glist);
     return a;
 }
 
@@ -836,175 +826,218 @@ __device__ void stage_all_offsets(const AdvParams& p, uint8_t* smem) {
     __syncthreads();
 }
 
-// block 0 during phase A: validation, member lists, GRPO advantage (readings R1, R2,
-// R14) of every trajectory into smem and adv_hat
-__device__ void small_group_pre(const AdvParams& p, uint8_t* smem, int32_t* s_w) {
-    const SmallArrays a = small_arrays(p, smem);
-    int32_t st = 0;
-    if (threadIdx.x == 0) p.blk_chunk[0] = 0;  // the statistics block streams no tokens
-    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
-        a.gcnt[j] = 0;
-        a.gfill[j] = 0;
-    }
-    __syncthreads();
-    // the trajectory table and the offsets in one pass (independent loads in flight together)
-    int64_t* s_off = reinterpret_cast<int64_t*>(smem + p.lay.soff);
-    for (int32_t g = threadIdx.x; g <= p.n_traj; g += COOP_THREADS) {
-        s_off[g] = p.off[g];
-        if (g == p.n_traj) break;
-        const int32_t j = p.group_id[g], i = p.task_id[g];
-        a.rew[g] = p.rewards[g];
-        a.tid[g] = i;
-        a.ah[g] = 0.0;
-        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
-            st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-            a.gid[g] = -1;
-            p.adv_hat[g] = 0.0;
-        } else {
-            a.gid[g] = j;
-            atomicAdd(&a.gcnt[j], 1);
-        }
-    }
-    __syncthreads();
-    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS)
-        if (a.off[g + 1] < a.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
-    if (threadIdx.x == 0 && (a.off[0] != 0 || a.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
-    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) a.gstart[j] = a.gcnt[j];
-    __syncthreads();
-    coop_block_scan_array(a.gstart, p.n_groups, s_w);
-    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
-        const int32_t j = a.gid[g];
-        if (j >= 0) a.mem[a.gstart[j] + atomicAdd(&a.gfill[j], 1)] = g;
-    }
-    __syncthreads();
-    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
-        const int32_t K = a.gcnt[j];
-        int32_t* mb = a.mem + a.gstart[j];
-        for (int q = 1; q < K; ++q) {  // members in index order (deterministic sums)
-            const int32_t x = mb[q];
-            int b = q - 1;
-            while (b >= 0 && mb[b] > x) {
-                mb[b + 1] = mb[b];
-                --b;
-            }
-            mb[b + 1] = x;
-        }
-        int32_t task0 = -1;
-        if (K > 0) {
-            if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
-            task0 = a.tid[mb[0]];
-            double sum = 0.0, rmax = a.rew[mb[0]], rmin = rmax;
-            for (int q = 0; q < K; ++q) {
-                const double r = a.rew[mb[q]];
-                if (a.tid[mb[q]] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-                sum += r;
-                rmax = fmax(rmax, r);
-                rmin = fmin(rmin, r);
-            }
-            const bool flat = rmax == rmin;
-            const double mean = sum / (double)K;
-            double ss = 0.0;
-            if (!flat)
-                for (int q = 0; q < K; ++q) {
-                    const double dlt = (double)a.rew[mb[q]] - mean;
-                    ss += dlt * dlt;
-                }
-            const double sd = sqrt(ss / (double)K);
-            const double den = sd > p.eps_std ? sd : p.eps_std;
-            for (int q = 0; q < K; ++q) {
-                const int32_t g = mb[q];
-                const double ah = flat ? 0.0 : ((double)a.rew[g] - mean) / den;
-                a.ah[g] = ah;
-                p.adv_hat[g] = ah;
-            }
-        }
-        a.gtask[j] = task0;
-        p.grp_task[j] = task0;
-        p.grp_cnt[j] = K;
-        p.grp_start[j] = a.gstart[j];
-        for (int q = 0; q < K; ++q) p.members[a.gstart[j] + q] = mb[q];
-    }
-    if (st) atomicOr(p.d_status, st);
+__device__ __forceinline__ bool small_member(const AdvParams& p, int32_t j, int32_t i) {
+    return j >= 0 && j < p.n_groups && i >= 0 && i < p.n_tasks;
 }
 
-// After phase A, in every block (identical code and order, so identical results): n_g (the
-// per-block counts of each trajectory summed in block order: exact integers), per-group and
-// per-task (N, S, Q) in fixed orders, then mu_i, max(sigma_i, eps) into the
-// block's s_task.  Streaming blocks first load the group table block 0 published during
-// phase A.  publish (block 0): n_g, task_stats, N, G and the local masked-row count;
-// stats_only (second launch follows the all-reduce): block 0 writes the raw per-task sums.
-__device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_t* s_w,
-                            bool publish, bool stats_only, int32_t* s_pre = nullptr) {
-    const SmallArrays a = small_arrays(p, smem);
-    const bool blk0 = blockIdx.x == 0;
-    const int64_t GS = G - 1;  // streaming blocks 1..G-1
-    int32_t rows = 0;  // local masked rows = sum of the streaming blocks' totals
-    if (blk0 && publish)
-        for (int64_t b = 1 + threadIdx.x; b < G; b += COOP_THREADS) rows += p.blk_chunk[b];
-    // one pass, all loads independent: the group table and members / A^ / task ids block 0
-    // published (streaming blocks), the per-block counts of every trajectory (-> n_g), and the
-    // per-block masked totals for the compaction bases (s_pre, streaming blocks)
-    const int64_t nloop = max(max((int64_t)p.n_traj, (int64_t)p.n_groups), s_pre ? G : 0);
-    for (int64_t i = threadIdx.x; i < nloop; i += COOP_THREADS) {
-        if (!blk0 && i < p.n_groups) {
-            a.gcnt[i] = p.grp_cnt[i];
-            a.gstart[i] = p.grp_start[i];
-            a.gtask[i] = p.grp_task[i];
+// the whole trajectory table into smem (every load issued before the first store); the
+// trajectories this block owns are validated here (ids, offsets; A^ = 0 outside any group)
+__device__ void small_load_table(const AdvParams& p, uint8_t* smem, int32_t& st) {
+    const SmallT a = small_t(p, smem);
+    int64_t* s_off = reinterpret_cast<int64_t*>(smem + p.lay.soff);
+    const int64_t G = gridDim.x, B = blockIdx.x;
+    const int64_t t_lo = part_lo(p.n_traj, B, G), t_hi = part_lo(p.n_traj, B + 1, G);
+    for (int32_t g = threadIdx.x; g <= p.n_traj; g += COOP_THREADS) {
+        const int64_t o = p.off[g];
+        int32_t j = -1, i = -1;
+        float r = 0.f;
+        if (g < p.n_traj) {
+            j = p.group_id[g];
+            i = p.task_id[g];
+            r = p.rewards[g];
         }
-        if (s_pre && i < G) s_pre[i] = p.blk_chunk[i];
-        if (i < p.n_traj) {
-            const int32_t g = (int32_t)i;
-            if (!blk0) {
-                a.mem[g] = p.members[g];
-                a.ah[g] = p.adv_hat[g];
-                a.tid[g] = p.task_id[g];
+        s_off[g] = o;
+        if (g < p.n_traj) {
+            a.gid[g] = j;
+            a.tid[g] = i;
+            a.rew[g] = r;
+            a.ah[g] = 0.0;
+            if (g >= t_lo && g < t_hi && !small_member(p, j, i)) {
+                st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                p.adv_hat[g] = 0.0;
             }
-            const int64_t s0 = a.off[g], e = a.off[g + 1];
-            int32_t n = 0;
-            if (e > s0 && s0 >= 0 && GS > 0) {
-                const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
-                const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
-                for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
-            }
-            a.ng[g] = n;
-            if (blk0) p.n_g[g] = n;
         }
     }
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) a.gflag[j] = 0;
     __syncthreads();
-    if (s_pre) {  // exclusive prefix of the block totals (compaction base of every block)
-        const int32_t total = coop_block_scan_array(s_pre, G, s_w);
-        if (threadIdx.x == 0) s_pre[G] = total;
-        __syncthreads();
-    }
-    unsigned long long nz = 0;
-    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
-        const int32_t K = a.gcnt[j];
-        const int32_t* mb = a.mem + a.gstart[j];
-        double N = 0.0, S = 0.0, Q = 0.0;
-        for (int q = 0; q < K; ++q) {
-            const int32_t g = mb[q];
-            const double n = (double)a.ng[g], ah = a.ah[g];
-            N += n;
-            S += n * ah;
-            Q += n * ah * ah;
+    for (int64_t g = t_lo + threadIdx.x; g < t_hi; g += COOP_THREADS)
+        if (s_off[g + 1] < s_off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
+    if (B == 0 && threadIdx.x == 0 && (s_off[0] != 0 || s_off[p.n_traj] != p.T))
+        st |= AGENTRL_ST_BAD_OFFSETS;
+}
+
+// One warp, group j (readings R1 population std, R2 exact-equal rule and eps floor,
+// R14 K == 1): members = trajectories with group id j and valid task id, found by ballot scans
+// of the staged table in index order.  A^ of every member -> a.ah; the group's task (its
+// lowest-index member's) -> a.gtask.  own: also publishes K_j, the task and A^, and the status.
+// Every block that handles j runs the same code on the same smem copy: identical bits.
+__device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j, bool own,
+                                 int32_t* s_mb /* 32 ints of this warp */, int32_t& st,
+                                 int32_t& nz) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    int32_t K = 0, first = -1;
+    double sum = 0.0, rmax = -INFINITY, rmin = INFINITY;
+    for (int32_t i0 = 0; i0 < p.n_traj; i0 += 32) {
+        const int32_t i = i0 + lane;
+        bool hit = false;
+        float r = 0.f;
+        if (i < p.n_traj) {
+            hit = a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks;
+            r = a.rew[i];
         }
-        nz += K > 0;  // groups present in the batch (GRPO group mean)
-        a.gnsq[3 * j] = N;
-        a.gnsq[3 * j + 1] = S;
-        a.gnsq[3 * j + 2] = Q;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const int32_t rk = K + __popc(bal & lt);
+            if (rk < 32) s_mb[rk] = i;  // the first 32 members, in index order
+            sum += (double)r;
+            rmax = fmax(rmax, (double)r);
+            rmin = fmin(rmin, (double)r);
+        }
+        if (first < 0 && bal) first = i0 + __ffs(bal) - 1;
+        K += __popc(bal);
     }
-    int32_t nzt = 0, rows_t = 0;
-    (void)coop_block_exscan((int32_t)nz, s_w, nzt);  // also orders the gnsq writes
-    if (blk0 && publish) (void)coop_block_exscan(rows, s_w, rows_t);
-    __shared__ double s_st[64 * 3];  // per-task (N, S, Q) (n_tasks <= 64 on this driver)
+    // butterflies: a + b == b + a, so every lane ends with the same bits
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+    }
+    __syncwarp();
+    if (K == 0) {
+        if (lane == 0) {
+            a.gtask[j] = -1;
+            if (own) {
+                p.grp_cnt[j] = 0;
+                p.grp_task[j] = -1;
+            }
+        }
+        return;
+    }
+    const int32_t task0 = a.tid[first];
+    const bool flat = rmax == rmin;
+    const double mean = sum / (double)K;
+    const bool few = K <= 32;  // members in registers (lane L = member L)
+    const int32_t m = (few && lane < K) ? s_mb[lane] : -1;
+    double ss = 0.0;
+    bool spans = false;
+    if (few) {
+        if (m >= 0) {
+            spans = a.tid[m] != task0;
+            const double dl = (double)a.rew[m] - mean;
+            ss = flat ? 0.0 : dl * dl;
+        }
+    } else {
+        for (int32_t i = lane; i < p.n_traj; i += 32)
+            if (a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks) {
+                spans |= a.tid[i] != task0;
+                const double dl = (double)a.rew[i] - mean;
+                ss += flat ? 0.0 : dl * dl;
+            }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    spans = __any_sync(0xffffffffu, spans);
+    const double sd = sqrt(ss / (double)K);
+    const double den = sd > p.eps_std ? sd : p.eps_std;
+    auto put = [&](int32_t i) {
+        const double ah = flat ? 0.0 : ((double)a.rew[i] - mean) / den;
+        a.ah[i] = ah;
+        if (own) p.adv_hat[i] = ah;
+    };
+    if (few) {
+        if (m >= 0) put(m);
+    } else {
+        for (int32_t i = lane; i < p.n_traj; i += 32)
+            if (a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks) put(i);
+    }
+    if (lane == 0) {
+        a.gtask[j] = task0;
+        if (own) {
+            p.grp_cnt[j] = K;
+            p.grp_task[j] = task0;
+            if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+            if (spans) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+            nz += 1;  // a group present in the batch (GRPO group mean)
+        }
+    }
+}
+
+__device__ __forceinline__ void small_range(const AdvParams& p, int64_t& c_lo, int64_t& c_hi) {
+    c_lo = part_lo(p.n_chunks, blockIdx.x, gridDim.x);
+    c_hi = part_lo(p.n_chunks, (int64_t)blockIdx.x + 1, gridDim.x);
+}
+
+// the trajectories overlapping the block's token range [f, l] (stream_phase's staging rule);
+// false: the block has no chunks
+__device__ __forceinline__ bool small_traj_range(const AdvParams& p, const int64_t* s_off,
+                                                 int64_t c_lo, int64_t c_hi, int32_t& f,
+                                                 int32_t& l) {
+    if (c_lo >= c_hi || p.n_traj <= 0) return false;
+    f = smem_find_in(s_off, 0, p.n_traj, c_lo * WCHUNK);
+    l = smem_find_in(s_off, 0, p.n_traj, min(c_hi * WCHUNK, p.T) - 1);
+    f = min(max(f, 0), p.n_traj - 1);
+    l = min(max(l, f), p.n_traj - 1);
+    return true;
+}
+
+// phase A + group advantages + the block's partial moments (everything before the barrier)
+__device__ void small_pre_barrier(const AdvParams& p, uint8_t* smem, WarpRing& r, int32_t* s_w) {
+    const SmallT a = small_t(p, smem);
+    const int64_t G = gridDim.x, B = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    int32_t st = 0;
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    int32_t warp_total = 0;
+    // the trajectory table is staged while the block's first mask copies are in flight
+    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false,
+                    [&]() { small_load_table(p, smem, st); });
+    phase_mark(1);
+    chunk_bases(p, c_lo, c_hi, s_w);  // per-chunk compaction bases, blk_chunk[B]
+    // ---- the groups this block needs: those of its trajectories (bit 0), those it owns (bit 1)
+    int32_t f = 0, l = -1;
+    const bool any = small_traj_range(p, s_off, c_lo, c_hi, f, l);
+    const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
+    if (any)
+        for (int32_t g = f + threadIdx.x; g <= l; g += COOP_THREADS)
+            if (small_member(p, a.gid[g], a.tid[g])) atomicOr(&a.gflag[a.gid[g]], 1);
+    for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) atomicOr(&a.gflag[j], 2);
+    __shared__ int32_t s_nl, s_nz;
+    if (threadIdx.x == 0) s_nl = s_nz = 0;
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS)
+        if (a.gflag[j]) a.glist[atomicAdd(&s_nl, 1)] = j;
+    __syncthreads();
+    __shared__ int32_t s_mb[NWARPS][32];
+    int32_t nz = 0;
+    for (int32_t q = wid; q < s_nl; q += NWARPS) {
+        const int32_t j = a.glist[q];
+        small_group_warp(p, a, j, (a.gflag[j] & 2) != 0, s_mb[wid], st, nz);
+    }
+    if (lane == 0 && nz) atomicAdd(&s_nz, nz);
+    __syncthreads();  // A^ of the block's trajectories and the groups' tasks in smem
+    phase_mark(2);
+    // ---- per-task partial (N, S, Q) = sum over the block's trajectories of c_{g,B} (1, A^,
+    // A^^2), attributed to the group's task; fixed order (lanes stride the trajectories,
+    // shuffle tree).  Counts: the window's s_aux (one staged window) or the block's slots.
+    const int32_t* s_aux = reinterpret_cast<const int32_t*>(smem + p.lay.saux);
+    const bool one_window = c_hi - c_lo <= KC_CAP;
     for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
         double N = 0.0, S = 0.0, Q = 0.0;
-        for (int32_t j = lane; j < p.n_groups; j += 32)
-            if (a.gtask[j] == i) {
-                N += a.gnsq[3 * j];
-                S += a.gnsq[3 * j + 1];
-                Q += a.gnsq[3 * j + 2];
+        if (any)
+            for (int32_t g = f + lane; g <= l; g += 32) {
+                const int32_t j = a.gid[g];
+                if (!small_member(p, j, a.tid[g]) || a.gtask[j] != i) continue;
+                // (an empty trajectory between two windows has no slot: count 0)
+                const int32_t c = one_window ? s_aux[g - f]
+                                  : s_off[g + 1] > s_off[g] ? p.blk_cnt[g + B] : 0;
+                const double n = (double)c, ah = a.ah[g];
+                N += n;
+                S += n * ah;
+                Q += n * ah * ah;
             }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1013,152 +1046,30 @@ __device__ void small_stats(const AdvParams& p, uint8_t* smem, int64_t G, int32_
             Q += __shfl_down_sync(0xffffffffu, Q, o);
         }
         if (lane == 0) {
-            s_st[3 * i] = N;
-            s_st[3 * i + 1] = S;
-            s_st[3 * i + 2] = Q;
-            if (blk0 && stats_only) {
-                p.stats[3 * i] = N;
-                p.stats[3 * i + 1] = S;
-                p.stats[3 * i + 2] = Q;
-            }
+            double* bp = p.blk_part + 3 * (B * p.n_tasks + i);
+            bp[0] = N;
+            bp[1] = S;
+            bp[2] = Q;
         }
     }
-    if (blk0 && stats_only && threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)nzt;  // G
-    if (stats_only) return;
-    __syncthreads();
-    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
-    for (int32_t i = threadIdx.x; i < p.n_tasks; i += COOP_THREADS) {
-        const double N = s_st[3 * i], S = s_st[3 * i + 1], Q = s_st[3 * i + 2];
-        const double mu = N > 0.0 ? S / N : 0.0;
-        const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
-        s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
-        if (blk0 && publish && p.task_stats_out) {
-            p.task_stats_out[3 * i] = N;
-            p.task_stats_out[3 * i + 1] = mu;
-            p.task_stats_out[3 * i + 2] = sd;
-        }
-    }
-    if (blk0 && publish && threadIdx.x < 32) {
-        double nsum = 0.0;
-        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += s_st[3 * i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
-        if (threadIdx.x == 0) {
-            const int64_t n = (int64_t)nsum;
-            p.meta[0] = rows_t;  // local masked rows
-            p.meta[1] = n;       // global N
-            p.meta[2] = nzt;     // global G (groups)
-            if (p.n_mask_global_out) *p.n_mask_global_out = n;
-            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
-        }
-    }
-    __syncthreads();  // s_task visible to the staging
+    if (threadIdx.x == 0) p.blk_grp[B] = s_nz;
+    if (st) atomicOr(p.d_status, st);
 }
 
-// Small driver, single launch, after the first grid barrier (every block, distributed):
-// block B takes trajectories [part_lo(n_traj, B), part_lo(n_traj, B+1)): n_g = the sum of the
-// per-block counts of the trajectory in block order (exact integers; published), and the
-// block's per-task partial (N, S, Q) = sum n_g (1, A^, A^^2) in a fixed order (thread strides,
-// shuffle tree, warp order) -> blk_part[B]; groups [part_lo(n_groups, B), ...) with members
-// -> blk_grp[B].  Also the exclusive prefix of the streaming blocks' masked totals (s_pre, the
-// compaction bases).  P:557-578 (Eq.1's token-set moments).
-__device__ void small_partials(const AdvParams& p, int64_t G, int32_t* s_w, int32_t* s_pre) {
-    const int64_t B = blockIdx.x;
-    const int64_t GS = G - 1;
-    const int64_t g_lo = part_lo(p.n_traj, B, G), g_hi = part_lo(p.n_traj, B + 1, G);
-    const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
-    for (int64_t b = threadIdx.x; b < G; b += COOP_THREADS) s_pre[b] = p.blk_chunk[b];
-    // at most one trajectory per thread in every BASELINE config (n_traj <= 2048, G >= 2)
-    __shared__ double s_wp[NWARPS][TASK_BATCH][3];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // per-thread: its trajectories in stride order, (task, n, A^) kept for the task loop below;
-    // a trajectory with an invalid group or task id is in no group (as in the member lists)
-    constexpr int MAXT = 2;  // trajectories per thread held in registers (else re-read)
-    int32_t tt[MAXT] = {-1, -1};
-    double nn[MAXT] = {0.0, 0.0}, aa[MAXT] = {0.0, 0.0};
-    int q = 0;
-    for (int64_t g = g_lo + threadIdx.x; g < g_hi; g += COOP_THREADS, ++q) {
-        const int64_t s0 = p.off[g], e = p.off[g + 1];
-        int32_t n = 0;
-        if (e > s0 && s0 >= 0 && GS > 0) {
-            const int64_t b0 = 1 + part_owner(p.n_chunks, s0 / WCHUNK, GS);
-            const int64_t b1 = 1 + part_owner(p.n_chunks, (e - 1) / WCHUNK, GS);
-            for (int64_t b = max(b0, (int64_t)1); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
-        }
-        p.n_g[g] = n;
-        const int32_t ti = p.task_id[g], j = p.group_id[g];
-        if (q < MAXT) {
-            tt[q] = (ti >= 0 && ti < p.n_tasks && j >= 0 && j < p.n_groups) ? ti : -1;
-            nn[q] = (double)n;
-            aa[q] = p.adv_hat[g];
-        }
-    }
-    const bool in_regs = (g_hi - g_lo) <= (int64_t)MAXT * COOP_THREADS;
-    __syncthreads();  // n_g of this block's trajectories published (re-read below if needed)
-    for (int32_t i0 = 0; i0 < p.n_tasks; i0 += TASK_BATCH) {
-        const int32_t nb = min(TASK_BATCH, p.n_tasks - i0);
-        for (int32_t ii = 0; ii < nb; ++ii) {
-            double N = 0.0, S = 0.0, Q = 0.0;
-            if (in_regs) {
-#pragma unroll
-                for (int k = 0; k < MAXT; ++k)
-                    if (tt[k] == i0 + ii) {
-                        N += nn[k];
-                        S += nn[k] * aa[k];
-                        Q += nn[k] * aa[k] * aa[k];
-                    }
-            } else {
-                for (int64_t g = g_lo + threadIdx.x; g < g_hi; g += COOP_THREADS)
-                    if (p.task_id[g] == i0 + ii && p.group_id[g] >= 0 &&
-                        p.group_id[g] < p.n_groups) {
-                        const double n = (double)p.n_g[g], ah = p.adv_hat[g];
-                        N += n;
-                        S += n * ah;
-                        Q += n * ah * ah;
-                    }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                N += __shfl_down_sync(0xffffffffu, N, o);
-                S += __shfl_down_sync(0xffffffffu, S, o);
-                Q += __shfl_down_sync(0xffffffffu, Q, o);
-            }
-            if (lane == 0) {
-                s_wp[wid][ii][0] = N;
-                s_wp[wid][ii][1] = S;
-                s_wp[wid][ii][2] = Q;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < 3 * nb) {
-            const int ii = threadIdx.x / 3, k = threadIdx.x % 3;
-            double v = 0.0;
-            for (int w = 0; w < NWARPS; ++w) v += s_wp[w][ii][k];
-            p.blk_part[3 * (B * p.n_tasks + i0 + ii) + k] = v;
-        }
-        __syncthreads();
-    }
-    // groups with members (G of the GRPO group mean) and the compaction bases
-    int32_t ng = 0;
-    for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) ng += p.grp_cnt[j] > 0;
-    int32_t ngt = 0;
-    (void)coop_block_exscan(ng, s_w, ngt);
-    if (threadIdx.x == 0) p.blk_grp[B] = ngt;
-    const int32_t total = coop_block_scan_array(s_pre, G, s_w);
-    if (threadIdx.x == 0) s_pre[G] = total;
-    __syncthreads();
-}
-
-// after the second grid barrier (every block, identical order -> identical results): per-task
+// after the barrier (every block, identical code and order -> identical results): the per-task
 // moments = the block partials summed in block order (warp w: tasks w, w+8, ...; lanes stride
-// the blocks, then a fixed shuffle tree), mu_i and max(sigma_i, eps) into s_task; block 0
-// publishes task_stats, N, G and the local masked-row count (s_pre[G]).
-__device__ void small_moments(const AdvParams& p, uint8_t* smem, int64_t G, const int32_t* s_pre) {
+// the blocks, shuffle tree); mu_i and max(sigma_i, eps) into s_task; s_pre = exclusive prefix
+// of the blocks' masked totals (compaction bases).  Block 0 publishes task_stats, N, G and the
+// local masked-row count; stats_only (a communicator follows): block 0 writes the raw sums.
+__device__ void small_moments(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w,
+                              bool stats_only) {
     double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
     __shared__ double s_nsum[NWARPS];
     __shared__ int32_t s_ngrp;
+    const int64_t G = gridDim.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool blk0 = blockIdx.x == 0;
+    if (stats_only && !blk0) return;
     double nsum = 0.0;
     for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
         double N = 0.0, S = 0.0, Q = 0.0;
@@ -1175,15 +1086,20 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int64_t G, cons
             Q += __shfl_down_sync(0xffffffffu, Q, o);
         }
         if (lane == 0) {
-            const double mu = N > 0.0 ? S / N : 0.0;
-            const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
-            s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
-            if (blk0 && p.task_stats_out) {
-                p.task_stats_out[3 * i] = N;
-                p.task_stats_out[3 * i + 1] = mu;
-                p.task_stats_out[3 * i + 2] = sd;
+            if (stats_only) {
+                p.stats[3 * i] = N;
+                p.stats[3 * i + 1] = S;
+                p.stats[3 * i + 2] = Q;
+            } else {
+                const double mu = N > 0.0 ? S / N : 0.0;
+                const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
+                s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
+                if (blk0 && p.task_stats_out) {
+                    p.task_stats_out[3 * i] = N;
+                    p.task_stats_out[3 * i + 1] = mu;
+                    p.task_stats_out[3 * i + 2] = sd;
+                }
             }
-            if (blk0) p.stats[3 * i] = N;
             nsum += N;
         }
     }
@@ -1197,11 +1113,16 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int64_t G, cons
             if (lane == 0) s_ngrp = c;
         }
     }
-    __syncthreads();
+    if (stats_only) {
+        __syncthreads();
+        if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)s_ngrp;  // G (local)
+        return;
+    }
+    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // (its barriers also order s_task / s_nsum)
     if (blk0 && threadIdx.x == 0) {
         double n = 0.0;
-        // tasks were summed warp by warp: add the warp totals in task order (task i in warp
-        // i % NWARPS) -- any fixed order gives an exact integer here
+        // tasks were summed warp by warp: add the warp totals in warp order -- any fixed order
+        // gives the exact integer here
         for (int w = 0; w < NWARPS; ++w) n += s_nsum[w];
         const int64_t nn = (int64_t)n;
         p.meta[0] = s_pre[G];  // local masked rows
@@ -1213,38 +1134,23 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int64_t G, cons
     __syncthreads();
 }
 
-__device__ __forceinline__ void small_range(const AdvParams& p, int64_t& c_lo, int64_t& c_hi) {
-    const int64_t GS = gridDim.x - 1, B = (int64_t)blockIdx.x - 1;
-    c_lo = B < 0 ? 0 : part_lo(p.n_chunks, B, GS);
-    c_hi = B < 0 ? 0 : part_lo(p.n_chunks, B + 1, GS);
+// n_g of the trajectories this block owns: the slots of the blocks whose ranges it spans,
+// summed in block order (exact integers)
+__device__ void small_publish_ng(const AdvParams& p, const int64_t* s_off) {
+    const int64_t G = gridDim.x, B = blockIdx.x;
+    const int64_t t_lo = part_lo(p.n_traj, B, G), t_hi = part_lo(p.n_traj, B + 1, G);
+    for (int64_t g = t_lo + threadIdx.x; g < t_hi; g += COOP_THREADS) {
+        const int64_t s0 = s_off[g], e = s_off[g + 1];
+        int32_t n = 0;
+        if (e > s0 && s0 >= 0) {
+            const int64_t b0 = part_owner(p.n_chunks, s0 / WCHUNK, G);
+            const int64_t b1 = part_owner(p.n_chunks, (e - 1) / WCHUNK, G);
+            for (int64_t b = max(b0, (int64_t)0); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+        }
+        p.n_g[g] = n;
+    }
 }
 
-__device__ __forceinline__ void small_count(const AdvParams& p, uint8_t* smem, WarpRing& r,
-                                            int32_t* s_w) {
-    int64_t c_lo, c_hi;
-    small_range(p, c_lo, c_hi);
-    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-    int32_t warp_total = 0;
-    // the offsets are staged while the block's first mask copies are in flight
-    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false,
-                    [&]() { stage_all_offsets(p, smem); });
-    chunk_bases(p, c_lo, c_hi, s_w);
-}
-
-// phase C of a streaming block.  fused (single kernel, no communicator): the mask is still in
-// the ring and s_task was computed by small_stats; else (second launch after the all-reduce)
-// everything is reloaded and mu, sigma come from the reduced stats.
-__device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
-                                            int32_t* s_pre, int32_t* s_w, bool fused) {
-    int64_t c_lo, c_hi;
-    small_range(p, c_lo, c_hi);
-    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-    if (!fused) load_task_params(p, smem, s_pre, s_w);  // fused: s_pre, s_task from small_stats
-    const SmallArrays a = small_arrays(p, smem);
-    int32_t dummy = 0;
-    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, fused, NoPre(),
-                    fused ? a.ah : nullptr, fused ? a.tid : nullptr);
-}
 
 // masked tokens before position t (large driver, after phase A): block prefix + the chunk's
 // local base + the popcount of the chunk's lane bits below t
@@ -1605,58 +1511,58 @@ __global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_appl
     large_apply(p, smem, r, ss.s_pre, ss.s_w);
 }
 
-// phase stamps (agentrl_debug_adv_phase_ns), small driver: [0] start and [1] counts done in
-// streaming block 1, [2] block 0's group work done, [3] after the first grid barrier, [4] after
-// the second (partials done everywhere), [5] apply done (block 1)
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_all(const AdvParams p) {
+// phase C of the second launch (after the all-reduce): everything reloaded, mu, sigma from the
+// reduced stats, A^ and task ids from global
+__device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
+                                            int32_t* s_pre, int32_t* s_w) {
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    load_task_params(p, smem, s_pre, s_w);
+    int32_t dummy = 0;
+    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, false);
+}
+
+// phase stamps (agentrl_debug_adv_phase_ns), small driver, block 0: [0] start, [1] counts done,
+// [2] group advantages done, [3] after the grid barrier, [4] moments done, [5] apply done
+__global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_all(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    phase_mark(0, 1);
-    WarpRing r{};
-    if (blockIdx.x == 0) {
-        small_group_pre(p, smem, ss.s_w);  // stages the offsets itself
-        phase_mark(2, 0);
-    } else {
-        r = ring_setup(p, smem);
-        small_count(p, smem, r, ss.s_w);
-        phase_mark(1, 1);
-    }
+    phase_mark(0);
+    WarpRing r = ring_setup(p, smem);
+    small_pre_barrier(p, smem, r, ss.s_w);
     grid.sync();
-    phase_mark(3, 1);
-    small_partials(p, gridDim.x, ss.s_w, ss.s_pre);  // n_g and per-block task partials
-    grid.sync();
-    phase_mark(4, 1);
-    small_moments(p, smem, gridDim.x, ss.s_pre);  // every block: mu_i, sigma_i
-    if (blockIdx.x != 0) {
-        int64_t c_lo, c_hi;
-        small_range(p, c_lo, c_hi);
-        const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-        int32_t dummy = 0;
-        // the mask is still in the ring from phase A; A^ and task ids come from global
-        stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, ss.s_pre[blockIdx.x], dummy, true);
-    }
-    phase_mark(5, 1);
+    phase_mark(3);
+    small_moments(p, smem, ss.s_pre, ss.s_w, false);  // every block: mu_i, sigma_i, bases
+    phase_mark(4);
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    const SmallT a = small_t(p, smem);
+    int32_t dummy = 0;
+    // the mask is still in the ring from phase A; A^ and task ids from smem
+    stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, ss.s_pre[blockIdx.x], dummy, true,
+                    NoPre(), a.ah, a.tid);
+    phase_mark(5);
+    small_publish_ng(p, s_off);
 }
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_stats(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    if (blockIdx.x == 0) {
-        small_group_pre(p, smem, ss.s_w);  // stages the offsets itself
-    } else {
-        WarpRing r = ring_setup(p, smem);
-        small_count(p, smem, r, ss.s_w);
-    }
+    WarpRing r = ring_setup(p, smem);
+    small_pre_barrier(p, smem, r, ss.s_w);
     grid.sync();
-    if (blockIdx.x == 0) small_stats(p, smem, gridDim.x, ss.s_w, false, true);
+    small_moments(p, smem, ss.s_pre, ss.s_w, true);  // block 0: raw (N, S, Q) and G
+    small_publish_ng(p, reinterpret_cast<const int64_t*>(smem + p.lay.soff));
 }
-__global__ void __launch_bounds__(COOP_THREADS, 2) k_adv_small_apply(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     stage_all_offsets(p, smem);
     WarpRing r = ring_setup(p, smem);
-    small_apply(p, smem, r, ss.s_pre, ss.s_w, false);  // block 0 publishes meta / task_stats
+    small_apply(p, smem, r, ss.s_pre, ss.s_w);  // block 0 publishes meta / task_stats
 }
 
 static int coop_grid(const void* kern, size_t smem, int64_t want) {

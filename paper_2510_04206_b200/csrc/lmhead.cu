@@ -319,6 +319,55 @@ __global__ void __launch_bounds__(256)
 constexpr int RS_ROWS = 32;
 constexpr int RS_WARPS = 8;
 
+// The row statistics over the tiles of this rank's columns, in the fixed order above (shared by
+// k_row_stats and the vocab-parallel slot kernel, so a one-rank vocab-parallel head reproduces
+// the single-GPU bits): returns M and the first tile jM holding it; warp w's L' partial is left
+// in s_l[w][lane] (the caller sums the warps in warp order after a barrier).
+__device__ __forceinline__ void rs_max_sum(const float2* __restrict__ part, int64_t ld,
+                                           int32_t n_tiles, int64_t p, bool ok,
+                                           float (&s_m)[RS_WARPS][RS_ROWS],
+                                           int (&s_j)[RS_WARPS][RS_ROWS],
+                                           float (&s_l)[RS_WARPS][RS_ROWS], float& M, int& jM) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float LOG2E = 1.4426950408889634f;
+    // ---- row max and the first tile holding it (tiles in increasing order per warp)
+    float m = -INFINITY;
+    int jm = 0x7fffffff;
+    if (ok)
+#pragma unroll 4
+        for (int j = w; j < n_tiles; j += RS_WARPS) {
+            const float x = part[(int64_t)j * ld + p].x;
+            if (x > m) {
+                m = x;
+                jm = j;
+            }
+        }
+    s_m[w][lane] = m;
+    s_j[w][lane] = jm;
+    __syncthreads();
+    M = s_m[0][lane];
+    jM = s_j[0][lane];
+#pragma unroll
+    for (int q = 1; q < RS_WARPS; ++q) {
+        const float x = s_m[q][lane];
+        const int jq = s_j[q][lane];
+        if (x > M || (x == M && jq < jM)) {
+            M = x;
+            jM = jq;
+        }
+    }
+    // ---- L' partials
+    float L = 0.f;
+    if (ok)
+#pragma unroll 4
+        for (int j = w; j < n_tiles; j += RS_WARPS) {
+            const float2 ml = part[(int64_t)j * ld + p];
+            L += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
+        }
+    s_l[w][lane] = L;
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(RS_ROWS * RS_WARPS)
     k_row_stats(const int64_t* __restrict__ rows_dev, const int64_t* __restrict__ nglob_dev,
                 int32_t n_tiles, int64_t ld, const float2* __restrict__ part /* [n_tiles][ld] */,
@@ -347,42 +396,9 @@ __global__ void __launch_bounds__(RS_ROWS * RS_WARPS)
     for (int64_t p0 = (int64_t)blockIdx.x * RS_ROWS; p0 < rows; p0 += (int64_t)gridDim.x * RS_ROWS) {
         const int64_t p = p0 + lane;
         const bool ok = p < rows;
-        // ---- row max and the first tile holding it (tiles in increasing order per warp)
-        float m = -INFINITY;
-        int jm = 0x7fffffff;
-        if (ok)
-#pragma unroll 4
-            for (int j = w; j < n_tiles; j += RS_WARPS) {
-                const float x = part[(int64_t)j * ld + p].x;
-                if (x > m) {
-                    m = x;
-                    jm = j;
-                }
-            }
-        s_m[w][lane] = m;
-        s_j[w][lane] = jm;
-        __syncthreads();
-        float M = s_m[0][lane];
-        int jM = s_j[0][lane];
-#pragma unroll
-        for (int q = 1; q < RS_WARPS; ++q) {
-            const float x = s_m[q][lane];
-            const int jq = s_j[q][lane];
-            if (x > M || (x == M && jq < jM)) {
-                M = x;
-                jM = jq;
-            }
-        }
-        // ---- L' partials
-        float L = 0.f;
-        if (ok)
-#pragma unroll 4
-            for (int j = w; j < n_tiles; j += RS_WARPS) {
-                const float2 ml = part[(int64_t)j * ld + p];
-                L += j == jM ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
-            }
-        s_l[w][lane] = L;
-        __syncthreads();
+        float M;
+        int jM;
+        rs_max_sum(part, ld, n_tiles, p, ok, s_m, s_j, s_l, M, jM);
         if (w == 0) {
             float Lm1 = 0.f;
 #pragma unroll
@@ -574,34 +590,28 @@ LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
 // same token rows).  Per row, this rank's statistics over its columns: M_r = max z,
 // L'_r = sum exp(z - M_r) - 1 (the first max left out, as in the tile merge) -> its slot of the
 // all-gather buffer (the other slots are zero; a sum all-reduce then fills every slot).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(RS_ROWS * RS_WARPS)
     k_vp_row_stats(const int64_t* __restrict__ rows_dev, int32_t n_tiles, int64_t ld,
                    const float2* __restrict__ part /* [n_tiles][ld] */,
                    float2* __restrict__ slot) {
+    __shared__ float s_m[RS_WARPS][RS_ROWS];
+    __shared__ int s_j[RS_WARPS][RS_ROWS];
+    __shared__ float s_l[RS_WARPS][RS_ROWS];
     const int64_t rows = *rows_dev;
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const float LOG2E = 1.4426950408889634f;
-    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < rows;
-         p += nw) {
-        const float2* pr = part + p;
-        float M = -INFINITY;
-        for (int j = lane; j < n_tiles; j += 32) M = fmaxf(M, pr[j * ld].x);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t p0 = (int64_t)blockIdx.x * RS_ROWS; p0 < rows; p0 += (int64_t)gridDim.x * RS_ROWS) {
+        const int64_t p = p0 + lane;
+        const bool ok = p < rows;
+        float M;
+        int jM;
+        rs_max_sum(part, ld, n_tiles, p, ok, s_m, s_j, s_l, M, jM);
+        if (w == 0 && ok) {
+            float Lm1 = 0.f;  // warp partials in warp order, as in k_row_stats
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        int jm = 0x7fffffff;
-        for (int j = lane; j < n_tiles; j += 32)
-            if (pr[j * ld].x == M) jm = min(jm, j);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) jm = min(jm, __shfl_xor_sync(0xffffffffu, jm, o));
-        float L = 0.f;
-        for (int j = lane; j < n_tiles; j += 32) {
-            const float2 ml = pr[j * ld];
-            L += j == jm ? ml.y : (1.f + ml.y) * ex2_approx((ml.x - M) * LOG2E);
+            for (int q = 0; q < RS_WARPS; ++q) Lm1 += s_l[q][lane];
+            slot[p] = make_float2(M, Lm1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-        if (lane == 0) slot[p] = make_float2(M, L);
+        __syncthreads();
     }
 }
 
@@ -807,7 +817,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     float2* vpstat = vp ? reinterpret_cast<float2*>(ws + w.vpstat) : nullptr;
     if (vp) {  // all-gather of (M_r, L'_r) per row and the owner's z_y (sum all-reduces)
         AG_CUDA(cudaMemsetAsync(vpstat, 0, sizeof(float2) * (size_t)vp_R * rows_cap, stream));
-        k_vp_row_stats<<<num_sms() * 4, 256, 0, stream>>>(
+        k_vp_row_stats<<<(unsigned)std::max<int64_t>(ceil_div(rows_cap, RS_ROWS), 1),
+                         RS_ROWS * RS_WARPS, 0, stream>>>(
             rows_dev, w.n_tiles, rows_cap, part, vpstat + (size_t)comm_rank(comm) * rows_cap);
         count_launch();
         AG_CUDA(cudaGetLastError());
