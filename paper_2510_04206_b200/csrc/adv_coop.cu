@@ -63,6 +63,7 @@ constexpr int KC_CAP = ADV_KC_CAP;      // chunks per staged window (chunk -> tr
                                         // a block with more chunks stages 64-chunk windows
 constexpr int SMALL_TRAJ = 2048;        // small driver: all offsets staged in every block
 constexpr int SMALL_GROUPS = 512;
+constexpr int CT_CAP = 1024;   // small driver: chunk totals kept in smem up to this many chunks
 constexpr int TASK_BATCH = 16;  // tasks reduced per barrier in the per-block partials
 constexpr int REG_K = 16;       // groups up to this size are handled in registers (phase B3)
 
@@ -80,7 +81,7 @@ __device__ __forceinline__ void phase_mark(int i, unsigned blk = 0) {
 // dynamic shared memory layout (byte offsets), identical on host and device
 struct Lay {
     uint32_t ring, bars, ostage, soff, srel, saux, skc, stask, cidx, cadv;
-    uint32_t sgid, stid, srew, sah, gflag, gtask, glist;  // small driver: trajectory table
+    uint32_t sgid, stid, srew, sah, gflag, gtask, glist, sct;  // small driver
     uint32_t total;
 };
 __host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
@@ -115,6 +116,7 @@ __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, i
     L.gflag = lay_take(o, 4u * ng);
     L.gtask = lay_take(o, 4u * ng);
     L.glist = lay_take(o, 4u * ng);
+    L.sct = lay_take(o, small ? 4u * CT_CAP : 0u);  // per-chunk masked totals of the block
     (void)stream_begin;
     (void)stream_end;
     L.total = o;
@@ -527,6 +529,9 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         if (l - f + 1 > WIN_TRAJ) wlen = WIN_CHUNKS;
     }
     int32_t* s_kc = reinterpret_cast<int32_t*>(smem + p.lay.skc);
+    // small driver, phase C of the fused kernel with one window: phase A's s_rel and s_kc are
+    // still in smem (the same window), only the values s_aux are restaged
+    const bool reuse = PH == 1 && small && resident && wlen >= c_hi - c_lo;
     int32_t kseq = 0;
     int32_t prev_last = -1;  // last trajectory of the previous window (block-uniform)
     for (int64_t w0 = c_lo; w0 < c_hi; w0 += wlen) {
@@ -550,7 +555,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             if (w.staged) {
                 for (int32_t k = threadIdx.x; k <= w.nbt; k += COOP_THREADS) {
                     const int64_t o = (small ? s_offall[f + k] : p.off[f + k]) - w.base;
-                    s_rel[k] = (int32_t)min(max(o, (int64_t)0), (int64_t)INT_MAX);
+                    if (!reuse) s_rel[k] = (int32_t)min(max(o, (int64_t)0), (int64_t)INT_MAX);
                     if (k < w.nbt)
                         s_aux[k] = PH == 0 ? 0
                                    : (ah_s ? __float_as_int(adv_tilde_s(p, s_task, ah_s, tid_s, f + k))
@@ -559,7 +564,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             }
         }
         __syncthreads();
-        if (w.staged) {  // chunk -> first trajectory of the window (no searches)
+        if (w.staged && !reuse) {  // chunk -> first trajectory of the window (no searches)
             const int32_t nwc = (int32_t)(w1 - w0);
             for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
                 const int32_t lo = (w.s_rel[k] + WCHUNK - 1) / WCHUNK;
@@ -599,7 +604,11 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             } else if (PH == 0) {  // small driver: every window is staged
                 int32_t tot = 0;
                 if (any_traj) (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
-                if (lane == 0) p.chunk[c] = tot;
+                if (lane == 0) {
+                    p.chunk[c] = tot;
+                    if (c - c_lo < CT_CAP)
+                        reinterpret_cast<int32_t*>(smem + p.lay.sct)[c - c_lo] = tot;
+                }
                 warp_total += tot;
             } else {
                 const LaneMask lm = from_bits ? lane_mask_bits(sbits) : lane_mask(mk);
@@ -830,29 +839,37 @@ __device__ __forceinline__ bool small_member(const AdvParams& p, int32_t j, int3
     return j >= 0 && j < p.n_groups && i >= 0 && i < p.n_tasks;
 }
 
-// the whole trajectory table into smem (every load issued before the first store); the
-// trajectories this block owns are validated here (ids, offsets; A^ = 0 outside any group)
+// the whole trajectory table into smem: every load of a thread is issued before its first store
+// (one DRAM round trip); the trajectories this block owns are validated here (ids, offsets;
+// A^ = 0 outside any group)
+constexpr int TBL_PER = (SMALL_TRAJ + 1 + COOP_THREADS - 1) / COOP_THREADS;
 __device__ void small_load_table(const AdvParams& p, uint8_t* smem, int32_t& st) {
     const SmallT a = small_t(p, smem);
     int64_t* s_off = reinterpret_cast<int64_t*>(smem + p.lay.soff);
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t t_lo = part_lo(p.n_traj, B, G), t_hi = part_lo(p.n_traj, B + 1, G);
-    for (int32_t g = threadIdx.x; g <= p.n_traj; g += COOP_THREADS) {
-        const int64_t o = p.off[g];
-        int32_t j = -1, i = -1;
-        float r = 0.f;
+    int64_t o[TBL_PER];
+    int32_t jj[TBL_PER], ii[TBL_PER];
+    float rr[TBL_PER];
+#pragma unroll
+    for (int q = 0; q < TBL_PER; ++q) {
+        const int32_t g = threadIdx.x + q * COOP_THREADS;
+        o[q] = g <= p.n_traj ? p.off[g] : 0;
+        const bool in = g < p.n_traj;
+        jj[q] = in ? p.group_id[g] : -1;
+        ii[q] = in ? p.task_id[g] : -1;
+        rr[q] = in ? p.rewards[g] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < TBL_PER; ++q) {
+        const int32_t g = threadIdx.x + q * COOP_THREADS;
+        if (g <= p.n_traj) s_off[g] = o[q];
         if (g < p.n_traj) {
-            j = p.group_id[g];
-            i = p.task_id[g];
-            r = p.rewards[g];
-        }
-        s_off[g] = o;
-        if (g < p.n_traj) {
-            a.gid[g] = j;
-            a.tid[g] = i;
-            a.rew[g] = r;
+            a.gid[g] = small_member(p, jj[q], ii[q]) ? jj[q] : -1;  // -1: in no group
+            a.tid[g] = ii[q];
+            a.rew[g] = rr[q];
             a.ah[g] = 0.0;
-            if (g >= t_lo && g < t_hi && !small_member(p, j, i)) {
+            if (g >= t_lo && g < t_hi && !small_member(p, jj[q], ii[q])) {
                 st |= AGENTRL_ST_GROUP_SPANS_TASKS;
                 p.adv_hat[g] = 0.0;
             }
@@ -877,33 +894,38 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     int32_t K = 0, first = -1;
-    double sum = 0.0, rmax = -INFINITY, rmin = INFINITY;
+    double sum = 0.0;
+    float fmx = -INFINITY, fmn = INFINITY;
+    // a.gid holds the group id of members and -1 otherwise (invalid group or task id)
+#pragma unroll 4
     for (int32_t i0 = 0; i0 < p.n_traj; i0 += 32) {
         const int32_t i = i0 + lane;
-        bool hit = false;
-        float r = 0.f;
-        if (i < p.n_traj) {
-            hit = a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks;
-            r = a.rew[i];
-        }
+        const bool hit = i < p.n_traj && a.gid[i] == j;
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (hit) {
+            const float r = a.rew[i];
             const int32_t rk = K + __popc(bal & lt);
             if (rk < 32) s_mb[rk] = i;  // the first 32 members, in index order
             sum += (double)r;
-            rmax = fmax(rmax, (double)r);
-            rmin = fmin(rmin, (double)r);
+            fmx = fmaxf(fmx, r);
+            fmn = fminf(fmn, r);
         }
         if (first < 0 && bal) first = i0 + __ffs(bal) - 1;
         K += __popc(bal);
     }
-    // butterflies: a + b == b + a, so every lane ends with the same bits
+    // butterfly: a + b == b + a, so every lane ends with the same bits; max / min of the f32
+    // rewards through order-preserving integer keys (one redux each)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-        rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
-    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    auto okey = [](float x) {
+        const uint32_t u = __float_as_uint(x);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    };
+    auto ounkey = [](uint32_t k) {
+        return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+    };
+    const double rmax = (double)ounkey(__reduce_max_sync(0xffffffffu, okey(fmx)));
+    const double rmin = (double)ounkey(__reduce_min_sync(0xffffffffu, okey(fmn)));
     __syncwarp();
     if (K == 0) {
         if (lane == 0) {
@@ -930,7 +952,7 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
         }
     } else {
         for (int32_t i = lane; i < p.n_traj; i += 32)
-            if (a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks) {
+            if (a.gid[i] == j) {
                 spans |= a.tid[i] != task0;
                 const double dl = (double)a.rew[i] - mean;
                 ss += flat ? 0.0 : dl * dl;
@@ -950,7 +972,7 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
         if (m >= 0) put(m);
     } else {
         for (int32_t i = lane; i < p.n_traj; i += 32)
-            if (a.gid[i] == j && a.tid[i] >= 0 && a.tid[i] < p.n_tasks) put(i);
+            if (a.gid[i] == j) put(i);
     }
     if (lane == 0) {
         a.gtask[j] = task0;
@@ -982,22 +1004,14 @@ __device__ __forceinline__ bool small_traj_range(const AdvParams& p, const int64
     return true;
 }
 
-// phase A + group advantages + the block's partial moments (everything before the barrier)
-__device__ void small_pre_barrier(const AdvParams& p, uint8_t* smem, WarpRing& r, int32_t* s_w) {
+// the groups this block needs -- those of the trajectories overlapping its token range (bit
+// 0) and those it owns (bit 1) -- one warp each; blk_grp[B] = the owned groups with members
+__device__ void small_groups(const AdvParams& p, uint8_t* smem, int64_t c_lo, int64_t c_hi,
+                             int32_t& st) {
     const SmallT a = small_t(p, smem);
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
-    int32_t st = 0;
-    int64_t c_lo, c_hi;
-    small_range(p, c_lo, c_hi);
-    int32_t warp_total = 0;
-    // the trajectory table is staged while the block's first mask copies are in flight
-    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false,
-                    [&]() { small_load_table(p, smem, st); });
-    phase_mark(1);
-    chunk_bases(p, c_lo, c_hi, s_w);  // per-chunk compaction bases, blk_chunk[B]
-    // ---- the groups this block needs: those of its trajectories (bit 0), those it owns (bit 1)
     int32_t f = 0, l = -1;
     const bool any = small_traj_range(p, s_off, c_lo, c_hi, f, l);
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
@@ -1019,10 +1033,57 @@ __device__ void small_pre_barrier(const AdvParams& p, uint8_t* smem, WarpRing& r
     }
     if (lane == 0 && nz) atomicAdd(&s_nz, nz);
     __syncthreads();  // A^ of the block's trajectories and the groups' tasks in smem
-    phase_mark(2);
+    if (threadIdx.x == 0) p.blk_grp[B] = s_nz;
+}
+
+// block-local exclusive scan of the block's chunk totals (kept in smem by phase A up to CT_CAP
+// chunks) -> chunk_base; blk_chunk[B] = the block total
+__device__ void small_chunk_bases(const AdvParams& p, uint8_t* smem, int64_t c_lo, int64_t c_hi,
+                                  int32_t* s_w) {
+    const int64_t n = c_hi - c_lo;
+    if (n > CT_CAP) {
+        chunk_bases(p, c_lo, c_hi, s_w);
+        return;
+    }
+    const int32_t* s_ct = reinterpret_cast<const int32_t*>(smem + p.lay.sct);
+    __syncthreads();  // chunk totals of all warps written
+    const int64_t per = (n + COOP_THREADS - 1) / COOP_THREADS;
+    const int64_t lo = min(n, (int64_t)threadIdx.x * per), hi = min(n, lo + per);
+    int32_t sum = 0;
+    for (int64_t c = lo; c < hi; ++c) sum += s_ct[c];
+    int32_t total;
+    int32_t run = coop_block_exscan(sum, s_w, total);
+    for (int64_t c = lo; c < hi; ++c) {
+        p.chunk_base[c_lo + c] = run;
+        run += s_ct[c];
+    }
+    if (threadIdx.x == 0) p.blk_chunk[blockIdx.x] = total;
+}
+
+// phase A (with the trajectory table and the group advantages computed while the block's first
+// mask copies are in flight) + the block's partial moments: everything before the barrier
+__device__ void small_pre_barrier(const AdvParams& p, uint8_t* smem, WarpRing& r, int32_t* s_w) {
+    const SmallT a = small_t(p, smem);
+    const int64_t B = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
+    int32_t st = 0;
+    int64_t c_lo, c_hi;
+    small_range(p, c_lo, c_hi);
+    int32_t warp_total = 0;
+    stream_phase<0>(p, smem, r, c_lo, c_hi, true, s_off, 0, warp_total, false, [&]() {
+        small_load_table(p, smem, st);
+        phase_mark(1);
+        small_groups(p, smem, c_lo, c_hi, st);
+        phase_mark(2);
+    });
+    phase_mark(3);
+    small_chunk_bases(p, smem, c_lo, c_hi, s_w);  // per-chunk compaction bases, blk_chunk[B]
     // ---- per-task partial (N, S, Q) = sum over the block's trajectories of c_{g,B} (1, A^,
     // A^^2), attributed to the group's task; fixed order (lanes stride the trajectories,
     // shuffle tree).  Counts: the window's s_aux (one staged window) or the block's slots.
+    int32_t f = 0, l = -1;
+    const bool any = small_traj_range(p, s_off, c_lo, c_hi, f, l);
     const int32_t* s_aux = reinterpret_cast<const int32_t*>(smem + p.lay.saux);
     const bool one_window = c_hi - c_lo <= KC_CAP;
     for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
@@ -1052,7 +1113,7 @@ __device__ void small_pre_barrier(const AdvParams& p, uint8_t* smem, WarpRing& r
             bp[2] = Q;
         }
     }
-    if (threadIdx.x == 0) p.blk_grp[B] = s_nz;
+    phase_mark(4);
     if (st) atomicOr(p.d_status, st);
 }
 
@@ -1070,11 +1131,26 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int32_t* s_pre,
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool blk0 = blockIdx.x == 0;
     if (stats_only && !blk0) return;
+    // one round trip: every block partial, the block totals (compaction bases) and the group
+    // counts are loaded by the whole block into smem (the idle output-staging region) first
+    const bool one = G <= COOP_THREADS;
+    const int64_t nparts = 3 * G * (int64_t)p.n_tasks;
+    double* s_bp = reinterpret_cast<double*>(smem + p.lay.ostage);
+    const bool staged = nparts <= (int64_t)(NWARPS * WCHUNK * 4 / sizeof(double));
+    const int32_t my_cnt = (one && !stats_only && threadIdx.x < G) ? p.blk_chunk[threadIdx.x] : 0;
+    const int32_t my_grp = (one && blk0 && threadIdx.x < G) ? p.blk_grp[threadIdx.x] : 0;
+    if (threadIdx.x == 0) s_ngrp = 0;
+    if (staged) {
+        for (int64_t k = threadIdx.x; k < nparts; k += COOP_THREADS) s_bp[k] = p.blk_part[k];
+    }
+    __syncthreads();
+    if (one && my_grp) atomicAdd(&s_ngrp, my_grp);  // integers: exact in any order
+    const double* bsrc = staged ? s_bp : p.blk_part;
     double nsum = 0.0;
     for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
         double N = 0.0, S = 0.0, Q = 0.0;
         for (int64_t b = lane; b < G; b += 32) {
-            const double* bp = p.blk_part + 3 * (b * p.n_tasks + i);
+            const double* bp = bsrc + 3 * (b * p.n_tasks + i);
             N += bp[0];
             S += bp[1];
             Q += bp[2];
@@ -1105,7 +1181,7 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int32_t* s_pre,
     }
     if (blk0) {
         if (lane == 0) s_nsum[wid] = nsum;
-        if (wid == 0) {
+        if (wid == 0 && !one) {
             int32_t c = 0;
             for (int64_t b = lane; b < G; b += 32) c += p.blk_grp[b];
 #pragma unroll
@@ -1118,7 +1194,15 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int32_t* s_pre,
         if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)s_ngrp;  // G (local)
         return;
     }
-    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // (its barriers also order s_task / s_nsum)
+    if (one) {  // (the scan's barriers also order s_task / s_nsum)
+        int32_t total;
+        const int32_t pre = coop_block_exscan(my_cnt, s_w, total);
+        if (threadIdx.x < G) s_pre[threadIdx.x] = pre;
+        if (threadIdx.x == 0) s_pre[G] = total;
+        __syncthreads();
+    } else {
+        block_prefix_smem(p.blk_chunk, G, s_pre, s_w);
+    }
     if (blk0 && threadIdx.x == 0) {
         double n = 0.0;
         // tasks were summed warp by warp: add the warp totals in warp order -- any fixed order
@@ -1135,19 +1219,39 @@ __device__ void small_moments(const AdvParams& p, uint8_t* smem, int32_t* s_pre,
 }
 
 // n_g of the trajectories this block owns: the slots of the blocks whose ranges it spans,
-// summed in block order (exact integers)
-__device__ void small_publish_ng(const AdvParams& p, const int64_t* s_off) {
+// summed in block order (exact integers).  Loaded before phase C (the loads are in flight
+// while it streams), stored after it.
+constexpr int NG_PER = (SMALL_TRAJ + COOP_THREADS - 1) / COOP_THREADS;
+struct NgRegs {
+    int32_t n[NG_PER];
+};
+__device__ __forceinline__ NgRegs small_ng_load(const AdvParams& p, const int64_t* s_off) {
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t t_lo = part_lo(p.n_traj, B, G), t_hi = part_lo(p.n_traj, B + 1, G);
-    for (int64_t g = t_lo + threadIdx.x; g < t_hi; g += COOP_THREADS) {
-        const int64_t s0 = s_off[g], e = s_off[g + 1];
+    NgRegs r;
+#pragma unroll
+    for (int q = 0; q < NG_PER; ++q) {
+        const int64_t g = t_lo + threadIdx.x + (int64_t)q * COOP_THREADS;
         int32_t n = 0;
-        if (e > s0 && s0 >= 0) {
-            const int64_t b0 = part_owner(p.n_chunks, s0 / WCHUNK, G);
-            const int64_t b1 = part_owner(p.n_chunks, (e - 1) / WCHUNK, G);
-            for (int64_t b = max(b0, (int64_t)0); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+        if (g < t_hi) {
+            const int64_t s0 = s_off[g], e = s_off[g + 1];
+            if (e > s0 && s0 >= 0) {
+                const int64_t b0 = part_owner(p.n_chunks, s0 / WCHUNK, G);
+                const int64_t b1 = part_owner(p.n_chunks, (e - 1) / WCHUNK, G);
+                for (int64_t b = max(b0, (int64_t)0); b <= min(b1, G - 1); ++b) n += p.blk_cnt[g + b];
+            }
         }
-        p.n_g[g] = n;
+        r.n[q] = n;
+    }
+    return r;
+}
+__device__ __forceinline__ void small_ng_store(const AdvParams& p, const NgRegs& r) {
+    const int64_t G = gridDim.x, B = blockIdx.x;
+    const int64_t t_lo = part_lo(p.n_traj, B, G), t_hi = part_lo(p.n_traj, B + 1, G);
+#pragma unroll
+    for (int q = 0; q < NG_PER; ++q) {
+        const int64_t g = t_lo + threadIdx.x + (int64_t)q * COOP_THREADS;
+        if (g < t_hi) p.n_g[g] = r.n[q];
     }
 }
 
@@ -1523,8 +1627,9 @@ __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, W
     stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, s_pre[blockIdx.x], dummy, false);
 }
 
-// phase stamps (agentrl_debug_adv_phase_ns), small driver, block 0: [0] start, [1] counts done,
-// [2] group advantages done, [3] after the grid barrier, [4] moments done, [5] apply done
+// phase stamps (agentrl_debug_adv_phase_ns), small driver, block 0: [0] start, [1] trajectory
+// table staged, [2] group advantages done, [3] counts done, [4] partial moments written, [5] after
+// the grid barrier, [6] moments done, [7] apply done
 __global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_all(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
@@ -1533,19 +1638,20 @@ __global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_all(const AdvPara
     WarpRing r = ring_setup(p, smem);
     small_pre_barrier(p, smem, r, ss.s_w);
     grid.sync();
-    phase_mark(3);
+    phase_mark(5);
     small_moments(p, smem, ss.s_pre, ss.s_w, false);  // every block: mu_i, sigma_i, bases
-    phase_mark(4);
+    phase_mark(6);
     int64_t c_lo, c_hi;
     small_range(p, c_lo, c_hi);
     const int64_t* s_off = reinterpret_cast<const int64_t*>(smem + p.lay.soff);
     const SmallT a = small_t(p, smem);
+    const NgRegs ng = small_ng_load(p, s_off);
     int32_t dummy = 0;
     // the mask is still in the ring from phase A; A^ and task ids from smem
     stream_phase<1>(p, smem, r, c_lo, c_hi, true, s_off, ss.s_pre[blockIdx.x], dummy, true,
                     NoPre(), a.ah, a.tid);
-    phase_mark(5);
-    small_publish_ng(p, s_off);
+    phase_mark(7);
+    small_ng_store(p, ng);
 }
 __global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1555,7 +1661,7 @@ __global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_stats(const AdvPa
     small_pre_barrier(p, smem, r, ss.s_w);
     grid.sync();
     small_moments(p, smem, ss.s_pre, ss.s_w, true);  // block 0: raw (N, S, Q) and G
-    small_publish_ng(p, reinterpret_cast<const int64_t*>(smem + p.lay.soff));
+    small_ng_store(p, small_ng_load(p, reinterpret_cast<const int64_t*>(smem + p.lay.soff)));
 }
 __global__ void __launch_bounds__(COOP_THREADS, 1) k_adv_small_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];

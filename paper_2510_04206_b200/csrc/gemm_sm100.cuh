@@ -49,8 +49,13 @@ constexpr int GEMM_BM = 128;  // rows per CTA
 constexpr int GEMM_BN = 256;  // columns per MMA (and per FWD statistics tile)
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 192;     // producer, MMA, 4 epilogue warps
-constexpr int GEMM_THREADS_XF = 320;  // + 4 transform warps (XF)
+constexpr int GEMM_THREADS_XF = 352;  // + 4 transform warps and 1 input-loader warp (XF)
 constexpr int XF_WARP0 = 6;
+constexpr int XF_LOADER_WARP = XF_WARP0 + 4;
+// XF: per-stage side buffer of the transform's inputs, filled by the loader warp: grad_hidden:
+// the 128 rows' scales f (512 B); grad_W: the 64 tokens' scales (256 B) and (target column,
+// G value) pairs (512 B)
+constexpr int XIN_STAGE = 1024;
 
 // KSUB: 64-wide K atoms per pipeline stage (K-major operands only).  KSUB = 2 stages 128 K
 // per k-block: 8 MMAs per barrier round trip instead of 4, for the short-K forward GEMM whose
@@ -297,7 +302,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     uint64_t* tq_full = tempty + 2;   // tile queue (dynamic scheduler): QD slots
     uint64_t* tq_empty = tq_full + QD;
     uint64_t* ready = tq_empty + QD;  // XF: stage transformed (leader's is the one used)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + STAGES);
+    uint64_t* xin_full = ready + STAGES;  // XF: the stage's transform inputs are in smem
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xin_full + STAGES);
+    // XF: the transform inputs of each stage after the 1 KB barrier region (then the grad_W slab)
+    uint8_t* xin = reinterpret_cast<uint8_t*>(bars) + 1024;
+    const uint32_t xin_base = smem_u32(xin);
+    (void)xin_base;
     volatile int32_t* tile_q = reinterpret_cast<volatile int32_t*>(tmem_slot + 4);
     const bool dyn = p.tile_counter != nullptr;
 
@@ -327,14 +337,17 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         }
         for (int q = 0; q < QD; ++q) {
             mbar_init(&tq_full[q], 1);
-            // consumers of a queue slot: leader MMA + 4 epilogue warps (+ 4 transform warps)
-            // (+ peer producer and its 4 epilogue (+ 4 transform) warps); only the leader's
+            // consumers of a queue slot: leader MMA + 4 epilogue warps (+ 4 transform warps and
+            // the input loader) (+ the peer's producer and the same warps); only the leader's
             // tq_empty is used
-            constexpr int per_cta = XF ? 8 : 4;
+            constexpr int per_cta = XF ? 9 : 4;
             mbar_init(&tq_empty[q], PAIR ? 2 + 2 * per_cta : 1 + per_cta);
         }
         if constexpr (XF)
-            for (int s = 0; s < STAGES; ++s) mbar_init(&ready[s], PAIR ? 8 : 4);
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&ready[s], PAIR ? 8 : 4);
+                mbar_init(&xin_full[s], 32);  // every lane of the loader warp
+            }
         fence_mbar_init();
         fence_proxy_async_smem();
     }
@@ -408,7 +421,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         // peer's TMA completes its bytes on it directly)
                         if (leader) mbar_arrive_expect_tx(&full[stage], Cfg::TX_BYTES);
                     } else {
-                        // XF: each CTA's own bytes on its own barrier (its transform warps)
+                        // XF: each CTA's own bytes (tile + the transform's inputs) on its own
+                        // barrier (its transform warps wait on it)
                         mbar_arrive_expect_tx(&full[stage], XF && PAIR ? Cfg::TX_BYTES / 2
                                                                        : Cfg::TX_BYTES);
                     }
@@ -483,12 +497,15 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             }
         }
         __syncwarp();
-    } else if (XF && warp >= XF_WARP0) {
-        // ------------------------------------------------------------ transform (XF)
+    } else if (XF && warp == XF_LOADER_WARP) {
+        // ------------------------------------------------------------ input loader (XF)
+        // The transform's per-stage inputs -- grad_hidden: the 128 rows' scales f of the
+        // stage's 256-column tile; grad_W: the 64 tokens' scales and (target column, G value)
+        // -- loaded with plain loads and stored to xin[stage] as soon as the stage is free (the
+        // producer's `empty`), then published with xin_full (release / acquire).  Kept out of
+        // the transform warps, whose proxy fence would otherwise wait for these loads.
         if constexpr (XF) {
-            const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127: the line this thread owns
             const int64_t rows = *p.xf_rows;
-            const uint32_t ready_leader = PAIR ? mapa_shared(smem_u32(&ready[0]), 0) : 0u;
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t it = 0;; ++it) {
@@ -509,88 +526,122 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 int64_t m_blk, n_blk;
                 tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int64_t m0 = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM;
-                // A_MN = false (grad_hidden): line t = token row m0 + t, K = vocabulary.
+                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    float fv[4];
+                    int2 yv[2];
+                    // loads first (rows past the valid range are never used: zero lines)
+                    if constexpr (!A_MN) {
+                        const float* src = p.xf_scale + ((kb * GEMM_BK) >> 8) * p.xf_ld + m0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int64_t r = m0 + q * 32 + lane;
+                            fv[q] = r < rows ? __ldg(src + q * 32 + lane) : 0.f;
+                        }
+                    } else {
+                        const int64_t k0 = kb * GEMM_BK;
+                        const float* src = p.xf_scale + (m0 >> 8) * p.xf_ld + k0;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int64_t r = k0 + q * 32 + lane;
+                            fv[q] = r < rows ? __ldg(src + q * 32 + lane) : 0.f;
+                            yv[q] = r < rows ? __ldg(p.xf_row + r) : make_int2(-1, 0);
+                        }
+                    }
+                    mbar_wait_sleep(&empty[stage], phase ^ 1);  // the stage's previous use done
+                    const uint32_t xs = xin_base + stage * XIN_STAGE;
+                    if constexpr (!A_MN) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) sts32f(xs + 4 * (q * 32 + lane), fv[q]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            sts32f(xs + 4 * (q * 32 + lane), fv[q]);
+                            sts64i2(xs + 256 + 8 * (q * 32 + lane), yv[q]);
+                        }
+                    }
+                    mbar_arrive(&xin_full[stage]);  // release: the stores above
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (XF && warp >= XF_WARP0) {
+        // ------------------------------------------------------------ transform (XF)
+        if constexpr (XF) {
+            // Thread t owns line t of each staged A tile.  The stage's scales (and, for grad_W,
+            // the tokens' target columns) come from xin[stage] (the loader warp), so this loop
+            // issues no global loads in steady state: its proxy fence waits only for its own
+            // shared-memory stores.
+            const int t = threadIdx.x - XF_WARP0 * 32;
+            const int64_t rows = *p.xf_rows;
+            const uint32_t ready_leader = PAIR ? mapa_shared(smem_u32(&ready[0]), 0) : 0u;
+            const int line = A_MN ? (t & 63) : t;
+            const uint32_t line_off = smem_u32(sA) + (A_MN ? (t >> 6) * 8192 : 0) + line * 128;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t it = 0;; ++it) {
+                int64_t tile;
+                if (!dyn) {
+                    tile = unit + it * n_units;
+                } else {
+                    const int slot = (int)(it & (QD - 1));
+                    mbar_wait_sleep(&tq_full[slot], (uint32_t)(it / QD) & 1u);
+                    tile = tile_q[slot];
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (leader) mbar_arrive(&tq_empty[slot]);
+                        else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
+                    }
+                }
+                if (tile >= num_tiles) break;
+                int64_t m_blk, n_blk;
+                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                const int64_t m0 = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM;
+                // A_MN = false (grad_hidden): line t = token row m0 + t, K = vocabulary; the
+                // row's (target column, G value) is fixed for the tile.
                 // A_MN = true (grad_W): line t = token k0 + (t & 63) of the vocabulary atom
                 // m0 + 64 (t >> 6), K = tokens.
-                int64_t tok = 0, vcol0 = 0;  // fixed per tile: the row (grad_h) / vocab atom (grad_W)
                 int2 yr = make_int2(-1, 0);
-                if constexpr (!A_MN) {
-                    tok = m0 + t;
-                    if (tok < rows) yr = p.xf_row[tok];
-                } else {
-                    vcol0 = m0 + 64 * (t >> 6);
-                }
+                const int64_t tok = m0 + t;
+                if (!A_MN && tok < rows) yr = __ldg(p.xf_row + tok);
+                const int64_t vcol0 = m0 + 64 * (t >> 6);
                 const bool vcol_ok = !A_MN || vcol0 < M;
-                // per k-block inputs: scale f, target column in the line (or -1), its G value,
-                // zero line.  grad_hidden: f changes once per 256-column tile (4 k-blocks),
-                // the target is the row's; grad_W: each k-block holds 64 new tokens.  Loads of
-                // k-block group g+1 (4 k-blocks, tile-major scales: coalesced) are issued before
-                // group g is transformed, so their latency hides behind 4 k-blocks of MMAs.
-                constexpr int XD = 4;
-                struct XIn {
-                    float f, gy;
-                    int ycol;
+                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait_sleep(&xin_full[stage], phase);  // the stage's scales
+                    mbar_wait_sleep(&full[stage], phase);      // the stage's P~ tile
+                    const uint32_t xs = xin_base + stage * XIN_STAGE;
+                    float f;
+                    int ycol = -1;
+                    float gy;
                     bool zero;
-                };
-                // loads only here (f, and for grad_W the row's (target, G value)); the
-                // target column is derived when the k-block is transformed, so nothing waits on
-                // these loads before the group that needs them
-                auto inputs = [&](int64_t kb) -> XIn {
-                    XIn x{0.f, 0.f, -1, true};
-                    if (kb >= num_kb) return x;
-                    const int64_t k0 = kb * GEMM_BK;
                     if constexpr (!A_MN) {
-                        x.zero = tok >= rows;
-                        if (!x.zero) x.f = __ldg(p.xf_scale + (k0 >> 8) * p.xf_ld + tok);
+                        zero = tok >= rows;
+                        f = lds32f(xs + 4 * t);
+                        const int64_t yl = (int64_t)yr.x - kb * GEMM_BK;
+                        if (yr.x >= 0 && yl >= 0 && yl < 64) ycol = (int)yl;
+                        gy = __int_as_float(yr.y);
                     } else {
-                        const int64_t tk = k0 + (t & 63);
-                        x.zero = tk >= rows || !vcol_ok;
-                        if (!x.zero) {
-                            x.f = __ldg(p.xf_scale + (vcol0 >> 8) * p.xf_ld + tk);
-                            const int2 y2 = __ldg(p.xf_row + tk);
-                            x.ycol = y2.x;  // the global target column (resolved at use)
-                            x.gy = __int_as_float(y2.y);
-                        }
+                        const int64_t tk = kb * GEMM_BK + (t & 63);
+                        zero = tk >= rows || !vcol_ok;
+                        f = lds32f(xs + 4 * (t & 63));
+                        const int2 y2 = lds64i2(xs + 256 + 8 * (t & 63));
+                        const int64_t yl = (int64_t)y2.x - vcol0;
+                        if (y2.x >= 0 && yl >= 0 && yl < 64) ycol = (int)yl;
+                        gy = __int_as_float(y2.y);
                     }
-                    return x;
-                };
-                // target column of k-block kb inside this thread's line, or -1
-                auto ycol_of = [&](const XIn& x, int64_t kb) -> int {
-                    int64_t yl;
-                    if constexpr (!A_MN) yl = (int64_t)yr.x - kb * GEMM_BK;
-                    else yl = (int64_t)x.ycol - vcol0;
-                    const int y = A_MN ? x.ycol : yr.x;
-                    return (y >= 0 && yl >= 0 && yl < 64) ? (int)yl : -1;
-                };
-                XIn cur[XD], nxt[XD];
-#pragma unroll
-                for (int u = 0; u < XD; ++u) cur[u] = inputs(u);
-                const int line = A_MN ? (t & 63) : t;
-                const uint32_t line_off = smem_u32(sA) + (A_MN ? (t >> 6) * 8192 : 0) + line * 128;
-                for (int64_t kg = 0; kg < num_kb; kg += XD) {
-#pragma unroll
-                    for (int u = 0; u < XD; ++u) nxt[u] = inputs(kg + XD + u);
-#pragma unroll
-                    for (int u = 0; u < XD; ++u) {
-                        if (kg + u < num_kb) {
-                            mbar_wait_sleep(&full[stage], phase);
-                            xf_line(line_off + stage * Cfg::A_STAGE, line, cur[u].f,
-                                    ycol_of(cur[u], kg + u), A_MN ? cur[u].gy : __int_as_float(yr.y),
-                                    cur[u].zero);
-                            fence_proxy_async_smem();  // generic smem writes -> the MMA's proxy
-                            __syncwarp();
-                            if (lane == 0) {
-                                if constexpr (PAIR) mbar_arrive_cluster(ready_leader + stage * 8);
-                                else mbar_arrive(&ready[stage]);
-                            }
-                            if (++stage == STAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
-                        }
+                    xf_line(line_off + stage * Cfg::A_STAGE, line, f, ycol, gy, zero);
+                    fence_proxy_async_smem();  // generic smem writes -> the MMA's proxy
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (PAIR) mbar_arrive_cluster(ready_leader + stage * 8);
+                        else mbar_arrive(&ready[stage]);
                     }
-#pragma unroll
-                    for (int u = 0; u < XD; ++u) cur[u] = nxt[u];
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
         }
@@ -728,7 +779,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     // the warp's smem slab; then row i of the warp's 32 rows is written by the
                     // 32 lanes as 128 contiguous bytes straight into its owner's window
                     const float s = num_kb > 0 ? p.scale : 0.f;
-                    float* slab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024) +
+                    float* slab = reinterpret_cast<float*>(xin + (XF ? STAGES * XIN_STAGE : 0)) +
                                   q * (32 * 33);
                     const int64_t row0 = row - lane;
                     const int64_t o0 = row0 / p.peer_rows;  // owner of the warp's first row

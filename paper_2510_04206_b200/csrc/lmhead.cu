@@ -154,7 +154,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     if constexpr (kPair) {
         auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB, XF>;
         constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM +
-                             (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0);
+                             (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0) +
+                             (XF ? GemmCfg<true, NSPLIT, KSUB>::STAGES * XIN_STAGE : 0);
         static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
         int64_t grid = AGENTRL_GEMM_FULLGRID
@@ -165,7 +166,7 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
         kern<<<(unsigned)grid, threads, smem, stream>>>(a, b, g);
     } else {
         auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN, XF>;
-        constexpr int smem = GemmCfg<false, 1>::SMEM;
+        constexpr int smem = GemmCfg<false, 1>::SMEM + (XF ? GemmCfg<false, 1>::STAGES * XIN_STAGE : 0);
         static std::atomic<uint64_t> attr_done{0};
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
         int grid = AGENTRL_GEMM_FULLGRID
@@ -537,10 +538,10 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ---------------------------------------------------------------------------- host
-// rows_cap: the row capacity of the per-row buffers, max_rows (<= 0: T) rounded up to GEMM_BM
+// rows_cap: the row capacity of the per-row buffers, max_rows (<= 0: T) rounded up to 256
 int64_t loss_rows_cap(int64_t T, int64_t max_rows) {
     const int64_t r = (max_rows > 0 && max_rows < T) ? max_rows : T;
-    return ceil_div(std::max<int64_t>(r, 1), GEMM_BM) * GEMM_BM;
+    return ceil_div(std::max<int64_t>(r, 1), 2 * GEMM_BM) * (2 * GEMM_BM);  // whole pair tiles
 }
 
 LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
@@ -851,6 +852,8 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
         if ((rc = comm_allreduce_f64(comm, o->loss, 1, stream))) return rc;
     }
     auto xf_args = [&](GemmArgs& g) {
+        g.P = P;  // the transform warps' A source (register path)
+        g.ldP = V;
         g.xf_scale = fscale;
         g.xf_row = xrow;
         g.xf_rows = rows_dev;

@@ -55,7 +55,7 @@ def time_adv(b, iters=20, graph=False):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
                 call()
-        times = []
+        times, phs = [], []
         for _ in range(iters):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -67,13 +67,16 @@ def time_adv(b, iters=20, graph=False):
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
+            phs.append(ag.debug_adv_phase_ns())
     times.sort()
     ms = times[len(times) // 2]
-    ph = ag.debug_adv_phase_ns()
-    # stamps relative to stamp 0 (small driver: [1] counts done, [2] block 0's group work,
-    # [3] after the grid barrier, [4] moments, [5] apply done; large driver: one per phase)
-    phases = [round((ph[i] - ph[0]) / 1e3, 1) if 0 <= ph[i] - ph[0] < 1e9 else None
-              for i in range(1, 8)]
+    # stamps relative to stamp 0, median over the timed calls (small driver: [1] trajectory
+    # table, [2] group advantages, [3] counts, [4] partial moments, [5] after the grid barrier,
+    # [6] moments, [7] apply done; large driver: one per phase)
+    phases = []
+    for i in range(1, 8):
+        v = sorted((ph[i] - ph[0]) / 1e3 for ph in phs if 0 <= ph[i] - ph[0] < 1e9)
+        phases.append(round(v[len(v) // 2], 1) if v else None)
     return ms, int(nm.item()), phases
 
 
