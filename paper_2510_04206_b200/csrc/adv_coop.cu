@@ -80,8 +80,8 @@ __device__ __forceinline__ void phase_mark(int i, unsigned blk = 0) {
 
 // dynamic shared memory layout (byte offsets), identical on host and device
 struct Lay {
-    uint32_t ring, bars, ostage, soff, srel, saux, skc, stask, cidx, cadv;
-    uint32_t sgid, stid, srew, sah, gflag, gtask, glist, sct;  // small driver
+    uint32_t ring, rwarp, bars, ostage, soff, srel, saux, skc, stask, cidx, cadv;
+    uint32_t sgid, stid, srew, sah, gflag, gtask, glist, gfirst, glast, sct;  // small driver
     uint32_t total;
 };
 __host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
@@ -90,13 +90,16 @@ __host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
     o += bytes;
     return r;
 }
+// bits_only: the large driver's apply launch, whose ring carries 64 B of stored lane bits per
+// chunk instead of 512 mask bytes (a smaller block, more of them per SM)
 __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, int n_traj,
-                                        int n_groups) {
+                                        int n_groups, bool bits_only = false) {
     Lay L;
     uint32_t o = 0;
     L.bars = lay_take(o, NWARPS * RING * 8);
     const uint32_t stream_begin = (o + 127u) & ~127u;
-    L.ring = lay_take(o, NWARPS * RING * WCHUNK);
+    L.rwarp = RING * (bits_only ? 64u : (uint32_t)WCHUNK);
+    L.ring = lay_take(o, NWARPS * L.rwarp);
     L.ostage = lay_take(o, NWARPS * WCHUNK * 4);
     L.cidx = lay_take(o, compact ? NWARPS * WCHUNK * 4 : 0);
     L.cadv = lay_take(o, compact ? NWARPS * WCHUNK * 4 : 0);
@@ -116,6 +119,8 @@ __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, i
     L.gflag = lay_take(o, 4u * ng);
     L.gtask = lay_take(o, 4u * ng);
     L.glist = lay_take(o, 4u * ng);
+    L.gfirst = lay_take(o, 4u * ng);  // first / last member of each group (scan bounds)
+    L.glast = lay_take(o, 4u * ng);
     L.sct = lay_take(o, small ? 4u * CT_CAP : 0u);  // per-chunk masked totals of the block
     (void)stream_begin;
     (void)stream_end;
@@ -136,6 +141,8 @@ struct AdvParams {
     int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
     int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
+    int32_t* chunk_gbase;          // [n_chunks] global compaction base (large driver)
+    int32_t g_stats;               // grid of the statistics launch (its per-block arrays)
     int32_t* blk_cnt;              // small driver: per-block trajectory counts at [g + block]
     uint16_t* lanebits;            // large driver: the 16-token mask bits of each lane of each
                                    // chunk, [n_chunks * 32] (phase A writes them; phase C and
@@ -270,7 +277,7 @@ struct WarpRing {
 __device__ __forceinline__ WarpRing ring_setup(const AdvParams& p, uint8_t* smem) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpRing r;
-    r.buf = smem + p.lay.ring + warp * RING * WCHUNK;
+    r.buf = smem + p.lay.ring + warp * p.lay.rwarp;
     r.bar = reinterpret_cast<uint64_t*>(smem + p.lay.bars) + warp * RING;
     r.par = 0u;
     r.on = (reinterpret_cast<uintptr_t>(p.mask) & 15) == 0;
@@ -308,7 +315,7 @@ __device__ __forceinline__ void lane_issue_bits(const AdvParams& p, WarpRing& r,
     const int lane = threadIdx.x & 31;
     if (valid && lane < 4)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         smem_u32(r.buf + slot * WCHUNK + lane * 16)),
+                         smem_u32(r.buf + slot * 64 + lane * 16)),
                      "l"(reinterpret_cast<const uint8_t*>(p.lanebits) + c * 64 + lane * 16)
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -581,7 +588,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             if (from_bits || (ADV_LDGSTS && r.on && !res)) lane_wait_oldest();  // this chunk's group
             if (from_bits) {
                 __syncwarp();  // lanes 0..3 copied the slot: their completed copies -> every lane
-                sbits = reinterpret_cast<const uint16_t*>(r.buf + slot * WCHUNK)[lane];
+                sbits = reinterpret_cast<const uint16_t*>(r.buf + slot * 64)[lane];
             } else if (r.on && c < n_full) {
                 if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
@@ -660,7 +667,8 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 if (t0 - lane * 16 < p.T) store_transposed(p, os, c, outv, vec_ok);
                 if (p.compact) {
                     __syncwarp();
-                    const int32_t wbase = blk_base + p.chunk_base[c];
+                    const int32_t wbase =
+                        small ? blk_base + p.chunk_base[c] : p.chunk_gbase[c];  // (large: global)
                     for (int32_t i = lane; i < wtotal; i += 32) {
                         p.idx[wbase + i] = s_cidx[i];
                         p.adv_c[wbase + i] = s_cadv[i];
@@ -704,7 +712,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
 // task_stats, N, G
 __device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w) {
     double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
-    const int64_t G = gridDim.x, B = blockIdx.x;
+    const int64_t G = p.g_stats > 0 ? p.g_stats : gridDim.x, B = blockIdx.x;
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
         const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
         const double mu = N > 0.0 ? S / N : 0.0;
@@ -813,7 +821,7 @@ __device__ __forceinline__ void group_adv(const AdvParams& p, int32_t K, const i
 //   every block, so every block holds identical mu_i, sigma_i) and applies Eq.1 to its chunks,
 //   which are still resident in its ring; then it publishes n_g of the trajectories it owns.
 struct SmallT {
-    int32_t *gid, *tid, *gflag, *gtask, *glist;
+    int32_t *gid, *tid, *gflag, *gtask, *glist, *gfirst, *glast;
     float* rew;
     double* ah;
 };
@@ -826,6 +834,8 @@ __device__ __forceinline__ SmallT small_t(const AdvParams& p, uint8_t* smem) {
     a.gflag = reinterpret_cast<int32_t*>(smem + p.lay.gflag);
     a.gtask = reinterpret_cast<int32_t*>(smem + p.lay.gtask);
     a.glist = reinterpret_cast<int32_t*>(smem + p.lay.glist);
+    a.gfirst = reinterpret_cast<int32_t*>(smem + p.lay.gfirst);
+    a.glast = reinterpret_cast<int32_t*>(smem + p.lay.glast);
     return a;
 }
 
@@ -875,7 +885,11 @@ __device__ void small_load_table(const AdvParams& p, uint8_t* smem, int32_t& st)
             }
         }
     }
-    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) a.gflag[j] = 0;
+    for (int32_t j = threadIdx.x; j < p.n_groups; j += COOP_THREADS) {
+        a.gflag[j] = 0;
+        a.gfirst[j] = INT_MAX;
+        a.glast[j] = -1;
+    }
     __syncthreads();
     for (int64_t g = t_lo + threadIdx.x; g < t_hi; g += COOP_THREADS)
         if (s_off[g + 1] < s_off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
@@ -897,10 +911,11 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
     double sum = 0.0;
     float fmx = -INFINITY, fmn = INFINITY;
     // a.gid holds the group id of members and -1 otherwise (invalid group or task id)
+    const int32_t lo = a.gfirst[j], hi = a.glast[j];  // (INT_MAX, -1) for an empty group
 #pragma unroll 4
-    for (int32_t i0 = 0; i0 < p.n_traj; i0 += 32) {
+    for (int32_t i0 = lo & ~31; i0 <= hi; i0 += 32) {
         const int32_t i = i0 + lane;
-        const bool hit = i < p.n_traj && a.gid[i] == j;
+        const bool hit = i <= hi && a.gid[i] == j;
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (hit) {
             const float r = a.rew[i];
@@ -951,7 +966,7 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
             ss = flat ? 0.0 : dl * dl;
         }
     } else {
-        for (int32_t i = lane; i < p.n_traj; i += 32)
+        for (int32_t i = lo + lane; i <= hi; i += 32)
             if (a.gid[i] == j) {
                 spans |= a.tid[i] != task0;
                 const double dl = (double)a.rew[i] - mean;
@@ -971,7 +986,7 @@ __device__ void small_group_warp(const AdvParams& p, const SmallT& a, int32_t j,
     if (few) {
         if (m >= 0) put(m);
     } else {
-        for (int32_t i = lane; i < p.n_traj; i += 32)
+        for (int32_t i = lo + lane; i <= hi; i += 32)
             if (a.gid[i] == j) put(i);
     }
     if (lane == 0) {
@@ -1015,9 +1030,18 @@ __device__ void small_groups(const AdvParams& p, uint8_t* smem, int64_t c_lo, in
     int32_t f = 0, l = -1;
     const bool any = small_traj_range(p, s_off, c_lo, c_hi, f, l);
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
+    // every group's first and last member (the bounds of its ballot scans: one or two 32-wide
+    // steps when a group's members are contiguous), then the flags
+    for (int32_t g = threadIdx.x; g < p.n_traj; g += COOP_THREADS) {
+        const int32_t j = a.gid[g];
+        if (j >= 0) {
+            atomicMin(&a.gfirst[j], g);
+            atomicMax(&a.glast[j], g);
+        }
+    }
     if (any)
         for (int32_t g = f + threadIdx.x; g <= l; g += COOP_THREADS)
-            if (small_member(p, a.gid[g], a.tid[g])) atomicOr(&a.gflag[a.gid[g]], 1);
+            if (a.gid[g] >= 0) atomicOr(&a.gflag[a.gid[g]], 1);
     for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) atomicOr(&a.gflag[j], 2);
     __shared__ int32_t s_nl, s_nz;
     if (threadIdx.x == 0) s_nl = s_nz = 0;
@@ -1281,52 +1305,87 @@ __device__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64
 }
 
 // ------------------------------------------------------------------ large driver
-__device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& r,
-                                   cg::grid_group& grid, int32_t* s_w, int32_t* s_pre) {
+// Three launches (round 2): k_adv_large_pop streams phase A at full occupancy; the cooperative
+// k_adv_large_stats runs the statistics phases B1..B4; k_adv_large_apply streams phase C with
+// its own (smaller) register and shared-memory budget.  With a communicator the all-reduce of
+// (N, S, Q) sits between the last two.
+
+// phase A as an ordinary kernel: per-lane mask bits and per-chunk masked counts (4 chunks per
+// warp iteration: 4 x 16 B loads in flight per lane), plus the per-trajectory work that needs
+// no counts -- K_j, validation, the chunk -> first-trajectory table.  grp_cnt / grp_fill are
+// zeroed by the host before the launch.
+constexpr int POP_THREADS = 256;
+constexpr int POP_UNROLL = 4;
+__global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p) {
+    phase_mark(0);
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * POP_THREADS + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * POP_THREADS) >> 5;
+    const int64_t n_full = p.T / WCHUNK;
+    const bool aligned = (reinterpret_cast<uintptr_t>(p.mask) & 15) == 0;
+    const bool any_traj = p.n_traj > 0;
+    for (int64_t c0 = gw * POP_UNROLL; c0 < p.n_chunks; c0 += nw * POP_UNROLL) {
+        uint4 mk[POP_UNROLL];
+#pragma unroll
+        for (int u = 0; u < POP_UNROLL; ++u) {
+            const int64_t c = c0 + u;
+            mk[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (c < n_full && aligned)
+                mk[u] = __ldcs(reinterpret_cast<const uint4*>(p.mask + c * WCHUNK) + lane);
+            else if (c < p.n_chunks)
+                mk[u] = mask_direct(p, c, lane);
+        }
+#pragma unroll
+        for (int u = 0; u < POP_UNROLL; ++u) {
+            const int64_t c = c0 + u;
+            if (c < p.n_chunks) {
+                const uint32_t lb = any_traj ? lane_mask(mk[u]).bits : 0u;
+                p.lanebits[c * 32 + lane] = (uint16_t)lb;  // 64 B per chunk
+                const int32_t tot = __reduce_add_sync(0xffffffffu, __popc(lb));
+                if (lane == 0) p.chunk[c] = tot;
+            }
+        }
+    }
+    const int64_t gtid = (int64_t)blockIdx.x * POP_THREADS + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * POP_THREADS;
+    int32_t st = 0;
+    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
+        const int64_t a = p.off[g], b = p.off[g + 1];
+        const int32_t j = p.group_id[g], i = p.task_id[g];
+        // chunks whose first token is in g
+        const int64_t lo = (a + WCHUNK - 1) / WCHUNK;
+        const int64_t hi = min((b + WCHUNK - 1) / WCHUNK, p.n_chunks);
+        for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
+        if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
+            st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+            continue;
+        }
+        atomicAdd(&p.grp_cnt[j], 1);
+        if (b < a) st |= AGENTRL_ST_BAD_OFFSETS;
+    }
+    if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
+    if (st) atomicOr(p.d_status, st);
+}
+
+__device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_group& grid,
+                                   int32_t* s_w, int32_t* s_pre) {
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t gtid = B * blockDim.x + threadIdx.x;
     const int64_t gstride = G * blockDim.x;
     int32_t st = 0;
-    phase_mark(0);
+    phase_mark(1);
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
-
-    // phase 0: zero scratch; chunk -> first-trajectory table
     if (gtid == 0) p.meta[3] = 0;  // local count of groups with members (G)
-    for (int64_t i = gtid; i < p.n_groups; i += gstride) {
-        p.grp_cnt[i] = 0;
-        p.grp_fill[i] = 0;
-    }
-    for (int64_t g = gtid; g < p.n_traj; g += gstride) {  // chunks whose first token is in g
-        const int64_t a = p.off[g], b = p.off[g + 1];
-        const int64_t lo = (a + WCHUNK - 1) / WCHUNK;
-        const int64_t hi = min((b + WCHUNK - 1) / WCHUNK, p.n_chunks);
-        for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
-    }
-    grid.sync();
-    phase_mark(1);
-
-    // phase A: counts (n_g via window flushes), per-chunk counts, K_j, validation
-    int32_t warp_total = 0;
-    auto validate = [&]() {  // K_j and validation, while the first mask copies are in flight
-        for (int64_t g = gtid; g < p.n_traj; g += gstride) {
-            const int32_t j = p.group_id[g], i = p.task_id[g];
-            if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
-                st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-                continue;
-            }
-            atomicAdd(&p.grp_cnt[j], 1);
-            if (p.off[g + 1] < p.off[g]) st |= AGENTRL_ST_BAD_OFFSETS;
-        }
-        if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
-    };
-    stream_phase<0>(p, smem, r, c_lo, c_hi, false, nullptr, 0, warp_total, false, validate);
-    chunk_bases(p, c_lo, c_hi, s_w);
+    chunk_bases(p, c_lo, c_hi, s_w);  // block-local bases of the popcount launch's chunk counts
     grid.sync();
     phase_mark(2);
 
-    // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers)
     block_prefix_smem(p.blk_chunk, G, s_pre, s_w);
+    // global compaction base of this block's chunks (the apply launch has its own grid)
+    for (int64_t c = c_lo + threadIdx.x; c < c_hi; c += COOP_THREADS)
+        p.chunk_gbase[c] = s_pre[B] + p.chunk_base[c];
+    // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers)
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int64_t a = p.off[g], e = p.off[g + 1];
         p.n_g[g] = e > a ? masked_before(p, s_pre, G, e) - masked_before(p, s_pre, G, a) : 0;
@@ -1574,13 +1633,15 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, WarpRing& 
     }
 }
 
+// phase C of the large driver (its own launch and grid): compaction positions come from the
+// global chunk bases, so the apply grid need not match the statistics grid
 __device__ __forceinline__ void large_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
                                             int32_t* s_pre, int32_t* s_w) {
     const int64_t G = gridDim.x, B = blockIdx.x;
     const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
     load_task_params(p, smem, s_pre, s_w);
     int32_t dummy = 0;
-    stream_phase<1>(p, smem, r, c_lo, c_hi, false, nullptr, s_pre[B], dummy);
+    stream_phase<1>(p, smem, r, c_lo, c_hi, false, nullptr, 0, dummy);
 }
 
 // static shared memory of the kernels (the rest is the dynamic Lay arena)
@@ -1589,30 +1650,22 @@ struct CoopStatic {
     int32_t s_pre[GMAX_BLOCKS + 1];
 };
 
-__global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_all(const AdvParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ CoopStatic ss;
-    cg::grid_group grid = cg::this_grid();
-    WarpRing r = ring_setup(p, smem);
-    large_stats_phases(p, smem, r, grid, ss.s_w, ss.s_pre);
-    grid.sync();
-    phase_mark(6);
-    large_apply(p, smem, r, ss.s_pre, ss.s_w);
-    grid.sync();
-    phase_mark(7);
-}
+#ifndef ADV_APPLY_MINB
+#define ADV_APPLY_MINB 3  // resident blocks per SM the apply launch's register budget is cut for
+#endif
 __global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
-    WarpRing r = ring_setup(p, smem);
-    large_stats_phases(p, smem, r, grid, ss.s_w, ss.s_pre);
+    large_stats_phases(p, smem, grid, ss.s_w, ss.s_pre);
 }
-__global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_apply(const AdvParams p) {
+__global__ void __launch_bounds__(COOP_THREADS, ADV_APPLY_MINB) k_adv_large_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
+    phase_mark(6);
     WarpRing r = ring_setup(p, smem);
     large_apply(p, smem, r, ss.s_pre, ss.s_w);
+    phase_mark(7);
 }
 
 // phase C of the second launch (after the all-reduce): everything reloaded, mu, sigma from the
@@ -1749,46 +1802,88 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     // AGENTRL_ADV_SMALL=0 (build): always the large driver (A/B and layout tests)
     const bool small = AGENTRL_ADV_SMALL && b->n_traj <= SMALL_TRAJ &&
                        b->n_groups <= SMALL_GROUPS && b->n_tasks <= 64;
-    p.lay = make_lay(b->n_tasks, compact, small, b->n_traj, b->n_groups);
-    const size_t smem = p.lay.total;
-    if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;
-    const void* k_all = small ? (const void*)k_adv_small_all : (const void*)k_adv_large_all;
-    const void* k_stats = small ? (const void*)k_adv_small_stats : (const void*)k_adv_large_stats;
-    const void* k_apply = small ? (const void*)k_adv_small_apply : (const void*)k_adv_large_apply;
-    if (smem > 48 * 1024) {  // the attribute is per device: set once on each
-        static std::atomic<uint64_t> done[6];
-        const void* ks[6] = {(const void*)k_adv_small_all,   (const void*)k_adv_small_stats,
-                             (const void*)k_adv_small_apply, (const void*)k_adv_large_all,
-                             (const void*)k_adv_large_stats, (const void*)k_adv_large_apply};
-        for (int i = 0; i < 6; ++i)
+    p.chunk_gbase = reinterpret_cast<int32_t*>(ws + w.chunk_gbase);
+    p.g_stats = 0;
+    {  // dynamic smem attribute, per device, set once for every kernel of this file
+        static std::atomic<uint64_t> done[5];
+        const void* ks[5] = {(const void*)k_adv_small_all, (const void*)k_adv_small_stats,
+                             (const void*)k_adv_small_apply, (const void*)k_adv_large_stats,
+                             (const void*)k_adv_large_apply};
+        for (int i = 0; i < 5; ++i)
             if (!func_attr_once(done[i], ks[i], 200 * 1024)) return AGENTRL_ERR_UNSUPPORTED;
     }
-    // small: one statistics block + one warp chunk per warp
-    const int64_t want = small ? std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1) + 1
-                               : std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
-                                                    ceil_div(p.n_traj, COOP_THREADS),
-                                                    ceil_div(p.n_groups, COOP_THREADS), 1});
     void* args[] = {&p};
-    if (!comm) {
-        const int grid = coop_grid(k_all, smem, want);
-        if (!grid || (small && grid < 2)) return AGENTRL_ERR_UNSUPPORTED;
-        ProfScope ps(KID_STATS, stream);
-        AG_CUDA(cudaLaunchCooperativeKernel(k_all, grid, COOP_THREADS, args, smem, stream));
+    if (small) {
+        p.lay = make_lay(b->n_tasks, compact, true, b->n_traj, b->n_groups);
+        const size_t smem = p.lay.total;
+        if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+        const int64_t want = std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1);  // a chunk per warp
+        if (!comm) {
+            const int grid = coop_grid((const void*)k_adv_small_all, smem, want);
+            if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+            p.g_stats = grid;
+            ProfScope ps(KID_STATS, stream);
+            AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_small_all, grid, COOP_THREADS,
+                                                args, smem, stream));
+            count_launch();
+            return AGENTRL_OK;
+        }
+        const int grid = std::min(coop_grid((const void*)k_adv_small_stats, smem, want),
+                                  coop_grid((const void*)k_adv_small_apply, smem, want));
+        if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+        p.g_stats = grid;
+        {
+            ProfScope ps(KID_STATS, stream);
+            AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_small_stats, grid, COOP_THREADS,
+                                                args, smem, stream));
+            count_launch();
+        }
+        int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks + 1, stream);
+        if (rc != AGENTRL_OK) return rc;
+        ProfScope ps(KID_APPLY, stream);
+        // same grid as the stats launch: phase C reuses its contiguous chunk partition
+        AG_CUDA(cudaLaunchKernel((const void*)k_adv_small_apply, grid, COOP_THREADS, args, smem,
+                                 stream));
         count_launch();
         return AGENTRL_OK;
     }
-    const int grid = std::min(coop_grid(k_stats, smem, want), coop_grid(k_apply, smem, want));
-    if (!grid || (small && grid < 2)) return AGENTRL_ERR_UNSUPPORTED;
+    // large driver: popcount stream -> cooperative statistics -> [C1] -> apply stream
     {
         ProfScope ps(KID_STATS, stream);
-        AG_CUDA(cudaLaunchCooperativeKernel(k_stats, grid, COOP_THREADS, args, smem, stream));
+        // K_j and the member-list fill counters start at zero (contiguous in the workspace)
+        AG_CUDA(cudaMemsetAsync(p.grp_cnt, 0,
+                                (size_t)(reinterpret_cast<uint8_t*>(p.grp_fill + p.n_groups + 1) -
+                                         reinterpret_cast<uint8_t*>(p.grp_cnt)),
+                                stream));
+        const int64_t pop_want = std::max<int64_t>(
+            ceil_div(p.n_chunks, (int64_t)POP_UNROLL * (POP_THREADS / 32)), 1);
+        const int pop_grid = (int)std::min<int64_t>(pop_want, (int64_t)num_sms() * 8);
+        k_adv_large_pop<<<pop_grid, POP_THREADS, 0, stream>>>(p);
+        count_launch();
+        AG_CUDA(cudaGetLastError());
+        const int64_t want = std::max<int64_t>({ceil_div(p.n_chunks, NWARPS),
+                                                ceil_div(p.n_traj, COOP_THREADS),
+                                                ceil_div(p.n_groups, COOP_THREADS), 1});
+        const int grid = coop_grid((const void*)k_adv_large_stats, 0, want);
+        if (!grid) return AGENTRL_ERR_UNSUPPORTED;
+        p.g_stats = grid;
+        AG_CUDA(cudaLaunchCooperativeKernel((const void*)k_adv_large_stats, grid, COOP_THREADS,
+                                            args, 0, stream));
         count_launch();
     }
-    int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks + 1, stream);
-    if (rc != AGENTRL_OK) return rc;
+    if (comm) {
+        int rc = comm_allreduce_f64(comm, p.stats, (size_t)3 * b->n_tasks + 1, stream);
+        if (rc != AGENTRL_OK) return rc;
+    }
     ProfScope ps(KID_APPLY, stream);
-    // same grid as the stats launch: phase C reuses its contiguous chunk partition
-    AG_CUDA(cudaLaunchKernel(k_apply, grid, COOP_THREADS, args, smem, stream));
+    p.lay = make_lay(b->n_tasks, compact, false, b->n_traj, b->n_groups, true);
+    const size_t smem = p.lay.total;
+    if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    const int grid_a = coop_grid((const void*)k_adv_large_apply, smem,
+                                 std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1));
+    if (!grid_a) return AGENTRL_ERR_UNSUPPORTED;
+    AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, COOP_THREADS, args, smem,
+                             stream));
     count_launch();
     return AGENTRL_OK;
 }

@@ -422,6 +422,7 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.grp_nsq = p.take(sizeof(double) * 3 * (size_t)(n_groups + 1));
     w.chunk_first = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.wchunk_base = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
+    w.chunk_gbase = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.blk_cnt = p.take(sizeof(int32_t) * ((size_t)n_traj + 2049));
     w.lanebits = p.take(sizeof(uint16_t) * ((size_t)n_chunks * 32 + 32));
     w.blk_chunk = p.take(sizeof(int32_t) * 2048);

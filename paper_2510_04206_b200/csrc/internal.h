@@ -37,6 +37,7 @@ struct AdvWs {
     size_t chunk_first;  // int32 [n_chunks] trajectory holding each chunk's first token
     size_t blk_chunk, blk_grp, blk_part;  // per cooperative block: int32, int32, double[3*n_tasks]
     size_t wchunk_base;                   // int32 [n_chunks] local compaction base per chunk
+    size_t chunk_gbase;                   // int32 [n_chunks] global compaction base (large)
     size_t blk_cnt;  // int32 [n_traj + 2049] per-block trajectory counts (small coop driver)
     size_t lanebits;  // uint16 [n_chunks * 32] per-lane mask bits (large coop driver)
     size_t stats;     // double [3*n_tasks]: N_i, S_i, Q_i (local, then global)
