@@ -1315,7 +1315,10 @@ __device__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64
 // no counts -- K_j, validation, the chunk -> first-trajectory table.  grp_cnt / grp_fill are
 // zeroed by the host before the launch.
 constexpr int POP_THREADS = 256;
-constexpr int POP_UNROLL = 4;
+#ifndef ADV_POP_UNROLL
+#define ADV_POP_UNROLL 4
+#endif
+constexpr int POP_UNROLL = ADV_POP_UNROLL;
 __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p) {
     phase_mark(0);
     const int lane = threadIdx.x & 31;
