@@ -167,7 +167,7 @@ typedef struct {
                                           rows with global target ids in [0, V*world).  Per
                                           row (max, sum-exp) over the shards and the owner's
                                           target logit are all-gathered between the forward
-                                          GEMM and the merge; loss, logp and loss_stats come
+                                          GEMM and the row statistics; loss, logp and loss_stats come
                                           out identical on every rank; grad_hidden is the
                                           full gradient (fp32 partials summed over the group
                                           inside the call); grad_W is this rank's complete
@@ -336,8 +336,9 @@ int agentrl_last_launch_count(void);
  * record an event pair around each of its kernels (on the stream it launches
  * on), up to n pairs.  agentrl_profile_stop synchronises those events and
  * writes, per kernel id, the summed milliseconds and the launch count.  Kernel
- * ids: 0 count, 1 stats, 2 apply, 3 compact, 4 gather, 5 fwd GEMM, 6 merge+G,
- * 7 loss reduce, 8 grad_W GEMM, 9 grad_hidden GEMM, 10 log-prob GEMM, 11 log-prob merge. */
+ * ids: 0 count, 1 stats, 2 apply, 3 compact, 4 gather, 5 fwd GEMM, 6 row statistics
+ * (loss terms and gradient scales), 7 loss reduce, 8 grad_W GEMM, 9 grad_hidden GEMM,
+ * 10 log-prob GEMM, 11 log-prob merge. */
 #define AGENTRL_NUM_KERNEL_IDS 12
 int agentrl_profile_start(int max_pairs);
 int agentrl_profile_stop(double* host_ms_sum, int* host_counts, int n_ids);

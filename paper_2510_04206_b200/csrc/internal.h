@@ -156,7 +156,7 @@ void count_launch(int n = 1);
 
 // per-kernel event timing (agentrl_profile_start/stop)
 enum KernelId {
-    KID_COUNT = 0, KID_STATS, KID_APPLY, KID_COMPACT, KID_GATHER, KID_FWD, KID_MERGE,
+    KID_COUNT = 0, KID_STATS, KID_APPLY, KID_COMPACT, KID_GATHER, KID_FWD, KID_ROWSTATS,
     KID_REDUCE, KID_GRADW, KID_GRADH, KID_LOGP_GEMM, KID_LOGP_MERGE, KID_N
 };
 void prof_mark(int kid, bool begin, cudaStream_t s);

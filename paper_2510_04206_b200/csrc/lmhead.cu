@@ -589,7 +589,7 @@ LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
 // ---------------------------------------------------------------------------- vocab-parallel
 // (W_head sharded by vocabulary rows over the group, every rank holding the
 // same token rows).  Per row, this rank's statistics over its columns: M_r = max z,
-// L'_r = sum exp(z - M_r) - 1 (the first max left out, as in the tile merge) -> its slot of the
+// L'_r = sum exp(z - M_r) - 1 (the first max left out, as across tiles) -> its slot of the
 // all-gather buffer (the other slots are zero; a sum all-reduce then fills every slot).
 __global__ void __launch_bounds__(RS_ROWS * RS_WARPS)
     k_vp_row_stats(const int64_t* __restrict__ rows_dev, int32_t n_tiles, int64_t ld,
@@ -830,7 +830,7 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
     }
     // ---- K6 row statistics: loss terms, gradient scales and target columns
     {
-        ProfScope ps(KID_MERGE, stream);
+        ProfScope ps(KID_ROWSTATS, stream);
         k_row_stats<<<(unsigned)std::max<int64_t>(ceil_div(rows_cap, RS_ROWS), 1),
                       RS_ROWS * RS_WARPS, 0, stream>>>(
             rows_dev, nglob_dev, w.n_tiles, rows_cap, part, zy, tgt_c, old_c, adv_c_dev, idx_dev,
