@@ -49,6 +49,8 @@ VARIANTS = {
     "coop0": ["-DAGENTRL_ADV_COOP=0"],                 # 3-kernel adv-norm path
     "advlarge": ["-DAGENTRL_ADV_SMALL=0"],             # large cooperative adv-norm driver only
     "kc64": ["-DADV_KC_CAP=64"],                       # small driver in 64-chunk windows
+    "ksplit3": ["-DAGENTRL_KSPLIT_FORCE=3"],           # grad_hidden split into 3 k-ranges
+    "ksplitauto": ["-DAGENTRL_KSPLIT_FORCE=0"],        # grad_hidden split chosen per shape
 }
 
 

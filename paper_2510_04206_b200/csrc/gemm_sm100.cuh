@@ -123,6 +123,11 @@ struct GemmArgs {
     float* const* peer_out;
     int64_t peer_rows;
     int32_t peer_rank;
+    // split-K (grad_hidden at small shard sizes): ksplit > 1 splits every tile's k-blocks into
+    // ksplit contiguous ranges (work unit = tile * ksplit + split); the EPI_GRADW epilogue then
+    // writes split s's fp32 partial at gw + s * gw_split
+    int32_t ksplit;
+    int64_t gw_split;
     // dynamic tile scheduler: zeroed int counter (tiles claimed in global order), or null for
     // the static persistent schedule (tile = unit + i * units)
     int* tile_counter;
@@ -325,6 +330,15 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     const int64_t num_n = (p.N + Cfg::TILE_N - 1) / Cfg::TILE_N;
     const int64_t num_tiles = num_m * num_n;
     const int64_t num_kb = (K + Cfg::BK - 1) / Cfg::BK;
+    // work units: tile * S + split (S = 1: the tiles themselves)
+    const int64_t S = p.ksplit > 1 ? p.ksplit : 1;
+    const int64_t num_work = num_tiles * S;
+    auto split_unit = [&](int64_t w, int64_t& tt, int64_t& kb_b, int64_t& kb_e, int64_t& sp) {
+        tt = w / S;
+        sp = w - tt * S;
+        kb_b = sp * num_kb / S;
+        kb_e = (sp + 1) * num_kb / S;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -398,16 +412,18 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
                     }
                 }
-                if (tile >= num_tiles) {
+                if (tile >= num_work) {
                     if (throttle) prog_store(p.prog + unit, INT64_MAX);
                     break;
                 }
+                int64_t tt, kb_b, kb_e, sp;
+                split_unit(tile, tt, kb_b, kb_e, sp);
                 int64_t m_blk, n_blk;
-                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                tile_coords(tt, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int32_t m0 = (int32_t)(r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM);
                 const int32_t n0 = (int32_t)(n_blk * Cfg::TILE_N + rank * Cfg::B_ROWS);
                 const int64_t wave_pos = (tile / n_units) * num_kb;
-                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                for (int64_t kb = kb_b; kb < kb_e; ++kb) {
                     if (throttle && kb % p.prog_every == 0) {
                         prog_store(p.prog + unit, wave_pos + kb);
                         prog_throttle(p.prog, n_units, wave_pos + kb, p.prog_lead, prog_cached_min,
@@ -455,11 +471,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     tile = tile_q[slot];
                     mbar_arrive(&tq_empty[slot]);
                 }
-                if (tile >= num_tiles) break;
+                if (tile >= num_work) break;
+                int64_t tt, kb_b, kb_e, sp;
+                split_unit(tile, tt, kb_b, kb_e, sp);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_BN);
-                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                for (int64_t kb = kb_b; kb < kb_e; ++kb) {
                     mbar_wait(XF ? &ready[stage] : &full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sA + stage * Cfg::A_STAGE);
@@ -472,7 +490,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const uint64_t adesc =
                             A_MN ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
                                  : umma_desc_sw128(a_base + ka, 16, 1024);
-                        const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                        const uint32_t accum = (kb > kb_b || k > 0) ? 1u : 0u;
 #pragma unroll
                         for (int h = 0; h < NSPLIT; ++h) {
                             const uint32_t bh = b_base + h * Cfg::B_HALF;
@@ -522,11 +540,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
                     }
                 }
-                if (tile >= num_tiles) break;
+                if (tile >= num_work) break;
+                int64_t tt, kb_b, kb_e, sp;
+                split_unit(tile, tt, kb_b, kb_e, sp);
                 int64_t m_blk, n_blk;
-                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                tile_coords(tt, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int64_t m0 = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM;
-                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                for (int64_t kb = kb_b; kb < kb_e; ++kb) {
                     float fv[4];
                     int2 yv[2];
                     // loads first (rows past the valid range are never used: zero lines)
@@ -595,9 +615,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
                     }
                 }
-                if (tile >= num_tiles) break;
+                if (tile >= num_work) break;
+                int64_t tt, kb_b, kb_e, sp;
+                split_unit(tile, tt, kb_b, kb_e, sp);
                 int64_t m_blk, n_blk;
-                tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+                tile_coords(tt, num_m, num_n, p.group_m, m_blk, n_blk);
                 const int64_t m0 = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM;
                 // A_MN = false (grad_hidden): line t = token row m0 + t, K = vocabulary; the
                 // row's (target column, G value) is fixed for the tile.
@@ -608,7 +630,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 if (!A_MN && tok < rows) yr = __ldg(p.xf_row + tok);
                 const int64_t vcol0 = m0 + 64 * (t >> 6);
                 const bool vcol_ok = !A_MN || vcol0 < M;
-                for (int64_t kb = 0; kb < num_kb; ++kb) {
+                for (int64_t kb = kb_b; kb < kb_e; ++kb) {
                     mbar_wait_sleep(&xin_full[stage], phase);  // the stage's scales
                     mbar_wait_sleep(&full[stage], phase);      // the stage's P~ tile
                     const uint32_t xs = xin_base + stage * XIN_STAGE;
@@ -670,9 +692,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     else mbar_arrive_cluster(mapa_shared(smem_u32(&tq_empty[slot]), 0));
                 }
             }
-            if (tile >= num_tiles) break;
+            if (tile >= num_work) break;
+            int64_t tt, kb_b, kb_e, sp;
+            split_unit(tile, tt, kb_b, kb_e, sp);
+            const bool have_k = kb_e > kb_b;  // (else a zero tile: empty K range)
             int64_t m_blk, n_blk;
-            tile_coords(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+            tile_coords(tt, num_m, num_n, p.group_m, m_blk, n_blk);
             const int64_t row = r0 + m_blk * Cfg::TILE_M + rank * GEMM_BM + q * 32 + lane;
             const bool row_ok = row < M;
             mbar_wait_sleep(&tfull[acc], acc_phase);
@@ -778,14 +803,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     // EPI_GRADW fused with the reduce-scatter: each 32 x 32 chunk goes through
                     // the warp's smem slab; then row i of the warp's 32 rows is written by the
                     // 32 lanes as 128 contiguous bytes straight into its owner's window
-                    const float s = num_kb > 0 ? p.scale : 0.f;
+                    const float s = have_k ? p.scale : 0.f;
                     float* slab = reinterpret_cast<float*>(xin + (XF ? STAGES * XIN_STAGE : 0)) +
                                   q * (32 * 33);
                     const int64_t row0 = row - lane;
                     const int64_t o0 = row0 / p.peer_rows;  // owner of the warp's first row
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
-                        if (num_kb > 0) {
+                        if (have_k) {
                             tmem_ld_32x32b_x32(taddr + c * 32, r);
                             tmem_ld_wait();
                         } else {
@@ -814,7 +839,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         __syncwarp();
                     }
                 } else {  // EPI_GRADW
-                    const float s = num_kb > 0 ? p.scale : 0.f;
+                    const float s = have_k ? p.scale : 0.f;
                     const int64_t rr = row_ok ? row : 0;
                     float* orow;
                     if (p.peer_out) {  // straight into the owner's window (NVLink peer memory)
@@ -823,11 +848,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                ((int64_t)p.peer_rank * p.peer_rows + (rr - o * p.peer_rows)) * p.ldo +
                                col0;
                     } else {
-                        orow = p.gw + rr * p.ldo + col0;
+                        orow = p.gw + sp * p.gw_split + rr * p.ldo + col0;
                     }
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
-                        if (num_kb > 0) {
+                        if (have_k) {
                             tmem_ld_32x32b_x32(taddr + c * 32, r);
                             tmem_ld_wait();
                         } else {

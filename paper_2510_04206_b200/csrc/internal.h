@@ -79,10 +79,12 @@ struct LossWs {
     size_t rows_eff;                        // int64 [2]: min(T_eff, rows_cap)
     size_t sched;                           // int [32] GEMM tile counters (dynamic scheduler)
     size_t prog;                            // int64 [3][PROG_UNITS] GEMM progress
+    int32_t ksplit;                         // grad_hidden split-K factor (1: none)
+    size_t splitk;                          // float [ksplit][rows_cap, d] partials (ksplit > 1)
     size_t vpstat;                          // vocab-parallel: float2 [world][rows_cap] (M_r, L'_r)
     size_t vp_gh;                           // vocab-parallel: float [rows_cap, d] grad_h partial
     int32_t vp_world;                       // 0 = not planned for the vocab-parallel head
-    int64_t rows_cap;                       // row capacity (max_rows rounded up to 128)
+    int64_t rows_cap;                       // row capacity (max_rows rounded up to 256)
     size_t total;
     int32_t n_tiles;
 };

@@ -129,6 +129,14 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 #ifndef AGENTRL_THROTTLE_LEAD_FWD
 #define AGENTRL_THROTTLE_LEAD_FWD 0
 #endif
+// grad_hidden split-K: n > 0 forces n (1: never split, the default); 0 = chosen from the
+// workspace's row bound (tile-wave tails at small shard sizes).  Measured on the power-capped
+// part (profiles/r02_ksplit_ab.txt): the split grad_hidden is 5-7% faster at the 2/4/8-GPU
+// shard sizes, but the step is 0.4-1.7% slower -- the partials' round trip and the busier tail
+// cost power that the other GEMMs' clock pays for -- so it is off by default.
+#ifndef AGENTRL_KSPLIT_FORCE
+#define AGENTRL_KSPLIT_FORCE 1
+#endif
 // SMs left free for an NCCL C3 kernel while grad_hidden overlaps it (multi-rank only)
 #ifndef AGENTRL_COMM_SMS
 #define AGENTRL_COMM_SMS 16
@@ -544,6 +552,32 @@ int64_t loss_rows_cap(int64_t T, int64_t max_rows) {
     return ceil_div(std::max<int64_t>(r, 1), 2 * GEMM_BM) * (2 * GEMM_BM);  // whole pair tiles
 }
 
+// grad_hidden has ceil(rows/256) x ceil(d/512) equal-length tiles for the CTA pairs; when that
+// is a few waves with a partial last one, splitting every tile's k-blocks into S ranges (fp32
+// partials summed afterwards) fills the idle pairs.  Cost in tile-waves: ceil(tiles S / pairs)
+// / S, plus the partials' HBM round trip relative to the GEMM (8 S rows d bytes at ~6 TB/s
+// against 2 rows V d FLOP at ~1.3 PF/s: S * 1733 / V of the GEMM).  Needs the row bound.
+static int32_t choose_ksplit(int64_t max_rows, int32_t d, int32_t V) {
+    if (AGENTRL_KSPLIT_FORCE > 0) return AGENTRL_KSPLIT_FORCE;
+    const int pairs = num_sms() / 2;
+    if (max_rows <= 0 || pairs <= 0) return 1;
+    const int64_t tiles = ceil_div(max_rows, 2 * GEMM_BM) * ceil_div(d, 2 * GEMM_BN);
+    const double waves = (double)tiles / pairs;
+    // (small problems of less than one wave stay whole: their tiles already run in parallel)
+    if (!kWideN || waves < 1.0 || waves >= 16.0) return 1;
+    auto cost = [&](int S) {
+        return std::ceil((double)tiles * S / pairs) / S + (S > 1 ? waves * S * 1733.0 / V : 0.0);
+    };
+    int32_t best = 1;
+    double bc = cost(1);
+    for (int S = 2; S <= 4; ++S)
+        if (cost(S) < 0.98 * bc) {
+            bc = cost(S);
+            best = S;
+        }
+    return best;
+}
+
 LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
                  int32_t vp_world) {
     WsPlan p;
@@ -576,6 +610,8 @@ LossWs plan_loss(int64_t T, int64_t max_rows, int32_t d, int32_t V, size_t base,
     w.rows_eff = p.take(sizeof(int64_t) * 2);
     w.sched = p.take(sizeof(int) * 32);
     w.prog = p.take(sizeof(int64_t) * 3 * PROG_UNITS);
+    w.ksplit = vp_world > 0 ? 1 : choose_ksplit(max_rows > 0 && max_rows < T ? max_rows : 0, d, V);
+    w.splitk = w.ksplit > 1 ? p.take(sizeof(float) * (size_t)w.ksplit * rows_cap * d, 1024) : 0;
     w.vp_world = vp_world;
     w.vpstat = w.vp_gh = 0;
     if (vp_world > 0) {
@@ -629,6 +665,32 @@ __global__ void __launch_bounds__(256)
         uint2* dst = reinterpret_cast<uint2*>(gh + (int64_t)idx[p] * d);
         for (int c = lane; c < d / 4; c += 32) {
             const float4 v = src[c];
+            dst[c] = make_uint2(pack_bf162(v.x, v.y), pack_bf162(v.z, v.w));
+        }
+    }
+}
+
+// split-K grad_hidden: grad_hidden[idx[p]] = bf16(sum over splits s, in order, of partial s)
+__global__ void __launch_bounds__(256)
+    k_splitk_scatter(const int64_t* __restrict__ rows_dev, int32_t d, int32_t S, int64_t stride,
+                     const int32_t* __restrict__ idx, const float* __restrict__ parts,
+                     __nv_bfloat16* __restrict__ gh) {
+    const int64_t rows = *rows_dev;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < rows;
+         p += nw) {
+        const float4* src = reinterpret_cast<const float4*>(parts + p * d);
+        uint2* dst = reinterpret_cast<uint2*>(gh + (int64_t)idx[p] * d);
+        for (int c = lane; c < d / 4; c += 32) {
+            float4 v = src[c];
+            for (int s = 1; s < S; ++s) {
+                const float4 u = src[s * (stride / 4) + c];
+                v.x += u.x;
+                v.y += u.y;
+                v.z += u.z;
+                v.w += u.w;
+            }
             dst[c] = make_uint2(pack_bf162(v.x, v.y), pack_bf162(v.z, v.w));
         }
     }
@@ -924,6 +986,24 @@ int launch_policy_loss(const agentrl_loss_args* a, const agentrl_loss_out* o, ui
             if ((r = comm_allreduce_f32(comm, gh32, (size_t)rows_cap * d, s))) return r;
             k_vp_scatter<<<num_sms() * 4, 256, 0, s>>>(rows_dev, d, idx_dev, gh32,
                                                        reinterpret_cast<__nv_bfloat16*>(o->grad_hidden));
+            count_launch();
+            AG_CUDA(cudaGetLastError());
+            return AGENTRL_OK;
+        }
+        if (w.ksplit > 1 && kWideN) {
+            // split-K: fp32 partials of the ksplit k-ranges (EPI_GRADW rows = compacted rows),
+            // then one pass sums them in split order and scatters bf16 rows to idx
+            float* parts = reinterpret_cast<float*>(ws + w.splitk);
+            g.gw = parts;
+            g.gw_split = rows_cap * (int64_t)d;
+            g.ksplit = w.ksplit;
+            g.prog = nullptr;  // (the throttle assumes every unit walks the same k-blocks)
+            r = launch_gemm<EPI_GRADW, false, true, 2, 1, true>(mP_K, mW_MN, g, tiles * w.ksplit, s,
+                                                                rsv);
+            if (r) return r;
+            k_splitk_scatter<<<num_sms() * 4, 256, 0, s>>>(
+                rows_dev, d, w.ksplit, rows_cap * (int64_t)d, idx_dev, parts,
+                reinterpret_cast<__nv_bfloat16*>(o->grad_hidden));
             count_launch();
             AG_CUDA(cudaGetLastError());
             return AGENTRL_OK;
