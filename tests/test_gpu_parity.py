@@ -357,10 +357,25 @@ def _full_size_case(ag, cfg_name, n_spot=24, shard_of=None):
     gref = r["grad_hidden"][ok]
     err = np.abs(gh[rows][ok] - gref).max() / max(np.abs(gref).max(), 1e-30)
     assert err <= 2e-2, err
-    # properties that hold at any size:
+    # every masked row's log-prob and the loss against an INDEPENDENT full-size computation:
+    # plain fp32 torch (matmul + logsumexp on the same bf16 inputs, chunked; no TF32) for the
+    # log-probs and the oracle's advantages -- the loss is not recomputed from the GPU's logp
     m = b["loss_mask"] != 0
-    A = step.adv_tok.cpu().numpy()[m].astype(np.float64)
-    rho = np.exp(logp[m].astype(np.float64) - old[m])
+    assert not torch.backends.cuda.matmul.allow_tf32
+    Wt = bf16_dev(Wb).float()
+    hdev = bf16_dev(hb)
+    lp_ref = np.empty(len(an["idx"]), dtype=np.float64)
+    with torch.no_grad():
+        for s0 in range(0, len(an["idx"]), 4096):
+            ii = torch.from_numpy(an["idx"][s0:s0 + 4096].astype(np.int64)).cuda()
+            z = hdev[ii].float() @ Wt.T
+            yy = torch.from_numpy(y[an["idx"][s0:s0 + 4096]].astype(np.int64)).cuda()
+            lp = z.gather(1, yy[:, None])[:, 0] - torch.logsumexp(z, dim=1)
+            lp_ref[s0:s0 + len(ii)] = lp.double().cpu().numpy()
+    del Wt
+    assert np.abs(logp[an["idx"]] - lp_ref).max() <= 1e-3
+    A = an["adv_tok"][an["idx"]].astype(np.float32).astype(np.float64)
+    rho = np.exp(lp_ref - old[an["idx"]])
     term = np.minimum(rho * A, np.clip(rho, 0.8, 1.2) * A)
     L = -term.sum() / an["n_mask"]
     assert abs(step.loss.item() - L) <= 1e-3 * max(abs(L), np.abs(term).sum() / an["n_mask"])
