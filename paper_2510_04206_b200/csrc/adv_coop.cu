@@ -347,6 +347,16 @@ __device__ __forceinline__ void store_transposed(const AdvParams& p, float* os, 
         *reinterpret_cast<float4*>(os + lane * 16 + 4 * (q ^ ((lane >> 1) & 3))) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     __syncwarp();
+    if (vec_ok && (c + 1) * WCHUNK <= p.T) {  // a full chunk: no per-vector bounds checks
+        float4* dst = reinterpret_cast<float4*>(p.adv_tok + c * WCHUNK) + lane;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int lp = (i * 128 + lane * 4) >> 4, q = lane & 3;
+            dst[i * 32] = *reinterpret_cast<const float4*>(os + lp * 16 + 4 * (q ^ ((lp >> 1) & 3)));
+        }
+        __syncwarp();
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int tok = i * 128 + lane * 4;
@@ -458,6 +468,21 @@ __device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, 
     const int lane = threadIdx.x & 31;
     const int32_t tr0 = tc + lane * 16;
     const uint32_t v0 = (uint32_t)s_val[kc];
+    {  // the common case first: at most one trajectory start inside the chunk
+        const int32_t kb = kc + 1 + lane;
+        const int32_t b = kb < w.nbt ? w.s_rel[kb] : INT_MAX;
+        const uint32_t av = kb < w.nbt ? (uint32_t)s_val[kb] : 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, b < tc + WCHUNK);
+        if (bal <= 1u) {  // bal is 0 or 1: boundaries are sorted, so only lane 0 can hold one
+            const int32_t rel = bal ? __shfl_sync(0xffffffffu, b, 0) - tr0 : 16;
+            const uint32_t v = __shfl_sync(0xffffffffu, av, 0);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                out[i] = (i >= rel ? v : v0) &
+                         __byte_perm(m.byte[i >> 2], 0u, (i & 3) * 0x1111u);
+            return;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) out[i] = v0;
     for (int32_t jb = 0;; jb += 32) {
