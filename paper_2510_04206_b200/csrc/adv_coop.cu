@@ -477,9 +477,7 @@ __device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, 
             const int32_t rel = bal ? __shfl_sync(0xffffffffu, b, 0) - tr0 : 16;
             const uint32_t v = __shfl_sync(0xffffffffu, av, 0);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-                out[i] = (i >= rel ? v : v0) &
-                         __byte_perm(m.byte[i >> 2], 0u, (i & 3) * 0x1111u);
+            for (int i = 0; i < 16; ++i) out[i] = (m.bits & (1u << i)) ? (i >= rel ? v : v0) : 0u;
             return;
         }
     }
@@ -499,7 +497,7 @@ __device__ __forceinline__ void apply_chunk_bits(const LaneMask& m, int32_t tc, 
         if (nb < 32) break;
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) out[i] &= __byte_perm(m.byte[i >> 2], 0u, (i & 3) * 0x1111u);
+    for (int i = 0; i < 16; ++i) out[i] = (m.bits & (1u << i)) ? out[i] : 0u;
 }
 
 // resident (PH 1): the warp's chunks are still in its ring slots from phase A (same kernel,
@@ -1352,8 +1350,9 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
     const int64_t n_full = p.T / WCHUNK;
     const bool aligned = (reinterpret_cast<uintptr_t>(p.mask) & 15) == 0;
     const bool any_traj = p.n_traj > 0;
-    for (int64_t c0 = gw * POP_UNROLL; c0 < p.n_chunks; c0 += nw * POP_UNROLL) {
-        uint4 mk[POP_UNROLL];
+    // software-pipelined: the loads of the warp's next POP_UNROLL chunks are in flight while
+    // the current ones are reduced
+    auto load = [&](uint4 (&mk)[POP_UNROLL], int64_t c0) {
 #pragma unroll
         for (int u = 0; u < POP_UNROLL; ++u) {
             const int64_t c = c0 + u;
@@ -1363,16 +1362,25 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
             else if (c < p.n_chunks)
                 mk[u] = mask_direct(p, c, lane);
         }
+    };
+    const int64_t step = nw * POP_UNROLL;
+    uint4 cur[POP_UNROLL], nxt[POP_UNROLL];
+    int64_t c0 = gw * POP_UNROLL;
+    if (c0 < p.n_chunks) load(cur, c0);
+    for (; c0 < p.n_chunks; c0 += step) {
+        if (c0 + step < p.n_chunks) load(nxt, c0 + step);
 #pragma unroll
         for (int u = 0; u < POP_UNROLL; ++u) {
             const int64_t c = c0 + u;
             if (c < p.n_chunks) {
-                const uint32_t lb = any_traj ? lane_mask(mk[u]).bits : 0u;
+                const uint32_t lb = any_traj ? lane_mask(cur[u]).bits : 0u;
                 p.lanebits[c * 32 + lane] = (uint16_t)lb;  // 64 B per chunk
                 const int32_t tot = __reduce_add_sync(0xffffffffu, __popc(lb));
                 if (lane == 0) p.chunk[c] = tot;
             }
         }
+#pragma unroll
+        for (int u = 0; u < POP_UNROLL; ++u) cur[u] = nxt[u];
     }
     const int64_t gtid = (int64_t)blockIdx.x * POP_THREADS + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * POP_THREADS;
