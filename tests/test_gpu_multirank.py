@@ -161,3 +161,50 @@ def test_two_ranks_one_gpu_match_global_oracle(tmp_path, cfg_name, mode, p2p):
     for k in range(2):
         gh[r[k]["tok"]] = r[k]["gh"]
     assert max_abs_rel(gh, ref["grad_hidden"]) <= 2e-2
+
+
+def test_nccl_world1_large_driver_matches_no_comm():
+    """The large adv-norm driver (more than 2,048 trajectories: popcount launch, cooperative
+    statistics, apply launch) with a real NCCL communicator at world size 1 -- the all-reduce of
+    (N, S, Q, G) between the statistics and the apply launches -- gives bitwise the result of
+    the call without a communicator, and both match the fp64 oracle."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle
+    import synth
+    import paper_2510_04206_b200 as ag
+    from gpu_util import adv_close, batch_dev
+
+    b = synth.make_sweep_structure(1 << 20)  # 2,621 trajectories: the large driver
+    assert len(b["task_id"]) > 2048
+    T, n_traj = int(b["T"]), len(b["task_id"])
+    bd = batch_dev(b)
+
+    def run(comm):
+        ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
+                                                                        b["n_tasks"]))
+        adv = torch.full((T,), float("nan"), dtype=torch.float32, device="cuda")
+        ts = torch.zeros(b["n_tasks"], 3, dtype=torch.float64, device="cuda")
+        nm = torch.zeros(1, dtype=torch.int64, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rc = ag.agentrl_task_adv_norm(ag.make_batch(bd), 1e-6, adv, ts, nm, ws,
+                                      comm.handle if comm else None, st)
+        assert rc == 0, ag.status_string(rc)
+        torch.cuda.synchronize()
+        return adv.cpu().numpy(), ts.cpu().numpy(), int(nm.item()), int(st.item())
+
+    a0, t0, n0, s0 = run(None)
+    comm = ag.Comm(1, 0, ag.Comm.unique_id())
+    a1, t1, n1, s1 = run(comm)
+    comm.destroy()
+    np.testing.assert_array_equal(a0, a1)
+    np.testing.assert_array_equal(t0, t1)
+    assert n0 == n1 and s0 == s1
+    ref = oracle.task_adv_norm(b)
+    assert n0 == ref["n_mask"]
+    np.testing.assert_array_equal(t0[:, 0], ref["task_stats"][:, 0])
+    np.testing.assert_allclose(t0[:, 1:], ref["task_stats"][:, 1:], rtol=1e-9, atol=1e-12)
+    assert adv_close(a0, ref["adv_tok"])
