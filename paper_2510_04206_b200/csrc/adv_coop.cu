@@ -528,7 +528,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
     // large driver, phase C: the lane bits phase A stored replace the mask (64 B per chunk
     // through the same ring instead of 512 B)
-    const bool from_bits = ADV_LDGSTS && PH == 1 && !small;
+    const bool from_bits = PH == 1 && !small;  // (always per-lane cp.async: 64 B slots)
     const bool res = resident && n_mine <= RING && !from_bits;  // warp-uniform
     if (from_bits) {
         for (int s = 0; s < RING; ++s) {
