@@ -51,6 +51,7 @@ VARIANTS = {
     "kc64": ["-DADV_KC_CAP=64"],                       # small driver in 64-chunk windows
     "ksplit3": ["-DAGENTRL_KSPLIT_FORCE=3"],           # grad_hidden split into 3 k-ranges
     "ksplitauto": ["-DAGENTRL_KSPLIT_FORCE=0"],        # grad_hidden split chosen per shape
+    "pf8": ["-DAGENTRL_PREFETCH_KB=8"],                # backward L2 prefetch 8 k-blocks ahead
 }
 
 

@@ -56,6 +56,13 @@ constexpr int XF_LOADER_WARP = XF_WARP0 + 4;
 // the 128 rows' scales f (512 B); grad_W: the 64 tokens' scales (256 B) and (target column,
 // G value) pairs (512 B)
 constexpr int XIN_STAGE = 1024;
+// backward (XF) GEMMs: the producer also prefetches the operand boxes of k-block kb + this many
+// into L2 when it loads kb (0 = off, the default).  Measured at glm9b (profiles/r02_ab_pf.txt):
+// 8 or 16 k-blocks ahead made grad_W 29% and grad_hidden 14% slower -- the extra L2 requests of
+// 74 pairs prefetching overlapping boxes cost more than the latency they hide
+#ifndef AGENTRL_PREFETCH_KB
+#define AGENTRL_PREFETCH_KB 0
+#endif
 
 // KSUB: 64-wide K atoms per pipeline stage (K-major operands only).  KSUB = 2 stages 128 K
 // per k-block: 8 MMAs per barrier round trip instead of 4, for the short-K forward GEMM whose
@@ -246,6 +253,31 @@ __device__ __forceinline__ void load_stage(const CUtensorMap& tmA, const CUtenso
         } else {
 #pragma unroll
             for (int i = 0; i < Cfg::B_ROWS / 64; ++i) ld(tmB, bd + i * 8192, nh + i * 64, k0, pol_b);
+        }
+    }
+}
+
+// L2 prefetch of the boxes load_stage would load for k-block k0 (same coordinates)
+template <bool A_MN, bool B_MN, bool PAIR, int NSPLIT, int KSUB>
+__device__ __forceinline__ void prefetch_stage(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                               int32_t m0, int32_t n0, int32_t k0) {
+    using Cfg = GemmCfg<PAIR, NSPLIT, KSUB>;
+    if constexpr (!A_MN) {
+#pragma unroll
+        for (int a = 0; a < KSUB; ++a) tma_prefetch_l2_2d(&tmA, k0 + a * GEMM_BK, m0);
+    } else {
+#pragma unroll
+        for (int i = 0; i < GEMM_BM / 64; ++i) tma_prefetch_l2_2d(&tmA, m0 + i * 64, k0);
+    }
+#pragma unroll
+    for (int h = 0; h < NSPLIT; ++h) {
+        const int32_t nh = n0 + h * GEMM_BN;
+        if constexpr (!B_MN) {
+#pragma unroll
+            for (int a = 0; a < KSUB; ++a) tma_prefetch_l2_2d(&tmB, k0 + a * GEMM_BK, nh);
+        } else {
+#pragma unroll
+            for (int i = 0; i < Cfg::B_ROWS / 64; ++i) tma_prefetch_l2_2d(&tmB, nh + i * 64, k0);
         }
     }
 }
@@ -445,6 +477,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     load_stage<A_MN, B_MN, PAIR, NSPLIT, KSUB, XF>(
                         tmA, tmB, &full[stage], fb, sA + stage * Cfg::A_STAGE,
                         sB + stage * Cfg::B_STAGE, m0, n0, (int32_t)(kb * Cfg::BK), pol_a, pol_b);
+                    if constexpr (XF && AGENTRL_PREFETCH_KB > 0) {
+                        if (kb + AGENTRL_PREFETCH_KB < kb_e)
+                            prefetch_stage<A_MN, B_MN, PAIR, NSPLIT, KSUB>(
+                                tmA, tmB, m0, n0, (int32_t)((kb + AGENTRL_PREFETCH_KB) * Cfg::BK));
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;

@@ -28,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 VARIANTS = ["pair0", "static", "narrow", "fullgrid", "raster", "ksub1", "lead0", "pair0_lead2",
             "coop0", "ksplit3"]
 # switches that only change the schedule / staging / stream placement, never the arithmetic
-SCHEDULE_ONLY = ["lead0", "lockstep", "ksub1", "static", "fullgrid", "raster", "narrow"]
+SCHEDULE_ONLY = ["lead0", "lockstep", "ksub1", "static", "fullgrid", "raster", "narrow", "pf8"]
 
 
 def _cuda():
