@@ -90,15 +90,13 @@ __host__ __device__ inline uint32_t lay_take(uint32_t& o, uint32_t bytes) {
     o += bytes;
     return r;
 }
-// bits_only: the large driver's apply launch, whose ring carries 64 B of stored lane bits per
-// chunk instead of 512 mask bytes (a smaller block, more of them per SM)
 __host__ __device__ inline Lay make_lay(int n_tasks, bool compact, bool small, int n_traj,
-                                        int n_groups, bool bits_only = false) {
+                                        int n_groups) {
     Lay L;
     uint32_t o = 0;
     L.bars = lay_take(o, NWARPS * RING * 8);
     const uint32_t stream_begin = (o + 127u) & ~127u;
-    L.rwarp = RING * (bits_only ? 64u : (uint32_t)WCHUNK);
+    L.rwarp = RING * (uint32_t)WCHUNK;
     L.ring = lay_take(o, NWARPS * L.rwarp);
     L.ostage = lay_take(o, NWARPS * WCHUNK * 4);
     L.cidx = lay_take(o, compact ? NWARPS * WCHUNK * 4 : 0);
@@ -139,6 +137,9 @@ struct AdvParams {
     const uint8_t* mask;
     double eps_std;
     int32_t *n_g, *chunk, *grp_cnt, *grp_start, *grp_fill, *members, *grp_task, *chunk_first;
+    uint32_t *grp_lo, *grp_hi;  // large driver: ~(first member) and last member + 1 of each
+                                // group (atomicMax from zero)
+    int32_t* grp_flag;          // [0] != 0: some group is not one run of <= REG_K trajectories
     int32_t *blk_chunk, *blk_grp;  // per-block masked / member totals
     int32_t* chunk_base;           // [n_chunks] compaction base of each chunk within its block
     int32_t* chunk_gbase;          // [n_chunks] global compaction base (large driver)
@@ -308,18 +309,6 @@ __device__ __forceinline__ void lane_issue(const AdvParams& p, WarpRing& r, int 
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
-// bits variant (phase C of the large driver): lanes 0..3 copy the chunk's 64 bytes of stored
-// lane bits (one commit group per chunk on every lane, as above)
-__device__ __forceinline__ void lane_issue_bits(const AdvParams& p, WarpRing& r, int slot,
-                                                int64_t c, bool valid) {
-    const int lane = threadIdx.x & 31;
-    if (valid && lane < 4)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         smem_u32(r.buf + slot * 64 + lane * 16)),
-                     "l"(reinterpret_cast<const uint8_t*>(p.lanebits) + c * 64 + lane * 16)
-                     : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
 __device__ __forceinline__ void lane_wait_oldest() {
     asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
 }
@@ -409,19 +398,6 @@ __device__ __forceinline__ LaneMask lane_mask(const uint4& mk) {
         const uint32_t hb = ((((w[q] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w[q]) & 0x80808080u) >> 7;
         m.byte[q] = hb * 0xFFu;
         m.bits |= ((hb * 0x01020408u) >> 24) << (4 * q);
-    }
-    return m;
-}
-
-// the LaneMask of 16 stored mask bits (phase C of the large driver)
-__device__ __forceinline__ LaneMask lane_mask_bits(uint32_t bits) {
-    LaneMask m;
-    m.bits = bits & 0xffffu;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t x = (bits >> (4 * q)) & 0xfu;
-        const uint32_t y = (x | (x << 7) | (x << 14) | (x << 21)) & 0x01010101u;
-        m.byte[q] = y * 0xFFu;
     }
     return m;
 }
@@ -526,16 +502,8 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     // chunk indices fit in 32 bits (T < 2^31): keep the per-chunk bookkeeping 32-bit
     const int32_t n_full = (int32_t)(p.T / WCHUNK);  // chunks with all 512 tokens < T
     const int64_t n_mine = c_hi - c_lo > warp ? (c_hi - c_lo - warp + NWARPS - 1) / NWARPS : 0;
-    // large driver, phase C: the lane bits phase A stored replace the mask (64 B per chunk
-    // through the same ring instead of 512 B)
-    const bool from_bits = PH == 1 && !small;  // (always per-lane cp.async: 64 B slots)
-    const bool res = resident && n_mine <= RING && !from_bits;  // warp-uniform
-    if (from_bits) {
-        for (int s = 0; s < RING; ++s) {
-            const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
-            lane_issue_bits(p, r, s, c, c < c_hi);
-        }
-    } else if (ADV_LDGSTS && r.on && !res) {
+    const bool res = resident && n_mine <= RING;  // warp-uniform
+    if (ADV_LDGSTS && r.on && !res) {
         for (int s = 0; s < RING; ++s) {
             const int32_t c = (int32_t)c_lo + warp + s * NWARPS;
             lane_issue(p, r, s, c, c < c_hi && c < n_full);
@@ -547,13 +515,10 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         }
     }
     pre();
-    // large driver, phase A: a pure popcount stream (per-lane and per-chunk masked counts);
-    // the per-trajectory counts come later from prefix differences at the trajectory bounds
-    const bool pop = PH == 0 && !small;
     // staging plan: the block's whole range if its trajectories fit, else 64-chunk windows
     int64_t wlen = max(c_hi - c_lo, (int64_t)1);
-    if (wlen > KC_CAP && !pop) wlen = WIN_CHUNKS;
-    if (!small && !pop && any_traj && c_lo < c_hi) {
+    if (wlen > KC_CAP) wlen = WIN_CHUNKS;
+    if (!small && any_traj && c_lo < c_hi) {
         const int32_t f = p.chunk_first[c_lo];
         const int32_t l = c_hi < p.n_chunks ? p.chunk_first[c_hi] : p.n_traj - 1;
         if (l - f + 1 > WIN_TRAJ) wlen = WIN_CHUNKS;
@@ -568,7 +533,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         const int64_t w1 = min(c_hi, w0 + wlen);
         // ---- stage the window's trajectories (block-wide)
         Window w{0, 0, w0 * WCHUNK, s_rel, false};
-        if (any_traj && !pop) {
+        if (any_traj) {
             int32_t f, l;
             if (small) {
                 f = smem_find_in(s_offall, 0, p.n_traj, w0 * WCHUNK);
@@ -607,12 +572,8 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         for (int32_t c = (int32_t)w0 + warp; c < w1; c += NWARPS, ++kseq) {
             const int slot = kseq & (RING - 1);
             uint4 mk = make_uint4(0u, 0u, 0u, 0u);
-            uint32_t sbits = 0u;
-            if (from_bits || (ADV_LDGSTS && r.on && !res)) lane_wait_oldest();  // this chunk's group
-            if (from_bits) {
-                __syncwarp();  // lanes 0..3 copied the slot: their completed copies -> every lane
-                sbits = reinterpret_cast<const uint16_t*>(r.buf + slot * 64)[lane];
-            } else if (r.on && c < n_full) {
+            if (ADV_LDGSTS && r.on && !res) lane_wait_oldest();  // this chunk's group
+            if (r.on && c < n_full) {
                 if (!res && !ADV_LDGSTS) {
                     mbar_wait(&r.bar[slot], (r.par >> slot) & 1u);
                     r.par ^= 1u << slot;
@@ -624,14 +585,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
             const int64_t t0 = (int64_t)c * WCHUNK + lane * 16;
             const int32_t tc = (int32_t)((int64_t)c * WCHUNK - w.base);  // window-relative
             const int32_t kc = (any_traj && w.staged) ? s_kc[c - (int32_t)w0] : 0;
-            if (pop) {
-                const uint32_t lb = any_traj ? lane_mask(mk).bits : 0u;
-                const int32_t pc = __popc(lb);
-                p.lanebits[(int64_t)c * 32 + lane] = (uint16_t)lb;  // 64 B per chunk
-                const int32_t tot = __reduce_add_sync(0xffffffffu, pc);
-                if (lane == 0) p.chunk[c] = tot;
-                warp_total += tot;
-            } else if (PH == 0) {  // small driver: every window is staged
+            if (PH == 0) {  // small driver: every window is staged
                 int32_t tot = 0;
                 if (any_traj) (void)count_chunk_bits(lane_mask(mk), tc, kc, w, s_aux, tot);
                 if (lane == 0) {
@@ -641,7 +595,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 }
                 warp_total += tot;
             } else {
-                const LaneMask lm = from_bits ? lane_mask_bits(sbits) : lane_mask(mk);
+                const LaneMask lm = lane_mask(mk);
                 const int32_t mine = any_traj ? __popc(lm.bits) : 0;
                 int32_t wtotal = 0, pos = 0;
                 if (p.compact) {  // positions of the lane's masked tokens in the chunk
@@ -700,10 +654,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
                 }
             }
             __syncwarp();
-            if (from_bits) {
-                const int32_t c2 = c + RING * NWARPS;
-                lane_issue_bits(p, r, slot, c2, c2 < c_hi);
-            } else if (ADV_LDGSTS && r.on && !res) {
+            if (ADV_LDGSTS && r.on && !res) {
                 const int32_t c2 = c + RING * NWARPS;
                 lane_issue(p, r, slot, c2, c2 < c_hi && c2 < n_full);
             } else if (lane == 0 && r.on && !res) {
@@ -713,7 +664,7 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
         }
         __syncthreads();
         // ---- window epilogue (counting): per-trajectory counts out
-        if (PH == 0 && !pop && w.staged) {
+        if (PH == 0 && w.staged) {
             for (int32_t k = threadIdx.x; k < w.nbt; k += COOP_THREADS) {
                 if (small) {
                     // disjoint slot g + block; a trajectory that crosses from this block's
@@ -731,37 +682,44 @@ __device__ void stream_phase(const AdvParams& p, uint8_t* smem, WarpRing& r, int
     }
 }
 
-// per-task (mu, max(sigma, eps)) into smem from the (global) stats; block 0 publishes
-// task_stats, N, G
-__device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w) {
-    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
-    const int64_t G = p.g_stats > 0 ? p.g_stats : gridDim.x, B = blockIdx.x;
+// per-task (mu, max(sigma, eps)) into smem from the (global) stats (readings R1, R2);
+// block 0 also publishes task_stats
+__device__ void task_params_smem(const AdvParams& p, double2* s_task) {
     for (int32_t i = threadIdx.x; i < p.n_tasks; i += blockDim.x) {
         const double N = p.stats[3 * i], S = p.stats[3 * i + 1], Q = p.stats[3 * i + 2];
         const double mu = N > 0.0 ? S / N : 0.0;
         const double sd = N > 0.0 ? sqrt(fmax(Q / N - mu * mu, 0.0)) : 0.0;
         s_task[i] = make_double2(mu, sd > p.eps_std ? sd : p.eps_std);
-        if (B == 0 && p.task_stats_out) {
+        if (blockIdx.x == 0 && p.task_stats_out) {
             p.task_stats_out[3 * i] = N;
             p.task_stats_out[3 * i + 1] = mu;
             p.task_stats_out[3 * i + 2] = sd;
         }
     }
-    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // also orders the s_task writes
-    if (B == 0 && threadIdx.x < 32) {
-        double nsum = 0.0;
-        for (int32_t i = threadIdx.x; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
+}
+// one warp (block 0): meta = (local masked rows, global N, global G), n_mask_global, status
+__device__ void publish_meta(const AdvParams& p, int32_t local_rows) {
+    double nsum = 0.0;
+    for (int32_t i = threadIdx.x & 31; i < p.n_tasks; i += 32) nsum += p.stats[3 * i];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
-        if (threadIdx.x == 0) {
-            const int64_t n = (int64_t)nsum;
-            p.meta[0] = s_pre[G];  // local masked rows
-            p.meta[1] = n;         // global N
-            p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global G (groups)
-            if (p.n_mask_global_out) *p.n_mask_global_out = n;
-            if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
-        }
+    for (int o = 16; o > 0; o >>= 1) nsum += __shfl_down_sync(0xffffffffu, nsum, o);
+    if ((threadIdx.x & 31) == 0) {
+        const int64_t n = (int64_t)nsum;
+        p.meta[0] = local_rows;  // local masked rows
+        p.meta[1] = n;           // global N
+        p.meta[2] = (int64_t)p.stats[3 * p.n_tasks];  // global G (groups)
+        if (p.n_mask_global_out) *p.n_mask_global_out = n;
+        if (n == 0) atomicOr(p.d_status, AGENTRL_ST_NO_TOKENS);
     }
+}
+// the above for the small driver's apply, plus every block's prefix of the stats blocks'
+// masked totals (its compaction base)
+__device__ void load_task_params(const AdvParams& p, uint8_t* smem, int32_t* s_pre, int32_t* s_w) {
+    double2* s_task = reinterpret_cast<double2*>(smem + p.lay.stask);
+    const int64_t G = p.g_stats > 0 ? p.g_stats : gridDim.x;
+    task_params_smem(p, s_task);
+    block_prefix_smem(p.blk_chunk, G, s_pre, s_w);  // also orders the s_task writes
+    if (blockIdx.x == 0 && threadIdx.x < 32) publish_meta(p, s_pre[G]);
 }
 
 // block-local exclusive scan of the block's chunk counts -> chunk_base; block total
@@ -1305,7 +1263,7 @@ __device__ __forceinline__ void small_ng_store(const AdvParams& p, const NgRegs&
 
 // masked tokens before position t (large driver, after phase A): block prefix + the chunk's
 // local base + the popcount of the chunk's lane bits below t
-__device__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64_t G, int64_t t) {
+__device__ __forceinline__ int32_t masked_before(const AdvParams& p, const int32_t* s_pre, int64_t G, int64_t t) {
     if (t <= 0) return 0;
     if (t >= p.T) return s_pre[G];
     const int64_t c = t / WCHUNK;
@@ -1385,6 +1343,7 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
     const int64_t gtid = (int64_t)blockIdx.x * POP_THREADS + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * POP_THREADS;
     int32_t st = 0;
+    bool bad_member = false;
     for (int64_t g = gtid; g < p.n_traj; g += gstride) {
         const int64_t a = p.off[g], b = p.off[g + 1];
         const int32_t j = p.group_id[g], i = p.task_id[g];
@@ -1394,13 +1353,74 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
         for (int64_t c = max(lo, (int64_t)0); c < hi; ++c) p.chunk_first[c] = (int32_t)g;
         if (j < 0 || j >= p.n_groups || i < 0 || i >= p.n_tasks) {
             st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+            bad_member = true;
             continue;
         }
         atomicAdd(&p.grp_cnt[j], 1);
+        atomicMax(&p.grp_lo[j], ~(uint32_t)g);  // ~min(g)
+        atomicMax(&p.grp_hi[j], (uint32_t)g + 1u);
         if (b < a) st |= AGENTRL_ST_BAD_OFFSETS;
     }
+    if (bad_member) atomicOr(p.grp_flag, 1);  // a trajectory in no group: the general path
     if (gtid == 0 && (p.off[0] != 0 || p.off[p.n_traj] != p.T)) st |= AGENTRL_ST_BAD_OFFSETS;
     if (st) atomicOr(p.d_status, st);
+}
+
+// GRPO group advantage (R1, R2, R14) of a group of K <= REG_K members m[0..K), sorted
+// by index: the arithmetic and order of group_adv on register copies of the members' reward,
+// task and count (their loads issued together: no dependent global round trips)
+__device__ __forceinline__ void group_regs(const AdvParams& p, int32_t K, const int32_t (&m)[REG_K],
+                                           double& N, double& S, double& Q, int32_t& task0,
+                                           int32_t& st, unsigned long long& nz) {
+    float rr[REG_K];
+    int32_t tt[REG_K], nn[REG_K];
+#pragma unroll
+    for (int a = 0; a < REG_K; ++a) {
+        rr[a] = a < K ? p.rewards[m[a]] : 0.f;
+        tt[a] = a < K ? p.task_id[m[a]] : 0;
+        nn[a] = a < K ? p.n_g[m[a]] : 0;
+    }
+    // same arithmetic and order as group_adv, on the register copies
+    N = S = Q = 0.0;
+    task0 = -1;
+    if (K > 0) {
+        if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
+        task0 = tt[0];
+        double sum = 0.0, rmax = rr[0], rmin = rmax;
+#pragma unroll
+        for (int a = 0; a < REG_K; ++a)
+            if (a < K) {
+                const double rv = rr[a];
+                if (tt[a] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
+                sum += rv;
+                rmax = fmax(rmax, rv);
+                rmin = fmin(rmin, rv);
+            }
+        const bool flat = rmax == rmin;
+        const double mean = sum / (double)K;
+        double ss = 0.0;
+        if (!flat) {
+#pragma unroll
+            for (int a = 0; a < REG_K; ++a)
+                if (a < K) {
+                    const double dlt = (double)rr[a] - mean;
+                    ss += dlt * dlt;
+                }
+        }
+        const double sd = sqrt(ss / (double)K);
+        const double den = sd > p.eps_std ? sd : p.eps_std;
+#pragma unroll
+        for (int a = 0; a < REG_K; ++a)
+            if (a < K) {
+                const double ah = flat ? 0.0 : ((double)rr[a] - mean) / den;
+                p.adv_hat[m[a]] = ah;
+                const double n = (double)nn[a];
+                N += n;
+                S += n * ah;
+                Q += n * ah * ah;
+            }
+        nz += 1;  // a group present in the batch (GRPO group mean)
+    }
 }
 
 __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_group& grid,
@@ -1414,18 +1434,59 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
     const int64_t j_lo = part_lo(p.n_groups, B, G), j_hi = part_lo(p.n_groups, B + 1, G);
     if (gtid == 0) p.meta[3] = 0;  // local count of groups with members (G)
     chunk_bases(p, c_lo, c_hi, s_w);  // block-local bases of the popcount launch's chunk counts
+    // contiguous groups (the usual rollout layout: a prompt's K samples stored together): when
+    // every group is one run of at most REG_K trajectories (K_j == last - first + 1) and every
+    // trajectory is in a group, the members of group j are first_j .. first_j + K_j - 1 in index
+    // order, so the member-list phases B1/B2 and their two grid barriers are skipped
+    {
+        bool bad = false;
+        for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
+            const int32_t K = p.grp_cnt[j];
+            if (K > 0) bad |= K > REG_K || p.grp_hi[j] - ~p.grp_lo[j] != (uint32_t)K;
+        }
+        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(p.grp_flag, 1);
+    }
     grid.sync();
     phase_mark(2);
+    const bool contig = __ldcg(p.grp_flag) == 0;  // grid-uniform
 
     block_prefix_smem(p.blk_chunk, G, s_pre, s_w);
     // global compaction base of this block's chunks (the apply launch has its own grid)
     for (int64_t c = c_lo + threadIdx.x; c < c_hi; c += COOP_THREADS)
         p.chunk_gbase[c] = s_pre[B] + p.chunk_base[c];
-    // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers)
-    for (int64_t g = gtid; g < p.n_traj; g += gstride) {
-        const int64_t a = p.off[g], e = p.off[g + 1];
-        p.n_g[g] = e > a ? masked_before(p, s_pre, G, e) - masked_before(p, s_pre, G, a) : 0;
+    // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers), one
+    // masked_before per trajectory bound: warp iteration i covers bounds 31i .. 31i + 31 (lane
+    // L: bound 31i + L) and writes n_g of trajectories 31i .. 31i + 30 from the next lane's
+    // bound.  NG_U iterations' loads are issued together (this phase is latency-bound).
+    {
+        constexpr int NG_U = 4;
+        const int lane = threadIdx.x & 31;
+        const int64_t wg = gtid >> 5, nwg = gstride >> 5;
+        const int64_t n_it = ((int64_t)p.n_traj + 30) / 31;
+        for (int64_t i0 = wg; i0 < n_it; i0 += NG_U * nwg) {
+            int64_t t[NG_U];
+            int32_t mb[NG_U];
+#pragma unroll
+            for (int u = 0; u < NG_U; ++u) {
+                const int64_t i = i0 + u * nwg, k = i * 31 + lane;
+                t[u] = (i < n_it && k <= p.n_traj) ? p.off[k] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < NG_U; ++u) mb[u] = t[u] >= 0 ? masked_before(p, s_pre, G, t[u]) : 0;
+#pragma unroll
+            for (int u = 0; u < NG_U; ++u) {
+                const int64_t i = i0 + u * nwg, g = i * 31 + lane;
+                const int32_t mn = __shfl_down_sync(0xffffffffu, mb[u], 1);
+                const int64_t tn = __shfl_down_sync(0xffffffffu, t[u], 1);
+                if (lane < 31 && i < n_it && g < p.n_traj) p.n_g[g] = tn > t[u] ? mn - mb[u] : 0;
+            }
+        }
     }
+    if (contig) {
+        grid.sync();  // every n_g written
+        phase_mark(3);
+        phase_mark(4);
+    } else {
     // phase B1: local exclusive scan of K_j over this block's groups; block total
     {
         const int64_t n = j_hi - j_lo;
@@ -1478,6 +1539,7 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
     }
     grid.sync();
     phase_mark(4);
+    }  // !contig
 
     // phase B3: this block's groups, then the block's per-task partial (N, S, Q) in a fixed
     // order.  Groups of <= REG_K members: ids sorted by a register sorting network and their
@@ -1490,10 +1552,16 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
     double my_N = 0.0, my_S = 0.0, my_Q = 0.0;
     for (int64_t j = j_lo + threadIdx.x; j < j_hi; j += COOP_THREADS) {
         const int32_t K = p.grp_cnt[j];
-        int32_t* mbg = p.members + s_pre[B] + p.grp_start[j];
+        int32_t* mbg = contig ? nullptr : p.members + s_pre[B] + p.grp_start[j];
         double N, S, Q;
         int32_t task0;
-        if (K <= REG_K) {
+        if (contig) {  // members first_j .. first_j + K - 1: already in index order
+            const int32_t f = (int32_t)~p.grp_lo[j];
+            int32_t m[REG_K];
+#pragma unroll
+            for (int a = 0; a < REG_K; ++a) m[a] = a < K ? f + a : INT_MAX;
+            group_regs(p, K, m, N, S, Q, task0, st, nz);
+        } else if (K <= REG_K) {
             int32_t m[REG_K];
 #pragma unroll
             for (int a = 0; a < REG_K; ++a) m[a] = a < K ? mbg[a] : INT_MAX;
@@ -1513,55 +1581,7 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
                             }
                         }
                     }
-            float rr[REG_K];
-            int32_t tt[REG_K], nn[REG_K];
-#pragma unroll
-            for (int a = 0; a < REG_K; ++a) {
-                rr[a] = a < K ? p.rewards[m[a]] : 0.f;
-                tt[a] = a < K ? p.task_id[m[a]] : 0;
-                nn[a] = a < K ? p.n_g[m[a]] : 0;
-            }
-            // same arithmetic and order as group_adv, on the register copies
-            N = S = Q = 0.0;
-            task0 = -1;
-            if (K > 0) {
-                if (K == 1) st |= AGENTRL_ST_GROUP_TOO_SMALL;
-                task0 = tt[0];
-                double sum = 0.0, rmax = rr[0], rmin = rmax;
-#pragma unroll
-                for (int a = 0; a < REG_K; ++a)
-                    if (a < K) {
-                        const double rv = rr[a];
-                        if (tt[a] != task0) st |= AGENTRL_ST_GROUP_SPANS_TASKS;
-                        sum += rv;
-                        rmax = fmax(rmax, rv);
-                        rmin = fmin(rmin, rv);
-                    }
-                const bool flat = rmax == rmin;
-                const double mean = sum / (double)K;
-                double ss = 0.0;
-                if (!flat) {
-#pragma unroll
-                    for (int a = 0; a < REG_K; ++a)
-                        if (a < K) {
-                            const double dlt = (double)rr[a] - mean;
-                            ss += dlt * dlt;
-                        }
-                }
-                const double sd = sqrt(ss / (double)K);
-                const double den = sd > p.eps_std ? sd : p.eps_std;
-#pragma unroll
-                for (int a = 0; a < REG_K; ++a)
-                    if (a < K) {
-                        const double ah = flat ? 0.0 : ((double)rr[a] - mean) / den;
-                        p.adv_hat[m[a]] = ah;
-                        const double n = (double)nn[a];
-                        N += n;
-                        S += n * ah;
-                        Q += n * ah * ah;
-                    }
-                nz += 1;  // a group present in the batch (GRPO group mean)
-            }
+            group_regs(p, K, m, N, S, Q, task0, st, nz);
         } else {
             for (int a = 1; a < K; ++a) {
                 const int32_t x = mbg[a];
@@ -1638,20 +1658,30 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
         }
     }
     if (st) atomicOr(p.d_status, st);
-    grid.sync();
-    phase_mark(5);
 
-    // phase B4 (block 0): per-task moments over the token set = fixed-order sum
-    // of the block partials (warp w handles tasks w, w+8, ...; lanes stride over blocks)
-    if (B == 0) {
+    // phase B4 by the LAST block to finish B3 (a ticket instead of a grid barrier: every block
+    // fences its partials before taking its ticket, so the last one sees them all): per-task
+    // moments over the token set = fixed-order sum of the block partials (warp w
+    // handles tasks w, w+8, ...; lanes stride over blocks; the same bits whichever block it is).
+    // The ticket grp_fill[n_groups] is zeroed with the member-list counters before the launch.
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&p.grp_fill[p.n_groups], 1) == (int)G - 1;
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
+        phase_mark(5, (unsigned)B);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         for (int32_t i = wid; i < p.n_tasks; i += NWARPS) {
             double N = 0.0, S = 0.0, Q = 0.0;
             for (int64_t b = lane; b < G; b += 32) {
                 const double* bp = p.blk_part + 3 * (b * p.n_tasks + i);
-                N += bp[0];
-                S += bp[1];
-                Q += bp[2];
+                N += __ldcg(bp);
+                S += __ldcg(bp + 1);
+                Q += __ldcg(bp + 2);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -1665,19 +1695,176 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
                 p.stats[3 * i + 2] = Q;
             }
         }
-        if (threadIdx.x == 0) p.stats[3 * p.n_tasks] = (double)p.meta[3];  // G (local)
+        if (threadIdx.x == 0)  // G (local)
+            p.stats[3 * p.n_tasks] = (double)__ldcg(reinterpret_cast<const long long*>(p.meta + 3));
     }
 }
 
-// phase C of the large driver (its own launch and grid): compaction positions come from the
-// global chunk bases, so the apply grid need not match the statistics grid
-__device__ __forceinline__ void large_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
-                                            int32_t* s_pre, int32_t* s_w) {
-    const int64_t G = gridDim.x, B = blockIdx.x;
-    const int64_t c_lo = part_lo(p.n_chunks, B, G), c_hi = part_lo(p.n_chunks, B + 1, G);
-    load_task_params(p, smem, s_pre, s_w);
-    int32_t dummy = 0;
-    stream_phase<1>(p, smem, r, c_lo, c_hi, false, nullptr, 0, dummy);
+// phase C of the large driver (round 2, lean apply; its own launch and one-wave grid).
+// One warp per 512-token chunk, chunks strided over every warp of the grid (equal work per
+// warp: no block-range tail).  Lane L writes the float4s of tokens q*128 + 4L .. +3, q = 0..3,
+// so every store instruction writes 512 contiguous bytes without a shared-memory transpose.
+// The chunk's trajectories: the chunk -> first-trajectory table gives g0 (holding the chunk's
+// first token); lane L loads the start of trajectory g0 + 1 + L and a ballot finds those that
+// start inside the chunk (sorted: a prefix of the lanes).  Each lane computes Eq.1
+// for the trajectory it loaded and shuffles broadcast it.  The mask comes from phase A's
+// stored lane bits (64 B per chunk instead of 512 mask bytes).  Compaction positions (fused
+// step): the statistics launch's global chunk base + the popcount of the chunk's bits below
+// the token.
+constexpr int APPLY_THREADS = 256;
+static_assert(APPLY_THREADS == COOP_THREADS && POP_THREADS == COOP_THREADS,
+              "coop_grid sizes the one-wave grids with COOP_THREADS");
+#ifndef ADV_APPLY_MINB
+#define ADV_APPLY_MINB 4  // resident blocks per SM the apply launch's register budget is cut for
+#endif
+#ifndef ADV_APPLY_PF
+#define ADV_APPLY_PF 0  // 1: a chunk's loads are issued one iteration ahead (software pipeline)
+#endif
+// the loads one chunk needs (g0: the trajectory holding its first token; lane L: trajectory
+// g0 + 1 + L's start, A^ and task)
+struct ApplyLd {
+    int32_t g0, gbase, ti0, ti;
+    uint32_t bits;
+    double ah0, ah;
+    int64_t so;
+};
+__device__ __forceinline__ ApplyLd apply_load(const AdvParams& p, int64_t c, int32_t g_first,
+                                              bool any) {
+    const int lane = threadIdx.x & 31;
+    const int32_t last = p.n_traj - 1;
+    ApplyLd L;
+    L.g0 = min(max(g_first, 0), max(last, 0));
+    L.bits = any ? (uint32_t)p.lanebits[c * 32 + lane] : 0u;
+    L.gbase = p.compact ? p.chunk_gbase[c] : 0;
+    L.ah0 = L.ah = 0.0;
+    L.ti0 = L.ti = -1;
+    L.so = LLONG_MAX;
+    if (any) {
+        L.ah0 = p.adv_hat[L.g0];  // uniform over the warp
+        L.ti0 = p.task_id[L.g0];
+        const int64_t gs = (int64_t)L.g0 + 1 + lane;
+        if (gs <= last) {
+            L.so = p.off[gs];
+            L.ah = p.adv_hat[gs];
+            L.ti = p.task_id[gs];
+        }
+    }
+    return L;
+}
+// Eq.1 value of trajectory g as float bits (the arithmetic of adv_tilde)
+__device__ __forceinline__ uint32_t adv_tilde_u(const double2* s_task, int32_t n_tasks, double ah,
+                                                int32_t ti) {
+    return (ti >= 0 && ti < n_tasks) ? __float_as_uint((float)((ah - s_task[ti].x) / s_task[ti].y))
+                                     : 0u;
+}
+
+__global__ void __launch_bounds__(APPLY_THREADS, ADV_APPLY_MINB) k_adv_large_apply(const AdvParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    double2* s_task = reinterpret_cast<double2*>(smem);
+    phase_mark(6);
+    task_params_smem(p, s_task);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {  // local masked rows = sum of the stats blocks'
+        int32_t s = 0;                          // totals (exact integers, any order)
+        for (int32_t b = threadIdx.x; b < p.g_stats; b += 32) s += p.blk_chunk[b];
+        s = __reduce_add_sync(0xffffffffu, s);
+        publish_meta(p, s);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    constexpr int WPB = APPLY_THREADS / 32;
+    const int64_t nw = (int64_t)gridDim.x * WPB;
+    int64_t c = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
+    const bool any = p.n_traj > 0;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(p.adv_tok) & 15) == 0;
+    const int32_t last = p.n_traj - 1;
+    int32_t g_next = (any && c < p.n_chunks) ? p.chunk_first[c] : 0;
+#if ADV_APPLY_PF
+    ApplyLd nxt;
+    if (c < p.n_chunks) {
+        nxt = apply_load(p, c, g_next, any);
+        g_next = (any && c + nw < p.n_chunks) ? p.chunk_first[c + nw] : 0;
+    }
+#endif
+    for (; c < p.n_chunks; c += nw) {
+#if ADV_APPLY_PF
+        const ApplyLd L = nxt;
+        if (c + nw < p.n_chunks) nxt = apply_load(p, c + nw, g_next, any);
+        if (any && c + 2 * nw < p.n_chunks) g_next = p.chunk_first[c + 2 * nw];
+#else
+        const ApplyLd L = apply_load(p, c, g_next, any);
+        if (any && c + nw < p.n_chunks) g_next = p.chunk_first[c + nw];  // one chunk ahead
+#endif
+        const int64_t cb = c * WCHUNK;
+        const uint32_t bits = L.bits;
+        const int32_t gbase = L.gbase;
+        uint32_t o[16];
+        if (any) {
+            int64_t gs = (int64_t)L.g0 + 1 + lane, so = L.so;
+            double ah = L.ah;
+            int32_t ti = L.ti;
+            const uint32_t v0 = adv_tilde_u(s_task, p.n_tasks, L.ah0, L.ti0);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = v0;
+            for (int32_t jb = 0;; jb += 32) {
+                const bool in = so < cb + WCHUNK;
+                const int32_t rel = in ? (int32_t)(so - cb) : WCHUNK;
+                const uint32_t v = in ? adv_tilde_u(s_task, p.n_tasks, ah, ti) : 0u;
+                const int nb = __popc(__ballot_sync(0xffffffffu, in));
+                for (int j = 0; j < nb; ++j) {  // starts are sorted: later ones overwrite
+                    const int32_t sj = __shfl_sync(0xffffffffu, rel, j);
+                    const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            o[4 * q + e] = q * 128 + 4 * lane + e >= sj ? vj : o[4 * q + e];
+                }
+                if (nb < 32) break;
+                gs += 32;  // 32 or more starts inside the chunk (trajectories < 16 tokens)
+                const bool ex = gs <= last;
+                so = ex ? p.off[gs] : LLONG_MAX;
+                ah = ex ? p.adv_hat[gs] : 0.0;
+                ti = ex ? p.task_id[gs] : -1;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = 0u;
+        }
+        // the mask bits of tokens q*128 + 4L .. +3 sit in lane (8q + L/4)'s 16 bits, nibble L%4
+        int32_t E = 0;
+        if (p.compact) {
+            const int32_t pc = __popc(bits);
+            E = warp_incl_scan(pc) - pc;
+        }
+        const int sh = (lane & 3) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t word = __shfl_sync(0xffffffffu, bits, 8 * q + (lane >> 2));
+            const uint32_t nib = (word >> sh) & 0xfu;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[4 * q + e] = ((nib >> e) & 1u) ? o[4 * q + e] : 0u;
+            const int64_t t = cb + q * 128 + 4 * lane;
+            if (vec_ok && t + 4 <= p.T) {
+                *reinterpret_cast<uint4*>(p.adv_tok + t) =
+                    make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (t + e < p.T) p.adv_tok[t + e] = __uint_as_float(o[4 * q + e]);
+            }
+            if (p.compact) {
+                const int32_t Eq = __shfl_sync(0xffffffffu, E, 8 * q + (lane >> 2));
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((nib >> e) & 1u) {
+                        const int32_t pos = gbase + Eq + __popc(word & ((1u << (sh + e)) - 1u));
+                        p.idx[pos] = (int32_t)(t + e);
+                        p.adv_c[pos] = __uint_as_float(o[4 * q + e]);
+                    }
+            }
+        }
+    }
+    phase_mark(7);
 }
 
 // static shared memory of the kernels (the rest is the dynamic Lay arena)
@@ -1686,24 +1873,12 @@ struct CoopStatic {
     int32_t s_pre[GMAX_BLOCKS + 1];
 };
 
-#ifndef ADV_APPLY_MINB
-#define ADV_APPLY_MINB 3  // resident blocks per SM the apply launch's register budget is cut for
-#endif
 __global__ void __launch_bounds__(COOP_THREADS, ADV_LARGE_MINB) k_adv_large_stats(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CoopStatic ss;
     cg::grid_group grid = cg::this_grid();
     large_stats_phases(p, smem, grid, ss.s_w, ss.s_pre);
 }
-__global__ void __launch_bounds__(COOP_THREADS, ADV_APPLY_MINB) k_adv_large_apply(const AdvParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ CoopStatic ss;
-    phase_mark(6);
-    WarpRing r = ring_setup(p, smem);
-    large_apply(p, smem, r, ss.s_pre, ss.s_w);
-    phase_mark(7);
-}
-
 // phase C of the second launch (after the all-reduce): everything reloaded, mu, sigma from the
 // reduced stats, A^ and task ids from global
 __device__ __forceinline__ void small_apply(const AdvParams& p, uint8_t* smem, WarpRing& r,
@@ -1815,6 +1990,9 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     p.grp_cnt = reinterpret_cast<int32_t*>(ws + w.grp_cnt);
     p.grp_start = reinterpret_cast<int32_t*>(ws + w.grp_start);
     p.grp_fill = reinterpret_cast<int32_t*>(ws + w.grp_fill);
+    p.grp_lo = reinterpret_cast<uint32_t*>(ws + w.grp_lo);
+    p.grp_hi = reinterpret_cast<uint32_t*>(ws + w.grp_hi);
+    p.grp_flag = reinterpret_cast<int32_t*>(ws + w.grp_flag);
     p.members = reinterpret_cast<int32_t*>(ws + w.members);
     p.grp_task = reinterpret_cast<int32_t*>(ws + w.grp_task);
     p.chunk_first = reinterpret_cast<int32_t*>(ws + w.chunk_first);
@@ -1886,14 +2064,17 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     // large driver: popcount stream -> cooperative statistics -> [C1] -> apply stream
     {
         ProfScope ps(KID_STATS, stream);
-        // K_j and the member-list fill counters start at zero (contiguous in the workspace)
+        // K_j, the member-list fill counters (+ the B4 ticket), the group bounds and the
+        // contiguity flag start at zero (contiguous in the workspace)
         AG_CUDA(cudaMemsetAsync(p.grp_cnt, 0,
-                                (size_t)(reinterpret_cast<uint8_t*>(p.grp_fill + p.n_groups + 1) -
+                                (size_t)(reinterpret_cast<uint8_t*>(p.grp_flag + 4) -
                                          reinterpret_cast<uint8_t*>(p.grp_cnt)),
                                 stream));
         const int64_t pop_want = std::max<int64_t>(
             ceil_div(p.n_chunks, (int64_t)POP_UNROLL * (POP_THREADS / 32)), 1);
-        const int pop_grid = (int)std::min<int64_t>(pop_want, (int64_t)num_sms() * 8);
+        // one wave: a second partial wave of blocks left a tail (1,184 blocks for 888 slots)
+        const int pop_grid = coop_grid((const void*)k_adv_large_pop, 0, pop_want);
+        if (!pop_grid) return AGENTRL_ERR_UNSUPPORTED;
         k_adv_large_pop<<<pop_grid, POP_THREADS, 0, stream>>>(p);
         count_launch();
         AG_CUDA(cudaGetLastError());
@@ -1912,13 +2093,13 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
         if (rc != AGENTRL_OK) return rc;
     }
     ProfScope ps(KID_APPLY, stream);
-    p.lay = make_lay(b->n_tasks, compact, false, b->n_traj, b->n_groups, true);
-    const size_t smem = p.lay.total;
+    const size_t smem = (size_t)16 * std::max(b->n_tasks, 1);  // per-task (mu, sigma)
     if (smem > 200 * 1024) return AGENTRL_ERR_UNSUPPORTED;
+    // one wave (every block resident), chunks strided over its warps
     const int grid_a = coop_grid((const void*)k_adv_large_apply, smem,
-                                 std::max<int64_t>(ceil_div(p.n_chunks, NWARPS), 1));
+                                 std::max<int64_t>(ceil_div(p.n_chunks, APPLY_THREADS / 32), 1));
     if (!grid_a) return AGENTRL_ERR_UNSUPPORTED;
-    AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, COOP_THREADS, args, smem,
+    AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, APPLY_THREADS, args, smem,
                              stream));
     count_launch();
     return AGENTRL_OK;

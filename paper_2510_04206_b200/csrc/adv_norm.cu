@@ -413,6 +413,9 @@ AdvWs plan_adv(int64_t T, int32_t n_traj, int32_t n_groups, int32_t n_tasks, siz
     w.n_g = p.take(sizeof(int32_t) * (size_t)(n_traj + 1));
     w.grp_cnt = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
     w.grp_fill = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));
+    w.grp_lo = p.take(sizeof(uint32_t) * (size_t)(n_groups + 1));  // (zeroed with the above)
+    w.grp_hi = p.take(sizeof(uint32_t) * (size_t)(n_groups + 1));
+    w.grp_flag = p.take(sizeof(int32_t) * 4);
     w.chunk_cnt = p.take(sizeof(int32_t) * (size_t)(n_chunks + 1));
     w.chunk_base = w.chunk_cnt;  // scanned in place
     w.grp_start = p.take(sizeof(int32_t) * (size_t)(n_groups + 1));

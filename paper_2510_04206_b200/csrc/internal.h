@@ -31,6 +31,9 @@ struct WsPlan {
 // ---- part 1 workspace (see adv_norm.cu) ----
 struct AdvWs {
     size_t n_g, chunk_cnt, chunk_base, grp_cnt, grp_start, grp_fill, members;  // int32
+    size_t grp_lo, grp_hi;  // uint32 [n_groups + 1]: ~(first member), last member + 1 (large
+                            // coop driver: atomicMax from zero; contiguous-group check)
+    size_t grp_flag;        // int32 [4]: [0] some group is not one contiguous run of <= 16
     size_t adv_hat;                                                               // double
     size_t grp_task;  // int32 [n_groups] task of each group (cooperative path)
     size_t grp_nsq;   // double [3*n_groups] per-group (N, S, Q) partials (cooperative path)

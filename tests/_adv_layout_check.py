@@ -7,6 +7,8 @@ names (the default build or an adv-norm driver variant), against the oracle.  La
   shuffled group ids not contiguous in trajectory order, groups of 2..20 members (both sides
            of the 16-member register path), a task with no masked tokens
   bigtraj  > 2048 trajectories (the large driver), mixed lengths
+  contig   > 2048 trajectories in contiguous groups of 2..16 (the large driver's fast path
+           without member lists), mixed lengths with empty trajectories
   huge     16M tokens in 1,500 trajectories (small driver): with a -DADV_KC_CAP=64 build every
            block stages several windows and trajectories cross window boundaries
 The integer bookkeeping (n_g, K_j, the local masked count and the fused step's compaction idx)
@@ -42,23 +44,23 @@ def layout(kind, seed):
     elif kind == "shuffled":
         n_traj = 900
         lens = rng.integers(1, 200, n_traj)
-    else:  # bigtraj
-        n_traj = 5000
+    else:  # bigtraj, contig
+        n_traj = 5000 if kind == "bigtraj" else 6000
         lens = np.where(rng.random(n_traj) < 0.5, rng.integers(0, 8, n_traj),
                         rng.integers(100, 600, n_traj))
     # groups of 2..20 members, ids shuffled over trajectories, one task per group
     sizes = []
     left = n_traj
     while left > 0:
-        k = int(min(left, rng.integers(2, 21)))
-        if left - k == 1:
-            k += 1
+        k = int(min(left, rng.integers(2, 17 if kind == "contig" else 21)))
+        if left - k == 1:  # no group of one
+            k = k + 1 if (kind != "contig" or k < 16) else k - 1
         sizes.append(k)
         left -= k
     n_groups = len(sizes)
     n_tasks = 5
     gid = np.repeat(np.arange(n_groups), sizes)
-    if kind not in ("long", "huge"):
+    if kind not in ("long", "huge", "contig"):
         rng.shuffle(gid)
     gtask = rng.integers(0, n_tasks - 1, n_groups)  # task n_tasks-1 has no trajectories
     tid = gtask[gid]
@@ -73,12 +75,19 @@ def layout(kind, seed):
                 n_groups=n_groups, n_tasks=n_tasks)
 
 
-def run_adv(b):
+def run_adv(b, mask_offset=0, out_offset=0):
+    """out_offset / mask_offset: the output / mask pointers start that many elements into
+    their buffers (not 16-byte aligned: the scalar store and direct-load paths)"""
     bd = batch_dev(b)
     T, n_traj = b["T"], len(b["task_id"])
+    if mask_offset:
+        mbuf = torch.zeros(T + mask_offset, dtype=torch.uint8, device="cuda")
+        mbuf[mask_offset:] = bd["loss_mask"]
+        bd["loss_mask"] = mbuf[mask_offset:]
     ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
                                                                     b["n_tasks"]))
-    adv = torch.full((max(T, 1),), float("nan"), dtype=torch.float32, device="cuda")
+    adv = torch.full((max(T, 1) + out_offset,), float("nan"), dtype=torch.float32,
+                     device="cuda")[out_offset:]
     ts = torch.zeros(b["n_tasks"], 3, dtype=torch.float64, device="cuda")
     nm = torch.zeros(1, dtype=torch.int64, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -147,13 +156,17 @@ def check_step(kind, b, d=64, V=512):
 
 
 def main():
-    for i, kind in enumerate(("short", "long", "shuffled", "bigtraj", "huge")):
+    for i, kind in enumerate(("short", "long", "shuffled", "bigtraj", "huge", "contig")):
         b = layout(kind, 2510_04206 + 500 + i)
         check_adv(kind, b)
         if kind != "huge":
             check_idx(kind, b, oracle.task_adv_norm(b))
         if kind in ("short", "shuffled"):
             check_step(kind, b)
+        if kind in ("short", "bigtraj", "contig"):  # T % 512 != 0; misaligned pointers
+            ref = oracle.task_adv_norm(b)
+            adv, _, nm, _, _ = run_adv(b, mask_offset=3, out_offset=1)
+            assert nm == ref["n_mask"] and adv_close(adv, ref["adv_tok"]), kind + " misaligned"
     print("adv layouts ok", ag.LIB_PATH)
 
 
