@@ -52,8 +52,9 @@ VARIANTS = {
     "ksplit3": ["-DAGENTRL_KSPLIT_FORCE=3"],           # grad_hidden split into 3 k-ranges
     "ksplitauto": ["-DAGENTRL_KSPLIT_FORCE=0"],        # grad_hidden split chosen per shape
     "pf8": ["-DAGENTRL_PREFETCH_KB=8"],                # backward L2 prefetch 8 k-blocks ahead
-    "applypf": ["-DADV_APPLY_PF=1", "-DADV_APPLY_MINB=3"],  # large apply: loads one chunk ahead
-    "applyminb3": ["-DADV_APPLY_MINB=3"],              # large apply: 3 blocks/SM, no spills
+    "applysc4": ["-DADV_APPLY_SC=4", "-DADV_APPLY_MINB=3"],  # large apply: 4-chunk units
+    "applysc16": ["-DADV_APPLY_SC=16", "-DADV_APPLY_MINB=2"],  # large apply: 16-chunk units
+    "popu8": ["-DADV_POP_UNROLL=8", "-DADV_POP_PIPE=0"],  # popcount: 8 loads, no pipelining
 }
 
 

@@ -1300,6 +1300,9 @@ constexpr int POP_THREADS = 256;
 #define ADV_POP_UNROLL 4
 #endif
 constexpr int POP_UNROLL = ADV_POP_UNROLL;
+#ifndef ADV_POP_PIPE
+#define ADV_POP_PIPE 1  // the next POP_UNROLL chunks' loads in flight while the current reduce
+#endif
 __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p) {
     phase_mark(0);
     const int lane = threadIdx.x & 31;
@@ -1322,11 +1325,20 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
         }
     };
     const int64_t step = nw * POP_UNROLL;
-    uint4 cur[POP_UNROLL], nxt[POP_UNROLL];
+    uint4 cur[POP_UNROLL];
+#if ADV_POP_PIPE
+    uint4 nxt[POP_UNROLL];
+#endif
     int64_t c0 = gw * POP_UNROLL;
+#if ADV_POP_PIPE
     if (c0 < p.n_chunks) load(cur, c0);
+#endif
     for (; c0 < p.n_chunks; c0 += step) {
+#if ADV_POP_PIPE
         if (c0 + step < p.n_chunks) load(nxt, c0 + step);
+#else
+        load(cur, c0);
+#endif
 #pragma unroll
         for (int u = 0; u < POP_UNROLL; ++u) {
             const int64_t c = c0 + u;
@@ -1337,8 +1349,10 @@ __global__ void __launch_bounds__(POP_THREADS) k_adv_large_pop(const AdvParams p
                 if (lane == 0) p.chunk[c] = tot;
             }
         }
+#if ADV_POP_PIPE
 #pragma unroll
         for (int u = 0; u < POP_UNROLL; ++u) cur[u] = nxt[u];
+#endif
     }
     const int64_t gtid = (int64_t)blockIdx.x * POP_THREADS + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * POP_THREADS;
@@ -1701,61 +1715,118 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
 }
 
 // phase C of the large driver (round 2, lean apply; its own launch and one-wave grid).
-// One warp per 512-token chunk, chunks strided over every warp of the grid (equal work per
-// warp: no block-range tail).  Lane L writes the float4s of tokens q*128 + 4L .. +3, q = 0..3,
-// so every store instruction writes 512 contiguous bytes without a shared-memory transpose.
-// The chunk's trajectories: the chunk -> first-trajectory table gives g0 (holding the chunk's
-// first token); lane L loads the start of trajectory g0 + 1 + L and a ballot finds those that
-// start inside the chunk (sorted: a prefix of the lanes).  Each lane computes Eq.1
-// for the trajectory it loaded and shuffles broadcast it.  The mask comes from phase A's
-// stored lane bits (64 B per chunk instead of 512 mask bytes).  Compaction positions (fused
-// step): the statistics launch's global chunk base + the popcount of the chunk's bits below
-// the token.
+// A warp takes a unit of APPLY_SC consecutive 512-token chunks; units are strided over every
+// warp of the grid (equal work per warp: no block-range tail).  All loads of a unit are issued
+// together (one memory round trip per 4 chunks: the launch is otherwise latency-bound on these
+// cold loads): the chunk -> first-trajectory table gives g0 (holding the unit's first token,
+// loaded one unit ahead); lane L loads the start, A^ and task of trajectory g0 + 1 + L, and a
+// ballot finds the starts inside the unit (sorted: a prefix of the lanes); each lane computes
+// Eq.1 for the trajectory it loaded, and shuffles broadcast the values.  Lane L
+// writes the float4s of tokens q*128 + 4L .. +3 (q = 0..3) of each chunk, so every store
+// instruction writes 512 contiguous bytes with no shared-memory transpose.  The mask comes from
+// phase A's stored lane bits (64 B per chunk instead of 512 mask bytes).  Compaction positions
+// (fused step): the statistics launch's global chunk base + the popcount of the chunk's bits
+// below the token.  A unit with 32 or more trajectory starts (trajectories shorter than ~64
+// tokens) takes its chunks one at a time with global batches of starts.
 constexpr int APPLY_THREADS = 256;
 static_assert(APPLY_THREADS == COOP_THREADS && POP_THREADS == COOP_THREADS,
               "coop_grid sizes the one-wave grids with COOP_THREADS");
 #ifndef ADV_APPLY_MINB
-#define ADV_APPLY_MINB 4  // resident blocks per SM the apply launch's register budget is cut for
+#define ADV_APPLY_MINB 2  // resident blocks per SM the apply launch's register budget is cut for
 #endif
-#ifndef ADV_APPLY_PF
-#define ADV_APPLY_PF 0  // 1: a chunk's loads are issued one iteration ahead (software pipeline)
+#ifndef ADV_APPLY_SC
+#define ADV_APPLY_SC 8  // 512-token chunks per warp unit of the apply (one load round trip each)
 #endif
-// the loads one chunk needs (g0: the trajectory holding its first token; lane L: trajectory
-// g0 + 1 + L's start, A^ and task)
-struct ApplyLd {
-    int32_t g0, gbase, ti0, ti;
-    uint32_t bits;
-    double ah0, ah;
-    int64_t so;
-};
-__device__ __forceinline__ ApplyLd apply_load(const AdvParams& p, int64_t c, int32_t g_first,
-                                              bool any) {
-    const int lane = threadIdx.x & 31;
-    const int32_t last = p.n_traj - 1;
-    ApplyLd L;
-    L.g0 = min(max(g_first, 0), max(last, 0));
-    L.bits = any ? (uint32_t)p.lanebits[c * 32 + lane] : 0u;
-    L.gbase = p.compact ? p.chunk_gbase[c] : 0;
-    L.ah0 = L.ah = 0.0;
-    L.ti0 = L.ti = -1;
-    L.so = LLONG_MAX;
-    if (any) {
-        L.ah0 = p.adv_hat[L.g0];  // uniform over the warp
-        L.ti0 = p.task_id[L.g0];
-        const int64_t gs = (int64_t)L.g0 + 1 + lane;
-        if (gs <= last) {
-            L.so = p.off[gs];
-            L.ah = p.adv_hat[gs];
-            L.ti = p.task_id[gs];
-        }
-    }
-    return L;
-}
+constexpr int APPLY_SC = ADV_APPLY_SC;
 // Eq.1 value of trajectory g as float bits (the arithmetic of adv_tilde)
 __device__ __forceinline__ uint32_t adv_tilde_u(const double2* s_task, int32_t n_tasks, double ah,
                                                 int32_t ti) {
     return (ti >= 0 && ti < n_tasks) ? __float_as_uint((float)((ah - s_task[ti].x) / s_task[ti].y))
                                      : 0u;
+}
+
+// the 16 values of one 512-token chunk c from its own trajectory starts, 32 starts per global
+// batch (a unit with 32 or more trajectory starts: trajectories shorter than ~64 tokens)
+// mask (the chunk's stored lane bits bk), store the 16 values of one chunk starting at token cbk
+// and, in the fused step, its compaction (global base gbk)
+__device__ __forceinline__ void apply_emit(const AdvParams& p, int64_t cbk, uint32_t (&o)[16],
+                                           uint32_t bk, int32_t gbk, bool vec_ok) {
+    const int lane = threadIdx.x & 31;
+    // the mask bits of tokens q*128 + 4L .. +3 sit in lane (8q + L/4)'s 16 bits,
+    // nibble L%4
+    const int sh = (lane & 3) * 4;
+    if (!p.compact && vec_ok && cbk + WCHUNK <= p.T) {  // the common case: no per-vector checks
+        uint4* dst = reinterpret_cast<uint4*>(p.adv_tok + cbk) + lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t nib = __shfl_sync(0xffffffffu, bk, 8 * q + (lane >> 2)) >> sh;
+            dst[32 * q] = make_uint4((nib & 1u) ? o[4 * q] : 0u, (nib & 2u) ? o[4 * q + 1] : 0u,
+                                     (nib & 4u) ? o[4 * q + 2] : 0u, (nib & 8u) ? o[4 * q + 3] : 0u);
+        }
+        return;
+    }
+    int32_t E = 0;
+    if (p.compact) {
+        const int32_t pc = __popc(bk);
+        E = warp_incl_scan(pc) - pc;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t word = __shfl_sync(0xffffffffu, bk, 8 * q + (lane >> 2));
+        const uint32_t nib = (word >> sh) & 0xfu;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[4 * q + e] = ((nib >> e) & 1u) ? o[4 * q + e] : 0u;
+        const int64_t t = cbk + q * 128 + 4 * lane;
+        if (vec_ok && t + 4 <= p.T) {
+            *reinterpret_cast<uint4*>(p.adv_tok + t) =
+                make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (t + e < p.T) p.adv_tok[t + e] = __uint_as_float(o[4 * q + e]);
+        }
+        if (p.compact) {
+            const int32_t Eq = __shfl_sync(0xffffffffu, E, 8 * q + (lane >> 2));
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((nib >> e) & 1u) {
+                    const int32_t pos = gbk + Eq + __popc(word & ((1u << (sh + e)) - 1u));
+                    p.idx[pos] = (int32_t)(t + e);
+                    p.adv_c[pos] = __uint_as_float(o[4 * q + e]);
+                }
+        }
+    }
+}
+
+__device__ __forceinline__ void apply_chunk_global(const AdvParams& p, const double2* s_task, int64_t c,
+                                                uint32_t bk, int32_t gbk, bool vec_ok) {
+    uint32_t o[16];
+    const int lane = threadIdx.x & 31;
+    const int32_t last = p.n_traj - 1;
+    const int64_t cb = c * WCHUNK;
+    const int32_t g0 = min(max(p.chunk_first[c], 0), last);
+    const uint32_t v0 = adv_tilde_u(s_task, p.n_tasks, p.adv_hat[g0], p.task_id[g0]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = v0;
+    for (int64_t gs = (int64_t)g0 + 1 + lane;; gs += 32) {
+        const bool ex = gs <= last;
+        const int64_t so = ex ? p.off[gs] : LLONG_MAX;
+        const bool in = so < cb + WCHUNK;
+        const int32_t rel = in ? (int32_t)(so - cb) : WCHUNK;
+        const uint32_t v = in ? adv_tilde_u(s_task, p.n_tasks, p.adv_hat[gs], p.task_id[gs]) : 0u;
+        const int nb = __popc(__ballot_sync(0xffffffffu, in));
+        for (int j = 0; j < nb; ++j) {
+            const int32_t sj = __shfl_sync(0xffffffffu, rel, j);
+            const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    o[4 * q + e] = q * 128 + 4 * lane + e >= sj ? vj : o[4 * q + e];
+        }
+        if (nb < 32) break;
+    }
+    apply_emit(p, c * WCHUNK, o, bk, gbk, vec_ok);
 }
 
 __global__ void __launch_bounds__(APPLY_THREADS, ADV_APPLY_MINB) k_adv_large_apply(const AdvParams p) {
@@ -1772,96 +1843,101 @@ __global__ void __launch_bounds__(APPLY_THREADS, ADV_APPLY_MINB) k_adv_large_app
     __syncthreads();
     const int lane = threadIdx.x & 31;
     constexpr int WPB = APPLY_THREADS / 32;
+    constexpr int32_t USPAN = APPLY_SC * WCHUNK;  // tokens per unit
+    const int64_t n_units = (p.n_chunks + APPLY_SC - 1) / APPLY_SC;
     const int64_t nw = (int64_t)gridDim.x * WPB;
-    int64_t c = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
+    const int64_t gw = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
+    // units strided over the warps (the grid writes one advancing front; a contiguous range
+    // per warp measured 5% slower at 2^27)
+    int64_t u = gw;
+    const int64_t u_end = n_units, u_step = nw;
     const bool any = p.n_traj > 0;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(p.adv_tok) & 15) == 0;
     const int32_t last = p.n_traj - 1;
-    int32_t g_next = (any && c < p.n_chunks) ? p.chunk_first[c] : 0;
-#if ADV_APPLY_PF
-    ApplyLd nxt;
-    if (c < p.n_chunks) {
-        nxt = apply_load(p, c, g_next, any);
-        g_next = (any && c + nw < p.n_chunks) ? p.chunk_first[c + nw] : 0;
-    }
-#endif
-    for (; c < p.n_chunks; c += nw) {
-#if ADV_APPLY_PF
-        const ApplyLd L = nxt;
-        if (c + nw < p.n_chunks) nxt = apply_load(p, c + nw, g_next, any);
-        if (any && c + 2 * nw < p.n_chunks) g_next = p.chunk_first[c + 2 * nw];
-#else
-        const ApplyLd L = apply_load(p, c, g_next, any);
-        if (any && c + nw < p.n_chunks) g_next = p.chunk_first[c + nw];  // one chunk ahead
-#endif
-        const int64_t cb = c * WCHUNK;
-        const uint32_t bits = L.bits;
-        const int32_t gbase = L.gbase;
-        uint32_t o[16];
-        if (any) {
-            int64_t gs = (int64_t)L.g0 + 1 + lane, so = L.so;
-            double ah = L.ah;
-            int32_t ti = L.ti;
-            const uint32_t v0 = adv_tilde_u(s_task, p.n_tasks, L.ah0, L.ti0);
+    int32_t g_next = (any && u < u_end) ? p.chunk_first[u * APPLY_SC] : 0;
+    for (; u < u_end; u += u_step) {
+        const int64_t c0 = u * APPLY_SC, cb = c0 * WCHUNK;
+        const int nsub = (int)min((int64_t)APPLY_SC, p.n_chunks - c0);
+        const int32_t g0 = min(max(g_next, 0), max(last, 0));
+        if (any && u + u_step < u_end) g_next = p.chunk_first[(u + u_step) * APPLY_SC];  // ahead
+        // every load of the unit issued together: the lane bits of its chunks,
+        // A^ / task of g0 (uniform) and of trajectory g0 + 1 + lane with its start
+        uint32_t bits[APPLY_SC];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = v0;
-            for (int32_t jb = 0;; jb += 32) {
-                const bool in = so < cb + WCHUNK;
-                const int32_t rel = in ? (int32_t)(so - cb) : WCHUNK;
-                const uint32_t v = in ? adv_tilde_u(s_task, p.n_tasks, ah, ti) : 0u;
-                const int nb = __popc(__ballot_sync(0xffffffffu, in));
-                for (int j = 0; j < nb; ++j) {  // starts are sorted: later ones overwrite
-                    const int32_t sj = __shfl_sync(0xffffffffu, rel, j);
+        for (int k = 0; k < APPLY_SC; ++k)
+            bits[k] = (any && k < nsub) ? (uint32_t)p.lanebits[(c0 + k) * 32 + lane] : 0u;
+        uint32_t v0 = 0u, v = 0u;
+        int32_t rel = USPAN;
+        bool in = false;
+        if (any) {
+            const double ah0 = p.adv_hat[g0];
+            const int32_t ti0 = p.task_id[g0];
+            const int64_t gs = (int64_t)g0 + 1 + lane;
+            int64_t so = LLONG_MAX;
+            double ah = 0.0;
+            int32_t ti = -1;
+            if (gs <= last) {
+                so = p.off[gs];
+                ah = p.adv_hat[gs];
+                ti = p.task_id[gs];
+            }
+            v0 = adv_tilde_u(s_task, p.n_tasks, ah0, ti0);
+            in = so < cb + USPAN;  // starts are sorted: the in-lanes are a prefix
+            rel = in ? (int32_t)(so - cb) : USPAN;
+            v = in ? adv_tilde_u(s_task, p.n_tasks, ah, ti) : 0u;
+        }
+        const bool many = __ballot_sync(0xffffffffu, in) == 0xffffffffu;  // >= 32 starts
+#pragma unroll 1
+        for (int k = 0; k < nsub; ++k) {  // not unrolled: a small loop body stays in the I-cache
+            const int32_t lo = k * WCHUNK;  // the chunk's first token, unit-relative
+            uint32_t bk = bits[0];
+#pragma unroll
+            for (int i = 1; i < APPLY_SC; ++i) bk = k == i ? bits[i] : bk;  // no local memory
+            const int32_t gbk = p.compact ? p.chunk_gbase[c0 + k] : 0;  // (fused step only)
+            uint32_t o[16];
+            if (!any) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[i] = 0u;
+            } else if (!many) {
+                // value at the chunk's first token: the last start at or before it; then the
+                // starts inside the chunk (lanes ka .. kb - 1) overwrite in order
+                const int ka = __popc(__ballot_sync(0xffffffffu, in && rel <= lo));
+                const int kb = __popc(__ballot_sync(0xffffffffu, in && rel < lo + WCHUNK));
+                const uint32_t vs = ka ? __shfl_sync(0xffffffffu, v, max(ka - 1, 0)) : v0;
+                // per float4 of the lane: one value unless a start falls strictly inside it
+                uint32_t w[4] = {vs, vs, vs, vs};
+                bool split = false;
+                for (int j = ka; j < kb; ++j) {
+                    // start relative to the lane's first token of float4 q = 0
+                    const int32_t dj = __shfl_sync(0xffffffffu, rel, j) - lo - 4 * lane;
                     const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            o[4 * q + e] = q * 128 + 4 * lane + e >= sj ? vj : o[4 * q + e];
-                }
-                if (nb < 32) break;
-                gs += 32;  // 32 or more starts inside the chunk (trajectories < 16 tokens)
-                const bool ex = gs <= last;
-                so = ex ? p.off[gs] : LLONG_MAX;
-                ah = ex ? p.adv_hat[gs] : 0.0;
-                ti = ex ? p.task_id[gs] : -1;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = 0u;
-        }
-        // the mask bits of tokens q*128 + 4L .. +3 sit in lane (8q + L/4)'s 16 bits, nibble L%4
-        int32_t E = 0;
-        if (p.compact) {
-            const int32_t pc = __popc(bits);
-            E = warp_incl_scan(pc) - pc;
-        }
-        const int sh = (lane & 3) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t word = __shfl_sync(0xffffffffu, bits, 8 * q + (lane >> 2));
-            const uint32_t nib = (word >> sh) & 0xfu;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) o[4 * q + e] = ((nib >> e) & 1u) ? o[4 * q + e] : 0u;
-            const int64_t t = cb + q * 128 + 4 * lane;
-            if (vec_ok && t + 4 <= p.T) {
-                *reinterpret_cast<uint4*>(p.adv_tok + t) =
-                    make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (t + e < p.T) p.adv_tok[t + e] = __uint_as_float(o[4 * q + e]);
-            }
-            if (p.compact) {
-                const int32_t Eq = __shfl_sync(0xffffffffu, E, 8 * q + (lane >> 2));
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if ((nib >> e) & 1u) {
-                        const int32_t pos = gbase + Eq + __popc(word & ((1u << (sh + e)) - 1u));
-                        p.idx[pos] = (int32_t)(t + e);
-                        p.adv_c[pos] = __uint_as_float(o[4 * q + e]);
+                    for (int q = 0; q < 4; ++q) {
+                        const int32_t r = dj - q * 128;  // relative to float4 q's first token
+                        w[q] = r <= 0 ? vj : w[q];
+                        split |= (uint32_t)(r - 1) < 3u;  // at element 1..3 of the float4
                     }
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[i] = w[i >> 2];
+                if (__any_sync(0xffffffffu, split)) {  // rare: element-wise over the starts
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[i] = vs;
+                    for (int j = ka; j < kb; ++j) {
+                        const int32_t dj = __shfl_sync(0xffffffffu, rel, j) - lo - 4 * lane;
+                        const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                o[4 * q + e] = q * 128 + e >= dj ? vj : o[4 * q + e];
+                    }
+                }
+            } else {
+                apply_chunk_global(p, s_task, c0 + k, bk, gbk, vec_ok);
+                continue;
             }
+            apply_emit(p, cb + lo, o, bk, gbk, vec_ok);
         }
     }
     phase_mark(7);

@@ -5,18 +5,20 @@
 set -o pipefail
 python paper_2510_04206_b200/build.py > /dev/null
 python -c "import oracle; oracle.build()"
-PF=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applypf')['AGENTRL_LIB'])")
-M3=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applyminb3')['AGENTRL_LIB'])")
+PF=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applysc4')['AGENTRL_LIB'])")
+M3=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applysc16')['AGENTRL_LIB'])")
+CT=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('popu8')['AGENTRL_LIB'])")
 timeout 1500 python -m pytest tests/test_gpu_adv_layouts.py tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q -m gpu 2>&1 | tail -3 | tee gpurun_out/adv_lean_pytest.log
 for r in 1 2; do
-  for v in new pf m3 old; do
+  for v in new sc4 sc16 popu8 old; do
     case $v in
       old) export AGENTRL_LIB=$PWD/ab_old/libagentrl.so ;;
-      pf) export AGENTRL_LIB=$PF ;;
-      m3) export AGENTRL_LIB=$M3 ;;
+      sc4) export AGENTRL_LIB=$PF ;;
+      sc16) export AGENTRL_LIB=$M3 ;;
+      popu8) export AGENTRL_LIB=$CT ;;
       *) unset AGENTRL_LIB ;;
     esac
-    timeout 300 python tools/adv_sweep.py --sizes 20,24,27 --configs glm9b --iters 20 > gpurun_out/adv_lean_$v.jsonl 2>&1
+    timeout 300 python tools/adv_sweep.py --sizes 24,27 --configs glm9b --iters 20 > gpurun_out/adv_lean_$v.jsonl 2>&1
     python -c "
 import json
 for l in open('gpurun_out/adv_lean_$v.jsonl'):
