@@ -53,8 +53,8 @@ VARIANTS = {
     "ksplitauto": ["-DAGENTRL_KSPLIT_FORCE=0"],        # grad_hidden split chosen per shape
     "pf8": ["-DAGENTRL_PREFETCH_KB=8"],                # backward L2 prefetch 8 k-blocks ahead
     "applysc4": ["-DADV_APPLY_SC=4", "-DADV_APPLY_MINB=3"],  # large apply: 4-chunk units
-    "applysc16": ["-DADV_APPLY_SC=16", "-DADV_APPLY_MINB=2"],  # large apply: 16-chunk units
-    "popu8": ["-DADV_POP_UNROLL=8", "-DADV_POP_PIPE=0"],  # popcount: 8 loads, no pipelining
+    "applynopf": ["-DADV_APPLY_PF=0", "-DADV_APPLY_PDL=0"],  # large apply: no unit prefetch, no PDL
+    "applydiag": ["-DADV_APPLY_DIAG=1"],               # timing only: the apply's stores alone
 }
 
 

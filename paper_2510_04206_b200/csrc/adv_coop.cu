@@ -1465,9 +1465,11 @@ __device__ void large_stats_phases(const AdvParams& p, uint8_t* smem, cg::grid_g
     const bool contig = __ldcg(p.grp_flag) == 0;  // grid-uniform
 
     block_prefix_smem(p.blk_chunk, G, s_pre, s_w);
-    // global compaction base of this block's chunks (the apply launch has its own grid)
-    for (int64_t c = c_lo + threadIdx.x; c < c_hi; c += COOP_THREADS)
-        p.chunk_gbase[c] = s_pre[B] + p.chunk_base[c];
+    // global compaction base of this block's chunks (the apply launch has its own grid; only
+    // the fused step compacts)
+    if (p.compact)
+        for (int64_t c = c_lo + threadIdx.x; c < c_hi; c += COOP_THREADS)
+            p.chunk_gbase[c] = s_pre[B] + p.chunk_base[c];
     // n_g = masked tokens in [off_g, off_{g+1}) from prefix differences (exact integers), one
     // masked_before per trajectory bound: warp iteration i covers bounds 31i .. 31i + 31 (lane
     // L: bound 31i + L) and writes n_g of trajectories 31i .. 31i + 30 from the next lane's
@@ -1738,6 +1740,15 @@ static_assert(APPLY_THREADS == COOP_THREADS && POP_THREADS == COOP_THREADS,
 #define ADV_APPLY_SC 8  // 512-token chunks per warp unit of the apply (one load round trip each)
 #endif
 constexpr int APPLY_SC = ADV_APPLY_SC;
+#ifndef ADV_APPLY_PF
+#define ADV_APPLY_PF 1  // 1: a unit's loads are issued while the previous unit is processed
+#endif
+#ifndef ADV_APPLY_DIAG
+#define ADV_APPLY_DIAG 0  // timing experiment: stores only (wrong results; never a product build)
+#endif
+#ifndef ADV_APPLY_PDL
+#define ADV_APPLY_PDL 1  // 1: the apply is a programmatic dependent launch of the statistics
+#endif
 // Eq.1 value of trajectory g as float bits (the arithmetic of adv_tilde)
 __device__ __forceinline__ uint32_t adv_tilde_u(const double2* s_task, int32_t n_tasks, double ah,
                                                 int32_t ti) {
@@ -1832,6 +1843,11 @@ __device__ __forceinline__ void apply_chunk_global(const AdvParams& p, const dou
 __global__ void __launch_bounds__(APPLY_THREADS, ADV_APPLY_MINB) k_adv_large_apply(const AdvParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     double2* s_task = reinterpret_cast<double2*>(smem);
+#if ADV_APPLY_PDL
+    // launched as a programmatic dependent of the statistics launch (no communicator): wait
+    // until that grid has completed and its memory is visible before reading anything it wrote
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     phase_mark(6);
     task_params_smem(p, s_task);
     if (blockIdx.x == 0 && threadIdx.x < 32) {  // local masked rows = sum of the stats blocks'
@@ -1854,38 +1870,69 @@ __global__ void __launch_bounds__(APPLY_THREADS, ADV_APPLY_MINB) k_adv_large_app
     const bool any = p.n_traj > 0;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(p.adv_tok) & 15) == 0;
     const int32_t last = p.n_traj - 1;
+    // a unit's loads: the lane bits of its chunks, A^ / task of g0 (uniform) and of trajectory
+    // g0 + 1 + lane with its start (issued together; with ADV_APPLY_PF one unit ahead)
+    struct UnitLd {
+        uint32_t bits[APPLY_SC];
+        double ah0, ah;
+        int32_t ti0, ti;
+        int64_t so;
+    };
+    auto load_unit = [&](int64_t uu, int32_t gf) {
+        UnitLd L;
+        const int64_t c0 = uu * APPLY_SC;
+        const int32_t g0 = min(max(gf, 0), max(last, 0));
+#pragma unroll
+        for (int k = 0; k < APPLY_SC; ++k)
+            L.bits[k] = (any && c0 + k < p.n_chunks) ? (uint32_t)p.lanebits[(c0 + k) * 32 + lane] : 0u;
+        L.ah0 = L.ah = 0.0;
+        L.ti0 = L.ti = -1;
+        L.so = LLONG_MAX;
+        if (any) {
+            L.ah0 = p.adv_hat[g0];
+            L.ti0 = p.task_id[g0];
+            const int64_t gs = (int64_t)g0 + 1 + lane;
+            if (gs <= last) {
+                L.so = p.off[gs];
+                L.ah = p.adv_hat[gs];
+                L.ti = p.task_id[gs];
+            }
+        }
+        return L;
+    };
     int32_t g_next = (any && u < u_end) ? p.chunk_first[u * APPLY_SC] : 0;
+#if ADV_APPLY_PF
+    UnitLd nxt;
+    if (u < u_end) {
+        nxt = load_unit(u, g_next);
+        g_next = (any && u + u_step < u_end) ? p.chunk_first[(u + u_step) * APPLY_SC] : 0;
+    }
+#endif
     for (; u < u_end; u += u_step) {
         const int64_t c0 = u * APPLY_SC, cb = c0 * WCHUNK;
         const int nsub = (int)min((int64_t)APPLY_SC, p.n_chunks - c0);
-        const int32_t g0 = min(max(g_next, 0), max(last, 0));
-        if (any && u + u_step < u_end) g_next = p.chunk_first[(u + u_step) * APPLY_SC];  // ahead
-        // every load of the unit issued together: the lane bits of its chunks,
-        // A^ / task of g0 (uniform) and of trajectory g0 + 1 + lane with its start
-        uint32_t bits[APPLY_SC];
+#if ADV_APPLY_DIAG  // timing experiment only (NOT the method): the unit's stores alone
+        for (int k = 0; k < nsub; ++k)
+            if (cb + (k + 1) * WCHUNK <= p.T)
 #pragma unroll
-        for (int k = 0; k < APPLY_SC; ++k)
-            bits[k] = (any && k < nsub) ? (uint32_t)p.lanebits[(c0 + k) * 32 + lane] : 0u;
-        uint32_t v0 = 0u, v = 0u;
-        int32_t rel = USPAN;
-        bool in = false;
-        if (any) {
-            const double ah0 = p.adv_hat[g0];
-            const int32_t ti0 = p.task_id[g0];
-            const int64_t gs = (int64_t)g0 + 1 + lane;
-            int64_t so = LLONG_MAX;
-            double ah = 0.0;
-            int32_t ti = -1;
-            if (gs <= last) {
-                so = p.off[gs];
-                ah = p.adv_hat[gs];
-                ti = p.task_id[gs];
-            }
-            v0 = adv_tilde_u(s_task, p.n_tasks, ah0, ti0);
-            in = so < cb + USPAN;  // starts are sorted: the in-lanes are a prefix
-            rel = in ? (int32_t)(so - cb) : USPAN;
-            v = in ? adv_tilde_u(s_task, p.n_tasks, ah, ti) : 0u;
-        }
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<uint4*>(p.adv_tok + cb + k * WCHUNK)[32 * q + lane] =
+                        make_uint4(0u, 0u, 0u, 0u);
+        continue;
+#endif
+#if ADV_APPLY_PF
+        const UnitLd L = nxt;
+        if (u + u_step < u_end) nxt = load_unit(u + u_step, g_next);
+        if (any && u + 2 * u_step < u_end) g_next = p.chunk_first[(u + 2 * u_step) * APPLY_SC];
+#else
+        const UnitLd L = load_unit(u, g_next);
+        if (any && u + u_step < u_end) g_next = p.chunk_first[(u + u_step) * APPLY_SC];  // ahead
+#endif
+        const uint32_t(&bits)[APPLY_SC] = L.bits;
+        const uint32_t v0 = any ? adv_tilde_u(s_task, p.n_tasks, L.ah0, L.ti0) : 0u;
+        const bool in = L.so < cb + USPAN;  // starts are sorted: the in-lanes are a prefix
+        const int32_t rel = in ? (int32_t)(L.so - cb) : USPAN;
+        const uint32_t v = in ? adv_tilde_u(s_task, p.n_tasks, L.ah, L.ti) : 0u;
         const bool many = __ballot_sync(0xffffffffu, in) == 0xffffffffu;  // >= 32 starts
 #pragma unroll 1
         for (int k = 0; k < nsub; ++k) {  // not unrolled: a small loop body stays in the I-cache
@@ -2175,8 +2222,22 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
     const int grid_a = coop_grid((const void*)k_adv_large_apply, smem,
                                  std::max<int64_t>(ceil_div(p.n_chunks, APPLY_THREADS / 32), 1));
     if (!grid_a) return AGENTRL_ERR_UNSUPPORTED;
-    AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, APPLY_THREADS, args, smem,
-                             stream));
+    if (ADV_APPLY_PDL && !comm) {  // its launch overlaps the statistics launch's tail
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid_a);
+        cfg.blockDim = dim3(APPLY_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        AG_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k_adv_large_apply, args));
+    } else {
+        AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, APPLY_THREADS, args,
+                                 smem, stream));
+    }
     count_launch();
     return AGENTRL_OK;
 }
