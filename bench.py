@@ -495,11 +495,18 @@ def adv_norm_timing(ag, bd, lb, dev, hbm_gbs, iters=20):
         sbd["task_id"] = sbd["task_id"].int()
         sbd["group_id"] = sbd["group_id"].int()
         sms = _adv_time(ag, sbd, sb, dev, 10, False)
+        try:
+            sgms = _adv_time(ag, sbd, sb, dev, 10, True)
+        except Exception:  # graph capture unavailable
+            sgms = None
         sby = 5 * int(sb["T"]) + 20 * len(sb["task_id"])
         out["bandwidth_point"] = {"T": int(sb["T"]), "n_traj": len(sb["task_id"]),
                                   "latency_us": sms * 1e3, "alg_bytes": sby,
                                   "GBps": sby / (sms / 1e3) / 1e9,
-                                  "frac_hbm": sby / (sms / 1e3) / 1e9 / hbm_gbs}
+                                  "frac_hbm": sby / (sms / 1e3) / 1e9 / hbm_gbs,
+                                  "graph_latency_us": None if sgms is None else sgms * 1e3,
+                                  "graph_frac_hbm": None if sgms is None else
+                                  sby / sgms * 1e3 / 1e9 / hbm_gbs}
         del sbd
         torch.cuda.empty_cache()
     except Exception as e:  # noqa: BLE001 -- report, never fail the bench line

@@ -24,7 +24,7 @@ def alg_bytes(b):
     return int(b["T"]) * 5 + 20 * len(b["task_id"])
 
 
-def time_adv(b, iters=20, graph=False):
+def time_adv(b, iters=20, graph=False, clean=False):
     dev = "cuda"
     bd = {k: (torch.from_numpy(np.ascontiguousarray(v)).to(dev) if isinstance(v, np.ndarray) else v)
           for k, v in b.items()}
@@ -40,6 +40,9 @@ def time_adv(b, iters=20, graph=False):
     batch = ag.make_batch(bd)
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+    # clean: after the write flush, read another 2 x L2 buffer so that L2 holds clean lines
+    # (the flush's dirty lines are written back outside the timed region)
+    rbuf = torch.ones(2 * l2 // 4, dtype=torch.float32, device=dev) if clean else None
     stream = torch.cuda.Stream()
 
     def call():
@@ -58,6 +61,8 @@ def time_adv(b, iters=20, graph=False):
         times, phs = [], []
         for _ in range(iters):
             flush.fill_(1.0)
+            if rbuf is not None:
+                rbuf.sum()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if g is not None:
@@ -85,6 +90,8 @@ def main():
     ap.add_argument("--sizes", default="17,20,24,27")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--configs", default="qwen7b,glm9b,qwen32b,skew14b")
+    ap.add_argument("--clean", action="store_true",
+                    help="leave L2 clean before each call (write flush, then a read flush)")
     a = ap.parse_args()
     hbm = 6551.4
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -94,12 +101,12 @@ def main():
     cases += [(c, synth.make_structure(synth.CONFIGS[c])) for c in a.configs.split(",") if c]
     for name, b in cases:
         for graph in (False, True):
-            ms, nm, phases = time_adv(b, a.iters, graph)
+            ms, nm, phases = time_adv(b, a.iters, graph, a.clean)
             by = alg_bytes(b)
             print(json.dumps({"case": name, "T": int(b["T"]), "n_traj": len(b["task_id"]),
                               "graph": graph, "latency_us": ms * 1e3, "alg_bytes": by,
                               "GBps": by / (ms / 1e3) / 1e9, "frac_hbm": by / (ms / 1e3) / 1e9 / hbm,
-                              "n_mask": nm, "phase_us": phases}), flush=True)
+                              "n_mask": nm, "phase_us": phases, "clean_l2": a.clean}), flush=True)
 
 
 if __name__ == "__main__":
