@@ -19,9 +19,17 @@
 //          holds the whole trajectory table in smem; A + the A^ of its groups + its partial
 //          moments -> ONE grid barrier -> moments (identical in every block) -> C.  Per-block
 //          trajectory counts go to disjoint slots (index g + block): no zeroing pass.
-//   large  phase 0 (zero, chunk -> first-trajectory table) | A | B1 K_j scans | B2 member lists
-//          | B3 group advantages (members of groups of <= 16 sorted in registers) | B4 task
-//          moments | C.
+//   large  three launches: (1) popcount stream (phase A: per-lane mask bits, chunk counts, K_j,
+//          group bounds, the chunk -> first-trajectory table); (2) cooperative statistics:
+//          chunk bases | n_g from prefix differences at the trajectory bounds | [B1 K_j scans |
+//          B2 member lists: skipped when every group is one contiguous run of <= 16] | B3 group
+//          advantages | B4 task moments by the last block (ticket); (3) apply (phase C) in
+//          8-chunk warp units, a programmatic dependent launch of (2) without a communicator.
+//          Measured and dropped: loading the first n_g bounds before the
+//          grid barrier (4 us slower: the barrier waits for the slowest block's extra loads);
+//          writing the all-zero sectors of adv_tok from the popcount launch (its strided
+//          stores took it from 30 to 135 us, and the apply did not get faster: the L2's
+//          deferred write-back of those lines lands in the apply anyway).
 // Every floating-point reduction has a fixed order: results are bitwise run-to-run
 // deterministic.
 #include <cooperative_groups.h>

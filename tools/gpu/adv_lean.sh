@@ -1,22 +1,18 @@
-# large adv-norm driver, round 2 rework (lean apply, one-wave popcount grid, batched n_g,
-# contiguous-group fast path, ticket B4): adv tests under every driver, interleaved sweep A/B
-# against the previous library (ab_old/) and two apply variants, ncu --set full of the three
-# large launches at 2^27
+# large adv-norm driver A/B: adv tests under every driver, interleaved sweep against the
+# round's start (ab_old/) and the previous step (ab_prev/) and one variant build, ncu --set full
+# of the three large launches at 2^27 with per-line source views
 set -o pipefail
 python paper_2510_04206_b200/build.py > /dev/null
 python -c "import oracle; oracle.build()"
-PF=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applynopf')['AGENTRL_LIB'])")
-M3=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applydiag')['AGENTRL_LIB'])")
-CT=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('applysc4')['AGENTRL_LIB'])")
+PF=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('nozs')['AGENTRL_LIB'])")
 timeout 1500 python -m pytest tests/test_gpu_adv_layouts.py tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q -m gpu 2>&1 | tail -3 | tee gpurun_out/adv_lean_pytest.log
 for L in $PF; do AGENTRL_LIB=$L timeout 600 python tests/_adv_layout_check.py 2>&1 | tail -1 | tee -a gpurun_out/adv_lean_pytest.log; done
 for r in 1 2; do
-  for v in new nopf diag sc4 old; do
+  for v in new nozs prev old; do
     case $v in
       old) export AGENTRL_LIB=$PWD/ab_old/libagentrl.so ;;
-      nopf) export AGENTRL_LIB=$PF ;;
-      diag) export AGENTRL_LIB=$M3 ;;
-      sc4) export AGENTRL_LIB=$CT ;;
+      nozs) export AGENTRL_LIB=$PF ;;
+      prev) export AGENTRL_LIB=$PWD/ab_prev/libagentrl.so ;;
       *) unset AGENTRL_LIB ;;
     esac
     timeout 300 python tools/adv_sweep.py --sizes 24,27 --configs glm9b --iters 20 > gpurun_out/adv_lean_$v.jsonl 2>&1
@@ -31,7 +27,7 @@ done
 unset AGENTRL_LIB
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_adv_large -c 3 -o gpurun_out/adv_lean_2e27 -f python tools/adv_sweep.py --sizes 27 --configs "" --iters 1 > gpurun_out/ncu_adv_lean.log 2>&1
 ncu -i gpurun_out/adv_lean_2e27.ncu-rep --page raw --csv > gpurun_out/adv_lean_2e27.raw.csv 2>/dev/null
-ncu -i gpurun_out/adv_lean_2e27.ncu-rep --page source --csv --kernel-name regex:k_adv_large_stats > gpurun_out/adv_lean_stats_source.csv 2>/dev/null
-ncu -i gpurun_out/adv_lean_2e27.ncu-rep --page source --csv --kernel-name regex:k_adv_large_apply > gpurun_out/adv_lean_apply_source.csv 2>/dev/null
+ncu -i gpurun_out/adv_lean_2e27.ncu-rep --page source --csv --print-source cuda,sass --kernel-name regex:k_adv_large_stats > gpurun_out/adv_lean_stats_source.csv 2>/dev/null
+ncu -i gpurun_out/adv_lean_2e27.ncu-rep --page source --csv --print-source cuda,sass --kernel-name regex:k_adv_large_apply > gpurun_out/adv_lean_apply_source.csv 2>/dev/null
 tail -2 gpurun_out/ncu_adv_lean.log
 timeout 900 python -m pytest tests/test_gpu_variants.py -x -q -m gpu -k "coop0" 2>&1 | tail -2 | tee -a gpurun_out/adv_lean_pytest.log
