@@ -79,3 +79,62 @@ def test_grpo_step_graph_replay(ag, cfg_name):
         s.synchronize()
         _same(replayed, _snap(step))
         assert not torch.equal(replayed["grad_W"], direct["grad_W"])
+
+
+def test_large_adv_norm_graph_replay(ag):
+    """Part 1 alone with the large driver (> 2,048 trajectories: popcount, cooperative
+    statistics and the apply as a programmatic dependent launch) captured in a CUDA graph:
+    replays are bitwise the direct call, also after the rewards are rewritten in place, and the
+    direct call matches the oracle."""
+    import oracle
+    from gpu_util import adv_close
+    b = synth.make_sweep_structure(1 << 20)
+    assert len(b["task_id"]) > 2048
+    bd = batch_dev(b)
+    T, n_traj = int(b["T"]), len(b["task_id"])
+    ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
+                                                                    b["n_tasks"]))
+    outs = dict(adv=torch.empty(T, dtype=torch.float32, device="cuda"),
+                ts=torch.empty(b["n_tasks"], 3, dtype=torch.float64, device="cuda"),
+                nm=torch.empty(1, dtype=torch.int64, device="cuda"),
+                st=torch.zeros(1, dtype=torch.int32, device="cuda"))
+    batch = ag.make_batch(bd)
+
+    def call(s):
+        rc = ag.agentrl_task_adv_norm(batch, 1e-6, outs["adv"], outs["ts"], outs["nm"], ws, None,
+                                      outs["st"], stream=s)
+        assert rc == 0
+
+    def snap():
+        return {k: v.clone() for k, v in outs.items()}
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        call(s)
+        s.synchronize()
+        direct = snap()
+        ref = oracle.task_adv_norm(b)
+        assert int(direct["nm"].item()) == ref["n_mask"]
+        assert adv_close(direct["adv"].cpu().numpy(), ref["adv_tok"])
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            call(s)
+        for v in outs.values():
+            v.zero_()
+        g.replay()
+        s.synchronize()
+        for k in outs:
+            assert torch.equal(outs[k], direct[k]), k
+        # new rewards in place: the replay follows the data
+        rng = np.random.default_rng(5)
+        bd["rewards"].copy_(torch.from_numpy(
+            rng.choice(np.asarray([1.0, 0.0, -0.2], np.float32), n_traj)).cuda())
+        call(s)
+        s.synchronize()
+        direct2 = snap()
+        assert not torch.equal(direct2["adv"], direct["adv"])
+        g.replay()
+        s.synchronize()
+        for k in outs:
+            assert torch.equal(outs[k], direct2[k]), k
