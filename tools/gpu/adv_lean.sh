@@ -4,18 +4,15 @@
 set -o pipefail
 python paper_2510_04206_b200/build.py > /dev/null
 python -c "import oracle; oracle.build()"
-PF=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('nozs')['AGENTRL_LIB'])")
 timeout 1500 python -m pytest tests/test_gpu_adv_layouts.py tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q -m gpu 2>&1 | tail -3 | tee gpurun_out/adv_lean_pytest.log
-for L in $PF; do AGENTRL_LIB=$L timeout 600 python tests/_adv_layout_check.py 2>&1 | tail -1 | tee -a gpurun_out/adv_lean_pytest.log; done
 for r in 1 2; do
-  for v in new nozs prev old; do
+  for v in new prev; do
     case $v in
       old) export AGENTRL_LIB=$PWD/ab_old/libagentrl.so ;;
-      nozs) export AGENTRL_LIB=$PF ;;
       prev) export AGENTRL_LIB=$PWD/ab_prev/libagentrl.so ;;
       *) unset AGENTRL_LIB ;;
     esac
-    timeout 300 python tools/adv_sweep.py --sizes 24,27 --configs glm9b --iters 20 > gpurun_out/adv_lean_$v.jsonl 2>&1
+    timeout 300 python tools/adv_sweep.py --sizes 20,24,27 --configs glm9b --iters 20 > gpurun_out/adv_lean_$v.jsonl 2>&1
     python -c "
 import json
 for l in open('gpurun_out/adv_lean_$v.jsonl'):
