@@ -86,8 +86,10 @@ def run_adv(b, mask_offset=0, out_offset=0):
         bd["loss_mask"] = mbuf[mask_offset:]
     ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
                                                                     b["n_tasks"]))
-    adv = torch.full((max(T, 1) + out_offset,), float("nan"), dtype=torch.float32,
-                     device="cuda")[out_offset:]
+    # NaN canaries before (out_offset) and after (64) the output: no write may land there
+    buf = torch.full((max(T, 1) + out_offset + 64,), float("nan"), dtype=torch.float32,
+                     device="cuda")
+    adv = buf[out_offset:out_offset + max(T, 1)]
     ts = torch.zeros(b["n_tasks"], 3, dtype=torch.float64, device="cuda")
     nm = torch.zeros(1, dtype=torch.int64, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -95,6 +97,8 @@ def run_adv(b, mask_offset=0, out_offset=0):
     assert rc == 0, ag.status_string(rc)
     torch.cuda.synchronize()
     bk = ag.bookkeeping(ws, T, n_traj, b["n_groups"], b["n_tasks"])
+    canary = torch.cat([buf[:out_offset], buf[out_offset + max(T, 1):]])
+    assert bool(torch.isnan(canary).all()), "adv_tok write outside [0, T)"
     return adv[:T].cpu().numpy(), ts.cpu().numpy(), int(nm.item()), int(st.item()), bk
 
 

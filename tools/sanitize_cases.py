@@ -1,6 +1,7 @@
 """compute-sanitizer cases: one agentrl_grpo_step and one agentrl_logprob_fwd on
-`tiny` and `ragged` (ragged tiles in every dimension), then a device sync; exits 0 when every
-call returned OK.  Run under  compute-sanitizer --tool {memcheck,racecheck,synccheck}.
+`tiny` and `ragged` (ragged tiles in every dimension), then the large adv-norm driver on two
+adversarial layouts (standalone and in the fused step); a device sync after each; exits 0 when
+every call returned OK.  Run under  compute-sanitizer --tool {memcheck,racecheck,synccheck}.
 (Input generation and plumbing only.)"""
 import os
 import sys
@@ -39,6 +40,33 @@ def main():
         assert rc == 0, ag.status_string(rc)
         print(name, "grpo_step status", st, "loss", float(step.loss.item()),
               "logprob status", int(s2.item()), "launches", ag.last_launch_count(), flush=True)
+    # the large adv-norm driver (> 2,048 trajectories): popcount, cooperative statistics and
+    # the programmatic dependent apply, on a contiguous-group layout (no member lists) and a
+    # shuffled one (member lists), standalone and inside the fused step (compaction)
+    import _adv_layout_check as lay
+    for kind in ("contig", "bigtraj"):
+        b = lay.layout(kind, 2510_04206 + 900)
+        T, n_traj = b["T"], len(b["task_id"])
+        ws = ag.alloc_workspace(ag.agentrl_task_adv_norm_workspace_size(T, n_traj, b["n_groups"],
+                                                                        b["n_tasks"]))
+        adv = torch.empty(T, dtype=torch.float32, device="cuda")
+        ts = torch.empty(b["n_tasks"], 3, dtype=torch.float64, device="cuda")
+        nm = torch.empty(1, dtype=torch.int64, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rc = ag.agentrl_task_adv_norm(ag.make_batch(batch_dev(b)), 1e-6, adv, ts, nm, ws, None, st)
+        torch.cuda.synchronize()
+        assert rc == 0, ag.status_string(rc)
+        d, V = 64, 512
+        rng = np.random.default_rng(3)
+        hb = synth.to_bf16_bits(rng.standard_normal((T, d)).astype(np.float32))
+        Wb = synth.to_bf16_bits((rng.standard_normal((V, d)) * 3 / np.sqrt(d)).astype(np.float32))
+        y = rng.integers(0, V, T).astype(np.int32)
+        old = synth.make_old_logp_free(T, 5)
+        step = ag.Step(T, n_traj, b["n_groups"], b["n_tasks"], d, V)
+        step(batch_dev(b), bf16_dev(hb), bf16_dev(Wb), t(y, torch.int32), t(old, torch.float32))
+        torch.cuda.synchronize()
+        print(kind, "adv_norm n_mask", int(nm.item()), "status", int(st.item()),
+              "fused status", int(step.status.item()), flush=True)
     print("sanitize cases done")
 
 
