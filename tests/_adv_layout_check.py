@@ -11,6 +11,7 @@ names (the default build or an adv-norm driver variant), against the oracle.  La
            without member lists), mixed lengths with empty trajectories
   huge     16M tokens in 1,500 trajectories (small driver): with a -DADV_KC_CAP=64 build every
            block stages several windows and trajectories cross window boundaries
+  glm9b    the BASELINE glm9b batch structure (synth), under whichever driver the build picks
 The integer bookkeeping (n_g, K_j, the local masked count and the fused step's compaction idx)
 is compared bit-exactly (agentrl_debug_bookkeeping).
 Exit code 0 = parity holds.  (Input generation, plumbing and comparison only.)"""
@@ -171,6 +172,12 @@ def main():
             ref = oracle.task_adv_norm(b)
             adv, _, nm, _, _ = run_adv(b, mask_offset=3, out_offset=1)
             assert nm == ref["n_mask"] and adv_close(adv, ref["adv_tok"]), kind + " misaligned"
+    # a BASELINE config's real batch structure (glm9b: 131,072 tokens, 640 trajectories, ~40%
+    # assistant tokens): the small driver in the default build, the large one under advlarge
+    b = synth.make_structure(synth.CONFIGS["glm9b"])
+    b = {k: v for k, v in b.items() if k != "token_index"}
+    check_adv("glm9b", b)
+    check_idx("glm9b", b, oracle.task_adv_norm(b))
     print("adv layouts ok", ag.LIB_PATH)
 
 
