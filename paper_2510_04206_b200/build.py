@@ -55,6 +55,7 @@ VARIANTS = {
     "applysc4": ["-DADV_APPLY_SC=4", "-DADV_APPLY_MINB=3"],  # large apply: 4-chunk units
     "applynopf": ["-DADV_APPLY_PF=0", "-DADV_APPLY_PDL=0"],  # large apply: no unit prefetch, no PDL
     "applydiag": ["-DADV_APPLY_DIAG=1"],               # timing only: the apply's stores alone
+    "pstage0": ["-DAGENTRL_FWD_PSTAGE=0"],             # forward: P~ stored 16 B per row, no staging
 }
 
 

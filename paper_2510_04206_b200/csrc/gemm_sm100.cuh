@@ -90,6 +90,13 @@ struct GemmCfg {
 #endif
     static constexpr int EPI_STAGE = (NSPLIT == 2 && AGENTRL_EPI_SLAB) ? 4 * 32 * 33 * 4 : 0;
     // (EPI_STAGE is added by the launcher for the grad_W GEMM only)
+    // forward: a 32-row x 64-byte bf16 staging slot per epilogue warp, so each P~ store
+    // instruction writes 8 rows x 64 contiguous bytes (full 32-byte sectors) instead of 16 B
+    // from each of 32 rows (added by the launcher for the forward GEMM only)
+#ifndef AGENTRL_FWD_PSTAGE
+#define AGENTRL_FWD_PSTAGE 1
+#endif
+    static constexpr int PSTAGE = AGENTRL_FWD_PSTAGE ? 4 * 32 * 64 : 0;
     static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 1024;
     static constexpr int TX_BYTES = (A_STAGE + B_STAGE) * (PAIR ? 2 : 1);
 };
@@ -773,6 +780,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     const float mb = m * LOG2E;
                     __nv_bfloat16* prow =
                         kStoreP ? p.P + (row_ok ? row : 0) * p.ldP + col0 : nullptr;
+                    // the warp's staging slot (AGENTRL_FWD_PSTAGE): row r's four 16-byte pieces
+                    // at r * 4 + (piece ^ ((r >> 1) & 3)) -- conflict-free both ways
+                    uint4* pst = reinterpret_cast<uint4*>(xin) + q * (32 * 4);
+                    const int64_t row0 = row - lane;
+                    (void)pst;
+                    (void)row0;
 #pragma unroll 1
                     for (int c = 0; c < GEMM_BN / 32; ++c) {
                         tmem_ld_32x32b_x32(taddr + c * 32, r);
@@ -790,7 +803,28 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             if constexpr (!kStoreP) u = fmaf(e[j], ok ? m - z : 0.f, u);
                             if (c * 32 + j == yl && row_ok) p.zy[row] = z;
                         }
-                        if (kStoreP && row_ok) {
+                        if constexpr (kStoreP && Cfg::PSTAGE > 0) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                uint4 v;
+                                v.x = pack_bf162(e[j + 0], e[j + 1]);
+                                v.y = pack_bf162(e[j + 2], e[j + 3]);
+                                v.z = pack_bf162(e[j + 4], e[j + 5]);
+                                v.w = pack_bf162(e[j + 6], e[j + 7]);
+                                pst[lane * 4 + ((j >> 3) ^ ((lane >> 1) & 3))] = v;
+                            }
+                            __syncwarp();
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int rl = i * 8 + (lane >> 2), pc = lane & 3;
+                                const uint4 v = pst[rl * 4 + (pc ^ ((rl >> 1) & 3))];
+                                const int64_t rg = row0 + rl;
+                                if (rg < M && c * 32 + pc * 8 < ncol)
+                                    *reinterpret_cast<uint4*>(p.P + rg * p.ldP + col0 + c * 32 +
+                                                              pc * 8) = v;
+                            }
+                            __syncwarp();
+                        } else if (kStoreP && row_ok) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 8) {
                                 if (c * 32 + j < ncol) {

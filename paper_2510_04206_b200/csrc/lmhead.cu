@@ -163,6 +163,7 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
         auto kern = gemm_sm100_pair_kernel<EPI, A_MN, B_MN, NSPLIT, KSUB, XF>;
         constexpr int smem = GemmCfg<true, NSPLIT, KSUB>::SMEM +
                              (EPI == EPI_GRADW ? GemmCfg<true, NSPLIT, KSUB>::EPI_STAGE : 0) +
+                             (EPI == EPI_FWD ? GemmCfg<true, NSPLIT, KSUB>::PSTAGE : 0) +
                              (XF ? GemmCfg<true, NSPLIT, KSUB>::STAGES * XIN_STAGE : 0);
         static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
@@ -174,7 +175,8 @@ static int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
         kern<<<(unsigned)grid, threads, smem, stream>>>(a, b, g);
     } else {
         auto kern = gemm_sm100_kernel<EPI, A_MN, B_MN, XF>;
-        constexpr int smem = GemmCfg<false, 1>::SMEM + (XF ? GemmCfg<false, 1>::STAGES * XIN_STAGE : 0);
+        constexpr int smem = GemmCfg<false, 1>::SMEM + (XF ? GemmCfg<false, 1>::STAGES * XIN_STAGE : 0) +
+                             (EPI == EPI_FWD ? GemmCfg<false, 1>::PSTAGE : 0);
         static std::atomic<uint64_t> attr_done{0};
         if (!func_attr_once(attr_done, (const void*)kern, smem)) return AGENTRL_ERR_CUDA;
         int grid = AGENTRL_GEMM_FULLGRID
