@@ -56,6 +56,7 @@ VARIANTS = {
     "applynopf": ["-DADV_APPLY_PF=0", "-DADV_APPLY_PDL=0"],  # large apply: no unit prefetch, no PDL
     "applydiag": ["-DADV_APPLY_DIAG=1"],               # timing only: the apply's stores alone
     "pstage0": ["-DAGENTRL_FWD_PSTAGE=0"],             # forward: P~ stored 16 B per row, no staging
+    "gwstage0": ["-DAGENTRL_GRADW_STAGE=0"],           # local grad_W epilogue: 16 B per row stores
 }
 
 

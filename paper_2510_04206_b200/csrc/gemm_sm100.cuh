@@ -93,6 +93,9 @@ struct GemmCfg {
     // forward: a 32-row x 64-byte bf16 staging slot per epilogue warp, so each P~ store
     // instruction writes 8 rows x 64 contiguous bytes (full 32-byte sectors) instead of 16 B
     // from each of 32 rows (added by the launcher for the forward GEMM only)
+#ifndef AGENTRL_GRADW_STAGE
+#define AGENTRL_GRADW_STAGE 1  // the local grad_W epilogue staged for full-line stores
+#endif
 #ifndef AGENTRL_FWD_PSTAGE
 #define AGENTRL_FWD_PSTAGE 1
 #endif
@@ -906,6 +909,44 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                              c * 32 + lane;
                                 *dst = slab[i * 33 + lane];
                             }
+                        }
+                        __syncwarp();
+                    }
+                } else if (EPI == EPI_GRADW && Cfg::EPI_STAGE > 0 && AGENTRL_GRADW_STAGE) {
+                    // local grad_W (also the split-K and vocabulary-parallel fp32 partials): each
+                    // 32 x 32 chunk is staged in the warp's slab (row r's eight 16-byte pieces at
+                    // r * 8 + (piece ^ (r & 7)): conflict-free both ways), then every store
+                    // instruction writes 4 rows x 128 contiguous bytes (full lines) instead of
+                    // 16 B from each of 32 rows -- the same instruction count
+                    const float s = have_k ? p.scale : 0.f;
+                    float4* slab = reinterpret_cast<float4*>(
+                                       xin + (XF ? STAGES * XIN_STAGE : 0)) + q * (32 * 8);
+                    const int64_t row0 = row - lane;
+                    float* obase = p.gw + sp * p.gw_split + col0;
+#pragma unroll 1
+                    for (int c = 0; c < GEMM_BN / 32; ++c) {
+                        if (have_k) {
+                            tmem_ld_32x32b_x32(taddr + c * 32, r);
+                            tmem_ld_wait();
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) r[j] = 0u;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            slab[lane * 8 + (j ^ (lane & 7))] =
+                                make_float4(s * __uint_as_float(r[4 * j + 0]),
+                                            s * __uint_as_float(r[4 * j + 1]),
+                                            s * __uint_as_float(r[4 * j + 2]),
+                                            s * __uint_as_float(r[4 * j + 3]));
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int rl = i * 4 + (lane >> 3), pc = lane & 7;
+                            const float4 v = slab[rl * 8 + (pc ^ (rl & 7))];
+                            const int64_t ri = row0 + rl;
+                            if (ri < M && c * 32 + pc * 4 < ncol)
+                                *reinterpret_cast<float4*>(obase + ri * p.ldo + c * 32 + pc * 4) = v;
                         }
                         __syncwarp();
                     }
