@@ -4,7 +4,9 @@ set -o pipefail
 V=$1; SKIP=${2:-1}
 python paper_2510_04206_b200/build.py > /dev/null
 python -c "import oracle; oracle.build()"
+if [ -f "$V" ]; then P0=$PWD/$V; else  # a library path (e.g. ab_head/libagentrl.so) or a variant name
 P0=$(python -c "import sys; sys.path.insert(0,'tests'); from variants import variant_env; print(variant_env('$V')['AGENTRL_LIB'])")
+fi
 timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_vocab_parallel.py tests/test_gpu_multirank.py -x -q -m gpu 2>&1 | tail -3 | tee gpurun_out/gab_pytest.log
 timeout 900 python -m pytest tests/test_gpu_variants.py -x -q -m gpu -k "pair0 or ksplit3" 2>&1 | tail -2 | tee -a gpurun_out/gab_pytest.log
 rm -f gpurun_out/gab_ab.txt
