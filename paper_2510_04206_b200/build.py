@@ -43,6 +43,8 @@ VARIANTS = {
                "-DAGENTRL_L2POL_FWD_B=2", "-DAGENTRL_L2POL_BWD=2"],
     "ksub1": ["-DAGENTRL_FWD_KSUB=1"],                 # one 64-wide K atom per forward stage
     "lead0": ["-DAGENTRL_THROTTLE_LEAD=0"],            # backward progress throttle off
+    "lead64": ["-DAGENTRL_THROTTLE_LEAD=64"],          # backward throttle lead 64 k-blocks
+    "lead160": ["-DAGENTRL_THROTTLE_LEAD=160"],        # backward throttle lead 160 k-blocks
     "lockstep": ["-DAGENTRL_THROTTLE_LEAD=1", "-DAGENTRL_THROTTLE_EVERY=1"],
     "pair0_lead2": ["-DAGENTRL_GEMM_PAIR=0", "-DAGENTRL_THROTTLE_LEAD=2",
                     "-DAGENTRL_THROTTLE_EVERY=1"],
