@@ -2241,7 +2241,13 @@ int launch_adv_norm_coop(const agentrl_batch* b, double eps_std, float* adv_tok,
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        AG_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k_adv_large_apply, args));
+        if (cudaLaunchKernelExC(&cfg, (const void*)k_adv_large_apply, args) != cudaSuccess) {
+            // (a driver without programmatic dependent launch: an ordinary launch instead; the
+            // kernel's griddepcontrol.wait then returns at once)
+            (void)cudaGetLastError();
+            AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, APPLY_THREADS,
+                                     args, smem, stream));
+        }
     } else {
         AG_CUDA(cudaLaunchKernel((const void*)k_adv_large_apply, grid_a, APPLY_THREADS, args,
                                  smem, stream));
