@@ -45,6 +45,8 @@ VARIANTS = {
     "lead0": ["-DAGENTRL_THROTTLE_LEAD=0"],            # backward progress throttle off
     "lead64": ["-DAGENTRL_THROTTLE_LEAD=64"],          # backward throttle lead 64 k-blocks
     "lead160": ["-DAGENTRL_THROTTLE_LEAD=160"],        # backward throttle lead 160 k-blocks
+    "gm12": ["-DAGENTRL_GROUP_M=12"],                  # forward raster group of 12 row blocks
+    "gm24": ["-DAGENTRL_GROUP_M=24"],                  # forward raster group of 24 row blocks
     "lockstep": ["-DAGENTRL_THROTTLE_LEAD=1", "-DAGENTRL_THROTTLE_EVERY=1"],
     "pair0_lead2": ["-DAGENTRL_GEMM_PAIR=0", "-DAGENTRL_THROTTLE_LEAD=2",
                     "-DAGENTRL_THROTTLE_EVERY=1"],
