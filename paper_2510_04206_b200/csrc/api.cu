@@ -253,6 +253,7 @@ size_t agentrl_task_adv_norm_workspace_size(int64_t T, int32_t n_traj, int32_t n
 int agentrl_task_adv_norm(const agentrl_batch* b, double eps_std, float* adv_tok,
                           double* task_stats, int64_t* n_mask_global, void* ws, size_t ws_bytes,
                           agentrl_comm comm, int32_t* d_status, agentrl_stream stream) {
+    NvtxRange nvtx("agentrl_task_adv_norm");
     g_launches = 0;
     int rc = check_batch(b, eps_std);
     if (rc) return rc;
@@ -277,6 +278,7 @@ size_t agentrl_policy_loss_workspace_size_vp(int64_t T, int64_t max_rows, int32_
 int agentrl_policy_loss_fwd_bwd(const agentrl_loss_args* a, const agentrl_loss_out* o, void* ws,
                                 size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                                 agentrl_stream stream) {
+    NvtxRange nvtx("agentrl_policy_loss_fwd_bwd");
     g_launches = 0;
     int rc = check_loss(a, o, false);
     if (!rc && a->grad_W_mode == 2 && comm && a->V % comm_world(comm) != 0) rc = AGENTRL_ERR_SHAPE;
@@ -297,6 +299,7 @@ size_t agentrl_logprob_workspace_size(int64_t T, int64_t max_rows, int32_t d, in
 
 int agentrl_logprob_fwd(const agentrl_logprob_args* a, float* logp, float* entropy, void* ws,
                         size_t ws_bytes, int32_t* d_status, agentrl_stream stream) {
+    NvtxRange nvtx("agentrl_logprob_fwd");
     g_launches = 0;
     if (!a || !logp || !d_status || !ws || !a->hidden || !a->W_head || !a->target ||
         !a->loss_mask || !(a->logit_scale > 0.f))
@@ -322,6 +325,7 @@ int agentrl_grpo_step(const agentrl_batch* b, double eps_std, const agentrl_loss
                       const agentrl_loss_out* o, float* adv_tok_out, double* task_stats, void* ws,
                       size_t ws_bytes, agentrl_comm comm, int32_t* d_status,
                       agentrl_stream stream) {
+    NvtxRange nvtx("agentrl_grpo_step");
     g_launches = 0;
     int rc = check_batch(b, eps_std);
     if (rc) return rc;

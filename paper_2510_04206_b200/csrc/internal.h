@@ -6,6 +6,8 @@
 
 #include <atomic>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu --nvtx, no-ops without a tool
+
 #include "../../include/agentrl.h"
 
 namespace agentrl {
@@ -165,11 +167,21 @@ enum KernelId {
     KID_REDUCE, KID_GRADW, KID_GRADH, KID_LOGP_GEMM, KID_LOGP_MERGE, KID_N
 };
 void prof_mark(int kid, bool begin, cudaStream_t s);
-struct ProfScope {
+struct ProfScope {  // per-kernel event timing and an NVTX range named after the kernel
     int kid;
     cudaStream_t s;
-    ProfScope(int k, cudaStream_t st) : kid(k), s(st) { prof_mark(kid, true, s); }
-    ~ProfScope() { prof_mark(kid, false, s); }
+    ProfScope(int k, cudaStream_t st) : kid(k), s(st) {
+        nvtxRangePushA(agentrl_kernel_name(kid));
+        prof_mark(kid, true, s);
+    }
+    ~ProfScope() {
+        prof_mark(kid, false, s);
+        nvtxRangePop();
+    }
+};
+struct NvtxRange {  // host-side range around an ABI call
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 constexpr int MAX_DEVICES = 64;  // per-device caches (device ids are taken modulo this)
 int current_device();
